@@ -1,0 +1,819 @@
+// oracle/oracle.cpp — TEST INFRASTRUCTURE ONLY.
+//
+// A plain, slow, CPU, event-driven implementation of what the hot path
+// computes: for one candidate mapping (a linear index into the search space)
+// it predicts one training-iteration time in int64 ns.  Only tests/,
+// __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference legs
+// may load it.  It shares no code, header, table or constant generator with
+// the product (paper_2508_05370_b200/); its input structs are its own.
+//
+// It follows PAPER.md (arXiv 2508.05370) and the readings recorded in
+// DESIGN.md §2 (the paper gives no cost formulas beyond the link delay; every
+// other formula is a reading, listed there with its id A1..A24 / C.x).
+//
+// Style: literal.  Every replica of every class is simulated; every stage is
+// its own resource in a (time, seq)-ordered event queue;
+// stage durations are sums over their layers' op durations; every collective
+// (TP all-reduce, DP ring all-reduce) is simulated send by send on its ring.
+// No closed forms, no sub-classing, no precomputed tables.
+//
+// Exactness rules (DESIGN.md C.0): durations are ceil((double)x / r) with x an
+// int64 < 2^53 and r a double; everything else is int64 + and max.  Built with
+// -ffp-contract=off, no fast-math.
+//
+// Pins (tests/test_oracle_pins.py): Table 4 delays, ring all-reduce and 1F1B
+// closed forms, DAG longest path, Hamilton / Fig 3 shares, Table 1 payload,
+// parameter counts, brute-force tiny spaces, invariants.  Absolute iteration
+// times are "parity unpinned" (the paper prints none).
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <queue>
+#include <string>
+#include <thread>
+#include <tuple>
+#include <vector>
+
+typedef int64_t i64;
+
+// ----------------------------------------------------------------------------
+// Input structs (the oracle's own; built by oracle/oracle.py from the shared
+// workload dicts in hsim_inputs/ — field copies only).
+// ----------------------------------------------------------------------------
+extern "C" {
+struct orc_hop { double gbps; int32_t bidir; int32_t pad; };
+struct orc_path { int32_t n; int32_t pad; orc_hop hop[4]; };
+struct orc_type {
+  double peak_flop_per_ns, hbm_bytes_per_ns;
+  double eff_flop[5], eff_mem[5];
+  i64 mem_bytes;
+  int32_t gpus_per_node, n_link_kinds;
+  orc_path link_kind[4];
+  int32_t intra_kind[8][8];
+  orc_path gpu_nic;
+  double nic_gbps;
+  i64 nic_delay_ns;
+};
+struct orc_input {
+  int32_t n_types, n_nodes;
+  const orc_type* types;
+  const int32_t* node_type;
+  i64 rail_alpha_ns;
+  double rail_gbps;
+  i64 frame_bytes;
+  // model (Table 5 row + DESIGN A3 fields)
+  i64 L, h, heads, kv_heads, ffn, nm, seq, V, tied, E, topk, bpe_act, bpe_grad, B;
+  // search space (framework description as a space; DESIGN C.2)
+  int32_t n_b, bset[8];
+  int32_t n_tp[8], tpset[8][8];
+  int32_t n_p, pset[16];
+  int32_t homo, mixed, use_all, r_layer, pmax, r_batch;
+};
+}
+
+namespace {
+
+enum { ATTN = 0, MLP = 1, MOE = 2, EMB = 3, HEAD = 4 };
+
+// --- C.0 exactness ----------------------------------------------------------
+i64 ceilq(i64 x, double r) {  // one IEEE RN division, then ceil
+  if (x == 0) return 0;
+  return (i64)std::ceil((double)x / r);
+}
+i64 ceil_div(i64 a, i64 b) { return (a + b - 1) / b; }
+
+// --- links: PAPER.md:394-396 (delay = jumbo*8 / uni-dir Gbps), Table 4 ------
+struct Link { i64 alpha; double beta; };  // alpha ns, beta B/ns
+
+double uni_gbps(const orc_hop& hp) { return hp.bidir ? hp.gbps / 2.0 : hp.gbps; }
+
+// A path of hops: alpha = sum of per-hop delays (each ceil'd, A9), beta = the
+// slowest hop (uni Gbps / 8 = B/ns).
+Link path_link(const orc_path& p, i64 frame) {
+  Link l{0, 1e300};
+  for (int k = 0; k < p.n; ++k) {
+    double u = uni_gbps(p.hop[k]);
+    l.alpha += ceilq(frame * 8, u);
+    l.beta = std::min(l.beta, u / 8.0);
+  }
+  return l;
+}
+Link join(Link a, Link b) { return Link{a.alpha + b.alpha, std::min(a.beta, b.beta)}; }
+i64 tau(const Link& e, i64 x) { return e.alpha + ceilq(x, e.beta); }
+
+struct Cluster {
+  const orc_input* in;
+  std::vector<int> gpn;            // gpus per node, per node
+  std::vector<int> ntype;          // device type per node
+  std::vector<i64> n_of_type;      // total GPUs per type
+  std::vector<std::vector<int>> nodes_of_type;
+
+  const orc_type& T(int node) const { return in->types[ntype[node]]; }
+
+  // Fig 2 cases (a)(b)(c); DESIGN A10-A12.
+  Link gpu_to_gpu(int n1, int r1, int n2, int r2) const {
+    const i64 fr = in->frame_bytes;
+    if (n1 == n2) {
+      const orc_type& t = T(n1);
+      return path_link(t.link_kind[t.intra_kind[r1][r2]], fr);
+    }
+    // rail path GPU -> PCIe -> NIC -> rail switch -> NIC -> PCIe -> GPU
+    const orc_type& a = T(n1);
+    const orc_type& b = T(n2);
+    Link rail = path_link(a.gpu_nic, fr);
+    rail = join(rail, Link{a.nic_delay_ns, a.nic_gbps / 8.0});
+    rail = join(rail, Link{in->rail_alpha_ns, in->rail_gbps / 8.0});
+    rail = join(rail, Link{b.nic_delay_ns, b.nic_gbps / 8.0});
+    rail = join(rail, path_link(b.gpu_nic, fr));
+    if (r1 == r2) return rail;                                          // case (b)
+    return join(path_link(a.link_kind[a.intra_kind[r1][r2]], fr), rail);  // case (c)
+  }
+};
+
+// --- C.5: per-device FLOPs and bytes of one layer op -------------------------
+struct Cost { i64 flop, bytes; };
+Cost op_cost(const orc_input& m, int kind, i64 t, i64 b) {
+  const i64 T = b * m.seq, h = m.h, bpe = m.bpe_act;
+  const i64 hkv = m.kv_heads * h / m.heads;
+  switch (kind) {
+    case ATTN:
+      return {ceil_div(2 * T * h * (2 * h + 2 * hkv) + 4 * b * m.seq * m.seq * h, t),
+              ceil_div(bpe * h * (2 * h + 2 * hkv), t) + 2 * T * h * bpe};
+    case MLP:
+      return {ceil_div(2 * T * m.nm * h * m.ffn, t), ceil_div(bpe * m.nm * h * m.ffn, t) + 2 * T * h * bpe};
+    case MOE:
+      return {ceil_div(2 * T * m.topk * m.nm * h * m.ffn, t),
+              ceil_div(bpe * m.E * m.nm * h * m.ffn, t) + 2 * T * h * bpe};
+    case EMB:
+      return {0, 2 * T * h * bpe};
+    default:  // HEAD
+      return {ceil_div(2 * T * h * m.V, t), ceil_div(bpe * m.V * h, t) + T * h * bpe + ceil_div(T * m.V * bpe, t)};
+  }
+}
+// roofline duration; backward = 2x FLOP and 2x bytes, rounded on its own (A6)
+i64 op_dur(const orc_input& m, const orc_type& ty, int kind, bool bwd, i64 t, i64 b) {
+  Cost c = op_cost(m, kind, t, b);
+  i64 mul = bwd ? 2 : 1;
+  double rf = ty.peak_flop_per_ns * ty.eff_flop[kind];
+  double rm = ty.hbm_bytes_per_ns * ty.eff_mem[kind];
+  return std::max(ceilq(mul * c.flop, rf), ceilq(mul * c.bytes, rm));
+}
+
+// --- literal async ring (DESIGN C.11): rank r sends to r+1 over edge r --------
+// send(r,k).start = max(send(r,k-1).end, send(r-1,k-1).end)
+i64 ring_sim(const std::vector<i64>& edge_tau, int steps) {
+  const int n = (int)edge_tau.size();
+  std::vector<i64> end(n, 0), nxt(n);
+  for (int k = 0; k < steps; ++k) {
+    for (int r = 0; r < n; ++r) nxt[r] = std::max(end[r], end[(r + n - 1) % n]) + edge_tau[r];
+    end.swap(nxt);
+  }
+  i64 t = 0;
+  for (i64 e : end) t = std::max(t, e);
+  return t;
+}
+
+// --- Hamilton / largest remainder (DESIGN C.4): ties -> lower index ----------
+std::vector<i64> hamilton(i64 n, const std::vector<i64>& w) {
+  const int k = (int)w.size();
+  i64 W = 0;
+  for (i64 x : w) W += x;
+  std::vector<i64> q(k), rem(k);
+  i64 given = 0;
+  for (int i = 0; i < k; ++i) {
+    q[i] = n * w[i] / W;
+    rem[i] = n * w[i] % W;
+    given += q[i];
+  }
+  std::vector<int> order(k);
+  for (int i = 0; i < k; ++i) order[i] = i;
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return rem[a] > rem[b]; });
+  for (i64 s = 0; s < n - given; ++s) q[order[s]] += 1;
+  return q;
+}
+
+// --- candidate space (DESIGN C.2) --------------------------------------------
+struct StageSpec { int type; int tp; };
+struct ClassSpec { std::vector<StageSpec> st; int D; };
+struct Template { int b; std::vector<ClassSpec> cls; i64 radix; i64 prefix; };
+
+bool tp_ok(const orc_input& in, int type, int tp) {
+  return in.types[type].gpus_per_node % tp == 0 && in.heads % tp == 0 && in.kv_heads % tp == 0;
+}
+
+i64 ipow(i64 a, i64 e) { i64 r = 1; while (e-- > 0) r *= a; return r; }
+
+std::vector<Template> enumerate(const orc_input& in, const Cluster& cl) {
+  std::vector<Template> out;
+  std::vector<int> bs(in.bset, in.bset + in.n_b), ps(in.pset, in.pset + in.n_p);
+  std::sort(bs.begin(), bs.end());
+  std::sort(ps.begin(), ps.end());
+  const int nt = in.n_types;
+  for (int b : bs) {
+    if (in.B % b) continue;
+    const i64 M = in.B / b;
+    auto emit = [&](std::vector<ClassSpec> cls) {
+      i64 D = 0;
+      for (auto& c : cls) D += c.D;
+      if (M < D) return;  // the only structural filter
+      Template t{b, cls, 1, 0};
+      for (auto& c : cls) {
+        int P = (int)c.st.size();
+        if (P <= in.pmax) t.radix *= ipow(2 * in.r_layer + 1, P - 1);
+      }
+      t.radix *= ipow(2 * in.r_batch + 1, (i64)cls.size() - 1);
+      out.push_back(t);
+    };
+    if (in.homo) {
+      // per type: "unused" then (tp, P, D) ascending
+      struct Opt { int tp, P, D; };
+      std::vector<std::vector<Opt>> opts(nt);
+      for (int t = 0; t < nt; ++t) {
+        opts[t].push_back({0, 0, 0});
+        std::vector<int> tps(in.tpset[t], in.tpset[t] + in.n_tp[t]);
+        std::sort(tps.begin(), tps.end());
+        for (int tp : tps) {
+          if (!tp_ok(in, t, tp)) continue;
+          for (int P : ps) {
+            if (P > in.L) continue;
+            for (i64 D = 1; D * P * tp <= cl.n_of_type[t]; ++D) {
+              if (in.use_all && D * P * tp != cl.n_of_type[t]) continue;
+              opts[t].push_back({tp, P, (int)D});
+            }
+          }
+        }
+      }
+      std::vector<int> pick(nt, 0);
+      while (true) {
+        bool any = false;
+        for (int t = 0; t < nt; ++t) any |= pick[t] != 0;
+        if (any) {
+          std::vector<ClassSpec> cls;
+          for (int t = 0; t < nt; ++t) {
+            if (!pick[t]) continue;
+            Opt o = opts[t][pick[t]];
+            ClassSpec c;
+            c.D = o.D;
+            for (int s = 0; s < o.P; ++s) c.st.push_back({t, o.tp});
+            cls.push_back(c);
+          }
+          emit(cls);
+        }
+        int t = nt - 1;  // odometer, type 0 most significant
+        while (t >= 0 && ++pick[t] == (int)opts[t].size()) { pick[t] = 0; --t; }
+        if (t < 0) break;
+      }
+    }
+    if (in.mixed && nt >= 2) {
+      struct Opt { int tp, P; };
+      std::vector<std::vector<Opt>> opts(nt);
+      for (int t = 0; t < nt; ++t) {
+        std::vector<int> tps(in.tpset[t], in.tpset[t] + in.n_tp[t]);
+        std::sort(tps.begin(), tps.end());
+        for (int tp : tps) {
+          if (!tp_ok(in, t, tp)) continue;
+          for (int P : ps) opts[t].push_back({tp, P});
+        }
+      }
+      bool empty = false;
+      for (int t = 0; t < nt; ++t) empty |= opts[t].empty();
+      if (!empty) {
+        std::vector<int> pick(nt, 0);
+        while (true) {
+          int sumP = 0;
+          i64 Dmax = INT64_MAX;
+          for (int t = 0; t < nt; ++t) {
+            Opt o = opts[t][pick[t]];
+            sumP += o.P;
+            Dmax = std::min(Dmax, cl.n_of_type[t] / ((i64)o.P * o.tp));
+          }
+          if (sumP <= in.L && Dmax >= 1) {
+            for (i64 D = in.use_all ? Dmax : 1; D <= Dmax; ++D) {
+              ClassSpec c;
+              c.D = (int)D;
+              for (int t = 0; t < nt; ++t)
+                for (int s = 0; s < opts[t][pick[t]].P; ++s) c.st.push_back({t, opts[t][pick[t]].tp});
+              emit({c});
+            }
+          }
+          int t = nt - 1;
+          while (t >= 0 && ++pick[t] == (int)opts[t].size()) { pick[t] = 0; --t; }
+          if (t < 0) break;
+        }
+      }
+    }
+  }
+  i64 acc = 0;
+  for (auto& t : out) { t.prefix = acc; acc += t.radix; }
+  return out;
+}
+
+// --- one decoded, placed and partitioned candidate ---------------------------
+struct Group { int node, base; };  // a stage group: tp GPUs [base, base+tp) on node
+
+struct Plan {
+  const Template* tpl;
+  std::vector<std::vector<int>> delta;  // per class, per boundary (P-1)
+  std::vector<int> eps;                 // per class (C-1)
+  std::vector<std::vector<std::vector<Group>>> place;  // [class][replica][stage]
+  std::vector<std::vector<i64>> layers;  // [class][stage]
+  std::vector<std::vector<i64>> mb;      // [class][replica] micro-batches
+  int status = 0;
+};
+
+struct Oracle {
+  orc_input in;
+  std::vector<orc_type> types;
+  std::vector<int32_t> node_type;
+  Cluster cl;
+  std::vector<Template> tpls;
+  i64 N = 0;
+
+  void init() {
+    in.types = types.data();
+    in.node_type = node_type.data();
+    cl.in = &in;
+    cl.n_of_type.assign(in.n_types, 0);
+    cl.nodes_of_type.assign(in.n_types, {});
+    for (int n = 0; n < in.n_nodes; ++n) {
+      int t = node_type[n];
+      cl.ntype.push_back(t);
+      cl.gpn.push_back(types[t].gpus_per_node);
+      cl.n_of_type[t] += types[t].gpus_per_node;
+      cl.nodes_of_type[t].push_back(n);
+    }
+    tpls = enumerate(in, cl);
+    N = tpls.empty() ? 0 : tpls.back().prefix + tpls.back().radix;
+  }
+
+  // C.2 decode: template = max{tau : prefix <= i}; digits LSB first
+  Plan decode(i64 i) const {
+    Plan p;
+    size_t lo = 0, hi = tpls.size();
+    while (hi - lo > 1) {
+      size_t mid = (lo + hi) / 2;
+      if (tpls[mid].prefix <= i) lo = mid; else hi = mid;
+    }
+    p.tpl = &tpls[lo];
+    i64 local = i - p.tpl->prefix;
+    const int C = (int)p.tpl->cls.size();
+    p.delta.resize(C);
+    for (int c = 0; c < C; ++c) {
+      int P = (int)p.tpl->cls[c].st.size();
+      p.delta[c].assign(P > 0 ? P - 1 : 0, 0);
+      if (P <= in.pmax)
+        for (int s = 0; s < P - 1; ++s) {
+          p.delta[c][s] = (int)(local % (2 * in.r_layer + 1)) - in.r_layer;
+          local /= (2 * in.r_layer + 1);
+        }
+    }
+    p.eps.assign(C, 0);
+    for (int c = 0; c < C - 1; ++c) {
+      p.eps[c] = (int)(local % (2 * in.r_batch + 1)) - in.r_batch;
+      local /= (2 * in.r_batch + 1);
+    }
+    return p;
+  }
+
+  // C.3 placement: class-major, replica-major, stage-major; lowest-id node of
+  // the stage's type with a free tp-aligned block, lowest block.
+  void place(Plan& p) const {
+    std::vector<std::vector<char>> used(in.n_nodes);
+    for (int n = 0; n < in.n_nodes; ++n) used[n].assign(cl.gpn[n], 0);
+    const auto& cls = p.tpl->cls;
+    p.place.resize(cls.size());
+    for (size_t c = 0; c < cls.size(); ++c) {
+      p.place[c].resize(cls[c].D);
+      for (int r = 0; r < cls[c].D; ++r) {
+        for (const StageSpec& s : cls[c].st) {
+          Group g{-1, -1};
+          for (int n : cl.nodes_of_type[s.type]) {
+            for (int k = 0; k * s.tp < cl.gpn[n] && g.node < 0; ++k) {
+              bool fr = true;
+              for (int q = 0; q < s.tp; ++q) fr &= !used[n][k * s.tp + q];
+              if (fr) g = Group{n, k * s.tp};
+            }
+            if (g.node >= 0) break;
+          }
+          if (g.node < 0) { std::fprintf(stderr, "oracle: placement failed\n"); std::abort(); }
+          for (int q = 0; q < s.tp; ++q) used[g.node][g.base + q] = 1;
+          p.place[c][r].push_back(g);
+        }
+      }
+    }
+  }
+
+  // TP ring of a stage group: base -> base+1 -> ... -> base+t-1 -> base
+  std::vector<Link> tp_ring(const Group& g, int t) const {
+    std::vector<Link> e;
+    for (int q = 0; q < t; ++q) e.push_back(cl.gpu_to_gpu(g.node, g.base + q, g.node, g.base + (q + 1) % t));
+    return e;
+  }
+  i64 act_bytes(int b) const { return (i64)b * in.seq * in.h * in.bpe_act; }  // A5
+
+  // TP all-reduce after attention / MLP (A16): literal ring, 2(t-1) steps
+  i64 tp_allreduce(const Group& g, int t, int b) const {
+    if (t == 1) return 0;
+    std::vector<i64> taus;
+    for (const Link& e : tp_ring(g, t)) taus.push_back(tau(e, ceil_div(act_bytes(b), t)));
+    return ring_sim(taus, 2 * (t - 1));
+  }
+  // EP all-to-all (A17): g-1 rounds, each bounded by the slowest pair of the group
+  i64 ep_alltoall(const Group& g, int t, int b) const {
+    if (t == 1) return 0;
+    i64 per = ceil_div(act_bytes(b) * in.topk, (i64)t * t);
+    i64 slow = 0;
+    for (int x = 0; x < t; ++x)
+      for (int y = 0; y < t; ++y)
+        if (x != y) slow = std::max(slow, tau(cl.gpu_to_gpu(g.node, g.base + x, g.node, g.base + y), per));
+    return (i64)(t - 1) * slow;
+  }
+
+  i64 tcomp(const StageSpec& s, int b) const {  // compute-only fwd+bwd of one layer (C.4)
+    const orc_type& ty = types[s.type];
+    int mk = in.E > 1 ? MOE : MLP;
+    return op_dur(in, ty, ATTN, false, s.tp, b) + op_dur(in, ty, mk, false, s.tp, b) +
+           op_dur(in, ty, ATTN, true, s.tp, b) + op_dur(in, ty, mk, true, s.tp, b);
+  }
+  i64 extra_fb(const StageSpec& s, int b, int kind) const {
+    const orc_type& ty = types[s.type];
+    return op_dur(in, ty, kind, false, s.tp, b) + op_dur(in, ty, kind, true, s.tp, b);
+  }
+
+  // C.4 step 1: non-uniform partition
+  void partition(Plan& p) const {
+    const auto& cls = p.tpl->cls;
+    const int C = (int)cls.size(), b = p.tpl->b;
+    const i64 M = in.B / b;
+    p.layers.resize(C);
+    std::vector<i64> repl_w;  // class-major replica weights
+    for (int c = 0; c < C; ++c) {
+      const int P = (int)cls[c].st.size();
+      std::vector<i64> w(P);
+      for (int s = 0; s < P; ++s) w[s] = (i64(1) << 40) / tcomp(cls[c].st[s], b);
+      std::vector<i64> l = hamilton(in.L, w);
+      for (int s = 0; s < P; ++s) {
+        i64 d_here = s < P - 1 ? p.delta[c][s] : 0;
+        i64 d_prev = s > 0 ? p.delta[c][s - 1] : 0;
+        l[s] += d_here - d_prev;
+        if (l[s] < 1) p.status = -1;
+      }
+      p.layers[c] = l;
+      if (p.status) return;
+      i64 worst = 0;
+      for (int s = 0; s < P; ++s) {
+        i64 t = l[s] * tcomp(cls[c].st[s], b);
+        if (s == 0) t += extra_fb(cls[c].st[s], b, EMB);
+        if (s == P - 1) t += extra_fb(cls[c].st[s], b, HEAD);
+        worst = std::max(worst, t);
+      }
+      for (int r = 0; r < cls[c].D; ++r) repl_w.push_back((i64(1) << 40) / worst);
+    }
+    std::vector<i64> m = hamilton(M, repl_w);
+    p.mb.resize(C);
+    size_t k = 0;
+    i64 R = 0;
+    for (int c = 0; c < C; ++c) {
+      for (int r = 0; r < cls[c].D; ++r) {
+        i64 v = m[k++];
+        if (c < C - 1) v += p.eps[c];
+        p.mb[c].push_back(v);
+      }
+      if (c < C - 1) R -= (i64)cls[c].D * p.eps[c];
+    }
+    const i64 Dl = cls[C - 1].D;
+    i64 q = R >= 0 ? R / Dl : -((-R + Dl - 1) / Dl);  // floor
+    i64 rm = R - q * Dl;                               // in [0, Dl)
+    for (int r = 0; r < Dl; ++r) p.mb[C - 1][r] += q + (r < rm ? 1 : 0);
+    for (int c = 0; c < C; ++c)
+      for (i64 v : p.mb[c])
+        if (v < 1) p.status = -2;
+  }
+
+  // --- C.7 / C.11: event-driven 1F1B over every replica ------------------------
+  struct SimGroup {
+    int P, s, m;
+    i64 f, g, c_prev, c_next;  // c_prev: boundary s-1 -> s, c_next: s -> s+1
+    std::vector<std::pair<bool, int>> ops;  // (is_fwd, micro-batch)
+    size_t next = 0;
+    bool busy = false;
+    std::vector<char> inF, inB;
+  };
+  struct Ev {
+    i64 t, seq;
+    int kind;  // 0 = op done, 1 = F input arrives, 2 = B input arrives
+    int grp, j;
+    bool operator>(const Ev& o) const { return std::tie(t, seq) > std::tie(o.t, o.seq); }
+  };
+
+  static std::vector<std::pair<bool, int>> op_order(int P, int s, int m) {
+    std::vector<std::pair<bool, int>> o;
+    int w = std::min(P - 1 - s, m);
+    for (int j = 0; j < w; ++j) o.push_back({true, j});
+    for (int i = 0; i < m - w; ++i) { o.push_back({true, w + i}); o.push_back({false, i}); }
+    for (int j = m - w; j < m; ++j) o.push_back({false, j});
+    return o;
+  }
+
+  // Runs the listed pipelines (each a consecutive run of P groups); returns the
+  // time of the last event (T0).
+  static i64 run_pipelines(std::vector<SimGroup>& G) {
+    std::priority_queue<Ev, std::vector<Ev>, std::greater<Ev>> q;
+    i64 seq = 0, last = 0;
+    auto try_start = [&](int gi, i64 t) {
+      SimGroup& g = G[gi];
+      if (g.busy || g.next >= g.ops.size()) return;
+      auto op = g.ops[g.next];
+      bool ready = op.first ? g.inF[op.second] : g.inB[op.second];
+      if (!ready) return;
+      g.busy = true;
+      q.push(Ev{t + (op.first ? g.f : g.g), seq++, 0, gi, op.second});
+    };
+    for (size_t gi = 0; gi < G.size(); ++gi) {
+      G[gi].inF.assign(G[gi].m, G[gi].s == 0 ? 1 : 0);
+      G[gi].inB.assign(G[gi].m, 0);
+      G[gi].ops = op_order(G[gi].P, G[gi].s, G[gi].m);
+    }
+    for (size_t gi = 0; gi < G.size(); ++gi) try_start((int)gi, 0);
+    while (!q.empty()) {
+      Ev e = q.top();
+      q.pop();
+      last = std::max(last, e.t);
+      SimGroup& g = G[e.grp];
+      if (e.kind == 0) {
+        auto op = g.ops[g.next];
+        g.busy = false;
+        g.next++;
+        if (op.first) {
+          if (g.s < g.P - 1) q.push(Ev{e.t + g.c_next, seq++, 1, e.grp + 1, op.second});
+          else g.inB[op.second] = 1;  // last stage: B(P-1,j) follows F(P-1,j)
+        } else if (g.s > 0) {
+          q.push(Ev{e.t + g.c_prev, seq++, 2, e.grp - 1, op.second});
+        }
+        try_start(e.grp, e.t);
+      } else {
+        (e.kind == 1 ? g.inF : g.inB)[e.j] = 1;
+        try_start(e.grp, e.t);
+      }
+    }
+    return last;
+  }
+
+  i64 eval(i64 i) const {
+    if (i < 0 || i >= N) return INT64_MIN;
+    Plan p = decode(i);
+    place(p);
+    partition(p);
+    if (p.status) return p.status;
+    const auto& cls = p.tpl->cls;
+    const int C = (int)cls.size(), b = p.tpl->b;
+    const int mk = in.E > 1 ? MOE : MLP;
+
+    // steps 2-4: stage durations (sum over the stage's layers of its layer-op
+    // chain, C.5), p2p costs (C.6), 1F1B per replica (C.7)
+    std::vector<SimGroup> G;
+    for (int c = 0; c < C; ++c) {
+      const int P = (int)cls[c].st.size();
+      for (int r = 0; r < cls[c].D; ++r) {
+        for (int s = 0; s < P; ++s) {
+          const StageSpec& ss = cls[c].st[s];
+          const orc_type& ty = types[ss.type];
+          const Group& gr = p.place[c][r][s];
+          i64 ar = tp_allreduce(gr, ss.tp, b);
+          i64 a2a = in.E > 1 ? ep_alltoall(gr, ss.tp, b) : 0;
+          SimGroup g{};
+          g.P = P; g.s = s; g.m = (int)p.mb[c][r];
+          for (i64 l = 0; l < p.layers[c][s]; ++l) {
+            for (int bwd = 0; bwd < 2; ++bwd) {
+              i64 chain = op_dur(in, ty, ATTN, bwd, ss.tp, b) + ar;
+              if (in.E > 1) chain += a2a + op_dur(in, ty, MOE, bwd, ss.tp, b) + a2a;
+              else chain += op_dur(in, ty, mk, bwd, ss.tp, b) + ar;
+              (bwd ? g.g : g.f) += chain;
+            }
+          }
+          if (s == 0) { g.f += op_dur(in, ty, EMB, false, ss.tp, b); g.g += op_dur(in, ty, EMB, true, ss.tp, b); }
+          if (s == P - 1) { g.f += op_dur(in, ty, HEAD, false, ss.tp, b); g.g += op_dur(in, ty, HEAD, true, ss.tp, b); }
+          G.push_back(g);
+        }
+        // p2p per boundary: rank pairs i < min(t_s, t_{s+1}) in parallel (A8)
+        const size_t base = G.size() - P;
+        for (int s = 0; s + 1 < P; ++s) {
+          const Group& a = p.place[c][r][s];
+          const Group& z = p.place[c][r][s + 1];
+          int np = std::min(cls[c].st[s].tp, cls[c].st[s + 1].tp);
+          i64 cs = 0;
+          for (int q = 0; q < np; ++q)
+            cs = std::max(cs, tau(cl.gpu_to_gpu(a.node, a.base + q, z.node, z.base + q), act_bytes(b)));
+          G[base + s].c_next = cs;
+          G[base + s + 1].c_prev = cs;
+        }
+      }
+    }
+    const i64 T0 = run_pipelines(G);
+
+    // step 5: gradient sync after the barrier at T0 (A19, C.8)
+    i64 D = 0;
+    for (auto& c : cls) D += c.D;
+    if (D == 1) return T0;
+    std::vector<i64> cuts{0, in.L};
+    std::vector<std::vector<i64>> start(C);
+    for (int c = 0; c < C; ++c) {
+      i64 a = 0;
+      for (i64 l : p.layers[c]) { start[c].push_back(a); cuts.push_back(a); a += l; }
+    }
+    std::sort(cuts.begin(), cuts.end());
+    cuts.erase(std::unique(cuts.begin(), cuts.end()), cuts.end());
+    const i64 hkv = in.kv_heads * in.h / in.heads;
+    const i64 Wlayer = in.h * (2 * in.h + 2 * hkv) + in.nm * in.h * in.ffn * in.E + (in.E > 1 ? in.h * in.E : 0) + 2 * in.h;
+    // free time per stage group of every replica, all from the barrier
+    std::vector<std::vector<std::vector<i64>>> freet(C);
+    for (int c = 0; c < C; ++c) freet[c].assign(cls[c].D, std::vector<i64>(cls[c].st.size(), T0));
+    i64 Titer = T0;
+    for (size_t j = 0; j + 1 < cuts.size(); ++j) {
+      const i64 a = cuts[j], z = cuts[j + 1];
+      i64 S = (z - a) * Wlayer * in.bpe_grad;
+      if (a == 0) S += in.V * in.h * in.bpe_grad;
+      if (z == in.L) S += (in.V * in.h * (in.tied ? 0 : 1) + in.h) * in.bpe_grad;
+      std::vector<int> sc(C);
+      int tstar = 1 << 30;
+      for (int c = 0; c < C; ++c) {
+        int s = 0;
+        while (s + 1 < (int)start[c].size() && start[c][s + 1] <= a) ++s;
+        sc[c] = s;
+        tstar = std::min(tstar, cls[c].st[s].tp);
+      }
+      // reshard (A14): every group with tp != t* re-lays S into t* shards over its ring
+      i64 RS = 0;
+      for (int c = 0; c < C; ++c) {
+        const int tp = cls[c].st[sc[c]].tp;
+        if (tp == tstar) continue;
+        for (int r = 0; r < cls[c].D; ++r)
+          for (const Link& e : tp_ring(p.place[c][r][sc[c]], tp)) RS = std::max(RS, tau(e, ceil_div(S, tstar)));
+      }
+      // DP ring all-reduce: ring order class asc, replica asc, wrap; ring q < t*
+      std::vector<Group> ring;
+      for (int c = 0; c < C; ++c)
+        for (int r = 0; r < cls[c].D; ++r) ring.push_back(p.place[c][r][sc[c]]);
+      const i64 chunk = ceil_div(ceil_div(S, tstar), D);
+      i64 AR = 0;
+      for (int q = 0; q < tstar; ++q) {
+        std::vector<i64> taus;
+        for (size_t k = 0; k < ring.size(); ++k) {
+          const Group& u = ring[k];
+          const Group& v = ring[(k + 1) % ring.size()];
+          taus.push_back(tau(cl.gpu_to_gpu(u.node, u.base + q, v.node, v.base + q), chunk));
+        }
+        AR = std::max(AR, ring_sim(taus, (int)(2 * (D - 1))));
+      }
+      i64 st = 0;
+      for (int c = 0; c < C; ++c)
+        for (int r = 0; r < cls[c].D; ++r) st = std::max(st, freet[c][r][sc[c]]);
+      const i64 en = st + RS + AR;
+      for (int c = 0; c < C; ++c)
+        for (int r = 0; r < cls[c].D; ++r) freet[c][r][sc[c]] = en;
+      Titer = std::max(Titer, en);
+    }
+    return Titer;
+  }
+};
+
+thread_local std::string g_err;
+
+}  // namespace
+
+// ----------------------------------------------------------------------------
+// C API for oracle/oracle.py (ctypes)
+// ----------------------------------------------------------------------------
+extern "C" {
+
+const char* orc_last_error() { return g_err.c_str(); }
+
+void* orc_create(const orc_input* in) {
+  g_err.clear();
+  if (!in || in->n_types < 1 || in->n_types > 8 || in->n_nodes < 1 || in->B < 1 || in->L < 1) {
+    g_err = "invalid input";
+    return nullptr;
+  }
+  Oracle* o = new Oracle();
+  o->in = *in;
+  o->types.assign(in->types, in->types + in->n_types);
+  o->node_type.assign(in->node_type, in->node_type + in->n_nodes);
+  o->init();
+  return o;
+}
+void orc_destroy(void* h) { delete (Oracle*)h; }
+i64 orc_space_size(void* h) { return ((Oracle*)h)->N; }
+i64 orc_n_templates(void* h) { return (i64)((Oracle*)h)->tpls.size(); }
+i64 orc_template_prefix(void* h, i64 k) {
+  Oracle* o = (Oracle*)h;
+  if (k < 0 || k > (i64)o->tpls.size()) return -1;
+  return k == (i64)o->tpls.size() ? o->N : o->tpls[k].prefix;
+}
+i64 orc_eval(void* h, i64 i) { return ((Oracle*)h)->eval(i); }
+
+// Evaluates idx[0..n) (or the range [first, first+n) if idx == NULL) on
+// `threads` host threads.
+void orc_eval_many(void* h, const i64* idx, i64 first, i64 n, i64* out, int threads) {
+  Oracle* o = (Oracle*)h;
+  if (threads < 1) threads = 1;
+  std::atomic<i64> next{0};
+  auto work = [&]() {
+    for (;;) {
+      i64 k = next.fetch_add(64);
+      if (k >= n) return;
+      for (i64 t = k; t < std::min(n, k + 64); ++t) out[t] = o->eval(idx ? idx[t] : first + t);
+    }
+  };
+  std::vector<std::thread> pool;
+  for (int t = 0; t < threads; ++t) pool.emplace_back(work);
+  for (auto& t : pool) t.join();
+}
+
+// Human-readable plan (for tests / debugging): template, layers, micro-batches, placement.
+int orc_describe(void* h, i64 i, char* buf, int cap) {
+  Oracle* o = (Oracle*)h;
+  if (i < 0 || i >= o->N) return -1;
+  Plan p = o->decode(i);
+  o->place(p);
+  o->partition(p);
+  std::string s = "{\"b\":" + std::to_string(p.tpl->b) + ",\"status\":" + std::to_string(p.status) + ",\"classes\":[";
+  for (size_t c = 0; c < p.tpl->cls.size(); ++c) {
+    const ClassSpec& cs = p.tpl->cls[c];
+    s += c ? ",{" : "{";
+    s += "\"D\":" + std::to_string(cs.D) + ",\"stages\":[";
+    for (size_t k = 0; k < cs.st.size(); ++k)
+      s += (k ? ",[" : "[") + std::to_string(cs.st[k].type) + "," + std::to_string(cs.st[k].tp) + "]";
+    s += "],\"layers\":[";
+    for (size_t k = 0; k < p.layers[c].size(); ++k) s += (k ? "," : "") + std::to_string(p.layers[c][k]);
+    s += "],\"mb\":[";
+    if (c < p.mb.size())
+      for (size_t k = 0; k < p.mb[c].size(); ++k) s += (k ? "," : "") + std::to_string(p.mb[c][k]);
+    s += "],\"place\":[";
+    for (size_t r = 0; r < p.place[c].size(); ++r) {
+      s += r ? ",[" : "[";
+      for (size_t k = 0; k < p.place[c][r].size(); ++k)
+        s += (k ? ",[" : "[") + std::to_string(p.place[c][r][k].node) + "," + std::to_string(p.place[c][r][k].base) + "]";
+      s += "]";
+    }
+    s += "]}";
+  }
+  s += "]}";
+  if ((int)s.size() + 1 > cap) return (int)s.size() + 1;
+  std::memcpy(buf, s.c_str(), s.size() + 1);
+  return 0;
+}
+
+// --- building blocks exposed for the pin tests -------------------------------
+// per-hop delay before rounding: frame*8 / uni Gbps
+double orc_hop_delay_exact(double gbps, int bidir, i64 frame) {
+  orc_hop hp{gbps, bidir, 0};
+  return (double)(frame * 8) / uni_gbps(hp);
+}
+i64 orc_ring_sim(const i64* tau_edges, int n, int steps) {
+  return ring_sim(std::vector<i64>(tau_edges, tau_edges + n), steps);
+}
+// one pipeline (P stages, m micro-batches) through the event engine
+i64 orc_pipeline(int P, int m, const i64* f, const i64* g, const i64* c) {
+  std::vector<Oracle::SimGroup> G(P);
+  for (int s = 0; s < P; ++s) {
+    G[s].P = P; G[s].s = s; G[s].m = m; G[s].f = f[s]; G[s].g = g[s];
+    G[s].c_prev = s > 0 ? c[s - 1] : 0;
+    G[s].c_next = s + 1 < P ? c[s] : 0;
+  }
+  return Oracle::run_pipelines(G);
+}
+void orc_hamilton(i64 n, const i64* w, int k, i64* out) {
+  std::vector<i64> q = hamilton(n, std::vector<i64>(w, w + k));
+  for (int i = 0; i < k; ++i) out[i] = q[i];
+}
+// per-device FLOPs/bytes/duration of one op on device type `type` with TP t
+void orc_op(void* h, int type, int kind, int bwd, int t, int b, i64* flop, i64* bytes, i64* dur) {
+  Oracle* o = (Oracle*)h;
+  Cost c = op_cost(o->in, kind, t, b);
+  *flop = c.flop * (bwd ? 2 : 1);
+  *bytes = c.bytes * (bwd ? 2 : 1);
+  *dur = op_dur(o->in, o->types[type], kind, bwd != 0, t, b);
+}
+// gradient bytes of a sync segment of `n_layers` layers (C.6); Table 1 pin
+i64 orc_segment_bytes(void* h, i64 n_layers, int has_first, int has_last) {
+  const orc_input& in = ((Oracle*)h)->in;
+  const i64 hkv = in.kv_heads * in.h / in.heads;
+  const i64 Wlayer = in.h * (2 * in.h + 2 * hkv) + in.nm * in.h * in.ffn * in.E + (in.E > 1 ? in.h * in.E : 0) + 2 * in.h;
+  i64 S = n_layers * Wlayer * in.bpe_grad;
+  if (has_first) S += in.V * in.h * in.bpe_grad;
+  if (has_last) S += (in.V * in.h * (in.tied ? 0 : 1) + in.h) * in.bpe_grad;
+  return S;
+}
+i64 orc_act_bytes(void* h, int b) { return ((Oracle*)h)->act_bytes(b); }
+// link between two GPUs (node, local rank) -> alpha, beta
+void orc_link(void* h, int n1, int r1, int n2, int r2, i64* alpha, double* beta) {
+  Oracle* o = (Oracle*)h;
+  Link l = o->cl.gpu_to_gpu(n1, r1, n2, r2);
+  *alpha = l.alpha;
+  *beta = l.beta;
+}
+}

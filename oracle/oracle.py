@@ -1,0 +1,255 @@
+"""ctypes binding of the C++ oracle — TEST INFRASTRUCTURE ONLY.
+
+Only tests/, __graft_entry__.smoke() and bench.py (cpu_baseline leg and
+``--impl reference``) may import this module.  The product package never does.
+
+The binding only copies fields of a shared workload dict (hsim_inputs/) into
+the oracle's own input struct (defined in oracle.cpp); it holds none of the
+method's arithmetic.
+"""
+import ctypes as C
+import json
+import os
+import subprocess
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+SRC = os.path.join(HERE, "oracle.cpp")
+LIB = os.path.join(HERE, "liboracle.so")
+
+KIND = {"attn": 0, "mlp": 1, "moe": 2, "emb": 3, "head": 4}
+
+
+def build(force=False):
+    """Compile oracle.cpp -> liboracle.so (plain g++, IEEE double, no FMA)."""
+    if not force and os.path.exists(LIB) and os.path.getmtime(LIB) >= os.path.getmtime(SRC):
+        return LIB
+    cmd = ["g++", "-O2", "-std=c++17", "-fPIC", "-shared", "-ffp-contract=off",
+           "-fno-fast-math", "-pthread", SRC, "-o", LIB]
+    subprocess.check_call(cmd)
+    return LIB
+
+
+class _Hop(C.Structure):
+    _fields_ = [("gbps", C.c_double), ("bidir", C.c_int32), ("pad", C.c_int32)]
+
+
+class _Path(C.Structure):
+    _fields_ = [("n", C.c_int32), ("pad", C.c_int32), ("hop", _Hop * 4)]
+
+
+class _Type(C.Structure):
+    _fields_ = [("peak_flop_per_ns", C.c_double), ("hbm_bytes_per_ns", C.c_double),
+                ("eff_flop", C.c_double * 5), ("eff_mem", C.c_double * 5),
+                ("mem_bytes", C.c_int64),
+                ("gpus_per_node", C.c_int32), ("n_link_kinds", C.c_int32),
+                ("link_kind", _Path * 4),
+                ("intra_kind", (C.c_int32 * 8) * 8),
+                ("gpu_nic", _Path),
+                ("nic_gbps", C.c_double),
+                ("nic_delay_ns", C.c_int64)]
+
+
+class _Input(C.Structure):
+    _fields_ = [("n_types", C.c_int32), ("n_nodes", C.c_int32),
+                ("types", C.POINTER(_Type)), ("node_type", C.POINTER(C.c_int32)),
+                ("rail_alpha_ns", C.c_int64), ("rail_gbps", C.c_double), ("frame_bytes", C.c_int64)] + \
+               [(k, C.c_int64) for k in ("L", "h", "heads", "kv_heads", "ffn", "nm", "seq", "V",
+                                         "tied", "E", "topk", "bpe_act", "bpe_grad", "B")] + \
+               [("n_b", C.c_int32), ("bset", C.c_int32 * 8),
+                ("n_tp", C.c_int32 * 8), ("tpset", (C.c_int32 * 8) * 8),
+                ("n_p", C.c_int32), ("pset", C.c_int32 * 16),
+                ("homo", C.c_int32), ("mixed", C.c_int32), ("use_all", C.c_int32),
+                ("r_layer", C.c_int32), ("pmax", C.c_int32), ("r_batch", C.c_int32)]
+
+
+def _path(hops):
+    p = _Path()
+    p.n = len(hops)
+    for k, hp in enumerate(hops):
+        p.hop[k].gbps = hp["gbps"]
+        p.hop[k].bidir = hp["bidir"]
+    return p
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        _lib = C.CDLL(build())
+        L = _lib
+        L.orc_create.restype = C.c_void_p
+        L.orc_create.argtypes = [C.POINTER(_Input)]
+        L.orc_destroy.argtypes = [C.c_void_p]
+        for f in ("orc_space_size", "orc_n_templates"):
+            getattr(L, f).restype = C.c_int64
+            getattr(L, f).argtypes = [C.c_void_p]
+        L.orc_template_prefix.restype = C.c_int64
+        L.orc_template_prefix.argtypes = [C.c_void_p, C.c_int64]
+        L.orc_eval.restype = C.c_int64
+        L.orc_eval.argtypes = [C.c_void_p, C.c_int64]
+        L.orc_eval_many.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_void_p, C.c_int]
+        L.orc_describe.restype = C.c_int
+        L.orc_describe.argtypes = [C.c_void_p, C.c_int64, C.c_char_p, C.c_int]
+        L.orc_hop_delay_exact.restype = C.c_double
+        L.orc_hop_delay_exact.argtypes = [C.c_double, C.c_int, C.c_int64]
+        L.orc_ring_sim.restype = C.c_int64
+        L.orc_ring_sim.argtypes = [C.c_void_p, C.c_int, C.c_int]
+        L.orc_pipeline.restype = C.c_int64
+        L.orc_pipeline.argtypes = [C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]
+        L.orc_hamilton.argtypes = [C.c_int64, C.c_void_p, C.c_int, C.c_void_p]
+        L.orc_op.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                             C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
+        L.orc_link.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int,
+                               C.POINTER(C.c_int64), C.POINTER(C.c_double)]
+        L.orc_last_error.restype = C.c_char_p
+        L.orc_segment_bytes.restype = C.c_int64
+        L.orc_segment_bytes.argtypes = [C.c_void_p, C.c_int64, C.c_int, C.c_int]
+        L.orc_act_bytes.restype = C.c_int64
+        L.orc_act_bytes.argtypes = [C.c_void_p, C.c_int]
+    return _lib
+
+
+def _i64(a):
+    return np.ascontiguousarray(np.asarray(a, dtype=np.int64))
+
+
+class Oracle:
+    """The reference simulator for one workload dict (hsim_inputs.configs)."""
+
+    def __init__(self, cfg):
+        self.cfg = cfg
+        cl, md, se = cfg["cluster"], cfg["model"], cfg["search"]
+        nt = len(cl["types"])
+        self._types = (_Type * nt)()
+        for k, t in enumerate(cl["types"]):
+            T = self._types[k]
+            T.peak_flop_per_ns = t["peak_flop_per_ns"]
+            T.hbm_bytes_per_ns = t["hbm_bytes_per_ns"]
+            for q in range(5):
+                T.eff_flop[q] = t["eff_flop"][q]
+                T.eff_mem[q] = t["eff_mem"][q]
+            T.mem_bytes = t["mem_bytes"]
+            T.gpus_per_node = t["gpus_per_node"]
+            T.n_link_kinds = len(t["link_kinds"])
+            for q, hops in enumerate(t["link_kinds"]):
+                T.link_kind[q] = _path(hops)
+            for i, row in enumerate(t["intra_kind"]):
+                for j, v in enumerate(row):
+                    T.intra_kind[i][j] = v
+            T.gpu_nic = _path(t["gpu_nic"])
+            T.nic_gbps = t["nic_gbps"]
+            T.nic_delay_ns = t["nic_delay_ns"]
+        self._nodes = (C.c_int32 * len(cl["nodes"]))(*cl["nodes"])
+        I = _Input()
+        I.n_types, I.n_nodes = nt, len(cl["nodes"])
+        I.types = self._types
+        I.node_type = self._nodes
+        I.rail_alpha_ns, I.rail_gbps, I.frame_bytes = cl["rail_alpha_ns"], cl["rail_gbps"], cl["frame_bytes"]
+        for k, key in (("L", "layers"), ("h", "hidden"), ("heads", "heads"), ("kv_heads", "kv_heads"),
+                       ("ffn", "ffn"), ("nm", "mlp_mats"), ("seq", "seq"), ("V", "vocab"), ("tied", "tied"),
+                       ("E", "moe_experts"), ("topk", "moe_topk"), ("bpe_act", "bpe_act"),
+                       ("bpe_grad", "bpe_grad"), ("B", "global_batch")):
+            setattr(I, k, md[key])
+        I.n_b = len(se["bset"])
+        for q, v in enumerate(se["bset"]):
+            I.bset[q] = v
+        for t, tps in enumerate(se["tpset"]):
+            I.n_tp[t] = len(tps)
+            for q, v in enumerate(tps):
+                I.tpset[t][q] = v
+        I.n_p = len(se["pset"])
+        for q, v in enumerate(se["pset"]):
+            I.pset[q] = v
+        I.homo, I.mixed, I.use_all = se["homo"], se["mixed"], se["use_all"]
+        I.r_layer, I.pmax, I.r_batch = se["r_layer"], se["pmax_perturb"], se["r_batch"]
+        self._in = I
+        self.h = lib().orc_create(C.byref(I))
+        if not self.h:
+            raise ValueError(lib().orc_last_error().decode())
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.orc_destroy(self.h)
+            self.h = None
+
+    def space_size(self):
+        return lib().orc_space_size(self.h)
+
+    def n_templates(self):
+        return lib().orc_n_templates(self.h)
+
+    def template_prefix(self):
+        n = self.n_templates()
+        return np.array([lib().orc_template_prefix(self.h, k) for k in range(n + 1)], dtype=np.int64)
+
+    def eval(self, i):
+        return lib().orc_eval(self.h, int(i))
+
+    def eval_many(self, idx=None, first=0, n=None, threads=None):
+        threads = threads or os.cpu_count() or 1
+        if idx is not None:
+            idx = _i64(idx)
+            out = np.empty(len(idx), dtype=np.int64)
+            lib().orc_eval_many(self.h, idx.ctypes.data, 0, len(idx), out.ctypes.data, threads)
+        else:
+            out = np.empty(n, dtype=np.int64)
+            lib().orc_eval_many(self.h, None, first, n, out.ctypes.data, threads)
+        return out
+
+    def topk(self, k, threads=None):
+        """Brute force: evaluate every candidate, keep the k smallest (T, i)."""
+        n = self.space_size()
+        t = self.eval_many(first=0, n=n, threads=threads)
+        ok = np.nonzero(t >= 0)[0]
+        order = np.lexsort((ok, t[ok]))[:k]
+        return t[ok][order], ok[order].astype(np.int64)
+
+    def describe(self, i):
+        buf = C.create_string_buffer(1 << 20)
+        rc = lib().orc_describe(self.h, int(i), buf, len(buf))
+        if rc != 0:
+            raise IndexError(i)
+        return json.loads(buf.value.decode())
+
+    def op(self, type_idx, kind, bwd, tp, b):
+        f, by, d = C.c_int64(), C.c_int64(), C.c_int64()
+        lib().orc_op(self.h, type_idx, KIND.get(kind, kind), int(bwd), tp, b, C.byref(f), C.byref(by), C.byref(d))
+        return f.value, by.value, d.value
+
+    def segment_bytes(self, n_layers, has_first, has_last):
+        return lib().orc_segment_bytes(self.h, n_layers, int(has_first), int(has_last))
+
+    def act_bytes(self, b):
+        return lib().orc_act_bytes(self.h, b)
+
+    def link(self, n1, r1, n2, r2):
+        a, b = C.c_int64(), C.c_double()
+        lib().orc_link(self.h, n1, r1, n2, r2, C.byref(a), C.byref(b))
+        return a.value, b.value
+
+
+def hop_delay_exact(gbps, bidir, frame=9200):
+    return lib().orc_hop_delay_exact(gbps, int(bidir), frame)
+
+
+def ring_sim(taus, steps):
+    a = _i64(taus)
+    return lib().orc_ring_sim(a.ctypes.data, len(a), steps)
+
+
+def pipeline(f, g, c, m):
+    f, g = _i64(f), _i64(g)
+    P = len(f)
+    c = _i64(list(c) + [0]) if P > 1 else _i64([0])
+    return lib().orc_pipeline(P, m, f.ctypes.data, g.ctypes.data, c.ctypes.data)
+
+
+def hamilton(n, w):
+    w = _i64(w)
+    out = np.zeros(len(w), dtype=np.int64)
+    lib().orc_hamilton(n, w.ctypes.data, len(w), out.ctypes.data)
+    return out
