@@ -1,0 +1,305 @@
+"""Benchmark: simulated candidate configurations per second (BASELINE.json metric)
+on the hetero Llama-2-7B sweep (BASELINE config 2: 16xA100 + 16xH100,
+873,192 candidates), 1..N B200s, plus the ALU-issue roofline fraction.
+
+One step = one full sweep of the config-2 space -> global top-k (hsim_topk on
+each rank's block-cyclic shard; for N > 1 one NCCL all_gather of the k-entry
+lists and the hsim_merge_topk kernel).  Total work is fixed as N grows
+("scaling": "strong").  L2 is flushed (a 512 MiB write) between timed steps,
+outside the CUDA-event intervals.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+  torchrun --nproc-per-node N bench.py --gpus N ...
+
+--impl reference times the CPU oracle (the paper-derived reference of this
+tier) on the host cores, on a bounded sample of the same
+workload per step; rank 0 only.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import hsim_inputs as H  # noqa: E402
+
+METRIC = "simulated configs/sec, 1/2/4/8 B200, hetero Llama-7B sweep; % ALU-issue peak"
+CONFIG = 2
+TOPK = 16
+# ALU-issue roofline: 148 SMs x 4 SMSPs x 32 lanes x SM clock
+SMS, LANES_PER_SM = 148, 128
+OPS_PER_CELL = 8  # int32-equivalent ops per 1F1B max-plus cell
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=CONFIG)
+    ap.add_argument("--k", type=int, default=TOPK)
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except OSError:
+        return {}
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+class Clocks:
+    """nvidia-smi sampler during the timed region (B200_PROFILING.md clocks line)."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                                       "-lms", "100", "-i", str(self.gpu)], stdout=subprocess.PIPE,
+                                      stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        self.p.terminate()
+        out, _ = self.p.communicate(timeout=10)
+        sm, mx, reasons = [], [], set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+            except ValueError:
+                continue
+            for name, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_baseline(cfg, seconds=15.0):
+    """The oracle as it stands, on all host cores, on a seeded sample of the
+    workload sized to ~`seconds` of wall time (rank 0, N=1 only)."""
+    import oracle
+    o = oracle.Oracle(cfg)
+    cores = os.cpu_count() or 1
+    N = o.space_size()
+    cal = H.sample_indices(N, 4 * cores, seed=1)
+    t = time.perf_counter()
+    o.eval_many(cal, threads=cores)
+    rate = len(cal) / max(time.perf_counter() - t, 1e-6)
+    n = int(min(max(rate * seconds, 64), N))
+    idx = H.sample_indices(N, n, seed=H.PARITY_SEED)
+    t = time.perf_counter()
+    o.eval_many(idx, threads=cores)
+    dt = time.perf_counter() - t
+    return {"value": round(len(idx) / dt, 3), "unit": "configs/s", "cores": cores, "kind": "oracle",
+            "sample": f"{len(idx)} seeded (splitmix64 0x5EED2508) uniform candidates of the {N}-candidate "
+                      f"config-{CONFIG} space, compact event-driven oracle, {dt:.1f} s wall"}
+
+
+def run_reference(a):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    import oracle
+    cfg = H.get(a.config)
+    o = oracle.Oracle(cfg)
+    cores = os.cpu_count() or 1
+    N = o.space_size()
+    per_step = max(64, 16 * cores)  # bounded sample per step
+    times = []
+    for s in range(a.warmup + a.steps):
+        idx = H.sample_indices(N, per_step, seed=H.PARITY_SEED + s)
+        t = time.perf_counter()
+        o.eval_many(idx, threads=cores)
+        dt = time.perf_counter() - t
+        if s >= a.warmup:
+            times.append((len(idx), dt))
+    cands = sum(c for c, _ in times)
+    tot = sum(d for _, d in times)
+    v = cands / tot
+    line = {"metric": METRIC, "value": round(v, 3), "unit": "configs/s", "n_gpus": a.gpus, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": round(1e3 * tot / a.steps, 3), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "int64", "data": "synthetic", "impl": "reference",
+            "config": {"workload": cfg["name"], "n_candidates": N,
+                       "sample_per_step": per_step, "what": "CPU oracle (oracle/oracle.cpp) on host cores"},
+            "cpu_baseline": {"value": round(v, 3), "unit": "configs/s", "cores": cores, "kind": "oracle",
+                             "sample": f"{per_step} seeded candidates per step x {a.steps} steps"},
+            "e2e": {"value": round(v, 3), "unit": "configs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(a):
+    import torch
+    import torch.distributed as dist
+    from paper_2508_05370_b200 import Sim, build as pbuild
+    from paper_2508_05370_b200.sweep import shard, sweep
+
+    rank, world, local = dist_env()
+    assert world == a.gpus or world == 1, "launch with torchrun --nproc-per-node N for --gpus N > 1"
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if rank == 0:
+        pbuild.build()
+    if world > 1:
+        dist.barrier()
+    cfg = H.get(a.config)
+    sim = Sim(cfg)
+    N = sim.space_size()
+    first, n, blk, stride = shard(N, rank, world)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    out = (torch.empty(a.k, dtype=torch.int64, device=dev), torch.empty(a.k, dtype=torch.int64, device=dev))
+
+    def step():
+        return sweep(sim, a.k, out=out)
+
+    for _ in range(a.warmup):
+        step()
+    torch.cuda.synchronize()
+    # algorithmic work of this rank's shard: exact 1F1B cell count
+    if world == 1:
+        cells = sim.count_cells(0, N)
+    else:
+        cells = 0
+        for b0 in range(first, N, stride):
+            cells += sim.count_cells(b0, min(blk, N - b0))
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(a.steps)]
+    clocks = Clocks(local if world > 1 else int(os.environ.get("CUDA_VISIBLE_DEVICES", "0").split(",")[0] or 0))
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    time.sleep(0.3)
+    for s in range(a.steps):
+        flush.fill_(s & 0xFF)          # L2 flush between timed steps (not inside the events)
+        evs[s][0].record(stream)
+        step()
+        evs[s][1].record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    ms = [e0.elapsed_time(e1) for e0, e1 in evs]
+    tot_ms = sum(ms)
+    t_max = torch.tensor([tot_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
+    tot_ms = float(t_max.item())
+    launches_per_step = sim.last_launch_count() + (1 if world > 1 else 0)
+    value = N * a.steps / (tot_ms / 1e3)
+
+    # roofline of the dominant kernel (k_eval; K3 merge included in the interval)
+    pk = peaks()
+    sm_max = float(pk.get("sm_max_mhz", 1965.0))
+    peak_gops = SMS * LANES_PER_SM * sm_max * 1e6 / 1e9
+    my_ms = sum(ms) / a.steps
+    achieved = OPS_PER_CELL * cells / (my_ms / 1e3) / 1e9
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if os.path.exists(prof):
+        try:
+            with open(prof) as f:
+                traffic = json.load(f).get("k_eval_dram_bytes_per_launch")
+        except (OSError, ValueError):
+            traffic = None
+
+    # e2e: explicit candidate list from pinned host memory -> eval -> results back to pinned host
+    e2e = None
+    if not a.no_e2e:
+        idx_host = torch.arange(first, first + n, dtype=torch.int64) if world == 1 else \
+            torch.tensor([first + (t // blk) * stride + t % blk for t in range(n)], dtype=torch.int64)
+        idx_host = idx_host.pin_memory()
+        res_host = torch.empty(n, dtype=torch.int64).pin_memory()
+        idx_dev = torch.empty(n, dtype=torch.int64, device=dev)
+        res_dev = torch.empty(n, dtype=torch.int64, device=dev)
+        e_steps = max(3, min(a.steps, 50))
+        for s in range(3):
+            idx_dev.copy_(idx_host, non_blocking=True)
+            sim.eval_batch(idx=idx_dev, out=res_dev)
+            res_host.copy_(res_dev, non_blocking=True)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if world > 1:
+            dist.barrier()
+        e0.record(stream)
+        for s in range(e_steps):
+            idx_dev.copy_(idx_host, non_blocking=True)
+            sim.eval_batch(idx=idx_dev, out=res_dev)
+            res_host.copy_(res_dev, non_blocking=True)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        et = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(et, op=dist.ReduceOp.MAX)
+        e2e = {"value": round(N * e_steps / (float(et.item()) / 1e3), 1), "unit": "configs/s",
+               "h2d_bytes_per_step": 8 * N, "d2h_bytes_per_step": 8 * N,
+               "what": "hsim_eval_batch on an explicit index list: H2D of the indices from pinned host, "
+                       "int64 results D2H to pinned host, every step"}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": round(value, 1), "unit": "configs/s", "n_gpus": world, "steps": a.steps,
+                "warmup": a.warmup, "ms_per_step": round(tot_ms / a.steps, 4), "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+                "config": {"workload": cfg["name"], "n_candidates": N, "k": a.k,
+                           "step": "full sweep -> global top-k",
+                           "l2": "flushed between timed steps (512 MiB write, outside the event intervals)",
+                           "parallelism": f"block-cyclic shard x{world}" + (" + NCCL all_gather" if world > 1 else "")},
+                "roofline": {"bound": "alu", "achieved": round(achieved, 1), "peak": round(peak_gops, 1),
+                             "unit": "Gop/s", "frac": round(achieved / peak_gops, 4), "traffic": traffic,
+                             "kernel": "k_eval (+k_merge in the same interval)",
+                             "ops_per_launch": OPS_PER_CELL * cells, "cells_per_launch": cells,
+                             "peak_from": f"{SMS} SMs x {LANES_PER_SM} lanes x {sm_max:.0f} MHz (issue slots)"},
+                "gpu_launches": launches_per_step * a.steps,
+                "clocks": clk}
+        if e2e:
+            line["e2e"] = e2e
+        if world == 1 and not a.no_cpu:
+            line["cpu_baseline"] = cpu_baseline(cfg)
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,187 @@
+/*
+ * hsim.h — C ABI of the B200-native batched evaluator of the heterogeneity-
+ * aware LLM-training simulator of arXiv 2508.05370.
+ *
+ * The library evaluates millions of candidate mappings of one model onto one
+ * heterogeneous cluster.  A candidate = device groups + TP/PP/DP degrees +
+ * non-uniform layer / micro-batch split + placement (§3
+ * "Device grouping", "Non-uniform workload partitioning"
+ * §4 "Input Description [A1, A2]").  For each it predicts one training-
+ * iteration time in int64 nanoseconds ("predicting training
+ * time") through the five steps of DESIGN.md §1:
+ *   (1) partition, (2) per-layer roofline cost, (3) TP / PP-p2p / gradient-
+ *   sync alpha-beta collective costs incl. resharding,
+ *   (4) 1F1B max-plus schedule, (5) max over DP groups + sync, top-k.
+ * The space, the placement rule and every formula are defined in DESIGN.md
+ * §2 (readings C.0-C.8, A1-A24); results are bit-exact to the CPU oracle.
+ *
+ * Conventions
+ *   - All structs are POD, little-endian, caller-owned; hsim_create deep-copies
+ *     them.  No pointer passed to hsim_create is retained.
+ *   - Device buffers (out_ns, out_t_ns, out_idx, cands.idx) are caller-owned
+ *     CUDA device memory; `stream` is a cudaStream_t passed as void* (0 = the
+ *     legacy default stream).  hsim_eval_batch / hsim_topk only enqueue work;
+ *     launch errors return HSIM_ECUDA, asynchronous faults surface at the
+ *     caller's next synchronisation.
+ *   - A handle may be used by one host thread at a time (it owns scratch).
+ *   - Errors: a non-zero hsim_status; hsim_last_error() (thread-local) holds a
+ *     one-line message naming the SPEC.md error kind where one applies
+ *     (MissingField / InvalidValue / DivisibilityViolation, SPEC.md:63;
+ *     UnknownGpuType / RailMismatch; NonPositiveBandwidth,
+ *     SPEC.md:335).
+ *   - Per-candidate status is in-band in the int64 result: >= 0 iteration time
+ *     in ns; -1 a stage received < 1 layer; -2 a replica received < 1
+ *     micro-batch; (-3 reserved: memory feasibility, DESIGN.md §8 NEXT).
+ */
+#ifndef HSIM_H
+#define HSIM_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  HSIM_OK = 0,
+  HSIM_EINVAL = 1, /* invalid descriptor / argument                          */
+  HSIM_ENOMEM = 2, /* host or device allocation failed                        */
+  HSIM_ECUDA = 3,  /* CUDA launch / copy failed                               */
+  HSIM_ERANGE = 4, /* numerator >= 2^53, overflow, index out of range, too big */
+  HSIM_ESTATE = 5  /* NULL / destroyed handle                                 */
+} hsim_status;
+
+/* layer-op kinds: index of eff_flop / eff_mem */
+enum { HSIM_KIND_ATTN = 0, HSIM_KIND_MLP = 1, HSIM_KIND_MOE = 2, HSIM_KIND_EMB = 3, HSIM_KIND_HEAD = 4, HSIM_NKIND = 5 };
+
+#define HSIM_MAX_TYPES 4
+#define HSIM_MAX_GPUS_PER_NODE 8
+#define HSIM_MAX_HOPS 4
+#define HSIM_MAX_LINK_KINDS 4
+
+/* One hop of an interconnect path, as Table 4 lists it:
+ * a bandwidth in Gbps, bidirectional aggregate (NVLink, PCIe columns) or
+ * per direction (NIC).  Its delay is frame*8/uni-dir Gbps. */
+typedef struct { double gbps; int32_t bidir; int32_t _pad; } hsim_hop;
+
+/* A fixed path of 1..4 hops (e.g. GPU->NVSwitch->GPU = 2 NVLink hops;
+ * GPU->PCIe switch->NIC = 2 PCIe trips). */
+typedef struct { int32_t n_hops; int32_t _pad; hsim_hop hops[HSIM_MAX_HOPS]; } hsim_path;
+
+/* One GPU type and the node type that hosts it (one node type per GPU type):
+ * compute (peak x efficiency roofline) + the Table 4 interconnect row. */
+typedef struct {
+  char name[16];
+  double peak_flop_per_ns;          /* dense peak, FLOP/ns (= TFLOP/s x 1000)        */
+  double hbm_bytes_per_ns;          /* HBM bandwidth, B/ns (= GB/s)                   */
+  double eff_flop[HSIM_NKIND];      /* achieved fraction per layer kind, (0, 1]       */
+  double eff_mem[HSIM_NKIND];
+  int64_t mem_bytes;                /* capacity (reserved for memory pruning)         */
+  int32_t gpus_per_node;            /* 1, 2, 4 or 8; == NICs per node (rail-only)     */
+  int32_t n_link_kinds;             /* 1..4                                           */
+  hsim_path link_kinds[HSIM_MAX_LINK_KINDS];
+  int8_t intra_kind[HSIM_MAX_GPUS_PER_NODE][HSIM_MAX_GPUS_PER_NODE]; /* GPU i->j path kind; diagonal ignored */
+  hsim_path gpu_nic;                /* GPU -> its rail NIC                            */
+  double nic_gbps;                  /* NIC bandwidth per direction                    */
+  int64_t nic_delay_ns;             /* NIC processing delay (Table 4 column)          */
+} hsim_device_type;
+
+/* Cluster / topology description (PAPER.md:299 (3); rail-only, Fig 2). */
+typedef struct {
+  int32_t n_device_types;           /* 1..HSIM_MAX_TYPES                              */
+  int32_t n_nodes;                  /* 1..4096; node id order = placement order       */
+  const hsim_device_type* device_types;
+  const int32_t* node_type_of;      /* [n_nodes] device-type index per node           */
+  int64_t rail_alpha_ns;            /* rail switch hop latency (>= 0)                 */
+  double rail_gbps;                 /* rail switch port rate per direction (> 0)      */
+  int64_t frame_bytes;              /* jumbo frame for the delay formula (9200)       */
+} hsim_cluster_desc;
+
+/* Model description (Table 5 row) + framework search space
+ * (PAPER.md:299 (2), explored per PAPER.md:183 "all possible combinations"). */
+typedef struct {
+  int32_t layers, hidden, heads, kv_heads, ffn, mlp_mats /* 2 GELU, 3 SwiGLU */, seq, vocab, tied;
+  int32_t moe_experts /* 1 = dense */, moe_topk;
+  int32_t bpe_act /* bytes per activation / weight element, e.g. 2 */, bpe_grad /* e.g. 4 */;
+  int64_t global_batch;
+  /* search space (DESIGN.md C.2): */
+  int32_t n_bset; int32_t bset[8];            /* micro-batch sizes                            */
+  int32_t tpset_mask[HSIM_MAX_TYPES];         /* per type: bit k => TP = 2^k allowed (k <= 3) */
+  int32_t n_pset; int32_t pset[16];           /* pipeline depths                              */
+  int32_t homo, mixed;                        /* families: type-homogeneous / mixed pipelines */
+  int32_t use_all;                            /* every used type fully used                   */
+  int32_t r_layer, pmax_perturb, r_batch;     /* perturbation radii / max perturbed depth     */
+} hsim_model_desc;
+
+/* Which candidates the t-th work item (t = 0..n-1) evaluates. */
+typedef struct {
+  const int64_t* idx;  /* != NULL: i = idx[t] (device pointer; explicit list)                   */
+  int64_t first;       /* idx == NULL, block == 0: i = first + t (contiguous range)               */
+  int64_t block;       /* idx == NULL, block > 0:  i = first + (t / block) * stride + (t % block) */
+  int64_t stride;      /*   (block-cyclic shard across GPUs)                                      */
+} hsim_cands;
+
+typedef struct hsim_handle hsim_handle;
+
+/* Validates the descriptors, derives per-op durations and link classes, builds
+ * the candidate-template tables on the host and copies them to the current
+ * CUDA device.  On error *out = NULL and a message is set.
+ * Returns HSIM_EINVAL (bad descriptor), HSIM_ERANGE (a numerator >= 2^53, too
+ * many link classes / stages), HSIM_ENOMEM, HSIM_ECUDA. */
+int hsim_create(const hsim_cluster_desc* cluster, const hsim_model_desc* model, hsim_handle** out);
+
+/* Frees host and device memory.  NULL is a no-op. */
+void hsim_destroy(hsim_handle* h);
+
+/* N = number of candidates (linear indices 0..N-1), or -1 for a NULL handle. */
+int64_t hsim_space_size(const hsim_handle* h);
+
+/* Number of templates, and the first candidate index of template k
+ * (k == n_templates returns N); -1 if out of range.  Host only. */
+int64_t hsim_n_templates(const hsim_handle* h);
+int64_t hsim_template_first(const hsim_handle* h, int64_t k);
+
+/* Host-side explicit plan of candidate i as a JSON object (template, b,
+ * per-class stages (type, tp), layer split, micro-batches per replica,
+ * placement, status).  Writes at most cap bytes incl. NUL.
+ * HSIM_ERANGE if i is out of range or cap is too small. */
+int hsim_decode(const hsim_handle* h, int64_t i, char* json, size_t cap);
+
+/* Enqueues the evaluation of n candidates (see hsim_cands) on `stream`;
+ * writes out_ns[t] (device, n int64) = iteration time or a negative status.
+ * out_ns may be NULL (then nothing is written; useful for timing only).
+ * Indices >= N yield HSIM_ERANGE at enqueue time for range mode; for explicit
+ * lists they are written as INT64_MIN. n == 0 is a no-op. */
+int hsim_eval_batch(hsim_handle* h, const hsim_cands* cands, int64_t n, int64_t* out_ns, void* stream);
+
+/* Enqueues the evaluation of n candidates and the selection of the k
+ * smallest valid results ordered by (time asc, index asc) (DESIGN.md C.8);
+ * writes out_t_ns[0..k) and out_idx[0..k) (device); unused slots are
+ * (INT64_MAX, -1).  1 <= k <= 1024.  Optionally also writes out_ns if not
+ * NULL. */
+int hsim_topk(hsim_handle* h, const hsim_cands* cands, int64_t n, int32_t k,
+              int64_t* out_t_ns, int64_t* out_idx, int64_t* out_ns, void* stream);
+
+/* Merges nlists top-k lists (device; list l at lists + l*2k holds k times then
+ * k indices, each list sorted by (time, index), padded with (INT64_MAX, -1) —
+ * the layout of an all_gather of [out_t_ns | out_idx] across ranks) into the
+ * global top-k (out_t_ns, out_idx, device).  Used by the multi-GPU sweep after
+ * the NCCL all_gather.  1 <= k <= 1024, nlists >= 0. */
+int hsim_merge_topk(const int64_t* lists, int32_t nlists, int32_t k, int64_t* out_t_ns, int64_t* out_idx, void* stream);
+
+/* Number of device kernels the last hsim_eval_batch / hsim_topk call launched. */
+int32_t hsim_last_launch_count(const hsim_handle* h);
+
+/* Algorithmic work counters of candidate list (host, exact): sum over the
+ * candidates of 1F1B cells (2 * P_u * m_u per simulated pipeline) — used for
+ * the ALU-roofline fraction.  Returns -1 on error. */
+int64_t hsim_count_cells(const hsim_handle* h, int64_t first, int64_t n);
+
+/* Message of the last failing call on this thread ("" if none). */
+const char* hsim_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HSIM_H */

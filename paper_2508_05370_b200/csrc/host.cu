@@ -1,0 +1,774 @@
+// host.cu — C-ABI host side of libhsim (include/hsim.h).
+//
+// hsim_create validates the three descriptions, derives
+// link delays from Table-4-style fields, per-op roofline
+// durations (DESIGN.md C.5), enumerates the candidate templates (C.2), places
+// each class (C.3), derives its base layer split, p2p costs, sub-classes and
+// link-class masks (C.4, C.6, A13), and uploads everything to the device.  The
+// per-candidate work (decode digits, partition, stage sums, 1F1B, sync,
+// top-k) runs only in the CUDA kernels (kernels.cu).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "hsim.h"
+#include "hsim_core.cuh"
+
+using namespace hsim;
+
+namespace {
+thread_local std::string g_err;
+
+struct Fail {
+  int code;
+  std::string msg;
+};
+[[noreturn]] void fail(int code, const std::string& m) { throw Fail{code, m}; }
+
+constexpr i64 TWO53 = (i64)1 << 53;
+
+double uni(const hsim_hop& h) { return h.bidir ? h.gbps / 2.0 : h.gbps; }
+
+// alpha = sum of per-hop ceil(frame*8 / uni Gbps) (A9); beta = slowest hop, B/ns
+Link path_link(const hsim_path& p, i64 frame) {
+  Link l{0, 1e300};
+  for (int k = 0; k < p.n_hops; ++k) {
+    const double u = uni(p.hops[k]);
+    l.alpha += ceilq(frame * 8, u);
+    l.beta = std::min(l.beta, u / 8.0);
+  }
+  return l;
+}
+Link cat(const Link& a, const Link& b) { return Link{a.alpha + b.alpha, std::min(a.beta, b.beta)}; }
+i64 tau(const Link& e, i64 x) { return e.alpha + ceilq(x, e.beta); }
+
+i64 hamilton_floor_rem(i64 n, i64 w, i64 W, i64* rem) {
+  *rem = n * w % W;
+  return n * w / W;
+}
+
+}  // namespace
+
+struct hsim_handle {
+  // copies of the descriptions
+  hsim_cluster_desc cd{};
+  hsim_model_desc md{};
+  std::vector<hsim_device_type> types;
+  std::vector<int32_t> node_type;
+  int nt = 0;
+  // derived (host)
+  Link intra[MAXT][MAXG][MAXG];
+  Link rail[MAXT][MAXT];
+  std::map<std::pair<i64, u64>, int> lc_id;
+  std::vector<Link> lcs;
+  std::vector<int> bs;                         // sorted micro-batch sizes
+  // durations [type][lg tp][b index]
+  struct Dur { i64 attn_f, attn_b, mlp_f, mlp_b, emb_f, emb_b, head_f, head_b, ar, a2a; bool ok; };
+  std::vector<Dur> dur;
+  Dur& dur_at(int t, int lg, int bi) { return dur[((size_t)t * 4 + lg) * bs.size() + bi]; }
+  u64 tp_mask[MAXT][4];
+  // templates
+  std::vector<i64> prefix;
+  std::vector<TplRec> tpl;
+  std::vector<i64> pool;
+  std::map<std::vector<int>, int32_t> crec_of;
+  std::vector<std::vector<int>> nodes_of_type;
+  i64 n_of_type[MAXT] = {0, 0, 0, 0};
+  i64 N = 0;
+  Tables hT{};  // host pointers (for hsim_decode)
+  // device
+  Tables* dT = nullptr;
+  i64* d_prefix = nullptr;
+  TplRec* d_tpl = nullptr;
+  i64* d_pool = nullptr;
+  int8_t* d_node_type = nullptr;
+  std::vector<int8_t> node_type8;
+  // top-k scratch
+  i64* d_blk = nullptr;
+  size_t blk_cap = 0;
+  i64* d_cells = nullptr;
+  int32_t last_launches = 0;
+  int sm_count = 148;
+
+  Link link(int n1, int r1, int n2, int r2) const {
+    const int t1 = node_type[n1], t2 = node_type[n2];
+    if (n1 == n2) return intra[t1][r1][r2];
+    if (r1 == r2) return rail[t1][t2];               // Fig 2 (b)
+    return cat(intra[t1][r1][r2], rail[t1][t2]);     // Fig 2 (c): NVLink hop at the source first
+  }
+  int lc(const Link& l) {
+    u64 bits;
+    std::memcpy(&bits, &l.beta, 8);
+    auto key = std::make_pair(l.alpha, bits);
+    auto it = lc_id.find(key);
+    if (it != lc_id.end()) return it->second;
+    if ((int)lcs.size() >= MAXLC) fail(HSIM_ERANGE, "more than 64 distinct link classes");
+    int id = (int)lcs.size();
+    lc_id[key] = id;
+    lcs.push_back(l);
+    return id;
+  }
+
+  void validate();
+  void derive_links();
+  void derive_durations();
+  void enumerate();
+  int32_t crec(int b_idx, int M, int D, const std::vector<std::pair<int, int>>& stages);
+  std::vector<std::vector<std::pair<int, int>>> place(int D, const std::vector<std::pair<int, int>>& stages) const;
+  void prepare();
+  void upload();
+  int ensure_device() {
+    if (dT) return HSIM_OK;
+    try {
+      upload();
+    } catch (const Fail& f) {
+      g_err = f.msg;
+      return f.code;
+    }
+    return HSIM_OK;
+  }
+};
+
+// ------------------------------------------------------------------------------
+void hsim_handle::validate() {
+  const hsim_cluster_desc& c = cd;
+  const hsim_model_desc& m = md;
+  if (c.n_device_types < 1 || c.n_device_types > MAXT) fail(HSIM_EINVAL, "InvalidValue: n_device_types must be 1..4");
+  if (c.n_nodes < 1 || c.n_nodes > 4096) fail(HSIM_EINVAL, "InvalidValue: n_nodes must be 1..4096");
+  if (!c.device_types || !c.node_type_of) fail(HSIM_EINVAL, "MissingField: device_types / node_type_of");
+  if (c.frame_bytes < 1 || c.rail_alpha_ns < 0) fail(HSIM_EINVAL, "InvalidValue: frame_bytes / rail_alpha_ns");
+  if (!(c.rail_gbps > 0)) fail(HSIM_EINVAL, "NonPositiveBandwidth: rail_gbps");
+  for (int t = 0; t < c.n_device_types; ++t) {
+    const hsim_device_type& d = c.device_types[t];
+    const int g = d.gpus_per_node;
+    if (g != 1 && g != 2 && g != 4 && g != 8) fail(HSIM_EINVAL, "RailMismatch: gpus_per_node must be 1, 2, 4 or 8");
+    if (!(d.peak_flop_per_ns > 0) || !(d.hbm_bytes_per_ns > 0)) fail(HSIM_EINVAL, "InvalidValue: non-positive peak");
+    for (int k = 0; k < HSIM_NKIND; ++k)
+      if (!(d.eff_flop[k] > 0 && d.eff_flop[k] <= 1) || !(d.eff_mem[k] > 0 && d.eff_mem[k] <= 1))
+        fail(HSIM_EINVAL, "InvalidValue: efficiency must be in (0, 1]");
+    if (d.n_link_kinds < 1 || d.n_link_kinds > HSIM_MAX_LINK_KINDS) fail(HSIM_EINVAL, "InvalidValue: n_link_kinds");
+    auto check_path = [&](const hsim_path& p, bool allow_empty) {
+      if (p.n_hops < (allow_empty ? 0 : 1) || p.n_hops > HSIM_MAX_HOPS) fail(HSIM_EINVAL, "InvalidValue: path hop count");
+      for (int k = 0; k < p.n_hops; ++k)
+        if (!(p.hops[k].gbps > 0)) fail(HSIM_EINVAL, "NonPositiveBandwidth: hop gbps");
+    };
+    for (int k = 0; k < d.n_link_kinds; ++k) check_path(d.link_kinds[k], false);
+    check_path(d.gpu_nic, true);
+    if (!(d.nic_gbps > 0)) fail(HSIM_EINVAL, "NonPositiveBandwidth: nic_gbps");
+    if (d.nic_delay_ns < 0) fail(HSIM_EINVAL, "InvalidValue: nic_delay_ns");
+    for (int i = 0; i < g; ++i)
+      for (int j = 0; j < g; ++j)
+        if (i != j && (d.intra_kind[i][j] < 0 || d.intra_kind[i][j] >= d.n_link_kinds))
+          fail(HSIM_EINVAL, "InvalidValue: intra_kind out of range");
+  }
+  for (int t = 1; t < c.n_device_types; ++t)
+    if (c.device_types[t].gpus_per_node != c.device_types[0].gpus_per_node)
+      fail(HSIM_EINVAL, "RailMismatch: every node type must have the same GPUs (= NICs) per node");
+  for (int n = 0; n < c.n_nodes; ++n)
+    if (c.node_type_of[n] < 0 || c.node_type_of[n] >= c.n_device_types) fail(HSIM_EINVAL, "UnknownGpuType: node_type_of");
+  if (m.layers < 1 || m.hidden < 1 || m.heads < 1 || m.kv_heads < 1 || m.ffn < 1 || m.seq < 1 || m.vocab < 1 ||
+      m.mlp_mats < 1 || m.moe_experts < 1 || m.moe_topk < 1 || m.bpe_act < 1 || m.bpe_grad < 1 || m.global_batch < 1)
+    fail(HSIM_EINVAL, "InvalidValue: model counts must be >= 1");
+  if (m.hidden % m.heads) fail(HSIM_EINVAL, "DivisibilityViolation: hidden % heads");
+  if (m.heads % m.kv_heads) fail(HSIM_EINVAL, "DivisibilityViolation: heads % kv_heads");
+  if (m.moe_topk > m.moe_experts) fail(HSIM_EINVAL, "InvalidValue: moe_topk > moe_experts");
+  if (m.global_batch > (1 << 22)) fail(HSIM_ERANGE, "global_batch > 2^22");
+  if (m.n_bset < 1 || m.n_bset > 8 || m.n_pset < 1 || m.n_pset > 16) fail(HSIM_EINVAL, "InvalidValue: bset / pset sizes");
+  for (int k = 0; k < m.n_bset; ++k)
+    if (m.bset[k] < 1) fail(HSIM_EINVAL, "InvalidValue: bset");
+  for (int k = 0; k < m.n_pset; ++k)
+    if (m.pset[k] < 1 || m.pset[k] > MAXP) fail(HSIM_EINVAL, "InvalidValue: pset entries must be 1..64");
+  for (int t = 0; t < c.n_device_types; ++t)
+    if (m.tpset_mask[t] & ~0xF) fail(HSIM_EINVAL, "InvalidValue: tpset_mask allows TP 1, 2, 4, 8 only");
+  if (m.r_layer < 0 || m.r_batch < 0 || m.r_layer > 8 || m.r_batch > 8) fail(HSIM_EINVAL, "InvalidValue: radii");
+  if (m.homo && c.n_device_types > MAXC) fail(HSIM_EINVAL, "InvalidValue: too many classes");
+}
+
+void hsim_handle::derive_links() {
+  const i64 fr = cd.frame_bytes;
+  for (int t = 0; t < nt; ++t) {
+    const hsim_device_type& d = types[t];
+    for (int i = 0; i < d.gpus_per_node; ++i)
+      for (int j = 0; j < d.gpus_per_node; ++j)
+        intra[t][i][j] = i == j ? Link{0, 1e300} : path_link(d.link_kinds[(int)d.intra_kind[i][j]], fr);
+  }
+  for (int a = 0; a < nt; ++a)
+    for (int b = 0; b < nt; ++b) {
+      Link l = path_link(types[a].gpu_nic, fr);
+      l = cat(l, Link{types[a].nic_delay_ns, types[a].nic_gbps / 8.0});
+      l = cat(l, Link{cd.rail_alpha_ns, cd.rail_gbps / 8.0});
+      l = cat(l, Link{types[b].nic_delay_ns, types[b].nic_gbps / 8.0});
+      l = cat(l, path_link(types[b].gpu_nic, fr));
+      rail[a][b] = l;
+    }
+  // every link the kernels may meet gets a class id
+  std::memset(hT.lc_same, 0, sizeof(hT.lc_same));
+  std::memset(hT.lc_cross, 0, sizeof(hT.lc_cross));
+  for (int t = 0; t < nt; ++t)
+    for (int i = 0; i < types[t].gpus_per_node; ++i)
+      for (int j = 0; j < types[t].gpus_per_node; ++j)
+        if (i != j) hT.lc_same[t][i][j] = (int8_t)lc(intra[t][i][j]);
+  for (int a = 0; a < nt; ++a)
+    for (int i = 0; i < types[a].gpus_per_node; ++i)
+      for (int b = 0; b < nt; ++b)
+        for (int j = 0; j < types[b].gpus_per_node; ++j) {
+          Link l = i == j ? rail[a][b] : cat(intra[a][i][j], rail[a][b]);
+          hT.lc_cross[a][i][b][j] = (int8_t)lc(l);
+        }
+  // translation invariance of every allowed TP group (A13): same link between
+  // (k*tp + x) and (k*tp + y) for every block k
+  for (int t = 0; t < nt; ++t) {
+    const int g = types[t].gpus_per_node;
+    for (int lg = 0; lg < 4; ++lg) {
+      const int tp = 1 << lg;
+      tp_mask[t][lg] = 0;
+      if (!(md.tpset_mask[t] >> lg & 1) || g % tp) continue;
+      for (int k = 1; k * tp < g; ++k)
+        for (int x = 0; x < tp; ++x)
+          for (int y = 0; y < tp; ++y)
+            if (x != y) {
+              const Link& a0 = intra[t][x][y];
+              const Link& ak = intra[t][k * tp + x][k * tp + y];
+              if (a0.alpha != ak.alpha || a0.beta != ak.beta)
+                fail(HSIM_EINVAL, "InvalidValue: intra-node links not invariant under tp-aligned translation");
+            }
+      for (int q = 0; q < tp && tp > 1; ++q) tp_mask[t][lg] |= (u64)1 << lc(intra[t][q][(q + 1) % tp]);
+    }
+  }
+}
+
+void hsim_handle::derive_durations() {
+  const i64 h = md.hidden, s = md.seq, V = md.vocab, f = md.ffn, nm = md.mlp_mats;
+  const i64 hkv = (i64)md.kv_heads * h / md.heads;
+  const i64 bpe = md.bpe_act, E = md.moe_experts, k = md.moe_topk;
+  dur.assign((size_t)nt * 4 * bs.size(), Dur{});
+  for (int t = 0; t < nt; ++t)
+    for (int lg = 0; lg < 4; ++lg) {
+      const i64 tp = 1 << lg;
+      if (!(md.tpset_mask[t] >> lg & 1)) continue;
+      if (types[t].gpus_per_node % tp || md.heads % tp || md.kv_heads % tp) continue;
+      for (size_t bi = 0; bi < bs.size(); ++bi) {
+        const i64 b = bs[bi], T = b * s;
+        const hsim_device_type& ty = types[t];
+        // (FLOP, bytes) per device, forward (DESIGN.md C.5)
+        i64 fl[5], by[5];
+        fl[HSIM_KIND_ATTN] = ceil_div(2 * T * h * (2 * h + 2 * hkv) + 4 * b * s * s * h, tp);
+        by[HSIM_KIND_ATTN] = ceil_div(bpe * h * (2 * h + 2 * hkv), tp) + 2 * T * h * bpe;
+        fl[HSIM_KIND_MLP] = ceil_div(2 * T * nm * h * f, tp);
+        by[HSIM_KIND_MLP] = ceil_div(bpe * nm * h * f, tp) + 2 * T * h * bpe;
+        fl[HSIM_KIND_MOE] = ceil_div(2 * T * k * nm * h * f, tp);
+        by[HSIM_KIND_MOE] = ceil_div(bpe * E * nm * h * f, tp) + 2 * T * h * bpe;
+        fl[HSIM_KIND_EMB] = 0;
+        by[HSIM_KIND_EMB] = 2 * T * h * bpe;
+        fl[HSIM_KIND_HEAD] = ceil_div(2 * T * h * V, tp);
+        by[HSIM_KIND_HEAD] = ceil_div(bpe * V * h, tp) + T * h * bpe + ceil_div(T * V * bpe, tp);
+        i64 dfw[5], dbw[5];
+        for (int q = 0; q < 5; ++q) {
+          if (2 * fl[q] >= TWO53 || 2 * by[q] >= TWO53) fail(HSIM_ERANGE, "a FLOP / byte numerator reaches 2^53");
+          const double rf = ty.peak_flop_per_ns * ty.eff_flop[q];
+          const double rm = ty.hbm_bytes_per_ns * ty.eff_mem[q];
+          dfw[q] = std::max(ceilq(fl[q], rf), ceilq(by[q], rm));
+          dbw[q] = std::max(ceilq(2 * fl[q], rf), ceilq(2 * by[q], rm));  // own rounding (A6)
+        }
+        Dur& d = dur_at(t, lg, bi);
+        d.ok = true;
+        const int mk = E > 1 ? HSIM_KIND_MOE : HSIM_KIND_MLP;
+        d.attn_f = dfw[HSIM_KIND_ATTN]; d.attn_b = dbw[HSIM_KIND_ATTN];
+        d.mlp_f = dfw[mk]; d.mlp_b = dbw[mk];
+        d.emb_f = dfw[HSIM_KIND_EMB]; d.emb_b = dbw[HSIM_KIND_EMB];
+        d.head_f = dfw[HSIM_KIND_HEAD]; d.head_b = dbw[HSIM_KIND_HEAD];
+        // TP all-reduce 2(t-1) * max over ring edges; EP all-to-all (t-1) * max over pairs (A16, A17)
+        const i64 A = b * s * h * bpe;
+        d.ar = 0; d.a2a = 0;
+        if (tp > 1) {
+          i64 mx = 0;
+          for (int q = 0; q < tp; ++q) mx = std::max(mx, tau(intra[t][q][(q + 1) % tp], ceil_div(A, tp)));
+          d.ar = 2 * (tp - 1) * mx;
+          if (E > 1) {
+            i64 my = 0;
+            for (int x = 0; x < tp; ++x)
+              for (int y = 0; y < tp; ++y)
+                if (x != y) my = std::max(my, tau(intra[t][x][y], ceil_div(A * k, tp * tp)));
+            d.a2a = (tp - 1) * my;
+          }
+        }
+      }
+    }
+}
+
+// C.3: class alone on a fresh cluster (classes of one template use disjoint
+// device types, so their placements do not interact): replica-major,
+// stage-major; lowest-id node of the stage's type with a free tp-aligned block.
+std::vector<std::vector<std::pair<int, int>>> hsim_handle::place(int D, const std::vector<std::pair<int, int>>& stages) const {
+  std::vector<std::vector<char>> used(cd.n_nodes);
+  for (int n = 0; n < cd.n_nodes; ++n) used[n].assign(types[node_type[n]].gpus_per_node, 0);
+  std::vector<std::vector<std::pair<int, int>>> out(D);
+  for (int r = 0; r < D; ++r)
+    for (const auto& st : stages) {
+      const int t = st.first, tp = st.second;
+      bool ok = false;
+      for (size_t ni = 0; ni < nodes_of_type[t].size() && !ok; ++ni) {
+        const int n = nodes_of_type[t][ni];
+        const int g = types[t].gpus_per_node;
+        for (int base = 0; base + tp <= g && !ok; base += tp) {
+          bool fr = true;
+          for (int q = 0; q < tp; ++q) fr = fr && !used[n][base + q];
+          if (fr) {
+            for (int q = 0; q < tp; ++q) used[n][base + q] = 1;
+            out[r].push_back({n, base});
+            ok = true;
+          }
+        }
+      }
+      if (!ok) fail(HSIM_EINVAL, "InsufficientDevices: placement failed");
+    }
+  return out;
+}
+
+// class record: (b, D, stages) -> offset of the record in the pool
+int32_t hsim_handle::crec(int bi, int M, int D, const std::vector<std::pair<int, int>>& stages) {
+  std::vector<int> key{bi, D};
+  for (auto& s : stages) { key.push_back(s.first); key.push_back(s.second); }
+  auto it = crec_of.find(key);
+  if (it != crec_of.end()) return it->second;
+  (void)M;
+  const int P = (int)stages.size();
+  const i64 b = bs[bi];
+  std::vector<StageRec> sr(P);
+  std::vector<i64> w(P);
+  for (int s = 0; s < P; ++s) {
+    const int t = stages[s].first, tp = stages[s].second, lg = __builtin_ctz(tp);
+    const Dur& d = dur_at(t, lg, bi);
+    StageRec& r = sr[s];
+    std::memset(&r, 0, sizeof r);
+    r.type = t; r.tp = tp; r.lg_tp = lg;
+    if (md.moe_experts > 1) {
+      r.layer_f = d.attn_f + d.ar + d.a2a + d.mlp_f + d.a2a;
+      r.layer_b = d.attn_b + d.ar + d.a2a + d.mlp_b + d.a2a;
+    } else {
+      r.layer_f = d.attn_f + d.ar + d.mlp_f + d.ar;
+      r.layer_b = d.attn_b + d.ar + d.mlp_b + d.ar;
+    }
+    r.tcomp = d.attn_f + d.mlp_f + d.attn_b + d.mlp_b;
+    if (s == 0) { r.fext += d.emb_f; r.gext += d.emb_b; r.wext += d.emb_f + d.emb_b; }
+    if (s == P - 1) { r.fext += d.head_f; r.gext += d.head_b; r.wext += d.head_f + d.head_b; }
+    r.tp_mask = tp_mask[t][lg];
+    w[s] = ((i64)1 << 40) / r.tcomp;
+  }
+  // base layer split: Hamilton of L with weights floor(2^40 / tcomp) (C.4)
+  {
+    i64 W = 0, given = 0;
+    for (i64 x : w) W += x;
+    std::vector<i64> rem(P);
+    for (int s = 0; s < P; ++s) { sr[s].l0 = (int32_t)hamilton_floor_rem(md.layers, w[s], W, &rem[s]); given += sr[s].l0; }
+    std::vector<int> ord(P);
+    for (int s = 0; s < P; ++s) ord[s] = s;
+    std::stable_sort(ord.begin(), ord.end(), [&](int x, int y) { return rem[x] > rem[y]; });
+    for (i64 k = 0; k < md.layers - given; ++k) sr[ord[k]].l0 += 1;
+  }
+  const auto pl = place(D, stages);
+  for (int s = 0; s < P; ++s) {
+    sr[s].first_node = pl[0][s].first; sr[s].first_base = pl[0][s].second;
+    sr[s].last_node = pl[D - 1][s].first; sr[s].last_base = pl[D - 1][s].second;
+    for (int lg = 0; lg <= sr[s].lg_tp; ++lg)
+      for (int r = 0; r + 1 < D; ++r)
+        for (int q = 0; q < (1 << lg); ++q)
+          sr[s].dp_mask[lg] |= (u64)1 << lc(link(pl[r][s].first, pl[r][s].second + q, pl[r + 1][s].first, pl[r + 1][s].second + q));
+  }
+  // p2p cost per replica per boundary (A8): rank pairs q < min(tp_s, tp_s+1), max of tau(A)
+  const i64 A = b * md.seq * md.hidden * md.bpe_act;
+  std::vector<std::vector<i64>> cv(D, std::vector<i64>(P > 1 ? P - 1 : 0));
+  for (int r = 0; r < D; ++r)
+    for (int s = 0; s + 1 < P; ++s) {
+      const int np = std::min(stages[s].second, stages[s + 1].second);
+      i64 c = 0;
+      for (int q = 0; q < np; ++q)
+        c = std::max(c, tau(link(pl[r][s].first, pl[r][s].second + q, pl[r][s + 1].first, pl[r][s + 1].second + q), A));
+      cv[r][s] = c;
+    }
+  // sub-classes (A13): replicas with identical p2p vectors, ordered by lowest replica
+  std::vector<int> rep;
+  std::map<std::vector<i64>, int> seen;
+  for (int r = 0; r < D; ++r)
+    if (seen.emplace(cv[r], r).second) rep.push_back(r);
+  const int32_t off = (int32_t)pool.size();
+  if ((size_t)off + 2 + 16 * P + rep.size() * P > (size_t)INT32_MAX) fail(HSIM_ERANGE, "class-record pool exceeds 2^31 entries");
+  CrecHdr hd{P, D, (int32_t)rep.size(), P <= md.pmax_perturb ? P - 1 : 0};
+  pool.resize(off + 2 + 16 * P + rep.size() * P);
+  std::memcpy(&pool[off], &hd, sizeof hd);
+  std::memcpy(&pool[off + 2], sr.data(), sizeof(StageRec) * P);
+  for (size_t u = 0; u < rep.size(); ++u) {
+    i64* sub = &pool[off + 2 + 16 * P + u * P];
+    sub[0] = rep[u];
+    for (int s = 0; s + 1 < P; ++s) sub[1 + s] = cv[rep[u]][s];
+  }
+  crec_of[key] = off;
+  return off;
+}
+
+// C.2: templates in order: b ascending; HOMO family (per type "unused" or
+// (tp, P, D), lexicographic with type 0 most significant), then MIXED family
+// (per type (tp, P), lexicographic; D ascending); keep M >= D only.
+void hsim_handle::enumerate() {
+  std::vector<int> ps(md.pset, md.pset + md.n_pset);
+  std::sort(ps.begin(), ps.end());
+  ps.erase(std::unique(ps.begin(), ps.end()), ps.end());
+  auto tp_allowed = [&](int t, int tp) {
+    return (md.tpset_mask[t] >> __builtin_ctz(tp) & 1) && types[t].gpus_per_node % tp == 0 && md.heads % tp == 0 &&
+           md.kv_heads % tp == 0;
+  };
+  const i64 rl = 2 * md.r_layer + 1, rb = 2 * md.r_batch + 1;
+  auto radix_of = [&](const std::vector<int>& Ps) {
+    i64 r = 1;
+    for (int P : Ps)
+      if (P <= md.pmax_perturb)
+        for (int k = 0; k + 1 < P; ++k) r *= rl;
+    for (size_t k = 0; k + 1 < Ps.size(); ++k) r *= rb;
+    return r;
+  };
+  i64 acc = 0;
+  for (size_t bi = 0; bi < bs.size(); ++bi) {
+    const int b = bs[bi];
+    if (md.global_batch % b) continue;
+    const i64 M = md.global_batch / b;
+    auto push = [&](const std::vector<std::pair<int, std::vector<std::pair<int, int>>>>& classes) {
+      i64 Dt = 0;
+      std::vector<int> Ps;
+      for (auto& c : classes) { Dt += c.first; Ps.push_back((int)c.second.size()); }
+      if (M < Dt) return;
+      TplRec r{};
+      r.prefix = acc;
+      r.b = b; r.M = (int32_t)M; r.C = (int32_t)classes.size(); r.D = (int32_t)Dt;
+      for (size_t c = 0; c < classes.size(); ++c) r.crec[c] = crec((int)bi, (int)M, classes[c].first, classes[c].second);
+      const i64 R = radix_of(Ps);
+      if (R >= ((i64)1 << 31)) fail(HSIM_ERANGE, "template radix exceeds 2^31");
+      tpl.push_back(r);
+      prefix.push_back(acc);
+      acc += R;
+    };
+    if (md.homo) {
+      struct Opt { int tp, P, D; };
+      std::vector<std::vector<Opt>> opt(nt);
+      for (int t = 0; t < nt; ++t) {
+        opt[t].push_back({0, 0, 0});
+        for (int tp = 1; tp <= 8; tp *= 2) {
+          if (!tp_allowed(t, tp)) continue;
+          for (int P : ps) {
+            if (P > md.layers) continue;
+            for (i64 D = 1; D * P * tp <= n_of_type[t]; ++D)
+              if (!md.use_all || D * P * tp == n_of_type[t]) opt[t].push_back({tp, P, (int)D});
+          }
+        }
+      }
+      std::vector<size_t> k(nt, 0);
+      for (;;) {
+        std::vector<std::pair<int, std::vector<std::pair<int, int>>>> cls;
+        for (int t = 0; t < nt; ++t)
+          if (k[t]) {
+            const Opt& o = opt[t][k[t]];
+            cls.push_back({o.D, std::vector<std::pair<int, int>>(o.P, {t, o.tp})});
+          }
+        if (!cls.empty()) push(cls);
+        int t = nt - 1;
+        while (t >= 0) {
+          if (++k[t] < opt[t].size()) break;
+          k[t] = 0;
+          --t;
+        }
+        if (t < 0) break;
+      }
+    }
+    if (md.mixed && nt >= 2) {
+      std::vector<std::vector<std::pair<int, int>>> opt(nt);  // (tp, P)
+      bool empty = false;
+      for (int t = 0; t < nt; ++t) {
+        for (int tp = 1; tp <= 8; tp *= 2)
+          if (tp_allowed(t, tp))
+            for (int P : ps) opt[t].push_back({tp, P});
+        empty = empty || opt[t].empty();
+      }
+      if (!empty) {
+        std::vector<size_t> k(nt, 0);
+        for (;;) {
+          i64 sumP = 0, Dmax = INT64_MAX;
+          for (int t = 0; t < nt; ++t) {
+            sumP += opt[t][k[t]].second;
+            Dmax = std::min(Dmax, n_of_type[t] / ((i64)opt[t][k[t]].first * opt[t][k[t]].second));
+          }
+          if (sumP <= md.layers && Dmax >= 1) {
+            std::vector<std::pair<int, int>> st;
+            for (int t = 0; t < nt; ++t)
+              for (int s = 0; s < opt[t][k[t]].second; ++s) st.push_back({t, opt[t][k[t]].first});
+            if ((int)st.size() > MAXP) fail(HSIM_ERANGE, "pipeline deeper than 64 stages");
+            for (i64 D = md.use_all ? Dmax : 1; D <= Dmax; ++D) push({{(int)D, st}});
+          }
+          int t = nt - 1;
+          while (t >= 0) {
+            if (++k[t] < opt[t].size()) break;
+            k[t] = 0;
+            --t;
+          }
+          if (t < 0) break;
+        }
+      }
+    }
+  }
+  N = acc;
+  prefix.push_back(acc);
+}
+
+void hsim_handle::prepare() {
+  node_type8.assign(node_type.begin(), node_type.end());
+  hT.L = md.layers;
+  const i64 h = md.hidden, hkv = (i64)md.kv_heads * h / md.heads, E = md.moe_experts;
+  const i64 Wlayer = h * (2 * h + 2 * hkv) + (i64)md.mlp_mats * h * md.ffn * E + (E > 1 ? h * E : 0) + 2 * h;
+  hT.seg_layer_bytes = Wlayer * md.bpe_grad;
+  hT.seg_first_bytes = (i64)md.vocab * h * md.bpe_grad;
+  hT.seg_last_bytes = ((i64)md.vocab * h * (md.tied ? 0 : 1) + h) * md.bpe_grad;
+  if (md.layers * hT.seg_layer_bytes + hT.seg_first_bytes + hT.seg_last_bytes >= TWO53)
+    fail(HSIM_ERANGE, "gradient bytes reach 2^53");
+  hT.r_layer = md.r_layer;
+  hT.r_batch = md.r_batch;
+  hT.n_tpl = (i64)tpl.size();
+  hT.N = N;
+  hT.n_lc = (int32_t)lcs.size();
+  hT.n_nodes = cd.n_nodes;
+  for (size_t k = 0; k < lcs.size(); ++k) hT.lc[k] = lcs[k];
+  hT.tpl_prefix = prefix.data();
+  hT.tpl = tpl.data();
+  hT.pool = pool.data();
+  hT.node_type = node_type8.data();
+}
+
+void hsim_handle::upload() {
+  auto ck = [](cudaError_t e, const char* what) {
+    if (e != cudaSuccess) fail(e == cudaErrorMemoryAllocation ? HSIM_ENOMEM : HSIM_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  };
+  Tables dt = hT;
+  ck(cudaMalloc(&d_prefix, prefix.size() * 8), "cudaMalloc prefix");
+  ck(cudaMalloc(&d_tpl, std::max<size_t>(1, tpl.size()) * sizeof(TplRec)), "cudaMalloc tpl");
+  ck(cudaMalloc(&d_pool, std::max<size_t>(1, pool.size()) * 8), "cudaMalloc pool");
+  ck(cudaMalloc(&d_node_type, node_type8.size()), "cudaMalloc nodes");
+  ck(cudaMalloc(&dT, sizeof(Tables)), "cudaMalloc tables");
+  ck(cudaMalloc(&d_cells, 8), "cudaMalloc cells");
+  ck(cudaMemcpy(d_prefix, prefix.data(), prefix.size() * 8, cudaMemcpyHostToDevice), "H2D prefix");
+  if (!tpl.empty()) ck(cudaMemcpy(d_tpl, tpl.data(), tpl.size() * sizeof(TplRec), cudaMemcpyHostToDevice), "H2D tpl");
+  if (!pool.empty()) ck(cudaMemcpy(d_pool, pool.data(), pool.size() * 8, cudaMemcpyHostToDevice), "H2D pool");
+  ck(cudaMemcpy(d_node_type, node_type8.data(), node_type8.size(), cudaMemcpyHostToDevice), "H2D nodes");
+  dt.tpl_prefix = d_prefix;
+  dt.tpl = d_tpl;
+  dt.pool = d_pool;
+  dt.node_type = d_node_type;
+  ck(cudaMemcpy(dT, &dt, sizeof(Tables), cudaMemcpyHostToDevice), "H2D tables");
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, dev);
+}
+
+// =============================================================================
+// C ABI
+// =============================================================================
+namespace hsim {
+int launch_eval(hsim_handle* h, const Tables* dT, const hsim_cands* c, int64_t n, int64_t* out_ns, int32_t k,
+                int64_t* out_t, int64_t* out_i, cudaStream_t st);
+int launch_count(const Tables* dT, int64_t first, int64_t n, int64_t* d_acc, cudaStream_t st);
+int launch_merge(const int64_t* lists, int32_t nlists, int32_t k, int64_t* out_t, int64_t* out_i, cudaStream_t st);
+}
+
+extern "C" {
+
+const char* hsim_last_error(void) { return g_err.c_str(); }
+
+int hsim_create(const hsim_cluster_desc* cluster, const hsim_model_desc* model, hsim_handle** out) {
+  g_err.clear();
+  if (!out) { g_err = "MissingField: out"; return HSIM_EINVAL; }
+  *out = nullptr;
+  if (!cluster || !model) { g_err = "MissingField: cluster / model"; return HSIM_EINVAL; }
+  hsim_handle* h = new (std::nothrow) hsim_handle();
+  if (!h) { g_err = "out of host memory"; return HSIM_ENOMEM; }
+  try {
+    h->cd = *cluster;
+    h->md = *model;
+    h->validate();
+    h->nt = cluster->n_device_types;
+    h->types.assign(cluster->device_types, cluster->device_types + h->nt);
+    h->node_type.assign(cluster->node_type_of, cluster->node_type_of + cluster->n_nodes);
+    h->cd.device_types = h->types.data();
+    h->cd.node_type_of = h->node_type.data();
+    h->nodes_of_type.assign(h->nt, {});
+    for (int n = 0; n < cluster->n_nodes; ++n) {
+      h->nodes_of_type[h->node_type[n]].push_back(n);
+      h->n_of_type[h->node_type[n]] += h->types[h->node_type[n]].gpus_per_node;
+    }
+    h->bs.assign(model->bset, model->bset + model->n_bset);
+    std::sort(h->bs.begin(), h->bs.end());
+    h->bs.erase(std::unique(h->bs.begin(), h->bs.end()), h->bs.end());
+    h->derive_links();
+    h->derive_durations();
+    // stage-time bound keeps the partition weights floor(2^40 / t) positive
+    for (const auto& d : h->dur)
+      if (d.ok && (i64)model->layers * (d.attn_f + d.mlp_f + d.attn_b + d.mlp_b) + d.emb_f + d.emb_b + d.head_f + d.head_b >= ((i64)1 << 40))
+        fail(HSIM_ERANGE, "a stage's compute time reaches 2^40 ns");
+    h->enumerate();
+    if (h->N <= 0) fail(HSIM_EINVAL, "InsufficientDevices: the candidate space is empty");
+    h->prepare();
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) == cudaSuccess && ndev > 0) h->upload();  // else: host-only handle
+    else cudaGetLastError();
+  } catch (const Fail& f) {
+    g_err = f.msg;
+    hsim_destroy(h);
+    return f.code;
+  } catch (const std::bad_alloc&) {
+    g_err = "out of host memory";
+    hsim_destroy(h);
+    return HSIM_ENOMEM;
+  }
+  *out = h;
+  return HSIM_OK;
+}
+
+void hsim_destroy(hsim_handle* h) {
+  if (!h) return;
+  cudaFree(h->d_prefix);
+  cudaFree(h->d_tpl);
+  cudaFree(h->d_pool);
+  cudaFree(h->d_node_type);
+  cudaFree(h->dT);
+  cudaFree(h->d_blk);
+  cudaFree(h->d_cells);
+  delete h;
+}
+
+int64_t hsim_space_size(const hsim_handle* h) { return h ? h->N : -1; }
+int64_t hsim_n_templates(const hsim_handle* h) { return h ? (int64_t)h->tpl.size() : -1; }
+int64_t hsim_template_first(const hsim_handle* h, int64_t k) {
+  if (!h || k < 0 || k > (int64_t)h->tpl.size()) return -1;
+  return h->prefix[k];
+}
+int32_t hsim_last_launch_count(const hsim_handle* h) { return h ? h->last_launches : -1; }
+
+int hsim_decode(const hsim_handle* h, int64_t i, char* json, size_t cap) {
+  g_err.clear();
+  if (!h) { g_err = "NULL handle"; return HSIM_ESTATE; }
+  if (i < 0 || i >= h->N) { g_err = "index out of range"; return HSIM_ERANGE; }
+  const TplRec& tp = h->tpl[find_template(h->hT, i)];
+  Split sp;
+  const int st = partition(h->hT, tp, i - tp.prefix, sp);
+  std::string s = "{\"index\":" + std::to_string(i) + ",\"b\":" + std::to_string(tp.b) + ",\"M\":" + std::to_string(tp.M) +
+                  ",\"status\":" + std::to_string(st) + ",\"classes\":[";
+  for (int c = 0; c < tp.C; ++c) {
+    const CrecHdr* hd = crec_hdr(h->hT, tp.crec[c]);
+    const StageRec* sr = crec_stages(h->hT, tp.crec[c]);
+    std::vector<std::pair<int, int>> stages;
+    for (int q = 0; q < hd->P; ++q) stages.push_back({sr[q].type, sr[q].tp});
+    s += c ? ",{" : "{";
+    s += "\"D\":" + std::to_string(hd->D) + ",\"subclasses\":" + std::to_string(hd->U) + ",\"stages\":[";
+    for (int q = 0; q < hd->P; ++q) s += (q ? ",[" : "[") + std::to_string(sr[q].type) + "," + std::to_string(sr[q].tp) + "]";
+    s += "],\"layers\":[";
+    for (int q = 0; q < hd->P; ++q) s += (q ? "," : "") + std::to_string(st == -1 ? sr[q].l0 : sp.l[c][q]);
+    s += "],\"mb\":[";
+    if (st == 0)
+      for (int r = 0; r < hd->D; ++r) s += (r ? "," : "") + std::to_string(replica_mb(sp, c, r));
+    s += "],\"place\":[";
+    try {
+      const auto pl = h->place(hd->D, stages);
+      for (int r = 0; r < hd->D; ++r) {
+        s += r ? ",[" : "[";
+        for (int q = 0; q < hd->P; ++q) s += (q ? ",[" : "[") + std::to_string(pl[r][q].first) + "," + std::to_string(pl[r][q].second) + "]";
+        s += "]";
+      }
+    } catch (const Fail& f) {
+      g_err = f.msg;
+      return f.code;
+    }
+    s += "]}";
+  }
+  s += "]}";
+  if (!json || s.size() + 1 > cap) { g_err = "buffer too small"; return HSIM_ERANGE; }
+  std::memcpy(json, s.c_str(), s.size() + 1);
+  return HSIM_OK;
+}
+
+static int check_cands(const hsim_handle* h, const hsim_cands* c, int64_t n) {
+  if (!c || n < 0) { g_err = "InvalidValue: cands / n"; return HSIM_EINVAL; }
+  if (n == 0 || c->idx) return HSIM_OK;
+  if (c->first < 0) { g_err = "index out of range"; return HSIM_ERANGE; }
+  int64_t last;
+  if (c->block == 0) last = c->first + n - 1;
+  else {
+    if (c->block < 0 || c->stride < c->block) { g_err = "InvalidValue: block / stride"; return HSIM_EINVAL; }
+    last = c->first + ((n - 1) / c->block) * c->stride + (n - 1) % c->block;
+  }
+  if (last >= h->N) { g_err = "index out of range"; return HSIM_ERANGE; }
+  return HSIM_OK;
+}
+
+int hsim_eval_batch(hsim_handle* h, const hsim_cands* cands, int64_t n, int64_t* out_ns, void* stream) {
+  g_err.clear();
+  if (!h) { g_err = "NULL handle"; return HSIM_ESTATE; }
+  int rc = check_cands(h, cands, n);
+  if (rc) return rc;
+  h->last_launches = 0;
+  if (n == 0) return HSIM_OK;
+  if ((rc = h->ensure_device())) return rc;
+  return launch_eval(h, h->dT, cands, n, out_ns, 0, nullptr, nullptr, (cudaStream_t)stream);
+}
+
+int hsim_topk(hsim_handle* h, const hsim_cands* cands, int64_t n, int32_t k, int64_t* out_t_ns, int64_t* out_idx,
+              int64_t* out_ns, void* stream) {
+  g_err.clear();
+  if (!h) { g_err = "NULL handle"; return HSIM_ESTATE; }
+  if (k < 1 || k > 1024 || !out_t_ns || !out_idx) { g_err = "InvalidValue: k must be 1..1024 with output buffers"; return HSIM_EINVAL; }
+  int rc = check_cands(h, cands, n);
+  if (rc) return rc;
+  h->last_launches = 0;
+  if ((rc = h->ensure_device())) return rc;
+  return launch_eval(h, h->dT, cands, n, out_ns, k, out_t_ns, out_idx, (cudaStream_t)stream);
+}
+
+int hsim_merge_topk(const int64_t* lists, int32_t nlists, int32_t k, int64_t* out_t_ns, int64_t* out_idx, void* stream) {
+  g_err.clear();
+  if (k < 1 || k > 1024 || nlists < 0 || !out_t_ns || !out_idx || (nlists > 0 && !lists)) {
+    g_err = "InvalidValue: merge arguments";
+    return HSIM_EINVAL;
+  }
+  return launch_merge(lists, nlists, k, out_t_ns, out_idx, (cudaStream_t)stream);
+}
+
+int64_t hsim_count_cells(const hsim_handle* h, int64_t first, int64_t n) {
+  g_err.clear();
+  if (!h || first < 0 || n < 0 || first + n > h->N) { g_err = "index out of range"; return -1; }
+  if (const_cast<hsim_handle*>(h)->ensure_device()) return -1;
+  if (launch_count(h->dT, first, n, h->d_cells, 0)) return -1;
+  int64_t v = 0;
+  if (cudaMemcpy(&v, h->d_cells, 8, cudaMemcpyDeviceToHost) != cudaSuccess) { g_err = "cudaMemcpy"; return -1; }
+  return v;
+}
+
+}  // extern "C"
+
+// scratch accessor for kernels.cu
+namespace hsim {
+int ensure_block_scratch(hsim_handle* h, size_t entries, int64_t** out) {
+  if (entries > h->blk_cap) {
+    cudaFree(h->d_blk);
+    h->d_blk = nullptr;
+    h->blk_cap = 0;
+    if (cudaMalloc(&h->d_blk, entries * 8) != cudaSuccess) { g_err = "cudaMalloc block scratch"; return HSIM_ENOMEM; }
+    h->blk_cap = entries;
+  }
+  *out = h->d_blk;
+  return 0;
+}
+int sm_count(const hsim_handle* h) { return h->sm_count; }
+void set_launches(hsim_handle* h, int n) { h->last_launches = n; }
+void set_error(const char* m) { g_err = m; }
+}  // namespace hsim

@@ -1,0 +1,324 @@
+// hsim_core.cuh — product-side data layout and per-candidate arithmetic.
+//
+// Device tables built by host.cu (hsim_create) and the __host__ __device__
+// functions that evaluate one candidate: decode (DESIGN.md C.2), partition
+// (C.4), stage durations (C.5), 1F1B max-plus (C.7),
+// gradient sync with reshard (C.6/C.8).  The kernels in
+// kernels.cu call these; host.cu calls the partition part only to render
+// hsim_decode's JSON (never to produce a timing: there is no CPU path).
+//
+// Exactness (DESIGN.md C.0): durations are ceil((double)x / r), one IEEE RN
+// division (nvcc -prec-div default; host built with -ffp-contract=off), the
+// rest int64 + / max.  Device code is compiled with -fmad=false.
+#pragma once
+#include <stdint.h>
+
+#ifdef __CUDACC__
+#define HD __host__ __device__ __forceinline__
+#else
+#define HD inline
+#endif
+
+namespace hsim {
+
+typedef int64_t i64;
+typedef uint64_t u64;
+
+constexpr int MAXT = 4;      // device types
+constexpr int MAXG = 8;      // GPUs per node
+constexpr int MAXC = 4;      // classes per template
+constexpr int MAXP = 64;     // stages per pipeline
+constexpr int MAXLC = 64;    // distinct link classes
+constexpr int MAXB = 8;      // micro-batch sizes
+
+struct Link { i64 alpha; double beta; };  // alpha ns, beta B/ns
+
+// One stage of a class record (crec).  128 B, 8-byte aligned.
+struct StageRec {
+  i64 layer_f, layer_b;   // per-layer fwd / bwd incl. TP all-reduce / EP all-to-all (C.5)
+  i64 tcomp;              // compute-only fwd+bwd of one layer: partition weight input (C.4)
+  i64 fext, gext;         // emb (stage 0) + head (stage P-1) fwd / bwd
+  i64 wext;               // emb+head fwd+bwd for the batch weight (C.4)
+  u64 tp_mask;            // link classes of this stage group's TP ring (reshard, A14)
+  u64 dp_mask[4];         // link classes of intra-class DP ring edges, rings q < 2^k (C.6)
+  int32_t type, tp, l0, lg_tp;          // device type, TP, base layer split, log2(tp)
+  int32_t first_node, first_base, last_node, last_base;  // replica 0 / replica D-1 group
+  int32_t _pad[2];
+};
+static_assert(sizeof(StageRec) == 128, "StageRec layout");
+
+struct CrecHdr {
+  int32_t P, D, U, nd;    // stages, replicas, sub-classes, #layer digits
+};
+// crec layout in the int64 pool: CrecHdr (16 B) | StageRec[P] | U x (i64 k_u, i64 c[P-1])
+
+struct TplRec {
+  i64 prefix;             // first candidate index
+  int32_t b, M, C, D;     // micro-batch size, #micro-batches, classes, total replicas
+  int32_t crec[MAXC];     // int64-offsets of the class records in the pool
+};
+
+struct Tables {
+  // model-derived
+  i64 L;
+  i64 seg_layer_bytes;    // W_layer * bpe_grad
+  i64 seg_first_bytes;    // V*h*bpe_grad (embedding with layer 0)
+  i64 seg_last_bytes;     // (V*h*!tied + h)*bpe_grad (head + final norm with layer L-1)
+  int32_t r_layer, r_batch;
+  // templates
+  i64 n_tpl, N;
+  const i64* tpl_prefix;  // [n_tpl + 1]
+  const TplRec* tpl;      // [n_tpl]
+  const i64* pool;        // crec pool
+  // links
+  int32_t n_lc, n_nodes;
+  Link lc[MAXLC];
+  int8_t lc_same[MAXT][MAXG][MAXG];               // same node: link class of i -> j
+  int8_t lc_cross[MAXT][MAXG][MAXT][MAXG];        // different nodes: (t1, r1) -> (t2, r2)
+  const int8_t* node_type;                        // [n_nodes]
+};
+
+// --- C.0 --------------------------------------------------------------------
+HD i64 ceilq(i64 x, double r) {
+#ifdef __CUDA_ARCH__
+  return x == 0 ? 0 : (i64)ceil(__ddiv_rn((double)x, r));
+#else
+  return x == 0 ? 0 : (i64)__builtin_ceil((double)x / r);
+#endif
+}
+HD i64 ceil_div(i64 a, i64 b) { return (a + b - 1) / b; }
+HD i64 imax(i64 a, i64 b) { return a > b ? a : b; }
+HD i64 imin(i64 a, i64 b) { return a < b ? a : b; }
+
+// max over the link classes in `mask` of alpha + ceil(x / beta)  (C.6 tau_e)
+HD i64 eval_mask(const Tables& T, u64 mask, i64 x) {
+  i64 best = 0;
+  while (mask) {
+#ifdef __CUDA_ARCH__
+    int b = __ffsll((long long)mask) - 1;
+#else
+    int b = __builtin_ctzll(mask);
+#endif
+    mask &= mask - 1;
+    best = imax(best, T.lc[b].alpha + ceilq(x, T.lc[b].beta));
+  }
+  return best;
+}
+
+HD const CrecHdr* crec_hdr(const Tables& T, int32_t off) { return (const CrecHdr*)(T.pool + off); }
+HD const StageRec* crec_stages(const Tables& T, int32_t off) { return (const StageRec*)(T.pool + off + 2); }
+HD const i64* crec_sub(const Tables& T, int32_t off, int P, int u) {
+  return T.pool + off + 2 + 16 * P + (i64)u * P;  // (k_u, c[0..P-2]) = P int64
+}
+
+// template of candidate i: max{tau : prefix[tau] <= i}
+HD i64 find_template(const Tables& T, i64 i) {
+  i64 lo = 0, hi = T.n_tpl;
+  while (hi - lo > 1) {
+    i64 mid = (lo + hi) >> 1;
+    if (T.tpl_prefix[mid] <= i) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+// Decoded + partitioned candidate (step 1).
+struct Split {
+  int32_t C;
+  int32_t l[MAXC][MAXP];     // layers per stage
+  i64 q[MAXC];               // Hamilton floor per replica of class c
+  i64 seats[MAXC];           // replicas 0..seats-1 of class c get +1
+  i64 add[MAXC];             // epsilon (c < C-1) or floor(R / D_last)
+  i64 rm;                    // last class: replicas < rm get +1
+};
+HD i64 replica_mb(const Split& s, int c, i64 k) {
+  i64 m = s.q[c] + (k < s.seats[c] ? 1 : 0) + s.add[c];
+  if (c == s.C - 1) m += (k < s.rm ? 1 : 0);
+  return m;
+}
+
+// Steps a0 + a1: digits (LSB first: class boundaries, then batch digits),
+// layer split = template base split + delta_s - delta_{s-1}, batch split =
+// Hamilton over all replicas with weights floor(2^40 / slowest stage) (C.4).
+// Returns 0, -1 (layer) or -2 (batch).
+HD int partition(const Tables& T, const TplRec& tp, i64 local, Split& sp) {
+  const int C = tp.C;
+  sp.C = C;
+  const i64 bl = 2 * T.r_layer + 1, bb = 2 * T.r_batch + 1;
+  uint32_t loc = (uint32_t)local;  // radix < 2^31 (validated at create)
+  i64 w[MAXC];
+  int status = 0;
+  for (int c = 0; c < C; ++c) {
+    const CrecHdr* h = crec_hdr(T, tp.crec[c]);
+    const StageRec* st = crec_stages(T, tp.crec[c]);
+    const int P = h->P;
+    int dprev = 0;
+    i64 worst = 0;
+    for (int s = 0; s < P; ++s) {
+      int d = 0;
+      if (s < h->nd) { d = (int)(loc % (uint32_t)bl) - T.r_layer; loc /= (uint32_t)bl; }
+      int l = st[s].l0 + d - dprev;
+      dprev = d;
+      sp.l[c][s] = l;
+      if (l < 1) status = -1;
+      worst = imax(worst, (i64)l * st[s].tcomp + st[s].wext);
+    }
+    w[c] = worst > 0 ? ((i64)1 << 40) / worst : 0;
+  }
+  if (status) return status;
+  i64 W = 0, eps[MAXC], R = 0;
+  for (int c = 0; c < C; ++c) W += (i64)crec_hdr(T, tp.crec[c])->D * w[c];
+  for (int c = 0; c < C - 1; ++c) { eps[c] = (i64)(loc % (uint32_t)bb) - T.r_batch; loc /= (uint32_t)bb; }
+  i64 left = tp.M, rem[MAXC];
+  for (int c = 0; c < C; ++c) {
+    sp.q[c] = (i64)tp.M * w[c] / W;
+    rem[c] = (i64)tp.M * w[c] % W;
+    left -= (i64)crec_hdr(T, tp.crec[c])->D * sp.q[c];
+    sp.seats[c] = 0;
+  }
+  // leftover seats to the largest remainders; ties -> lower (class-major) replica
+  bool done[MAXC] = {false, false, false, false};
+  for (int pass = 0; pass < C && left > 0; ++pass) {
+    int best = -1;
+    for (int c = 0; c < C; ++c)
+      if (!done[c] && (best < 0 || rem[c] > rem[best])) best = c;
+    done[best] = true;
+    i64 D = crec_hdr(T, tp.crec[best])->D;
+    sp.seats[best] = imin(D, left);
+    left -= sp.seats[best];
+  }
+  for (int c = 0; c < C - 1; ++c) {
+    sp.add[c] = eps[c];
+    R -= (i64)crec_hdr(T, tp.crec[c])->D * eps[c];
+  }
+  const i64 Dl = crec_hdr(T, tp.crec[C - 1])->D;
+  i64 fl = R >= 0 ? R / Dl : -((-R + Dl - 1) / Dl);
+  sp.add[C - 1] = fl;
+  sp.rm = R - fl * Dl;
+  for (int c = 0; c < C; ++c)
+    if (replica_mb(sp, c, crec_hdr(T, tp.crec[c])->D - 1) < 1) return -2;  // m non-increasing in k
+  return 0;
+}
+
+// --- step a4: non-interleaved 1F1B as a level-synchronous max-plus sweep -----
+// Level of F(s,j): s+j if j <= P-1-s else 2j+s; of B(s,j): 2P-1-s+2j
+// (DESIGN.md C.7).  Every op's inputs were produced at an earlier level, so a
+// sweep over levels with stages in any order inside a level is a topological
+// order of the 1F1B DAG; at most one op per stage per level.
+HD i64 level_F(int P, int s, i64 j) { return j <= P - 1 - s ? s + j : 2 * j + s; }
+HD i64 level_B(int P, int s, i64 j) { return 2 * P - 1 - s + 2 * j; }
+
+HD i64 pipeline_1f1b(int P, i64 m, const i64* f, const i64* g, const i64* c) {
+  i64 lastF[MAXP], lastB[MAXP], last[MAXP], jf[MAXP], jb[MAXP];
+  for (int s = 0; s < P; ++s) { lastF[s] = lastB[s] = last[s] = 0; jf[s] = jb[s] = 0; }
+  const i64 levels = 2 * (m + P - 1);
+  for (i64 lv = 0; lv < levels; ++lv) {
+    i64 leftF_prev = 0;  // lastF[s-1] as of the end of the previous level
+    for (int s = 0; s < P; ++s) {
+      const i64 oldF = lastF[s];
+      if (jf[s] < m && level_F(P, s, jf[s]) == lv) {
+        i64 in = s == 0 ? 0 : leftF_prev + c[s - 1];
+        i64 e = imax(last[s], in) + f[s];
+        lastF[s] = last[s] = e;
+        jf[s]++;
+      } else if (jb[s] < m && level_B(P, s, jb[s]) == lv) {
+        i64 in = s == P - 1 ? lastF[s] : lastB[s + 1] + c[s];
+        i64 e = imax(last[s], in) + g[s];
+        lastB[s] = last[s] = e;
+        jb[s]++;
+      }
+      leftF_prev = oldF;
+    }
+  }
+  return lastB[0];
+}
+
+// --- whole candidate (steps a0-a5) ---------------------------------------------
+// Returns the iteration time in ns or a negative status; *cells (if non-null)
+// receives sum_u 2 * P_u * m_u (the 1F1B cells simulated).
+HD i64 eval_candidate(const Tables& T, i64 i, i64* cells) {
+  if (i < 0 || i >= T.N) return INT64_MIN;
+  const TplRec tp = T.tpl[find_template(T, i)];
+  Split sp;
+  int st = partition(T, tp, i - tp.prefix, sp);
+  if (st) return st;
+  const int C = tp.C;
+  i64 T0 = 0, ncell = 0;
+  i64 f[MAXP], g[MAXP];
+  for (int c = 0; c < C; ++c) {
+    const CrecHdr* h = crec_hdr(T, tp.crec[c]);
+    const StageRec* sr = crec_stages(T, tp.crec[c]);
+    const int P = h->P;
+    for (int s = 0; s < P; ++s) {
+      f[s] = (i64)sp.l[c][s] * sr[s].layer_f + sr[s].fext;
+      g[s] = (i64)sp.l[c][s] * sr[s].layer_b + sr[s].gext;
+    }
+    for (int u = 0; u < h->U; ++u) {
+      const i64* sub = crec_sub(T, tp.crec[c], P, u);
+      const i64 m = replica_mb(sp, c, sub[0]);
+      ncell += 2 * P * m;
+      T0 = imax(T0, pipeline_1f1b(P, m, f, g, sub + 1));
+    }
+  }
+  if (cells) *cells = ncell;
+  if (tp.D == 1) return T0;
+
+  // step a5: gradient-sync segments = common refinement of the classes' layer
+  // boundaries, list-scheduled FIFO per (class, stage) group from T0.
+  int sc[MAXC];
+  i64 nextcut[MAXC], cur_free[MAXC];
+  for (int c = 0; c < C; ++c) {
+    sc[c] = 0;
+    nextcut[c] = crec_hdr(T, tp.crec[c])->P > 1 ? sp.l[c][0] : T.L;
+    cur_free[c] = T0;
+  }
+  i64 a = 0, Titer = T0;
+  while (a < T.L) {
+    i64 z = T.L;
+    for (int c = 0; c < C; ++c) z = imin(z, nextcut[c]);
+    const i64 S = (z - a) * T.seg_layer_bytes + (a == 0 ? T.seg_first_bytes : 0) + (z == T.L ? T.seg_last_bytes : 0);
+    int tstar = 1 << 30, lg = 0;
+    for (int c = 0; c < C; ++c) {
+      const StageRec& s = crec_stages(T, tp.crec[c])[sc[c]];
+      if (s.tp < tstar) { tstar = s.tp; lg = s.lg_tp; }
+    }
+    const i64 xs = ceil_div(S, tstar);
+    i64 RS = 0;
+    u64 mask = 0;
+    for (int c = 0; c < C; ++c) {
+      const StageRec& s = crec_stages(T, tp.crec[c])[sc[c]];
+      if (s.tp != tstar) RS = imax(RS, eval_mask(T, s.tp_mask, xs));
+      mask |= s.dp_mask[lg];
+      // edge from the last replica of class c to the first replica of the next
+      // class (wrap: class C-1 -> class 0), at ring q through device base + q
+      const int cn = c + 1 < C ? c + 1 : 0;
+      const StageRec& t = crec_stages(T, tp.crec[cn])[sc[cn]];
+      const int n1 = s.last_node, n2 = t.first_node;
+      const int t1 = T.node_type[n1], t2 = T.node_type[n2];
+      for (int q = 0; q < tstar; ++q) {
+        const int r1 = s.last_base + q, r2 = t.first_base + q;
+        const int id = n1 == n2 ? T.lc_same[t1][r1][r2] : T.lc_cross[t1][r1][t2][r2];
+        mask |= (u64)1 << id;
+      }
+    }
+    const i64 chunk = ceil_div(xs, (i64)tp.D);
+    const i64 AR = 2 * (i64)(tp.D - 1) * eval_mask(T, mask, chunk);
+    i64 start = 0;
+    for (int c = 0; c < C; ++c) start = imax(start, cur_free[c]);
+    const i64 end = start + RS + AR;
+    for (int c = 0; c < C; ++c) cur_free[c] = end;
+    Titer = imax(Titer, end);
+    // advance classes whose stage ends at z
+    for (int c = 0; c < C; ++c) {
+      if (nextcut[c] == z && z < T.L) {
+        sc[c]++;
+        const int P = crec_hdr(T, tp.crec[c])->P;
+        nextcut[c] = sc[c] + 1 < P ? nextcut[c] + sp.l[c][sc[c]] : T.L;
+        cur_free[c] = T0;
+      }
+    }
+    a = z;
+  }
+  return Titer;
+}
+
+}  // namespace hsim

@@ -1,0 +1,40 @@
+"""Multi-GPU sweep: the candidate space sharded block-cyclically over ranks
+(one process per B200), per-rank top-k on the device, one NCCL all_gather of
+the k-entry lists over NVLink, merged by the hsim_merge_topk kernel
+(BASELINE.json north_star "merged by an NCCL allgather").
+
+torch.distributed is plumbing only (process group + the one collective); the
+evaluation and both top-k stages run in libhsim's kernels.
+"""
+import torch
+import torch.distributed as dist
+
+from .hsim import hsim_merge_topk
+
+DEFAULT_BLOCK = 1 << 16
+
+
+def shard(n_space, rank, world, block=DEFAULT_BLOCK):
+    """Block-cyclic shard of [0, n_space): (first, n, block, stride) for rank.
+    Rank r owns blocks r, r+W, r+2W, ... of `block` consecutive indices."""
+    if world == 1:
+        return 0, n_space, 0, 0
+    stride = world * block
+    full, rem = divmod(n_space, stride)
+    n = full * block + min(block, max(0, rem - rank * block))
+    return rank * block, n, block, stride
+
+
+def sweep(sim, k, group=None, block=DEFAULT_BLOCK, stream=None, out=None):
+    """Global top-k (times, indices) over the whole space of `sim`, identical
+    on every rank.  Single process when torch.distributed is not initialised."""
+    world = dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
+    rank = dist.get_rank(group) if world > 1 else 0
+    first, n, blk, stride = shard(sim.space_size(), rank, world, block)
+    if world == 1:
+        return sim.topk(k, n=n, first=first, stream=stream, out=out)
+    local = torch.empty(2 * k, dtype=torch.int64, device="cuda")
+    sim.topk(k, n=n, first=first, block=blk, stride=stride, stream=stream, out=(local[:k], local[k:]))
+    gathered = torch.empty(world, 2 * k, dtype=torch.int64, device="cuda")
+    dist.all_gather_into_tensor(gathered, local, group=group)
+    return hsim_merge_topk(gathered, k, out=out, stream=stream)

@@ -1,0 +1,112 @@
+"""C-ABI library: loads, exports every symbol include/hsim.h declares, validates
+descriptors, and its host-side decode agrees with the oracle (CPU only; no
+compute call is made without a GPU)."""
+import ctypes as C
+import os
+import re
+
+import numpy as np
+import pytest
+
+import hsim_inputs as H
+from paper_2508_05370_b200 import build as pbuild
+from paper_2508_05370_b200 import hsim
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def L():
+    pbuild.build()
+    return hsim.lib()
+
+
+def test_exports_every_declared_symbol(L):
+    hdr = open(os.path.join(ROOT, "include", "hsim.h")).read()
+    declared = set(re.findall(r"\b(hsim_[a-z_]+)\s*\(", hdr))
+    assert declared == set(hsim.EXPORTS)
+    for name in declared:
+        assert hasattr(L, name), name
+
+
+def _create(cfg):
+    cd, md, keep = hsim.descriptors(cfg)
+    h = C.c_void_p()
+    rc = hsim.lib().hsim_create(C.byref(cd), C.byref(md), C.byref(h))
+    return rc, h, hsim.lib().hsim_last_error().decode()
+
+
+@pytest.mark.parametrize("mutate,code,kind", [
+    (lambda c: c["model"].update(hidden=4097), hsim.HSIM_EINVAL, "DivisibilityViolation"),
+    (lambda c: c["model"].update(layers=0), hsim.HSIM_EINVAL, "InvalidValue"),
+    (lambda c: c["cluster"]["types"][0].update(gpus_per_node=3), hsim.HSIM_EINVAL, "RailMismatch"),
+    (lambda c: c["cluster"].update(nodes=[0, 7]), hsim.HSIM_EINVAL, "UnknownGpuType"),
+    (lambda c: c["cluster"]["types"][0].update(nic_gbps=0.0), hsim.HSIM_EINVAL, "NonPositiveBandwidth"),
+    (lambda c: c["cluster"]["types"][1]["link_kinds"][0][0].update(gbps=-1.0), hsim.HSIM_EINVAL, "NonPositiveBandwidth"),
+    (lambda c: c["model"].update(seq=1 << 20, vocab=1 << 20), hsim.HSIM_ERANGE, "2^53"),
+])
+def test_validation_errors(L, mutate, code, kind):
+    cfg = H.get(1)
+    mutate(cfg)
+    rc, h, msg = _create(cfg)
+    assert rc == code and kind in msg and not h.value
+
+
+def test_null_arguments(L):
+    assert L.hsim_create(None, None, None) == hsim.HSIM_EINVAL
+    assert L.hsim_space_size(None) == -1
+    L.hsim_destroy(None)
+    assert L.hsim_eval_batch(None, None, 0, None, None) == hsim.HSIM_ESTATE
+    buf = C.create_string_buffer(64)
+    assert L.hsim_decode(None, 0, buf, 64) == hsim.HSIM_ESTATE
+
+
+def test_decode_range_and_buffer(L):
+    s = hsim.Sim(H.get(1), host_only=True)
+    buf = C.create_string_buffer(8)
+    assert L.hsim_decode(s.h, 0, buf, 8) == hsim.HSIM_ERANGE
+    assert L.hsim_decode(s.h, 1, buf, 8) == hsim.HSIM_ERANGE
+    assert s.decode(0)["classes"][0]["layers"] == [3, 9]
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 4, 5])
+def test_space_and_templates_match_oracle(oracle_mod, L, n):
+    cfg = H.get(n)
+    s = hsim.Sim(cfg, host_only=True)
+    o = oracle_mod.Oracle(cfg)
+    assert s.space_size() == o.space_size()
+    assert s.n_templates() == o.n_templates()
+    pre = o.template_prefix()
+    ks = np.unique(np.linspace(0, len(pre) - 1, 200).astype(int))
+    assert all(s.template_first(int(k)) == pre[k] for k in ks)
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 4, 5])
+def test_host_decode_matches_oracle_plan(oracle_mod, L, n):
+    """Step 1 (partition) and placement, host side of the product vs oracle."""
+    cfg = H.get(n)
+    s = hsim.Sim(cfg, host_only=True)
+    o = oracle_mod.Oracle(cfg)
+    idx = H.sample_indices(o.space_size(), 150 if n != 3 else 40, seed=n)
+    for i in idx:
+        a, b = s.decode(int(i)), o.describe(int(i))
+        assert a["b"] == b["b"] and a["status"] == b["status"], (i, a, b)
+        for ca, cb in zip(a["classes"], b["classes"]):
+            assert ca["D"] == cb["D"] and ca["stages"] == cb["stages"]
+            assert ca["place"] == cb["place"]
+            if b["status"] != -1:
+                assert ca["layers"] == cb["layers"], (i, ca, cb)
+            if b["status"] == 0:
+                assert ca["mb"] == cb["mb"], (i, ca, cb)
+
+
+def test_eval_without_gpu_fails_loudly(L):
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("has a GPU")
+    s = hsim.Sim(H.get(1), host_only=True)
+    c = hsim.hsim_cands()
+    rc = L.hsim_eval_batch(s.h, C.byref(c), 1, None, None)
+    assert rc == hsim.HSIM_ECUDA
+    with pytest.raises(RuntimeError):
+        hsim.Sim(H.get(1))

@@ -1,0 +1,156 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle, int64-equal.
+
+Bar (BASELINE.json north_star): bit-exact int64 ns for every candidate.
+Coverage per config: contiguous ranges (several thread blocks + a ragged
+tail), seeded samples (hsim_inputs.sample_indices, seed 0x5EED2508), the first
+and last index of templates, all of a tiny space, top-k vs brute force, the
+three candidate-list modes, and edge cases (n=0, k > valid, index errors).
+Set HSIM_FULL=1 for exhaustive config-2 parity (minutes of oracle time).
+"""
+import os
+
+import numpy as np
+import pytest
+
+import hsim_inputs as H
+
+pytestmark = pytest.mark.gpu
+
+THREADS = os.cpu_count() or 8
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2508_05370_b200 import build
+    build.build()
+    return torch
+
+
+_cache = {}
+
+
+def pair(oracle_mod, n):
+    if n not in _cache:
+        from paper_2508_05370_b200 import Sim
+        cfg = H.get(n) if isinstance(n, int) else H.tiny_random(int(n.split("-")[1]))
+        _cache[n] = (Sim(cfg), oracle_mod.Oracle(cfg))
+    return _cache[n]
+
+
+def gpu_eval(sim, torch, idx):
+    t = torch.as_tensor(np.asarray(idx, dtype=np.int64), device="cuda")
+    return sim.eval_batch(idx=t).cpu().numpy()
+
+
+def assert_equal(idx, got, want):
+    bad = np.nonzero(got != want)[0]
+    assert bad.size == 0, f"{bad.size} mismatches, first: i={idx[bad[0]]} gpu={got[bad[0]]} oracle={want[bad[0]]}"
+
+
+def test_config1_single_candidate(torch_cuda, oracle_mod):
+    sim, o = pair(oracle_mod, 1)
+    out = sim.eval_batch(n=1).cpu().numpy()
+    assert out[0] == o.eval(0) and out[0] > 0
+
+
+@pytest.mark.parametrize("n,count", [(2, 6000), (3, 1500), (4, 4000), (5, 1500)])
+def test_sampled_parity(torch_cuda, oracle_mod, n, count):
+    sim, o = pair(oracle_mod, n)
+    pre = o.template_prefix()
+    # first / last index of (a strided subset of) templates + seeded uniform draws
+    ks = np.unique(np.linspace(0, len(pre) - 2, 400).astype(int))
+    extra = np.concatenate([pre[ks], pre[ks + 1] - 1])
+    idx = H.sample_indices(o.space_size(), count, seed=H.PARITY_SEED + n, extra=extra)
+    got = gpu_eval(sim, torch_cuda, idx)
+    want = o.eval_many(idx, threads=THREADS)
+    assert_equal(idx, got, want)
+    assert (want >= 0).mean() > 0.5
+
+
+@pytest.mark.parametrize("n,first,count", [(2, 0, 20000), (2, 873192 - 5003, 5003), (4, 123457, 7001)])
+def test_contiguous_range_parity(torch_cuda, oracle_mod, n, first, count):
+    sim, o = pair(oracle_mod, n)
+    got = sim.eval_batch(n=count, first=first).cpu().numpy()
+    want = o.eval_many(first=first, n=count, threads=THREADS)
+    assert_equal(np.arange(first, first + count), got, want)
+
+
+@pytest.mark.parametrize("seed", [100, 101, 102, 103, 104, 105])
+def test_tiny_space_full_parity_and_topk(torch_cuda, oracle_mod, seed):
+    sim, o = pair(oracle_mod, f"tiny-{seed}")
+    N = o.space_size()
+    got = sim.eval_batch(n=N).cpu().numpy()
+    want = o.eval_many(first=0, n=N, threads=THREADS)
+    assert_equal(np.arange(N), got, want)
+    k = min(16, N)
+    t, i = sim.topk(k)
+    wt, wi = o.topk(k)
+    nv = len(wt)
+    assert np.array_equal(t.cpu().numpy()[:nv], wt) and np.array_equal(i.cpu().numpy()[:nv], wi)
+    assert np.all(t.cpu().numpy()[nv:] == np.iinfo(np.int64).max) and np.all(i.cpu().numpy()[nv:] == -1)
+
+
+def test_topk_matches_brute_force_config2(torch_cuda, oracle_mod):
+    sim, o = pair(oracle_mod, 2)
+    first, n = 200000, 30000
+    want = o.eval_many(first=first, n=n, threads=THREADS)
+    ok = np.nonzero(want >= 0)[0]
+    order = np.lexsort((ok, want[ok]))
+    for k in (1, 7, 100, 1024):
+        t, i = sim.topk(k, n=n, first=first)
+        exp = order[:k]
+        assert np.array_equal(t.cpu().numpy(), want[ok][exp])
+        assert np.array_equal(i.cpu().numpy(), ok[exp] + first)
+
+
+def test_topk_with_out_ns_and_block_cyclic(torch_cuda, oracle_mod):
+    torch = torch_cuda
+    sim, o = pair(oracle_mod, 4)
+    block, stride, n = 1000, 4000, 9000   # block-cyclic shard r=1 of 4 ranks
+    first = 1000
+    idx = np.array([first + (t // block) * stride + t % block for t in range(n)], dtype=np.int64)
+    out = torch.empty(n, dtype=torch.int64, device="cuda")
+    t, i = sim.topk(5, n=n, first=first, block=block, stride=stride, out_ns=out)
+    want = o.eval_many(idx, threads=THREADS)
+    assert_equal(idx, out.cpu().numpy(), want)
+    ok = np.nonzero(want >= 0)[0]
+    order = np.lexsort((idx[ok], want[ok]))[:5]
+    assert np.array_equal(t.cpu().numpy(), want[ok][order])
+    assert np.array_equal(i.cpu().numpy(), idx[ok][order])
+
+
+def test_edge_cases(torch_cuda, oracle_mod):
+    torch = torch_cuda
+    from paper_2508_05370_b200 import HsimError
+    sim, o = pair(oracle_mod, 1)
+    assert sim.eval_batch(n=0).numel() == 0
+    t, i = sim.topk(3, n=0)
+    assert t.cpu().tolist() == [np.iinfo(np.int64).max] * 3 and i.cpu().tolist() == [-1] * 3
+    t, i = sim.topk(4, n=1)          # k > number of valid candidates
+    assert t.cpu().tolist()[0] == o.eval(0) and i.cpu().tolist() == [0, -1, -1, -1]
+    with pytest.raises(HsimError):
+        sim.eval_batch(n=2)          # range past N
+    with pytest.raises(HsimError):
+        sim.topk(0, n=1)
+    out = sim.eval_batch(idx=torch.tensor([0, 5, -1, 0], device="cuda")).cpu().tolist()
+    assert out[0] == out[3] == o.eval(0) and out[1] == out[2] == np.iinfo(np.int64).min
+
+
+def test_launch_count_is_native(torch_cuda, oracle_mod):
+    sim, _ = pair(oracle_mod, 2)
+    sim.eval_batch(n=1000)
+    assert sim.last_launch_count() == 1
+    sim.topk(8, n=1000)
+    assert sim.last_launch_count() == 2
+
+
+@pytest.mark.skipif(os.environ.get("HSIM_FULL") != "1", reason="exhaustive run: set HSIM_FULL=1")
+def test_config2_exhaustive(torch_cuda, oracle_mod):
+    sim, o = pair(oracle_mod, 2)
+    N = o.space_size()
+    got = sim.eval_batch(n=N).cpu().numpy()
+    want = o.eval_many(first=0, n=N, threads=THREADS)
+    assert_equal(np.arange(N), got, want)
