@@ -75,7 +75,7 @@ struct hsim_handle {
   Dur& dur_at(int t, int lg, int bi) { return dur[((size_t)t * 4 + lg) * bs.size() + bi]; }
   u64 tp_mask[MAXT][4];
   // templates
-  std::vector<i64> prefix;
+  std::vector<i64> prefix, cprefix;
   std::vector<TplRec> tpl;
   std::vector<i64> pool;
   std::map<std::vector<int>, int32_t> crec_of;
@@ -86,6 +86,9 @@ struct hsim_handle {
   // device
   Tables* dT = nullptr;
   i64* d_prefix = nullptr;
+  i64* d_cprefix = nullptr;
+  i64* d_work = nullptr;      // work counter + per-range plan (kernels.cu)
+  size_t work_cap = 0;
   TplRec* d_tpl = nullptr;
   i64* d_pool = nullptr;
   int8_t* d_node_type = nullptr;
@@ -399,13 +402,20 @@ int32_t hsim_handle::crec(int bi, int M, int D, const std::vector<std::pair<int,
   for (int r = 0; r < D; ++r)
     if (seen.emplace(cv[r], r).second) rep.push_back(r);
   const int32_t off = (int32_t)pool.size();
-  if ((size_t)off + 2 + 16 * P + rep.size() * P > (size_t)INT32_MAX) fail(HSIM_ERANGE, "class-record pool exceeds 2^31 entries");
-  CrecHdr hd{P, D, (int32_t)rep.size(), P <= md.pmax_perturb ? P - 1 : 0};
-  pool.resize(off + 2 + 16 * P + rep.size() * P);
+  if ((size_t)off + HDR_WORDS + 16 * P + rep.size() * P > (size_t)INT32_MAX)
+    fail(HSIM_ERANGE, "class-record pool exceeds 2^31 entries");
+  CrecHdr hd{};
+  hd.P = P;
+  hd.D = D;
+  hd.U = (int32_t)rep.size();
+  hd.nd = P <= md.pmax_perturb ? P - 1 : 0;
+  hd.pw = 1;
+  for (int q = 0; q < hd.nd; ++q) hd.pw *= (u32)(2 * md.r_layer + 1);
+  pool.resize(off + HDR_WORDS + 16 * P + rep.size() * P);
   std::memcpy(&pool[off], &hd, sizeof hd);
-  std::memcpy(&pool[off + 2], sr.data(), sizeof(StageRec) * P);
+  std::memcpy(&pool[off + HDR_WORDS], sr.data(), sizeof(StageRec) * P);
   for (size_t u = 0; u < rep.size(); ++u) {
-    i64* sub = &pool[off + 2 + 16 * P + u * P];
+    i64* sub = &pool[off + HDR_WORDS + 16 * P + u * P];
     sub[0] = rep[u];
     for (int s = 0; s + 1 < P; ++s) sub[1 + s] = cv[rep[u]][s];
   }
@@ -541,7 +551,11 @@ void hsim_handle::prepare() {
   hT.n_lc = (int32_t)lcs.size();
   hT.n_nodes = cd.n_nodes;
   for (size_t k = 0; k < lcs.size(); ++k) hT.lc[k] = lcs[k];
+  cprefix.assign(prefix.size(), 0);
+  for (size_t k = 0; k + 1 < prefix.size(); ++k) cprefix[k + 1] = cprefix[k] + (prefix[k + 1] - prefix[k] + CHUNK - 1) / CHUNK;
+  hT.n_chunks = cprefix.back();
   hT.tpl_prefix = prefix.data();
+  hT.tpl_cprefix = cprefix.data();
   hT.tpl = tpl.data();
   hT.pool = pool.data();
   hT.node_type = node_type8.data();
@@ -553,6 +567,9 @@ void hsim_handle::upload() {
   };
   Tables dt = hT;
   ck(cudaMalloc(&d_prefix, prefix.size() * 8), "cudaMalloc prefix");
+  ck(cudaMalloc(&d_cprefix, cprefix.size() * 8), "cudaMalloc cprefix");
+  ck(cudaMemcpy(d_cprefix, cprefix.data(), cprefix.size() * 8, cudaMemcpyHostToDevice), "H2D cprefix");
+  dt.tpl_cprefix = d_cprefix;
   ck(cudaMalloc(&d_tpl, std::max<size_t>(1, tpl.size()) * sizeof(TplRec)), "cudaMalloc tpl");
   ck(cudaMalloc(&d_pool, std::max<size_t>(1, pool.size()) * 8), "cudaMalloc pool");
   ck(cudaMalloc(&d_node_type, node_type8.size()), "cudaMalloc nodes");
@@ -638,6 +655,8 @@ int hsim_create(const hsim_cluster_desc* cluster, const hsim_model_desc* model, 
 void hsim_destroy(hsim_handle* h) {
   if (!h) return;
   cudaFree(h->d_prefix);
+  cudaFree(h->d_cprefix);
+  cudaFree(h->d_work);
   cudaFree(h->d_tpl);
   cudaFree(h->d_pool);
   cudaFree(h->d_node_type);
@@ -673,7 +692,12 @@ int hsim_decode(const hsim_handle* h, int64_t i, char* json, size_t cap) {
     s += "\"D\":" + std::to_string(hd->D) + ",\"subclasses\":" + std::to_string(hd->U) + ",\"stages\":[";
     for (int q = 0; q < hd->P; ++q) s += (q ? ",[" : "[") + std::to_string(sr[q].type) + "," + std::to_string(sr[q].tp) + "]";
     s += "],\"layers\":[";
-    for (int q = 0; q < hd->P; ++q) s += (q ? "," : "") + std::to_string(st == -1 ? sr[q].l0 : sp.l[c][q]);
+    {
+      u32 dig = (u32)(i - tp.prefix);
+      for (int c2 = 0; c2 < c; ++c2) dig /= crec_hdr(h->hT, tp.crec[c2])->pw;
+      LayerWalk lw = walk(h->hT, hd, dig % hd->pw);
+      for (int q = 0; q < hd->P; ++q) s += (q ? "," : "") + std::to_string(lw.next(sr));
+    }
     s += "],\"mb\":[";
     if (st == 0)
       for (int r = 0; r < hd->D; ++r) s += (r ? "," : "") + std::to_string(replica_mb(sp, c, r));
@@ -757,6 +781,18 @@ int64_t hsim_count_cells(const hsim_handle* h, int64_t first, int64_t n) {
 
 // scratch accessor for kernels.cu
 namespace hsim {
+int ensure_work_scratch(hsim_handle* h, size_t entries, int64_t** out) {
+  if (entries > h->work_cap) {
+    cudaFree(h->d_work);
+    h->d_work = nullptr;
+    h->work_cap = 0;
+    if (cudaMalloc(&h->d_work, entries * 8) != cudaSuccess) { g_err = "cudaMalloc work scratch"; return HSIM_ENOMEM; }
+    h->work_cap = entries;
+  }
+  *out = h->d_work;
+  return 0;
+}
+const Tables& host_tables(const hsim_handle* h) { return h->hT; }
 int ensure_block_scratch(hsim_handle* h, size_t entries, int64_t** out) {
   if (entries > h->blk_cap) {
     cudaFree(h->d_blk);

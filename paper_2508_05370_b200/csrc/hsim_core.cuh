@@ -8,7 +8,7 @@
 // hsim_decode's JSON (never to produce a timing: there is no CPU path).
 //
 // Exactness (DESIGN.md C.0): durations are ceil((double)x / r), one IEEE RN
-// division (nvcc -prec-div default; host built with -ffp-contract=off), the
+// division (__ddiv_rn on the device; host built with -ffp-contract=off), the
 // rest int64 + / max.  Device code is compiled with -fmad=false.
 #pragma once
 #include <stdint.h>
@@ -23,13 +23,15 @@ namespace hsim {
 
 typedef int64_t i64;
 typedef uint64_t u64;
+typedef uint32_t u32;
 
 constexpr int MAXT = 4;      // device types
 constexpr int MAXG = 8;      // GPUs per node
 constexpr int MAXC = 4;      // classes per template
 constexpr int MAXP = 64;     // stages per pipeline
 constexpr int MAXLC = 64;    // distinct link classes
-constexpr int MAXB = 8;      // micro-batch sizes
+constexpr int FASTP = 8;     // pipelines up to this depth run register-resident (compile-time P)
+constexpr int CHUNK = 32;    // candidates per scheduling chunk (one warp)
 
 struct Link { i64 alpha; double beta; };  // alpha ns, beta B/ns
 
@@ -49,8 +51,12 @@ static_assert(sizeof(StageRec) == 128, "StageRec layout");
 
 struct CrecHdr {
   int32_t P, D, U, nd;    // stages, replicas, sub-classes, #layer digits
+  u32 pw;                 // (2 r_layer + 1)^nd: radix of the class's digit block
+  int32_t _pad[3];
 };
-// crec layout in the int64 pool: CrecHdr (16 B) | StageRec[P] | U x (i64 k_u, i64 c[P-1])
+static_assert(sizeof(CrecHdr) == 32, "CrecHdr layout");
+// crec layout in the int64 pool: CrecHdr (4 x i64) | StageRec[P] (16 x i64 each) | U x (i64 k_u, i64 c[P-1])
+constexpr int HDR_WORDS = 4;
 
 struct TplRec {
   i64 prefix;             // first candidate index
@@ -66,8 +72,9 @@ struct Tables {
   i64 seg_last_bytes;     // (V*h*!tied + h)*bpe_grad (head + final norm with layer L-1)
   int32_t r_layer, r_batch;
   // templates
-  i64 n_tpl, N;
-  const i64* tpl_prefix;  // [n_tpl + 1]
+  i64 n_tpl, N, n_chunks;
+  const i64* tpl_prefix;  // [n_tpl + 1] first candidate of each template
+  const i64* tpl_cprefix; // [n_tpl + 1] first chunk of each template (chunks never straddle templates)
   const TplRec* tpl;      // [n_tpl]
   const i64* pool;        // crec pool
   // links
@@ -106,29 +113,31 @@ HD i64 eval_mask(const Tables& T, u64 mask, i64 x) {
 }
 
 HD const CrecHdr* crec_hdr(const Tables& T, int32_t off) { return (const CrecHdr*)(T.pool + off); }
-HD const StageRec* crec_stages(const Tables& T, int32_t off) { return (const StageRec*)(T.pool + off + 2); }
+HD const StageRec* crec_stages(const Tables& T, int32_t off) { return (const StageRec*)(T.pool + off + HDR_WORDS); }
 HD const i64* crec_sub(const Tables& T, int32_t off, int P, int u) {
-  return T.pool + off + 2 + 16 * P + (i64)u * P;  // (k_u, c[0..P-2]) = P int64
+  return T.pool + off + HDR_WORDS + 16 * P + (i64)u * P;  // (k_u, c[0..P-2]) = P int64
 }
 
-// template of candidate i: max{tau : prefix[tau] <= i}
-HD i64 find_template(const Tables& T, i64 i) {
-  i64 lo = 0, hi = T.n_tpl;
+// upper_bound(x) - 1 over a sorted int64 array of n+1 entries (first entry 0)
+HD i64 bsearch_le(const i64* a, i64 n, i64 x) {
+  i64 lo = 0, hi = n;
   while (hi - lo > 1) {
     i64 mid = (lo + hi) >> 1;
-    if (T.tpl_prefix[mid] <= i) lo = mid; else hi = mid;
+    if (a[mid] <= x) lo = mid; else hi = mid;
   }
   return lo;
 }
+HD i64 find_template(const Tables& T, i64 i) { return bsearch_le(T.tpl_prefix, T.n_tpl, i); }
 
-// Decoded + partitioned candidate (step 1).
+// Decoded + partitioned candidate (steps a0 + a1), without per-stage arrays:
+// layer counts are re-derived from the class's digit block when needed.
 struct Split {
-  int32_t C;
-  int32_t l[MAXC][MAXP];     // layers per stage
+  u32 dig[MAXC];             // digit block of each class (boundary digits, LSB = boundary 0)
   i64 q[MAXC];               // Hamilton floor per replica of class c
   i64 seats[MAXC];           // replicas 0..seats-1 of class c get +1
   i64 add[MAXC];             // epsilon (c < C-1) or floor(R / D_last)
   i64 rm;                    // last class: replicas < rm get +1
+  int32_t C;
 };
 HD i64 replica_mb(const Split& s, int c, i64 k) {
   i64 m = s.q[c] + (k < s.seats[c] ? 1 : 0) + s.add[c];
@@ -136,38 +145,55 @@ HD i64 replica_mb(const Split& s, int c, i64 k) {
   return m;
 }
 
-// Steps a0 + a1: digits (LSB first: class boundaries, then batch digits),
-// layer split = template base split + delta_s - delta_{s-1}, batch split =
-// Hamilton over all replicas with weights floor(2^40 / slowest stage) (C.4).
-// Returns 0, -1 (layer) or -2 (batch).
+// Sequential walk over one class's stages: l_s = l0_s + delta_s - delta_{s-1}
+// with delta_s = digit_s - r (DESIGN.md C.2/C.4).
+struct LayerWalk {
+  u32 dig;
+  int nd, dprev, s;
+  u32 bl;
+  int r;
+  HD int next(const StageRec* st) {
+    int d = 0;
+    if (s < nd) { d = (int)(dig % bl) - r; dig /= bl; }
+    int l = st[s].l0 + d - dprev;
+    dprev = d;
+    ++s;
+    return l;
+  }
+};
+HD LayerWalk walk(const Tables& T, const CrecHdr* h, u32 dig) {
+  return LayerWalk{dig, h->nd, 0, 0, (u32)(2 * T.r_layer + 1), T.r_layer};
+}
+
+// Digits are least-significant first: class 0's boundaries, class 1's, ...,
+// then the batch digits of classes 0..C-2.  Layer split = template base split
+// + deltas; batch split = Hamilton over all replicas with weights
+// floor(2^40 / slowest stage) (C.4).  Returns 0, -1 (layer) or -2 (batch).
 HD int partition(const Tables& T, const TplRec& tp, i64 local, Split& sp) {
   const int C = tp.C;
   sp.C = C;
-  const i64 bl = 2 * T.r_layer + 1, bb = 2 * T.r_batch + 1;
-  uint32_t loc = (uint32_t)local;  // radix < 2^31 (validated at create)
+  const u32 bb = (u32)(2 * T.r_batch + 1);
+  u32 loc = (u32)local;  // radix < 2^31 (validated at create)
   i64 w[MAXC];
   int status = 0;
   for (int c = 0; c < C; ++c) {
     const CrecHdr* h = crec_hdr(T, tp.crec[c]);
     const StageRec* st = crec_stages(T, tp.crec[c]);
-    const int P = h->P;
-    int dprev = 0;
+    sp.dig[c] = loc % h->pw;
+    loc /= h->pw;
+    LayerWalk lw = walk(T, h, sp.dig[c]);
     i64 worst = 0;
-    for (int s = 0; s < P; ++s) {
-      int d = 0;
-      if (s < h->nd) { d = (int)(loc % (uint32_t)bl) - T.r_layer; loc /= (uint32_t)bl; }
-      int l = st[s].l0 + d - dprev;
-      dprev = d;
-      sp.l[c][s] = l;
+    for (int s = 0; s < h->P; ++s) {
+      const int l = lw.next(st);
       if (l < 1) status = -1;
       worst = imax(worst, (i64)l * st[s].tcomp + st[s].wext);
     }
-    w[c] = worst > 0 ? ((i64)1 << 40) / worst : 0;
+    w[c] = ((i64)1 << 40) / worst;
   }
   if (status) return status;
   i64 W = 0, eps[MAXC], R = 0;
   for (int c = 0; c < C; ++c) W += (i64)crec_hdr(T, tp.crec[c])->D * w[c];
-  for (int c = 0; c < C - 1; ++c) { eps[c] = (i64)(loc % (uint32_t)bb) - T.r_batch; loc /= (uint32_t)bb; }
+  for (int c = 0; c < C - 1; ++c) { eps[c] = (i64)(loc % bb) - T.r_batch; loc /= bb; }
   i64 left = tp.M, rem[MAXC];
   for (int c = 0; c < C; ++c) {
     sp.q[c] = (i64)tp.M * w[c] / W;
@@ -182,7 +208,7 @@ HD int partition(const Tables& T, const TplRec& tp, i64 local, Split& sp) {
     for (int c = 0; c < C; ++c)
       if (!done[c] && (best < 0 || rem[c] > rem[best])) best = c;
     done[best] = true;
-    i64 D = crec_hdr(T, tp.crec[best])->D;
+    const i64 D = crec_hdr(T, tp.crec[best])->D;
     sp.seats[best] = imin(D, left);
     left -= sp.seats[best];
   }
@@ -191,7 +217,7 @@ HD int partition(const Tables& T, const TplRec& tp, i64 local, Split& sp) {
     R -= (i64)crec_hdr(T, tp.crec[c])->D * eps[c];
   }
   const i64 Dl = crec_hdr(T, tp.crec[C - 1])->D;
-  i64 fl = R >= 0 ? R / Dl : -((-R + Dl - 1) / Dl);
+  const i64 fl = R >= 0 ? R / Dl : -((-R + Dl - 1) / Dl);
   sp.add[C - 1] = fl;
   sp.rm = R - fl * Dl;
   for (int c = 0; c < C; ++c)
@@ -201,74 +227,160 @@ HD int partition(const Tables& T, const TplRec& tp, i64 local, Split& sp) {
 
 // --- step a4: non-interleaved 1F1B as a level-synchronous max-plus sweep -----
 // Level of F(s,j): s+j if j <= P-1-s else 2j+s; of B(s,j): 2P-1-s+2j
-// (DESIGN.md C.7).  Every op's inputs were produced at an earlier level, so a
-// sweep over levels with stages in any order inside a level is a topological
-// order of the 1F1B DAG; at most one op per stage per level.
+// (DESIGN.md C.7).  Every op's inputs were produced at an earlier level, at
+// most one op per stage per level, and the only same-level hazard is F(s-1)
+// next to F(s) in the warm-up, so stages are visited in descending order.
+// State per stage: X = end of its last op, R = last F end + c_s (what stage
+// s+1 receives), Lb = last B end + c_{s-1} (what stage s-1 receives).
 HD i64 level_F(int P, int s, i64 j) { return j <= P - 1 - s ? s + j : 2 * j + s; }
 HD i64 level_B(int P, int s, i64 j) { return 2 * P - 1 - s + 2 * j; }
 
-HD i64 pipeline_1f1b(int P, i64 m, const i64* f, const i64* g, const i64* c) {
-  i64 lastF[MAXP], lastB[MAXP], last[MAXP], jf[MAXP], jb[MAXP];
-  for (int s = 0; s < P; ++s) { lastF[s] = lastB[s] = last[s] = 0; jf[s] = jb[s] = 0; }
+// generic depth (P <= MAXP), per-thread arrays
+HD i64 pipeline_generic(int P, i64 m, const i64* f, const i64* g, const i64* c) {
+  i64 X[MAXP], R[MAXP], Lb[MAXP];
+  i64 lastF = 0;
+  for (int s = 0; s < P; ++s) X[s] = R[s] = Lb[s] = 0;
   const i64 levels = 2 * (m + P - 1);
   for (i64 lv = 0; lv < levels; ++lv) {
-    i64 leftF_prev = 0;  // lastF[s-1] as of the end of the previous level
-    for (int s = 0; s < P; ++s) {
-      const i64 oldF = lastF[s];
-      if (jf[s] < m && level_F(P, s, jf[s]) == lv) {
-        i64 in = s == 0 ? 0 : leftF_prev + c[s - 1];
-        i64 e = imax(last[s], in) + f[s];
-        lastF[s] = last[s] = e;
-        jf[s]++;
-      } else if (jb[s] < m && level_B(P, s, jb[s]) == lv) {
-        i64 in = s == P - 1 ? lastF[s] : lastB[s + 1] + c[s];
-        i64 e = imax(last[s], in) + g[s];
-        lastB[s] = last[s] = e;
-        jb[s]++;
+    for (int s = P - 1; s >= 0; --s) {
+      const i64 jw = lv - s, js = lv - s, jb = lv - (2 * P - 1 - s);
+      const bool isF = (jw >= 0 && lv <= P - 1 && jw < m) || (lv >= 2 * P - s && !(js & 1) && (js >> 1) < m);
+      const bool isB = jb >= 0 && !(jb & 1) && (jb >> 1) < m;
+      if (isF) {
+        const i64 e = imax(X[s], s == 0 ? 0 : R[s - 1]) + f[s];
+        X[s] = e;
+        if (s < P - 1) R[s] = e + c[s]; else lastF = e;
+      } else if (isB) {
+        const i64 e = imax(X[s], s == P - 1 ? lastF : Lb[s + 1]) + g[s];
+        X[s] = e;
+        if (s > 0) Lb[s] = e + c[s - 1];
       }
-      leftF_prev = oldF;
     }
   }
-  return lastB[0];
+  return X[0];
 }
 
-// --- whole candidate (steps a0-a5) ---------------------------------------------
-// Returns the iteration time in ns or a negative status; *cells (if non-null)
-// receives sum_u 2 * P_u * m_u (the 1F1B cells simulated).
-HD i64 eval_candidate(const Tables& T, i64 i, i64* cells) {
-  if (i < 0 || i >= T.N) return INT64_MIN;
-  const TplRec tp = T.tpl[find_template(T, i)];
-  Split sp;
-  int st = partition(T, tp, i - tp.prefix, sp);
-  if (st) return st;
-  const int C = tp.C;
-  i64 T0 = 0, ncell = 0;
-  i64 f[MAXP], g[MAXP];
-  for (int c = 0; c < C; ++c) {
-    const CrecHdr* h = crec_hdr(T, tp.crec[c]);
-    const StageRec* sr = crec_stages(T, tp.crec[c]);
-    const int P = h->P;
-    for (int s = 0; s < P; ++s) {
-      f[s] = (i64)sp.l[c][s] * sr[s].layer_f + sr[s].fext;
-      g[s] = (i64)sp.l[c][s] * sr[s].layer_b + sr[s].gext;
-    }
-    for (int u = 0; u < h->U; ++u) {
-      const i64* sub = crec_sub(T, tp.crec[c], P, u);
-      const i64 m = replica_mb(sp, c, sub[0]);
-      ncell += 2 * P * m;
-      T0 = imax(T0, pipeline_1f1b(P, m, f, g, sub + 1));
+// compile-time depth: every array is register-resident; the steady phase
+// (levels [2P-1, 2m), every stage busy, F iff level = s mod 2) has no
+// per-cell bookkeeping: one int64 max and two int64 adds per cell.
+template <int P>
+struct Pipe {
+  i64 f[P], g[P], c[P], X[P], R[P], Lb[P], lastF;
+
+  HD void generic_level(i64 lv, i64 m) {
+#pragma unroll
+    for (int s = P - 1; s >= 0; --s) {
+      const i64 js = lv - s, jb = lv - (2 * P - 1 - s);
+      const bool isF = (js >= 0 && lv <= P - 1 && js < m) || (lv >= 2 * P - s && !(js & 1) && (js >> 1) < m);
+      const bool isB = jb >= 0 && !(jb & 1) && (jb >> 1) < m;
+      if (isF) {
+        const i64 e = imax(X[s], s == 0 ? (i64)0 : R[s == 0 ? 0 : s - 1]) + f[s];
+        X[s] = e;
+        if (s < P - 1) R[s] = e + c[s]; else lastF = e;
+      } else if (isB) {
+        const i64 e = imax(X[s], s == P - 1 ? lastF : Lb[s == P - 1 ? s : s + 1]) + g[s];
+        X[s] = e;
+        if (s > 0) Lb[s] = e + c[s == 0 ? 0 : s - 1];
+      }
     }
   }
-  if (cells) *cells = ncell;
-  if (tp.D == 1) return T0;
+  // one steady level of parity par: stages with s % 2 == par run F, the others B
+  template <int par>
+  HD void steady_level() {
+#pragma unroll
+    for (int s = P - 1; s >= 0; --s) {
+      if ((s & 1) == par) {
+        const i64 e = imax(X[s], s == 0 ? (i64)0 : R[s == 0 ? 0 : s - 1]) + f[s];
+        X[s] = e;
+        if (s < P - 1) R[s] = e + c[s]; else lastF = e;
+      } else {
+        const i64 e = imax(X[s], s == P - 1 ? lastF : Lb[s == P - 1 ? s : s + 1]) + g[s];
+        X[s] = e;
+        if (s > 0) Lb[s] = e + c[s == 0 ? 0 : s - 1];
+      }
+    }
+  }
+  HD i64 run(i64 m) {
+#pragma unroll
+    for (int s = 0; s < P; ++s) X[s] = R[s] = Lb[s] = 0;
+    lastF = 0;
+    const i64 total = 2 * (m + P - 1);
+    const i64 lo = 2 * P - 1;
+    const i64 hi = m >= P ? 2 * m : lo;
+    const i64 e1 = lo < total ? lo : total;
+    for (i64 lv = 0; lv < e1; ++lv) generic_level(lv, m);
+    if (hi > lo) {
+      steady_level<1>();  // level 2P-1 is odd
+      for (i64 k = 0; k < m - P; ++k) {
+        steady_level<0>();
+        steady_level<1>();
+      }
+    }
+    for (i64 lv = hi > lo ? hi : lo; lv < total; ++lv) generic_level(lv, m);
+    return X[0];
+  }
+};
 
-  // step a5: gradient-sync segments = common refinement of the classes' layer
-  // boundaries, list-scheduled FIFO per (class, stage) group from T0.
+// T_pipe of every sub-class of class c, max-reduced into T0; adds the cells.
+template <int P>
+HD void class_pipes(const Tables& T, const TplRec& tp, const Split& sp, int c, i64& T0, i64& cells) {
+  const int32_t off = tp.crec[c];
+  const CrecHdr* h = crec_hdr(T, off);
+  const StageRec* st = crec_stages(T, off);
+  Pipe<P> p;
+  LayerWalk lw = walk(T, h, sp.dig[c]);
+#pragma unroll
+  for (int s = 0; s < P; ++s) {
+    const i64 l = lw.next(st);
+    p.f[s] = l * st[s].layer_f + st[s].fext;
+    p.g[s] = l * st[s].layer_b + st[s].gext;
+  }
+  for (int u = 0; u < h->U; ++u) {
+    const i64* sub = crec_sub(T, off, P, u);
+#pragma unroll
+    for (int s = 0; s + 1 < P; ++s) p.c[s] = sub[1 + s];
+    const i64 m = replica_mb(sp, c, sub[0]);
+    cells += 2 * P * m;
+    T0 = imax(T0, p.run(m));
+  }
+}
+
+HD void class_pipes_generic(const Tables& T, const TplRec& tp, const Split& sp, int c, i64& T0, i64& cells) {
+  const int32_t off = tp.crec[c];
+  const CrecHdr* h = crec_hdr(T, off);
+  const StageRec* st = crec_stages(T, off);
+  const int P = h->P;
+  i64 f[MAXP], g[MAXP];
+  LayerWalk lw = walk(T, h, sp.dig[c]);
+  for (int s = 0; s < P; ++s) {
+    const i64 l = lw.next(st);
+    f[s] = l * st[s].layer_f + st[s].fext;
+    g[s] = l * st[s].layer_b + st[s].gext;
+  }
+  for (int u = 0; u < h->U; ++u) {
+    const i64* sub = crec_sub(T, off, P, u);
+    const i64 m = replica_mb(sp, c, sub[0]);
+    cells += 2 * P * m;
+    T0 = imax(T0, pipeline_generic(P, m, f, g, sub + 1));
+  }
+}
+
+// --- step a5: gradient sync (C.6, C.8) -----------------------------------------
+// Segments = common refinement of the classes' layer boundaries, in ascending
+// layer order, list-scheduled FIFO per (class, stage) group from T0.
+HD i64 grad_sync(const Tables& T, const TplRec& tp, const Split& sp, i64 T0) {
+  const int C = tp.C;
   int sc[MAXC];
   i64 nextcut[MAXC], cur_free[MAXC];
+  LayerWalk lw[MAXC];
+  const StageRec* st[MAXC];
   for (int c = 0; c < C; ++c) {
+    const CrecHdr* h = crec_hdr(T, tp.crec[c]);
+    st[c] = crec_stages(T, tp.crec[c]);
+    lw[c] = walk(T, h, sp.dig[c]);
     sc[c] = 0;
-    nextcut[c] = crec_hdr(T, tp.crec[c])->P > 1 ? sp.l[c][0] : T.L;
+    const i64 l0 = lw[c].next(st[c]);
+    nextcut[c] = h->P > 1 ? l0 : T.L;
     cur_free[c] = T0;
   }
   i64 a = 0, Titer = T0;
@@ -278,20 +390,20 @@ HD i64 eval_candidate(const Tables& T, i64 i, i64* cells) {
     const i64 S = (z - a) * T.seg_layer_bytes + (a == 0 ? T.seg_first_bytes : 0) + (z == T.L ? T.seg_last_bytes : 0);
     int tstar = 1 << 30, lg = 0;
     for (int c = 0; c < C; ++c) {
-      const StageRec& s = crec_stages(T, tp.crec[c])[sc[c]];
+      const StageRec& s = st[c][sc[c]];
       if (s.tp < tstar) { tstar = s.tp; lg = s.lg_tp; }
     }
     const i64 xs = ceil_div(S, tstar);
     i64 RS = 0;
     u64 mask = 0;
     for (int c = 0; c < C; ++c) {
-      const StageRec& s = crec_stages(T, tp.crec[c])[sc[c]];
-      if (s.tp != tstar) RS = imax(RS, eval_mask(T, s.tp_mask, xs));
+      const StageRec& s = st[c][sc[c]];
+      if (s.tp != tstar) RS = imax(RS, eval_mask(T, s.tp_mask, xs));  // reshard (A14)
       mask |= s.dp_mask[lg];
       // edge from the last replica of class c to the first replica of the next
-      // class (wrap: class C-1 -> class 0), at ring q through device base + q
+      // class (wrap: class C-1 -> class 0), ring q through device base + q
       const int cn = c + 1 < C ? c + 1 : 0;
-      const StageRec& t = crec_stages(T, tp.crec[cn])[sc[cn]];
+      const StageRec& t = st[cn][sc[cn]];
       const int n1 = s.last_node, n2 = t.first_node;
       const int t1 = T.node_type[n1], t2 = T.node_type[n2];
       for (int q = 0; q < tstar; ++q) {
@@ -307,18 +419,50 @@ HD i64 eval_candidate(const Tables& T, i64 i, i64* cells) {
     const i64 end = start + RS + AR;
     for (int c = 0; c < C; ++c) cur_free[c] = end;
     Titer = imax(Titer, end);
-    // advance classes whose stage ends at z
-    for (int c = 0; c < C; ++c) {
+    for (int c = 0; c < C; ++c) {  // advance classes whose stage ends at z
       if (nextcut[c] == z && z < T.L) {
         sc[c]++;
         const int P = crec_hdr(T, tp.crec[c])->P;
-        nextcut[c] = sc[c] + 1 < P ? nextcut[c] + sp.l[c][sc[c]] : T.L;
+        const i64 l = lw[c].next(st[c]);
+        nextcut[c] = sc[c] + 1 < P ? nextcut[c] + l : T.L;
         cur_free[c] = T0;
       }
     }
     a = z;
   }
   return Titer;
+}
+
+// --- whole candidate (steps a0-a5) ---------------------------------------------
+// Returns the iteration time in ns or a negative status; *cells (if non-null)
+// receives sum_u 2 * P_u * m_u (the 1F1B cells simulated).
+HD i64 eval_in_template(const Tables& T, const TplRec& tp, i64 local, i64* cells) {
+  Split sp;
+  const int st = partition(T, tp, local, sp);
+  if (st) return st;
+  i64 T0 = 0, ncell = 0;
+  for (int c = 0; c < tp.C; ++c) {
+    switch (crec_hdr(T, tp.crec[c])->P) {
+      case 1: class_pipes<1>(T, tp, sp, c, T0, ncell); break;
+      case 2: class_pipes<2>(T, tp, sp, c, T0, ncell); break;
+      case 3: class_pipes<3>(T, tp, sp, c, T0, ncell); break;
+      case 4: class_pipes<4>(T, tp, sp, c, T0, ncell); break;
+      case 5: class_pipes<5>(T, tp, sp, c, T0, ncell); break;
+      case 6: class_pipes<6>(T, tp, sp, c, T0, ncell); break;
+      case 7: class_pipes<7>(T, tp, sp, c, T0, ncell); break;
+      case 8: class_pipes<8>(T, tp, sp, c, T0, ncell); break;
+      default: class_pipes_generic(T, tp, sp, c, T0, ncell); break;
+    }
+  }
+  if (cells) *cells = ncell;
+  if (tp.D == 1) return T0;
+  return grad_sync(T, tp, sp, T0);
+}
+
+HD i64 eval_candidate(const Tables& T, i64 i, i64* cells) {
+  if (i < 0 || i >= T.N) return INT64_MIN;
+  const TplRec tp = T.tpl[find_template(T, i)];
+  return eval_in_template(T, tp, i - tp.prefix, cells);
 }
 
 }  // namespace hsim
