@@ -15,8 +15,13 @@
 
 #ifdef __CUDACC__
 #define HD __host__ __device__ __forceinline__
+#define HDN static __host__ __device__ __noinline__   // one copy of large per-candidate bodies (I-cache)
 #else
 #define HD inline
+#define HDN static
+#endif
+#ifndef HSIM_FASTP
+#define HSIM_FASTP 8   // deepest pipeline evaluated register-resident (compile-time P)
 #endif
 
 namespace hsim {
@@ -30,7 +35,7 @@ constexpr int MAXG = 8;      // GPUs per node
 constexpr int MAXC = 4;      // classes per template
 constexpr int MAXP = 64;     // stages per pipeline
 constexpr int MAXLC = 64;    // distinct link classes
-constexpr int FASTP = 8;     // pipelines up to this depth run register-resident (compile-time P)
+constexpr int FASTP = HSIM_FASTP;
 constexpr int CHUNK = 32;    // candidates per scheduling chunk (one warp)
 
 struct Link { i64 alpha; double beta; };  // alpha ns, beta B/ns
@@ -169,7 +174,7 @@ HD LayerWalk walk(const Tables& T, const CrecHdr* h, u32 dig) {
 // then the batch digits of classes 0..C-2.  Layer split = template base split
 // + deltas; batch split = Hamilton over all replicas with weights
 // floor(2^40 / slowest stage) (C.4).  Returns 0, -1 (layer) or -2 (batch).
-HD int partition(const Tables& T, const TplRec& tp, i64 local, Split& sp) {
+HDN int partition(const Tables& T, const TplRec& tp, i64 local, Split& sp) {
   const int C = tp.C;
   sp.C = C;
   const u32 bb = (u32)(2 * T.r_batch + 1);
@@ -323,7 +328,7 @@ struct Pipe {
 
 // T_pipe of every sub-class of class c, max-reduced into T0; adds the cells.
 template <int P>
-HD void class_pipes(const Tables& T, const TplRec& tp, const Split& sp, int c, i64& T0, i64& cells) {
+HDN void class_pipes(const Tables& T, const TplRec& tp, const Split& sp, int c, i64& T0, i64& cells) {
   const int32_t off = tp.crec[c];
   const CrecHdr* h = crec_hdr(T, off);
   const StageRec* st = crec_stages(T, off);
@@ -345,7 +350,7 @@ HD void class_pipes(const Tables& T, const TplRec& tp, const Split& sp, int c, i
   }
 }
 
-HD void class_pipes_generic(const Tables& T, const TplRec& tp, const Split& sp, int c, i64& T0, i64& cells) {
+HDN void class_pipes_generic(const Tables& T, const TplRec& tp, const Split& sp, int c, i64& T0, i64& cells) {
   const int32_t off = tp.crec[c];
   const CrecHdr* h = crec_hdr(T, off);
   const StageRec* st = crec_stages(T, off);
@@ -368,7 +373,7 @@ HD void class_pipes_generic(const Tables& T, const TplRec& tp, const Split& sp, 
 // --- step a5: gradient sync (C.6, C.8) -----------------------------------------
 // Segments = common refinement of the classes' layer boundaries, in ascending
 // layer order, list-scheduled FIFO per (class, stage) group from T0.
-HD i64 grad_sync(const Tables& T, const TplRec& tp, const Split& sp, i64 T0) {
+HDN i64 grad_sync(const Tables& T, const TplRec& tp, const Split& sp, i64 T0) {
   const int C = tp.C;
   int sc[MAXC];
   i64 nextcut[MAXC], cur_free[MAXC];
@@ -436,7 +441,7 @@ HD i64 grad_sync(const Tables& T, const TplRec& tp, const Split& sp, i64 T0) {
 // --- whole candidate (steps a0-a5) ---------------------------------------------
 // Returns the iteration time in ns or a negative status; *cells (if non-null)
 // receives sum_u 2 * P_u * m_u (the 1F1B cells simulated).
-HD i64 eval_in_template(const Tables& T, const TplRec& tp, i64 local, i64* cells) {
+HDN i64 eval_in_template(const Tables& T, const TplRec& tp, i64 local, i64* cells) {
   Split sp;
   const int st = partition(T, tp, local, sp);
   if (st) return st;
@@ -445,12 +450,24 @@ HD i64 eval_in_template(const Tables& T, const TplRec& tp, i64 local, i64* cells
     switch (crec_hdr(T, tp.crec[c])->P) {
       case 1: class_pipes<1>(T, tp, sp, c, T0, ncell); break;
       case 2: class_pipes<2>(T, tp, sp, c, T0, ncell); break;
+#if HSIM_FASTP >= 3
       case 3: class_pipes<3>(T, tp, sp, c, T0, ncell); break;
+#endif
+#if HSIM_FASTP >= 4
       case 4: class_pipes<4>(T, tp, sp, c, T0, ncell); break;
+#endif
+#if HSIM_FASTP >= 5
       case 5: class_pipes<5>(T, tp, sp, c, T0, ncell); break;
+#endif
+#if HSIM_FASTP >= 6
       case 6: class_pipes<6>(T, tp, sp, c, T0, ncell); break;
+#endif
+#if HSIM_FASTP >= 7
       case 7: class_pipes<7>(T, tp, sp, c, T0, ncell); break;
+#endif
+#if HSIM_FASTP >= 8
       case 8: class_pipes<8>(T, tp, sp, c, T0, ncell); break;
+#endif
       default: class_pipes_generic(T, tp, sp, c, T0, ncell); break;
     }
   }
@@ -458,6 +475,126 @@ HD i64 eval_in_template(const Tables& T, const TplRec& tp, i64 local, i64* cells
   if (tp.D == 1) return T0;
   return grad_sync(T, tp, sp, T0);
 }
+
+#ifdef __CUDACC__
+// --- warp-cooperative path for deep pipelines (FASTP < P <= 32) ----------------
+// Lanes sweep the 1F1B anti-diagonal wavefront: lane = one stage of one
+// candidate's pipeline, floor(32 / P) candidates per pass.  Each level every
+// lane takes its left neighbour's "R" (last F end + c) and its right
+// neighbour's "Lb" (last B end + c) as of the previous level by __shfl, then
+// runs its op of this level (if any).  Same recurrence as Pipe<P>.
+__device__ __forceinline__ i64 shfl64(i64 v, int src) { return __shfl_sync(0xffffffffu, v, src); }
+__device__ __forceinline__ i64 shfl_up64(i64 v) { return __shfl_up_sync(0xffffffffu, v, 1); }
+__device__ __forceinline__ i64 shfl_down64(i64 v) { return __shfl_down_sync(0xffffffffu, v, 1); }
+
+__device__ __forceinline__ int nth_set_lane(unsigned mask, int n) {
+  for (int q = 0; q < n; ++q) mask &= mask - 1;
+  return __ffs(mask) - 1;
+}
+
+// All 32 lanes call it.  `ok` marks lanes whose candidate (this warp's
+// template) has a valid split; T0 / cells of those lanes are updated.
+static __device__ __noinline__ void warp_class_pipes(const Tables& T, const TplRec& tp, const Split& sp, int c, bool ok, i64& T0,
+                                              i64& cells) {
+  const int lane = threadIdx.x & 31;
+  const int32_t off = tp.crec[c];
+  const CrecHdr* h = crec_hdr(T, off);
+  const StageRec* st = crec_stages(T, off);
+  const int P = h->P;
+  const int nseg = 32 / P;
+  const unsigned vmask = __ballot_sync(0xffffffffu, ok);
+  const int nv = __popc(vmask);
+  const int myrank = __popc(vmask & ((1u << lane) - 1));
+  const int seg = lane / P, s = lane - seg * P;
+  for (int u = 0; u < h->U; ++u) {
+    const i64* sub = crec_sub(T, off, P, u);
+    const i64 my_m = ok ? replica_mb(sp, c, sub[0]) : 0;
+    if (ok) cells += 2 * P * my_m;
+    const i64 cR = s + 1 < P ? sub[1 + s] : 0;  // c_s (stage s -> s+1)
+    const i64 cL = s > 0 ? sub[s] : 0;          // c_{s-1}
+    for (int base = 0; base < nv; base += nseg) {
+      const int rank = base + seg;
+      const bool act = seg < nseg && rank < nv;
+      const int jl = act ? nth_set_lane(vmask, rank) : 0;
+      const i64 m = shfl64(my_m, jl);
+      const u32 dig = (u32)__shfl_sync(0xffffffffu, (int)sp.dig[c], jl);
+      // this lane's stage durations for candidate jl
+      LayerWalk lw = walk(T, h, dig);
+      int l = 0;
+      for (int q = 0; q <= s; ++q) l = lw.next(st);
+      const i64 f = act ? (i64)l * st[s].layer_f + st[s].fext : 0;
+      const i64 g = act ? (i64)l * st[s].layer_b + st[s].gext : 0;
+      i64 mm = act ? m : 0;
+      i64 lvmax = act ? 2 * (m + P - 1) : 0;
+      for (int o = 16; o > 0; o >>= 1) lvmax = imax(lvmax, (i64)__shfl_xor_sync(0xffffffffu, (long long)lvmax, o));
+      i64 X = 0, R = 0, Lb = 0, lastF = 0;
+      for (i64 lv = 0; lv < lvmax; ++lv) {
+        const i64 inF0 = shfl_up64(R);
+        const i64 inB0 = shfl_down64(Lb);
+        const i64 js = lv - s, jb = lv - (2 * P - 1 - s);
+        const bool isF = (js >= 0 && lv <= P - 1 && js < mm) || (lv >= 2 * P - s && !(js & 1) && (js >> 1) < mm);
+        const bool isB = jb >= 0 && !(jb & 1) && (jb >> 1) < mm;
+        if (isF) {
+          const i64 e = imax(X, s == 0 ? 0 : inF0) + f;
+          X = e;
+          if (s < P - 1) R = e + cR; else lastF = e;
+        } else if (isB) {
+          const i64 e = imax(X, s == P - 1 ? lastF : inB0) + g;
+          X = e;
+          if (s > 0) Lb = e + cL;
+        }
+      }
+      // candidate lane L with rank in [base, base + nseg) reads its pipeline's stage-0 lane
+      const int src = ok && myrank >= base && myrank < base + nseg ? (myrank - base) * P : 0;
+      const i64 got = shfl64(X, src);
+      if (ok && myrank >= base && myrank < base + nseg) T0 = imax(T0, got);
+    }
+  }
+}
+
+// Evaluates the candidates of one template held by the lanes with in_g set
+// (all 32 lanes call it; the template is warp-uniform).
+__device__ __forceinline__ i64 eval_group(const Tables& T, const TplRec& tp, i64 local, bool in_g) {
+  Split sp;
+  int stt = 1;
+  if (in_g) stt = partition(T, tp, local, sp);
+  const bool ok = in_g && stt == 0;
+  i64 T0 = 0, ncell = 0;
+  for (int c = 0; c < tp.C; ++c) {
+    const int P = crec_hdr(T, tp.crec[c])->P;
+    if (P > FASTP && P <= 32) {
+      warp_class_pipes(T, tp, sp, c, ok, T0, ncell);
+    } else if (ok) {
+      switch (P) {
+        case 1: class_pipes<1>(T, tp, sp, c, T0, ncell); break;
+        case 2: class_pipes<2>(T, tp, sp, c, T0, ncell); break;
+#if HSIM_FASTP >= 3
+        case 3: class_pipes<3>(T, tp, sp, c, T0, ncell); break;
+#endif
+#if HSIM_FASTP >= 4
+        case 4: class_pipes<4>(T, tp, sp, c, T0, ncell); break;
+#endif
+#if HSIM_FASTP >= 5
+        case 5: class_pipes<5>(T, tp, sp, c, T0, ncell); break;
+#endif
+#if HSIM_FASTP >= 6
+        case 6: class_pipes<6>(T, tp, sp, c, T0, ncell); break;
+#endif
+#if HSIM_FASTP >= 7
+        case 7: class_pipes<7>(T, tp, sp, c, T0, ncell); break;
+#endif
+#if HSIM_FASTP >= 8
+        case 8: class_pipes<8>(T, tp, sp, c, T0, ncell); break;
+#endif
+        default: class_pipes_generic(T, tp, sp, c, T0, ncell); break;
+      }
+    }
+  }
+  if (!ok) return in_g ? (i64)stt : INT64_MIN;
+  if (tp.D == 1) return T0;
+  return grad_sync(T, tp, sp, T0);
+}
+#endif
 
 HD i64 eval_candidate(const Tables& T, i64 i, i64* cells) {
   if (i < 0 || i >= T.N) return INT64_MIN;

@@ -29,6 +29,9 @@ int sm_count(const hsim_handle* h);
 void set_launches(hsim_handle* h, int n);
 void set_error(const char* m);
 
+#ifndef HSIM_MINB
+#define HSIM_MINB 1
+#endif
 constexpr int NT = 128;         // threads per block of K1
 constexpr int WPB = NT / 32;    // warps per block
 constexpr int MT = 256;         // threads of K3
@@ -137,7 +140,7 @@ __device__ void warp_offer(WarpTopK& w, i64 t, i64 i, bool valid) {
   }
 }
 
-__global__ void __launch_bounds__(NT) k_eval(const Tables* __restrict__ gT, Cands c, i64 nr, i64* __restrict__ work,
+__global__ void __launch_bounds__(NT, HSIM_MINB) k_eval(const Tables* __restrict__ gT, Cands c, i64 nr, i64* __restrict__ work,
                                              i64* __restrict__ out, int k, i64* __restrict__ lists) {
   __shared__ Tables sT;
   load_tables(sT, gT);
@@ -152,31 +155,37 @@ __global__ void __launch_bounds__(NT) k_eval(const Tables* __restrict__ gT, Cand
     if (lane == 0) item = atomicAdd((unsigned long long*)work, 1ull);
     item = __shfl_sync(FULL, item, 0);
     if (item >= total) break;
-    i64 t = -1, i = -1, T = INT64_MIN;
+    i64 t = -1, i = -1, T = INT64_MIN, tau = -1;
     bool valid;
     if (c.idx) {
       t = item * 32 + lane;
       valid = t < c.n;
       if (valid) {
         i = c.idx[t];
-        T = eval_candidate(sT, i, nullptr);
+        if (i >= 0 && i < sT.N) tau = find_template(sT, i);
       }
     } else {
       const i64 r = bsearch_le(pre, nr, item);
       const i64 g = c0[r] + (item - pre[r]);
-      const i64 tau = bsearch_le(sT.tpl_cprefix, sT.n_tpl, g);
-      const i64 tpre = sT.tpl_prefix[tau];
-      const i64 lo = tpre + (g - sT.tpl_cprefix[tau]) * CHUNK;
+      tau = bsearch_le(sT.tpl_cprefix, sT.n_tpl, g);
+      const i64 lo = sT.tpl_prefix[tau] + (g - sT.tpl_cprefix[tau]) * CHUNK;
       const i64 start = c.block ? c.first + r * c.stride : c.first;
       const i64 len = c.block ? imin(c.block, c.n - r * c.block) : c.n;
       const i64 end = imin(start + len, sT.tpl_prefix[tau + 1]);
       i = lo + lane;
       valid = i >= start && i < end;
-      if (valid) {
-        t = (c.block ? r * c.block : 0) + (i - start);
-        const TplRec tp = sT.tpl[tau];
-        T = eval_in_template(sT, tp, i - tpre, nullptr);
-      }
+      if (valid) t = (c.block ? r * c.block : 0) + (i - start);
+    }
+    // evaluate each template present in the warp with warp-uniform code
+    // (chunk mode: exactly one; explicit lists: lanes grouped by template)
+    unsigned todo = __ballot_sync(FULL, tau >= 0);
+    while (todo) {
+      const i64 tg = __shfl_sync(FULL, tau, __ffs(todo) - 1);
+      const bool in_g = tau == tg;
+      todo &= ~__ballot_sync(FULL, in_g);
+      const TplRec tp = sT.tpl[tg];
+      const i64 Tg = eval_group(sT, tp, i - tp.prefix, in_g);
+      if (in_g) T = Tg;
     }
     if (valid && out) out[t] = T;
     if (k) warp_offer(tk, T, i, valid && T >= 0);

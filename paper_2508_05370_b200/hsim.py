@@ -12,7 +12,7 @@ import json
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libhsim.so")
+LIB_PATH = os.environ.get("HSIM_LIB", os.path.join(HERE, "libhsim.so"))  # override: kernel-variant experiments
 
 HSIM_OK, HSIM_EINVAL, HSIM_ENOMEM, HSIM_ECUDA, HSIM_ERANGE, HSIM_ESTATE = range(6)
 STATUS = {1: "HSIM_EINVAL", 2: "HSIM_ENOMEM", 3: "HSIM_ECUDA", 4: "HSIM_ERANGE", 5: "HSIM_ESTATE"}

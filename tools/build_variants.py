@@ -1,0 +1,26 @@
+"""Builds kernel variants (macro settings) as separate .so files for A/B timing."""
+import os
+import subprocess
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2508_05370_b200 import build as B  # noqa: E402
+
+VARIANTS = {
+    "f8_nb": ["-DHSIM_FASTP=8"],
+    "f8_b4": ["-DHSIM_FASTP=8", "-DHSIM_MINB=4"],
+    "f4_b6": ["-DHSIM_FASTP=4", "-DHSIM_MINB=6"],
+    "f4_b8": ["-DHSIM_FASTP=4", "-DHSIM_MINB=8"],
+    "f2_b8": ["-DHSIM_FASTP=2", "-DHSIM_MINB=8"],
+}
+out_dir = os.path.join(B.PKG, "variants")
+os.makedirs(out_dir, exist_ok=True)
+names = sys.argv[1:] or list(VARIANTS)
+for name in names:
+    out = os.path.join(out_dir, f"libhsim_{name}.so")
+    cmd = B.nvcc_cmd(out=out, extra=tuple(VARIANTS[name]) + ("-Xptxas", "-v"))
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    lines = r.stderr.splitlines()
+    info = [lines[k + 1].strip() + " | " + lines[k + 2].strip() for k, l in enumerate(lines)
+            if "Function properties for _ZN4hsim6k_eval" in l and k + 2 < len(lines)]
+    print(name, r.returncode, info)
