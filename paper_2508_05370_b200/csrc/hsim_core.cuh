@@ -478,76 +478,140 @@ HDN i64 eval_in_template(const Tables& T, const TplRec& tp, i64 local, i64* cell
 
 #ifdef __CUDACC__
 // --- warp-cooperative path for deep pipelines (FASTP < P <= 32) ----------------
-// Lanes sweep the 1F1B anti-diagonal wavefront: lane = one stage of one
-// candidate's pipeline, floor(32 / P) candidates per pass.  Each level every
-// lane takes its left neighbour's "R" (last F end + c) and its right
-// neighbour's "Lb" (last B end + c) as of the previous level by __shfl, then
-// runs its op of this level (if any).  Same recurrence as Pipe<P>.
+// Lanes sweep the 1F1B anti-diagonal wavefront (BASELINE north_star): lane =
+// one stage s of one pipeline "job" (candidate x sub-class), floor(32 / P)
+// jobs per pass.  Every lane exports one value, the output of its most
+// recent op (F: end + c_s, B: end + c_{s-1}); an F reads its left
+// neighbour's export, a B its right neighbour's, as of the previous level --
+// in 1F1B the producer's most recent op is always the right one (DESIGN.md
+// C.7), so one 64-bit __shfl per level suffices.  Warm-up / cool-down levels
+// use the closed-form op levels; the steady levels [2P-1, 2m) alternate F/B by
+// parity with no bookkeeping.
 __device__ __forceinline__ i64 shfl64(i64 v, int src) { return __shfl_sync(0xffffffffu, v, src); }
-__device__ __forceinline__ i64 shfl_up64(i64 v) { return __shfl_up_sync(0xffffffffu, v, 1); }
-__device__ __forceinline__ i64 shfl_down64(i64 v) { return __shfl_down_sync(0xffffffffu, v, 1); }
 
 __device__ __forceinline__ int nth_set_lane(unsigned mask, int n) {
   for (int q = 0; q < n; ++q) mask &= mask - 1;
   return __ffs(mask) - 1;
 }
 
+struct LanePipe {
+  int P, s, lane;
+  i64 m, f, g, cR, cL;  // cR = c_s (0 on the last stage), cL = c_{s-1}
+  i64 X, out;
+  // one level; every lane of the warp must call it (it shuffles).  In the
+  // steady range the op is given by the parity constants, else by the
+  // closed-form levels of F(s,j) / B(s,j).
+  __device__ __forceinline__ void level(i64 lv, bool steady, int srcS, i64 durS, i64 cS, i64 zS) {
+    int src = srcS;
+    i64 dur = durS, cc = cS, z = zS;
+    bool doOp = true;
+    if (!steady) {
+      const i64 js = lv - s, jb = lv - (2 * P - 1 - s);
+      const bool isF = (js >= 0 && lv <= P - 1 && js < m) || (lv >= 2 * P - s && !(js & 1) && (js >> 1) < m);
+      const bool isB = jb >= 0 && !(jb & 1) && (jb >> 1) < m;
+      doOp = isF || isB;
+      src = isF ? lane - 1 : lane + 1;
+      dur = isF ? f : g;
+      cc = isF ? cR : cL;
+      z = (isF && s == 0) || (isB && s == P - 1) ? 0 : -1;  // stage-0 input / B right after own F
+    }
+    const i64 v = shfl64(out, src) & z;
+    if (doOp) {
+      const i64 e = imax(X, v) + dur;
+      X = e;
+      out = e + cc;
+    }
+  }
+};
+
 // All 32 lanes call it.  `ok` marks lanes whose candidate (this warp's
 // template) has a valid split; T0 / cells of those lanes are updated.
-static __device__ __noinline__ void warp_class_pipes(const Tables& T, const TplRec& tp, const Split& sp, int c, bool ok, i64& T0,
-                                              i64& cells) {
+static __device__ __noinline__ void warp_class_pipes(const Tables& T, const TplRec& tp, const Split& sp, int c, bool ok,
+                                                     i64& T0, i64& cells) {
   const int lane = threadIdx.x & 31;
   const int32_t off = tp.crec[c];
   const CrecHdr* h = crec_hdr(T, off);
   const StageRec* st = crec_stages(T, off);
-  const int P = h->P;
+  const int P = h->P, U = h->U;
   const int nseg = 32 / P;
   const unsigned vmask = __ballot_sync(0xffffffffu, ok);
   const int nv = __popc(vmask);
   const int myrank = __popc(vmask & ((1u << lane) - 1));
   const int seg = lane / P, s = lane - seg * P;
-  for (int u = 0; u < h->U; ++u) {
+  if (ok)
+    for (int u = 0; u < U; ++u) cells += 2 * P * replica_mb(sp, c, crec_sub(T, off, P, u)[0]);
+  // this lane's stage layer count is the same for every job of one candidate;
+  // it is recomputed per job from the candidate's digit block
+  const int njobs = U * nv;
+  for (int base = 0; base < njobs; base += nseg) {
+    const int q = base + seg;
+    const bool act = seg < nseg && q < njobs;
+    const int u = act ? q / nv : 0, rank = act ? q - u * nv : 0;
+    const int jl = act ? nth_set_lane(vmask, rank) : 0;
+    // fetch the job's candidate split from its lane
+    Split sj;
+    sj.C = tp.C;  // warp-uniform (this lane's own split may be unset)
+    sj.q[c] = shfl64(sp.q[c], jl);
+    sj.seats[c] = shfl64(sp.seats[c], jl);
+    sj.add[c] = shfl64(sp.add[c], jl);
+    sj.rm = shfl64(sp.rm, jl);
+    const u32 dig = (u32)__shfl_sync(0xffffffffu, (int)sp.dig[c], jl);
     const i64* sub = crec_sub(T, off, P, u);
-    const i64 my_m = ok ? replica_mb(sp, c, sub[0]) : 0;
-    if (ok) cells += 2 * P * my_m;
-    const i64 cR = s + 1 < P ? sub[1 + s] : 0;  // c_s (stage s -> s+1)
-    const i64 cL = s > 0 ? sub[s] : 0;          // c_{s-1}
-    for (int base = 0; base < nv; base += nseg) {
-      const int rank = base + seg;
-      const bool act = seg < nseg && rank < nv;
-      const int jl = act ? nth_set_lane(vmask, rank) : 0;
-      const i64 m = shfl64(my_m, jl);
-      const u32 dig = (u32)__shfl_sync(0xffffffffu, (int)sp.dig[c], jl);
-      // this lane's stage durations for candidate jl
-      LayerWalk lw = walk(T, h, dig);
-      int l = 0;
-      for (int q = 0; q <= s; ++q) l = lw.next(st);
-      const i64 f = act ? (i64)l * st[s].layer_f + st[s].fext : 0;
-      const i64 g = act ? (i64)l * st[s].layer_b + st[s].gext : 0;
-      i64 mm = act ? m : 0;
-      i64 lvmax = act ? 2 * (m + P - 1) : 0;
-      for (int o = 16; o > 0; o >>= 1) lvmax = imax(lvmax, (i64)__shfl_xor_sync(0xffffffffu, (long long)lvmax, o));
-      i64 X = 0, R = 0, Lb = 0, lastF = 0;
-      for (i64 lv = 0; lv < lvmax; ++lv) {
-        const i64 inF0 = shfl_up64(R);
-        const i64 inB0 = shfl_down64(Lb);
-        const i64 js = lv - s, jb = lv - (2 * P - 1 - s);
-        const bool isF = (js >= 0 && lv <= P - 1 && js < mm) || (lv >= 2 * P - s && !(js & 1) && (js >> 1) < mm);
-        const bool isB = jb >= 0 && !(jb & 1) && (jb >> 1) < mm;
-        if (isF) {
-          const i64 e = imax(X, s == 0 ? 0 : inF0) + f;
-          X = e;
-          if (s < P - 1) R = e + cR; else lastF = e;
-        } else if (isB) {
-          const i64 e = imax(X, s == P - 1 ? lastF : inB0) + g;
-          X = e;
-          if (s > 0) Lb = e + cL;
-        }
+    LanePipe lp;
+    lp.P = P; lp.s = s; lp.lane = lane;
+    lp.m = act ? replica_mb(sj, c, sub[0]) : 0;
+    LayerWalk lw = walk(T, h, dig);
+    int l = 0;
+    for (int k = 0; k <= s; ++k) l = lw.next(st);
+    lp.f = act ? (i64)l * st[s].layer_f + st[s].fext : 0;
+    lp.g = act ? (i64)l * st[s].layer_b + st[s].gext : 0;
+    lp.cR = act && s + 1 < P ? sub[1 + s] : 0;
+    lp.cL = act && s > 0 ? sub[s] : 0;
+    lp.X = 0;
+    lp.out = 0;
+    // level ranges: warm-up [0, lo), steady [lo, hi) per job, cool-down to total
+    const i64 lo = 2 * P - 1;
+    const i64 hi = lp.m >= P ? 2 * lp.m : lo;
+    const i64 total = act ? 2 * (lp.m + P - 1) : 0;
+    i64 totMax = total;
+    for (int o = 16; o > 0; o >>= 1) totMax = imax(totMax, (i64)__shfl_xor_sync(0xffffffffu, (long long)totMax, o));
+    i64 hiMin = act ? hi : INT64_MAX;
+    for (int o = 16; o > 0; o >>= 1) hiMin = imin(hiMin, (i64)__shfl_xor_sync(0xffffffffu, (long long)hiMin, o));
+    // per-lane constants of the two steady level parities (lo = 2P-1 is odd)
+    const bool oddS = s & 1;
+    const int srcO = oddS ? lane - 1 : lane + 1, srcE = oddS ? lane + 1 : lane - 1;
+    const i64 durO = oddS ? lp.f : lp.g, durE = oddS ? lp.g : lp.f;
+    const i64 cO = oddS ? lp.cR : lp.cL, cE = oddS ? lp.cL : lp.cR;
+    const i64 zO = (!oddS && s == P - 1) ? 0 : -1;
+    const i64 zE = (oddS ? s == P - 1 : s == 0) ? 0 : -1;
+    i64 lv = 0;
+    for (; lv < lo && lv < totMax; ++lv) lp.level(lv, false, 0, 0, 0, 0);
+    // every job is in its steady range: no bookkeeping, one shuffle per level
+    for (; lv + 1 < hiMin; lv += 2) {
+      {
+        const i64 v = shfl64(lp.out, srcO) & zO;
+        const i64 e = imax(lp.X, v) + durO;
+        lp.X = e;
+        lp.out = e + cO;
       }
-      // candidate lane L with rank in [base, base + nseg) reads its pipeline's stage-0 lane
-      const int src = ok && myrank >= base && myrank < base + nseg ? (myrank - base) * P : 0;
-      const i64 got = shfl64(X, src);
-      if (ok && myrank >= base && myrank < base + nseg) T0 = imax(T0, got);
+      {
+        const i64 v = shfl64(lp.out, srcE) & zE;
+        const i64 e = imax(lp.X, v) + durE;
+        lp.X = e;
+        lp.out = e + cE;
+      }
+    }
+    // jobs leaving their steady range at different levels, then cool-down
+    for (; lv < totMax; ++lv) {
+      const bool odd = lv & 1;
+      lp.level(lv, lv >= lo && lv < hi, odd ? srcO : srcE, odd ? durO : durE, odd ? cO : cE, odd ? zO : zE);
+    }
+    // candidate lane L: its job (u, rank) sits in segment u*nv + rank - base
+    for (int uu = 0; uu < U; ++uu) {
+      const int qq = uu * nv + myrank;
+      const bool mine = ok && qq >= base && qq < base + nseg;
+      const i64 got = shfl64(lp.X, mine ? (qq - base) * P : 0);
+      if (mine) T0 = imax(T0, got);
     }
   }
 }
