@@ -81,6 +81,7 @@ struct hsim_handle {
   std::map<std::vector<int>, int32_t> crec_of;
   std::vector<std::vector<int>> nodes_of_type;
   i64 n_of_type[MAXT] = {0, 0, 0, 0};
+  uint32_t pmask_all = 0;   // union of template depth masks (which depth kernels to launch)
   i64 N = 0;
   Tables hT{};  // host pointers (for hsim_decode)
   // device
@@ -456,7 +457,11 @@ void hsim_handle::enumerate() {
       TplRec r{};
       r.prefix = acc;
       r.b = b; r.M = (int32_t)M; r.C = (int32_t)classes.size(); r.D = (int32_t)Dt;
-      for (size_t c = 0; c < classes.size(); ++c) r.crec[c] = crec((int)bi, (int)M, classes[c].first, classes[c].second);
+      for (size_t c = 0; c < classes.size(); ++c) {
+        r.crec[c] = crec((int)bi, (int)M, classes[c].first, classes[c].second);
+        r.pmask |= 1u << std::min<int>((int)classes[c].second.size(), 31);
+      }
+      pmask_all |= r.pmask;
       const i64 R = radix_of(Ps);
       if (R >= ((i64)1 << 31)) fail(HSIM_ERANGE, "template radix exceeds 2^31");
       tpl.push_back(r);
@@ -595,7 +600,7 @@ void hsim_handle::upload() {
 namespace hsim {
 int launch_eval(hsim_handle* h, const Tables* dT, const hsim_cands* c, int64_t n, int64_t* out_ns, int32_t k,
                 int64_t* out_t, int64_t* out_i, cudaStream_t st);
-int launch_count(const Tables* dT, int64_t first, int64_t n, int64_t* d_acc, cudaStream_t st);
+int launch_count(hsim_handle* h, const Tables* dT, int64_t first, int64_t n, int64_t* d_acc, cudaStream_t st);
 int launch_merge(const int64_t* lists, int32_t nlists, int32_t k, int64_t* out_t, int64_t* out_i, cudaStream_t st);
 }
 
@@ -679,8 +684,8 @@ int hsim_decode(const hsim_handle* h, int64_t i, char* json, size_t cap) {
   if (!h) { g_err = "NULL handle"; return HSIM_ESTATE; }
   if (i < 0 || i >= h->N) { g_err = "index out of range"; return HSIM_ERANGE; }
   const TplRec& tp = h->tpl[find_template(h->hT, i)];
-  Split sp;
-  const int st = partition(h->hT, tp, i - tp.prefix, sp);
+  ClassSplit cs[MAXC];
+  const int st = partition_any(h->hT, tp, i - tp.prefix, cs);
   std::string s = "{\"index\":" + std::to_string(i) + ",\"b\":" + std::to_string(tp.b) + ",\"M\":" + std::to_string(tp.M) +
                   ",\"status\":" + std::to_string(st) + ",\"classes\":[";
   for (int c = 0; c < tp.C; ++c) {
@@ -700,7 +705,7 @@ int hsim_decode(const hsim_handle* h, int64_t i, char* json, size_t cap) {
     }
     s += "],\"mb\":[";
     if (st == 0)
-      for (int r = 0; r < hd->D; ++r) s += (r ? "," : "") + std::to_string(replica_mb(sp, c, r));
+      for (int r = 0; r < hd->D; ++r) s += (r ? "," : "") + std::to_string(mb_of(cs[c], r));
     s += "],\"place\":[";
     try {
       const auto pl = h->place(hd->D, stages);
@@ -771,7 +776,7 @@ int64_t hsim_count_cells(const hsim_handle* h, int64_t first, int64_t n) {
   g_err.clear();
   if (!h || first < 0 || n < 0 || first + n > h->N) { g_err = "index out of range"; return -1; }
   if (const_cast<hsim_handle*>(h)->ensure_device()) return -1;
-  if (launch_count(h->dT, first, n, h->d_cells, 0)) return -1;
+  if (launch_count(const_cast<hsim_handle*>(h), h->dT, first, n, h->d_cells, 0)) return -1;
   int64_t v = 0;
   if (cudaMemcpy(&v, h->d_cells, 8, cudaMemcpyDeviceToHost) != cudaSuccess) { g_err = "cudaMemcpy"; return -1; }
   return v;
@@ -793,6 +798,7 @@ int ensure_work_scratch(hsim_handle* h, size_t entries, int64_t** out) {
   return 0;
 }
 const Tables& host_tables(const hsim_handle* h) { return h->hT; }
+uint32_t depth_mask(const hsim_handle* h) { return h->pmask_all; }
 int ensure_block_scratch(hsim_handle* h, size_t entries, int64_t** out) {
   if (entries > h->blk_cap) {
     cudaFree(h->d_blk);

@@ -67,6 +67,8 @@ struct TplRec {
   i64 prefix;             // first candidate index
   int32_t b, M, C, D;     // micro-batch size, #micro-batches, classes, total replicas
   int32_t crec[MAXC];     // int64-offsets of the class records in the pool
+  uint32_t pmask;         // bit min(P, 31) set for every class depth P
+  int32_t _pad;
 };
 
 struct Tables {
@@ -134,21 +136,18 @@ HD i64 bsearch_le(const i64* a, i64 n, i64 x) {
 }
 HD i64 find_template(const Tables& T, i64 i) { return bsearch_le(T.tpl_prefix, T.n_tpl, i); }
 
-// Decoded + partitioned candidate (steps a0 + a1), without per-stage arrays:
-// layer counts are re-derived from the class's digit block when needed.
-struct Split {
-  u32 dig[MAXC];             // digit block of each class (boundary digits, LSB = boundary 0)
-  i64 q[MAXC];               // Hamilton floor per replica of class c
-  i64 seats[MAXC];           // replicas 0..seats-1 of class c get +1
-  i64 add[MAXC];             // epsilon (c < C-1) or floor(R / D_last)
-  i64 rm;                    // last class: replicas < rm get +1
-  int32_t C;
+// Decoded + partitioned candidate, per class (steps a0 + a1), without
+// per-stage arrays: layer counts are re-derived from the class's digit block.
+// Replica k of the class gets m_k = q + [k < seats] + add + [k < rm]
+// (rm = 0 except for the last class), non-increasing in k.
+struct ClassSplit {
+  u32 dig;     // boundary digits of this class (LSB = boundary 0)
+  i64 q;       // Hamilton floor per replica
+  i64 seats;   // replicas 0..seats-1 get +1 (largest remainders)
+  i64 add;     // epsilon (c < C-1) or floor(R / D_last) (last class)
+  i64 rm;      // last class: replicas < rm get +1
 };
-HD i64 replica_mb(const Split& s, int c, i64 k) {
-  i64 m = s.q[c] + (k < s.seats[c] ? 1 : 0) + s.add[c];
-  if (c == s.C - 1) m += (k < s.rm ? 1 : 0);
-  return m;
-}
+HD i64 mb_of(const ClassSplit& cs, i64 k) { return cs.q + (k < cs.seats ? 1 : 0) + cs.add + (k < cs.rm ? 1 : 0); }
 
 // Sequential walk over one class's stages: l_s = l0_s + delta_s - delta_{s-1}
 // with delta_s = digit_s - r (DESIGN.md C.2/C.4).
@@ -174,19 +173,20 @@ HD LayerWalk walk(const Tables& T, const CrecHdr* h, u32 dig) {
 // then the batch digits of classes 0..C-2.  Layer split = template base split
 // + deltas; batch split = Hamilton over all replicas with weights
 // floor(2^40 / slowest stage) (C.4).  Returns 0, -1 (layer) or -2 (batch).
-HDN int partition(const Tables& T, const TplRec& tp, i64 local, Split& sp) {
-  const int C = tp.C;
-  sp.C = C;
+template <int C>
+HD int partition_c(const Tables& T, const TplRec& tp, i64 local, ClassSplit (&cs)[C]) {
   const u32 bb = (u32)(2 * T.r_batch + 1);
   u32 loc = (u32)local;  // radix < 2^31 (validated at create)
-  i64 w[MAXC];
+  i64 w[C], D[C];
   int status = 0;
+#pragma unroll
   for (int c = 0; c < C; ++c) {
     const CrecHdr* h = crec_hdr(T, tp.crec[c]);
     const StageRec* st = crec_stages(T, tp.crec[c]);
-    sp.dig[c] = loc % h->pw;
+    D[c] = h->D;
+    cs[c].dig = loc % h->pw;
     loc /= h->pw;
-    LayerWalk lw = walk(T, h, sp.dig[c]);
+    LayerWalk lw = walk(T, h, cs[c].dig);
     i64 worst = 0;
     for (int s = 0; s < h->P; ++s) {
       const int l = lw.next(st);
@@ -196,37 +196,39 @@ HDN int partition(const Tables& T, const TplRec& tp, i64 local, Split& sp) {
     w[c] = ((i64)1 << 40) / worst;
   }
   if (status) return status;
-  i64 W = 0, eps[MAXC], R = 0;
-  for (int c = 0; c < C; ++c) W += (i64)crec_hdr(T, tp.crec[c])->D * w[c];
-  for (int c = 0; c < C - 1; ++c) { eps[c] = (i64)(loc % bb) - T.r_batch; loc /= bb; }
-  i64 left = tp.M, rem[MAXC];
+  i64 W = 0, R = 0, left = tp.M, rem[C];
+#pragma unroll
+  for (int c = 0; c < C; ++c) W += D[c] * w[c];
+#pragma unroll
   for (int c = 0; c < C; ++c) {
-    sp.q[c] = (i64)tp.M * w[c] / W;
+    cs[c].q = (i64)tp.M * w[c] / W;
     rem[c] = (i64)tp.M * w[c] % W;
-    left -= (i64)crec_hdr(T, tp.crec[c])->D * sp.q[c];
-    sp.seats[c] = 0;
+    left -= D[c] * cs[c].q;
+    cs[c].seats = 0;
+    cs[c].rm = 0;
+    if (c < C - 1) {
+      cs[c].add = (i64)(loc % bb) - T.r_batch;
+      loc /= bb;
+      R -= D[c] * cs[c].add;
+    }
   }
-  // leftover seats to the largest remainders; ties -> lower (class-major) replica
-  bool done[MAXC] = {false, false, false, false};
-  for (int pass = 0; pass < C && left > 0; ++pass) {
-    int best = -1;
-    for (int c = 0; c < C; ++c)
-      if (!done[c] && (best < 0 || rem[c] > rem[best])) best = c;
-    done[best] = true;
-    const i64 D = crec_hdr(T, tp.crec[best])->D;
-    sp.seats[best] = imin(D, left);
-    left -= sp.seats[best];
+  // leftover seats (left < sum D) to the largest remainders; ties -> lower
+  // (class-major) replica index: rank of class c = #classes ahead of it
+#pragma unroll
+  for (int c = 0; c < C; ++c) {
+    i64 before = 0;
+#pragma unroll
+    for (int o = 0; o < C; ++o)
+      if (o != c && (rem[o] > rem[c] || (rem[o] == rem[c] && o < c))) before += D[o];
+    cs[c].seats = imax(0, imin(D[c], left - before));
   }
-  for (int c = 0; c < C - 1; ++c) {
-    sp.add[c] = eps[c];
-    R -= (i64)crec_hdr(T, tp.crec[c])->D * eps[c];
-  }
-  const i64 Dl = crec_hdr(T, tp.crec[C - 1])->D;
+  const i64 Dl = D[C - 1];
   const i64 fl = R >= 0 ? R / Dl : -((-R + Dl - 1) / Dl);
-  sp.add[C - 1] = fl;
-  sp.rm = R - fl * Dl;
+  cs[C - 1].add = fl;
+  cs[C - 1].rm = R - fl * Dl;
+#pragma unroll
   for (int c = 0; c < C; ++c)
-    if (replica_mb(sp, c, crec_hdr(T, tp.crec[c])->D - 1) < 1) return -2;  // m non-increasing in k
+    if (mb_of(cs[c], D[c] - 1) < 1) return -2;  // m non-increasing in k
   return 0;
 }
 
@@ -316,7 +318,7 @@ struct Pipe {
     for (i64 lv = 0; lv < e1; ++lv) generic_level(lv, m);
     if (hi > lo) {
       steady_level<1>();  // level 2P-1 is odd
-      for (i64 k = 0; k < m - P; ++k) {
+      for (int k = 0, kn = (int)(m - P); k < kn; ++k) {
         steady_level<0>();
         steady_level<1>();
       }
@@ -326,110 +328,147 @@ struct Pipe {
   }
 };
 
-// T_pipe of every sub-class of class c, max-reduced into T0; adds the cells.
+// T_pipe of every sub-class of a class (compile-time depth), max-reduced.
+struct PipeOut { i64 T0, cells; };
+
 template <int P>
-HDN void class_pipes(const Tables& T, const TplRec& tp, const Split& sp, int c, i64& T0, i64& cells) {
-  const int32_t off = tp.crec[c];
+HD PipeOut class_pipes_inl(const Tables& T, int32_t off, const ClassSplit& cs) {
   const CrecHdr* h = crec_hdr(T, off);
   const StageRec* st = crec_stages(T, off);
   Pipe<P> p;
-  LayerWalk lw = walk(T, h, sp.dig[c]);
+  LayerWalk lw = walk(T, h, cs.dig);
 #pragma unroll
   for (int s = 0; s < P; ++s) {
     const i64 l = lw.next(st);
     p.f[s] = l * st[s].layer_f + st[s].fext;
     p.g[s] = l * st[s].layer_b + st[s].gext;
   }
+  PipeOut r{0, 0};
   for (int u = 0; u < h->U; ++u) {
     const i64* sub = crec_sub(T, off, P, u);
 #pragma unroll
     for (int s = 0; s + 1 < P; ++s) p.c[s] = sub[1 + s];
-    const i64 m = replica_mb(sp, c, sub[0]);
-    cells += 2 * P * m;
-    T0 = imax(T0, p.run(m));
+    const i64 m = mb_of(cs, sub[0]);
+    r.cells += 2 * P * m;
+    r.T0 = imax(r.T0, p.run(m));
   }
+  return r;
 }
 
-HDN void class_pipes_generic(const Tables& T, const TplRec& tp, const Split& sp, int c, i64& T0, i64& cells) {
-  const int32_t off = tp.crec[c];
+template <int P>
+HDN PipeOut class_pipes(const Tables& T, int32_t off, const ClassSplit cs) { return class_pipes_inl<P>(T, off, cs); }
+
+HDN PipeOut class_pipes_generic(const Tables& T, int32_t off, const ClassSplit cs) {
   const CrecHdr* h = crec_hdr(T, off);
   const StageRec* st = crec_stages(T, off);
   const int P = h->P;
   i64 f[MAXP], g[MAXP];
-  LayerWalk lw = walk(T, h, sp.dig[c]);
+  LayerWalk lw = walk(T, h, cs.dig);
   for (int s = 0; s < P; ++s) {
     const i64 l = lw.next(st);
     f[s] = l * st[s].layer_f + st[s].fext;
     g[s] = l * st[s].layer_b + st[s].gext;
   }
+  PipeOut r{0, 0};
   for (int u = 0; u < h->U; ++u) {
     const i64* sub = crec_sub(T, off, P, u);
-    const i64 m = replica_mb(sp, c, sub[0]);
-    cells += 2 * P * m;
-    T0 = imax(T0, pipeline_generic(P, m, f, g, sub + 1));
+    const i64 m = mb_of(cs, sub[0]);
+    r.cells += 2 * P * m;
+    r.T0 = imax(r.T0, pipeline_generic(P, m, f, g, sub + 1));
+  }
+  return r;
+}
+
+HD PipeOut thread_pipes(const Tables& T, int32_t off, const ClassSplit& cs) {
+  switch (crec_hdr(T, off)->P) {
+    case 1: return class_pipes<1>(T, off, cs);
+    case 2: return class_pipes<2>(T, off, cs);
+#if HSIM_FASTP >= 3
+    case 3: return class_pipes<3>(T, off, cs);
+#endif
+#if HSIM_FASTP >= 4
+    case 4: return class_pipes<4>(T, off, cs);
+#endif
+#if HSIM_FASTP >= 5
+    case 5: return class_pipes<5>(T, off, cs);
+#endif
+#if HSIM_FASTP >= 6
+    case 6: return class_pipes<6>(T, off, cs);
+#endif
+#if HSIM_FASTP >= 7
+    case 7: return class_pipes<7>(T, off, cs);
+#endif
+#if HSIM_FASTP >= 8
+    case 8: return class_pipes<8>(T, off, cs);
+#endif
+    default: return class_pipes_generic(T, off, cs);
   }
 }
 
 // --- step a5: gradient sync (C.6, C.8) -----------------------------------------
 // Segments = common refinement of the classes' layer boundaries, in ascending
-// layer order, list-scheduled FIFO per (class, stage) group from T0.
-HDN i64 grad_sync(const Tables& T, const TplRec& tp, const Split& sp, i64 T0) {
-  const int C = tp.C;
-  int sc[MAXC];
-  i64 nextcut[MAXC], cur_free[MAXC];
-  LayerWalk lw[MAXC];
-  const StageRec* st[MAXC];
+// layer order, list-scheduled FIFO per (class, stage) group from T0: a
+// segment starts when every group it uses is free (all classes take part).
+template <int C>
+HD i64 grad_sync_c(const Tables& T, const TplRec& tp, const ClassSplit (&cs)[C], i64 T0) {
+  int sc[C], P[C];
+  i64 nextcut[C], cur_free[C];
+  LayerWalk lw[C];
+  const StageRec* st[C];
+#pragma unroll
   for (int c = 0; c < C; ++c) {
     const CrecHdr* h = crec_hdr(T, tp.crec[c]);
+    P[c] = h->P;
     st[c] = crec_stages(T, tp.crec[c]);
-    lw[c] = walk(T, h, sp.dig[c]);
+    lw[c] = walk(T, h, cs[c].dig);
     sc[c] = 0;
     const i64 l0 = lw[c].next(st[c]);
-    nextcut[c] = h->P > 1 ? l0 : T.L;
+    nextcut[c] = P[c] > 1 ? l0 : T.L;
     cur_free[c] = T0;
   }
   i64 a = 0, Titer = T0;
   while (a < T.L) {
     i64 z = T.L;
+#pragma unroll
     for (int c = 0; c < C; ++c) z = imin(z, nextcut[c]);
     const i64 S = (z - a) * T.seg_layer_bytes + (a == 0 ? T.seg_first_bytes : 0) + (z == T.L ? T.seg_last_bytes : 0);
     int tstar = 1 << 30, lg = 0;
+#pragma unroll
     for (int c = 0; c < C; ++c) {
-      const StageRec& s = st[c][sc[c]];
-      if (s.tp < tstar) { tstar = s.tp; lg = s.lg_tp; }
+      const int tpc = st[c][sc[c]].tp;
+      if (tpc < tstar) { tstar = tpc; lg = st[c][sc[c]].lg_tp; }
     }
     const i64 xs = ceil_div(S, tstar);
-    i64 RS = 0;
-    u64 mask = 0;
+    u64 rsmask = 0, mask = 0;
+#pragma unroll
     for (int c = 0; c < C; ++c) {
       const StageRec& s = st[c][sc[c]];
-      if (s.tp != tstar) RS = imax(RS, eval_mask(T, s.tp_mask, xs));  // reshard (A14)
+      if (s.tp != tstar) rsmask |= s.tp_mask;  // reshard over this group's TP ring (A14)
       mask |= s.dp_mask[lg];
       // edge from the last replica of class c to the first replica of the next
       // class (wrap: class C-1 -> class 0), ring q through device base + q
-      const int cn = c + 1 < C ? c + 1 : 0;
-      const StageRec& t = st[cn][sc[cn]];
+      const StageRec& t = st[c + 1 < C ? c + 1 : 0][sc[c + 1 < C ? c + 1 : 0]];
       const int n1 = s.last_node, n2 = t.first_node;
       const int t1 = T.node_type[n1], t2 = T.node_type[n2];
       for (int q = 0; q < tstar; ++q) {
         const int r1 = s.last_base + q, r2 = t.first_base + q;
-        const int id = n1 == n2 ? T.lc_same[t1][r1][r2] : T.lc_cross[t1][r1][t2][r2];
-        mask |= (u64)1 << id;
+        mask |= (u64)1 << (n1 == n2 ? T.lc_same[t1][r1][r2] : T.lc_cross[t1][r1][t2][r2]);
       }
     }
-    const i64 chunk = ceil_div(xs, (i64)tp.D);
-    const i64 AR = 2 * (i64)(tp.D - 1) * eval_mask(T, mask, chunk);
+    const i64 RS = rsmask ? eval_mask(T, rsmask, xs) : 0;
+    const i64 AR = 2 * (i64)(tp.D - 1) * eval_mask(T, mask, ceil_div(xs, (i64)tp.D));
     i64 start = 0;
+#pragma unroll
     for (int c = 0; c < C; ++c) start = imax(start, cur_free[c]);
     const i64 end = start + RS + AR;
-    for (int c = 0; c < C; ++c) cur_free[c] = end;
     Titer = imax(Titer, end);
+#pragma unroll
     for (int c = 0; c < C; ++c) {  // advance classes whose stage ends at z
+      cur_free[c] = end;
       if (nextcut[c] == z && z < T.L) {
         sc[c]++;
-        const int P = crec_hdr(T, tp.crec[c])->P;
         const i64 l = lw[c].next(st[c]);
-        nextcut[c] = sc[c] + 1 < P ? nextcut[c] + l : T.L;
+        nextcut[c] = sc[c] + 1 < P[c] ? nextcut[c] + l : T.L;
         cur_free[c] = T0;
       }
     }
@@ -438,55 +477,20 @@ HDN i64 grad_sync(const Tables& T, const TplRec& tp, const Split& sp, i64 T0) {
   return Titer;
 }
 
-// --- whole candidate (steps a0-a5) ---------------------------------------------
-// Returns the iteration time in ns or a negative status; *cells (if non-null)
-// receives sum_u 2 * P_u * m_u (the 1F1B cells simulated).
-HDN i64 eval_in_template(const Tables& T, const TplRec& tp, i64 local, i64* cells) {
-  Split sp;
-  const int st = partition(T, tp, local, sp);
-  if (st) return st;
-  i64 T0 = 0, ncell = 0;
-  for (int c = 0; c < tp.C; ++c) {
-    switch (crec_hdr(T, tp.crec[c])->P) {
-      case 1: class_pipes<1>(T, tp, sp, c, T0, ncell); break;
-      case 2: class_pipes<2>(T, tp, sp, c, T0, ncell); break;
-#if HSIM_FASTP >= 3
-      case 3: class_pipes<3>(T, tp, sp, c, T0, ncell); break;
-#endif
-#if HSIM_FASTP >= 4
-      case 4: class_pipes<4>(T, tp, sp, c, T0, ncell); break;
-#endif
-#if HSIM_FASTP >= 5
-      case 5: class_pipes<5>(T, tp, sp, c, T0, ncell); break;
-#endif
-#if HSIM_FASTP >= 6
-      case 6: class_pipes<6>(T, tp, sp, c, T0, ncell); break;
-#endif
-#if HSIM_FASTP >= 7
-      case 7: class_pipes<7>(T, tp, sp, c, T0, ncell); break;
-#endif
-#if HSIM_FASTP >= 8
-      case 8: class_pipes<8>(T, tp, sp, c, T0, ncell); break;
-#endif
-      default: class_pipes_generic(T, tp, sp, c, T0, ncell); break;
-    }
+// host-side rendering of a candidate's split (hsim_decode)
+HD int partition_any(const Tables& T, const TplRec& tp, i64 local, ClassSplit* out) {
+  int st = 0;
+  switch (tp.C) {
+    case 1: { ClassSplit cs[1]; st = partition_c<1>(T, tp, local, cs); for (int c = 0; c < 1; ++c) out[c] = cs[c]; break; }
+    case 2: { ClassSplit cs[2]; st = partition_c<2>(T, tp, local, cs); for (int c = 0; c < 2; ++c) out[c] = cs[c]; break; }
+    case 3: { ClassSplit cs[3]; st = partition_c<3>(T, tp, local, cs); for (int c = 0; c < 3; ++c) out[c] = cs[c]; break; }
+    default: { ClassSplit cs[4]; st = partition_c<4>(T, tp, local, cs); for (int c = 0; c < 4; ++c) out[c] = cs[c]; break; }
   }
-  if (cells) *cells = ncell;
-  if (tp.D == 1) return T0;
-  return grad_sync(T, tp, sp, T0);
+  return st;
 }
 
 #ifdef __CUDACC__
-// --- warp-cooperative path for deep pipelines (FASTP < P <= 32) ----------------
-// Lanes sweep the 1F1B anti-diagonal wavefront (BASELINE north_star): lane =
-// one stage s of one pipeline "job" (candidate x sub-class), floor(32 / P)
-// jobs per pass.  Every lane exports one value, the output of its most
-// recent op (F: end + c_s, B: end + c_{s-1}); an F reads its left
-// neighbour's export, a B its right neighbour's, as of the previous level --
-// in 1F1B the producer's most recent op is always the right one (DESIGN.md
-// C.7), so one 64-bit __shfl per level suffices.  Warm-up / cool-down levels
-// use the closed-form op levels; the steady levels [2P-1, 2m) alternate F/B by
-// parity with no bookkeeping.
+// --- lane-per-stage 1F1B wavefront (deep pipelines), used by kernels.cu ---------
 __device__ __forceinline__ i64 shfl64(i64 v, int src) { return __shfl_sync(0xffffffffu, v, src); }
 
 __device__ __forceinline__ int nth_set_lane(unsigned mask, int n) {
@@ -524,146 +528,6 @@ struct LanePipe {
   }
 };
 
-// All 32 lanes call it.  `ok` marks lanes whose candidate (this warp's
-// template) has a valid split; T0 / cells of those lanes are updated.
-static __device__ __noinline__ void warp_class_pipes(const Tables& T, const TplRec& tp, const Split& sp, int c, bool ok,
-                                                     i64& T0, i64& cells) {
-  const int lane = threadIdx.x & 31;
-  const int32_t off = tp.crec[c];
-  const CrecHdr* h = crec_hdr(T, off);
-  const StageRec* st = crec_stages(T, off);
-  const int P = h->P, U = h->U;
-  const int nseg = 32 / P;
-  const unsigned vmask = __ballot_sync(0xffffffffu, ok);
-  const int nv = __popc(vmask);
-  const int myrank = __popc(vmask & ((1u << lane) - 1));
-  const int seg = lane / P, s = lane - seg * P;
-  if (ok)
-    for (int u = 0; u < U; ++u) cells += 2 * P * replica_mb(sp, c, crec_sub(T, off, P, u)[0]);
-  // this lane's stage layer count is the same for every job of one candidate;
-  // it is recomputed per job from the candidate's digit block
-  const int njobs = U * nv;
-  for (int base = 0; base < njobs; base += nseg) {
-    const int q = base + seg;
-    const bool act = seg < nseg && q < njobs;
-    const int u = act ? q / nv : 0, rank = act ? q - u * nv : 0;
-    const int jl = act ? nth_set_lane(vmask, rank) : 0;
-    // fetch the job's candidate split from its lane
-    Split sj;
-    sj.C = tp.C;  // warp-uniform (this lane's own split may be unset)
-    sj.q[c] = shfl64(sp.q[c], jl);
-    sj.seats[c] = shfl64(sp.seats[c], jl);
-    sj.add[c] = shfl64(sp.add[c], jl);
-    sj.rm = shfl64(sp.rm, jl);
-    const u32 dig = (u32)__shfl_sync(0xffffffffu, (int)sp.dig[c], jl);
-    const i64* sub = crec_sub(T, off, P, u);
-    LanePipe lp;
-    lp.P = P; lp.s = s; lp.lane = lane;
-    lp.m = act ? replica_mb(sj, c, sub[0]) : 0;
-    LayerWalk lw = walk(T, h, dig);
-    int l = 0;
-    for (int k = 0; k <= s; ++k) l = lw.next(st);
-    lp.f = act ? (i64)l * st[s].layer_f + st[s].fext : 0;
-    lp.g = act ? (i64)l * st[s].layer_b + st[s].gext : 0;
-    lp.cR = act && s + 1 < P ? sub[1 + s] : 0;
-    lp.cL = act && s > 0 ? sub[s] : 0;
-    lp.X = 0;
-    lp.out = 0;
-    // level ranges: warm-up [0, lo), steady [lo, hi) per job, cool-down to total
-    const i64 lo = 2 * P - 1;
-    const i64 hi = lp.m >= P ? 2 * lp.m : lo;
-    const i64 total = act ? 2 * (lp.m + P - 1) : 0;
-    i64 totMax = total;
-    for (int o = 16; o > 0; o >>= 1) totMax = imax(totMax, (i64)__shfl_xor_sync(0xffffffffu, (long long)totMax, o));
-    i64 hiMin = act ? hi : INT64_MAX;
-    for (int o = 16; o > 0; o >>= 1) hiMin = imin(hiMin, (i64)__shfl_xor_sync(0xffffffffu, (long long)hiMin, o));
-    // per-lane constants of the two steady level parities (lo = 2P-1 is odd)
-    const bool oddS = s & 1;
-    const int srcO = oddS ? lane - 1 : lane + 1, srcE = oddS ? lane + 1 : lane - 1;
-    const i64 durO = oddS ? lp.f : lp.g, durE = oddS ? lp.g : lp.f;
-    const i64 cO = oddS ? lp.cR : lp.cL, cE = oddS ? lp.cL : lp.cR;
-    const i64 zO = (!oddS && s == P - 1) ? 0 : -1;
-    const i64 zE = (oddS ? s == P - 1 : s == 0) ? 0 : -1;
-    i64 lv = 0;
-    for (; lv < lo && lv < totMax; ++lv) lp.level(lv, false, 0, 0, 0, 0);
-    // every job is in its steady range: no bookkeeping, one shuffle per level
-    for (; lv + 1 < hiMin; lv += 2) {
-      {
-        const i64 v = shfl64(lp.out, srcO) & zO;
-        const i64 e = imax(lp.X, v) + durO;
-        lp.X = e;
-        lp.out = e + cO;
-      }
-      {
-        const i64 v = shfl64(lp.out, srcE) & zE;
-        const i64 e = imax(lp.X, v) + durE;
-        lp.X = e;
-        lp.out = e + cE;
-      }
-    }
-    // jobs leaving their steady range at different levels, then cool-down
-    for (; lv < totMax; ++lv) {
-      const bool odd = lv & 1;
-      lp.level(lv, lv >= lo && lv < hi, odd ? srcO : srcE, odd ? durO : durE, odd ? cO : cE, odd ? zO : zE);
-    }
-    // candidate lane L: its job (u, rank) sits in segment u*nv + rank - base
-    for (int uu = 0; uu < U; ++uu) {
-      const int qq = uu * nv + myrank;
-      const bool mine = ok && qq >= base && qq < base + nseg;
-      const i64 got = shfl64(lp.X, mine ? (qq - base) * P : 0);
-      if (mine) T0 = imax(T0, got);
-    }
-  }
-}
-
-// Evaluates the candidates of one template held by the lanes with in_g set
-// (all 32 lanes call it; the template is warp-uniform).
-__device__ __forceinline__ i64 eval_group(const Tables& T, const TplRec& tp, i64 local, bool in_g) {
-  Split sp;
-  int stt = 1;
-  if (in_g) stt = partition(T, tp, local, sp);
-  const bool ok = in_g && stt == 0;
-  i64 T0 = 0, ncell = 0;
-  for (int c = 0; c < tp.C; ++c) {
-    const int P = crec_hdr(T, tp.crec[c])->P;
-    if (P > FASTP && P <= 32) {
-      warp_class_pipes(T, tp, sp, c, ok, T0, ncell);
-    } else if (ok) {
-      switch (P) {
-        case 1: class_pipes<1>(T, tp, sp, c, T0, ncell); break;
-        case 2: class_pipes<2>(T, tp, sp, c, T0, ncell); break;
-#if HSIM_FASTP >= 3
-        case 3: class_pipes<3>(T, tp, sp, c, T0, ncell); break;
 #endif
-#if HSIM_FASTP >= 4
-        case 4: class_pipes<4>(T, tp, sp, c, T0, ncell); break;
-#endif
-#if HSIM_FASTP >= 5
-        case 5: class_pipes<5>(T, tp, sp, c, T0, ncell); break;
-#endif
-#if HSIM_FASTP >= 6
-        case 6: class_pipes<6>(T, tp, sp, c, T0, ncell); break;
-#endif
-#if HSIM_FASTP >= 7
-        case 7: class_pipes<7>(T, tp, sp, c, T0, ncell); break;
-#endif
-#if HSIM_FASTP >= 8
-        case 8: class_pipes<8>(T, tp, sp, c, T0, ncell); break;
-#endif
-        default: class_pipes_generic(T, tp, sp, c, T0, ncell); break;
-      }
-    }
-  }
-  if (!ok) return in_g ? (i64)stt : INT64_MIN;
-  if (tp.D == 1) return T0;
-  return grad_sync(T, tp, sp, T0);
-}
-#endif
-
-HD i64 eval_candidate(const Tables& T, i64 i, i64* cells) {
-  if (i < 0 || i >= T.N) return INT64_MIN;
-  const TplRec tp = T.tpl[find_template(T, i)];
-  return eval_in_template(T, tp, i - tp.prefix, cells);
-}
 
 }  // namespace hsim

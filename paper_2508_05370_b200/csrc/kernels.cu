@@ -1,20 +1,23 @@
 // kernels.cu — the hot path on the B200 (sm_100a).
 //
-// K0 k_plan   (1 block): maps the candidate list (a range, or a block-cyclic
-//             set of ranges) onto template-aligned chunks of <= 32 candidates
-//             and resets the work counter.
-// K1 k_eval   (persistent, grid = SMs x resident blocks): each warp pulls a
-//             chunk with one atomicAdd, so its 32 lanes share one template
-//             (same classes, depths, sub-classes: no divergence); lane = one
-//             candidate: decode -> partition -> stage durations -> 1F1B
-//             max-plus (register-resident for depth <= 8) -> gradient sync.
-//             Results are stored coalesced; in top-k mode each warp keeps a
-//             sorted top-k list (threshold-filtered insertion).
-//             Explicit index lists (idx != NULL) use 32 list entries per warp.
-// K3 k_merge  (1 block): merges the per-warp sorted lists (each abandoned at
-//             its first element above the running threshold).
-// K_count     evaluation that reduces the number of 1F1B cells (algorithmic
-//             work for the ALU-roofline fraction).
+// A call (hsim_eval_batch / hsim_topk / hsim_count_cells) is processed in
+// batches of up to 2^22 work items t (candidate i = cands(t)).  Per batch, in
+// stream order, each phase a small kernel with its own register budget:
+//
+//   K_split   thread per item: decode (template by binary search, mixed-radix
+//             digits) + step (1) partition -> compact per-class split in HBM.
+//   K_pipe<P> P = 1..8, one launch per depth present: lane = (item, class of
+//             depth P); register-resident 1F1B max-plus (step 4) with stage
+//             durations (step 2) and p2p costs (step 3) -> T_pipe per class.
+//             Warps pull 32-item chunks with one atomicAdd (cost varies ~1000x).
+//   K_deep    depth > 8: the warp sweeps the 1F1B anti-diagonal wavefront,
+//             lane = stage, __shfl max-plus (BASELINE north_star mapping).
+//   K_sync    thread per item: T0 = max over classes, step (5) gradient sync
+//             with reshard (step 3), coalesced int64 store, per-warp top-k.
+//   K_merge   (top-k only, once per call) merges the per-warp sorted lists.
+//
+// Scratch per item: template index, status, per-class split (20 B), per-class
+// T_pipe (8 B) — ~100 B, i.e. < 1 % of the time at HBM rates.
 #include <cuda_runtime.h>
 
 #include "hsim.h"
@@ -24,28 +27,53 @@ namespace hsim {
 
 int ensure_block_scratch(hsim_handle* h, size_t entries, int64_t** out);
 int ensure_work_scratch(hsim_handle* h, size_t entries, int64_t** out);
-const Tables& host_tables(const hsim_handle* h);
 int sm_count(const hsim_handle* h);
+uint32_t depth_mask(const hsim_handle* h);
 void set_launches(hsim_handle* h, int n);
 void set_error(const char* m);
 
-#ifndef HSIM_MINB
-#define HSIM_MINB 1
-#endif
-constexpr int NT = 128;         // threads per block of K1
-constexpr int WPB = NT / 32;    // warps per block
-constexpr int MT = 256;         // threads of K3
-constexpr int KMAX = 1024;      // max k
+constexpr int NT = 128;            // threads per block (phase kernels)
+constexpr int MT = 256;            // threads of K_merge
+constexpr int KMAX = 1024;         // max k
+constexpr i64 NBMAX = 1 << 22;     // work items per batch
 constexpr i64 KEY_INF = INT64_MAX;
+constexpr i64 LIST_PAD = 0x7F7F7F7F7F7F7F7FLL;  // memset(0x7F) sentinel of the per-warp lists
 constexpr unsigned FULL = 0xffffffffu;
+constexpr int CNT_DEEP = 0, CNT_CELLS = 15;      // counter slots (slot P = K_pipe<P>)
 
 struct Cands {
   const i64* idx;
-  i64 first, block, stride, n;
+  i64 first, block, stride;
 };
 
-__device__ __forceinline__ bool key_less(i64 t1, i64 i1, i64 t2, i64 i2) {
-  return t1 < t2 || (t1 == t2 && i1 < i2);
+__device__ __forceinline__ i64 cand_index(const Cands& c, i64 t) {
+  if (c.idx) return c.idx[t];
+  if (c.block == 0) return c.first + t;
+  return c.first + (t / c.block) * c.stride + (t % c.block);
+}
+
+// per-batch scratch (SoA; [MAXC][nb] arrays have row stride nb)
+struct Scratch {
+  int32_t* tau;       // template index, -1 = index out of range
+  int32_t* status;    // 0 ok, -1 / -2 invalid split
+  u32* dig;           // [MAXC][nb]
+  int32_t* q;         // [MAXC][nb]
+  int32_t* seats;     // [MAXC][nb]
+  int32_t* add;       // [MAXC][nb]
+  int32_t* rm;        // [nb] (last class)
+  i64* Tc;            // [MAXC][nb] max T_pipe over the class's sub-classes
+  unsigned long long* counters;  // [16]
+  i64 nb;
+};
+
+__device__ __forceinline__ ClassSplit load_split(const Scratch& S, int c, int C, i64 t) {
+  ClassSplit cs;
+  cs.dig = S.dig[c * S.nb + t];
+  cs.q = S.q[c * S.nb + t];
+  cs.seats = S.seats[c * S.nb + t];
+  cs.add = S.add[c * S.nb + t];
+  cs.rm = c == C - 1 ? S.rm[t] : 0;
+  return cs;
 }
 
 __device__ void load_tables(Tables& sT, const Tables* __restrict__ gT) {
@@ -56,57 +84,216 @@ __device__ void load_tables(Tables& sT, const Tables* __restrict__ gT) {
   __syncthreads();
 }
 
-__device__ __forceinline__ i64 chunk_of(const Tables& T, i64 i) {
-  const i64 tau = find_template(T, i);
-  return T.tpl_cprefix[tau] + (i - T.tpl_prefix[tau]) / CHUNK;
-}
-
-// work scratch layout: [0] counter, [1] total items, [2 .. 2+nr) c0, [2+nr .. 3+2nr) prefix
-__global__ void __launch_bounds__(1024) k_plan(const Tables* __restrict__ gT, Cands c, i64 nr, i64* __restrict__ work) {
+// ---- K_split -------------------------------------------------------------------
+__global__ void __launch_bounds__(NT) k_split(const Tables* __restrict__ gT, Cands c, i64 t0, Scratch S, i64 nb) {
   __shared__ Tables sT;
-  __shared__ i64 carry_s;
-  __shared__ i64 part[1024];
   load_tables(sT, gT);
-  i64* c0 = work + 2;
-  i64* pre = work + 2 + nr;
-  if (threadIdx.x == 0) carry_s = 0;
-  __syncthreads();
-  for (i64 base = 0; base < nr; base += 1024) {
-    const i64 r = base + threadIdx.x;
-    i64 cnt = 0;
-    if (r < nr) {
-      const i64 start = c.block ? c.first + r * c.stride : c.first;
-      const i64 len = c.block ? imin(c.block, c.n - r * c.block) : c.n;
-      const i64 a = chunk_of(sT, start), b = chunk_of(sT, start + len - 1);
-      c0[r] = a;
-      cnt = b - a + 1;
+  if (blockIdx.x == 0 && threadIdx.x < 16) S.counters[threadIdx.x] = 0;
+  for (i64 t = (i64)blockIdx.x * NT + threadIdx.x; t < nb; t += (i64)gridDim.x * NT) {
+    const i64 i = cand_index(c, t0 + t);
+    if (i < 0 || i >= sT.N) {
+      S.tau[t] = -1;
+      continue;
     }
-    part[threadIdx.x] = cnt;
-    __syncthreads();
-    for (int off = 1; off < 1024; off <<= 1) {  // inclusive scan
-      const i64 v = threadIdx.x >= off ? part[threadIdx.x - off] : 0;
-      __syncthreads();
-      part[threadIdx.x] += v;
-      __syncthreads();
+    const i64 tau = find_template(sT, i);
+    const TplRec& tp = sT.tpl[tau];
+    ClassSplit cs[MAXC];
+    const int st = partition_any(sT, tp, i - tp.prefix, cs);
+    S.tau[t] = (int32_t)tau;
+    S.status[t] = st;
+    if (st == 0) {
+      for (int k = 0; k < tp.C; ++k) {
+        S.dig[k * S.nb + t] = cs[k].dig;
+        S.q[k * S.nb + t] = (int32_t)cs[k].q;
+        S.seats[k * S.nb + t] = (int32_t)cs[k].seats;
+        S.add[k * S.nb + t] = (int32_t)cs[k].add;
+      }
+      S.rm[t] = (int32_t)cs[tp.C - 1].rm;
     }
-    if (r < nr) pre[r] = carry_s + part[threadIdx.x] - cnt;
-    __syncthreads();
-    if (threadIdx.x == 1023) carry_s += part[1023];
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) {
-    pre[nr] = carry_s;
-    work[0] = 0;
-    work[1] = carry_s;
   }
 }
 
-// --- per-warp top-k list in global memory: [k times | k indices], sorted ----------
+__device__ __forceinline__ i64 warp_sum(i64 v) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, (long long)v, o);
+  return v;
+}
+
+// ---- K_pipe<P> -------------------------------------------------------------------
+template <int P>
+__global__ void __launch_bounds__(NT) k_pipe(const Tables* __restrict__ gT, Scratch S, i64 nb, int count) {
+  __shared__ Tables sT;
+  load_tables(sT, gT);
+  const int lane = threadIdx.x & 31;
+  i64 cells = 0;
+  for (;;) {
+    i64 item = 0;
+    if (lane == 0) item = (i64)atomicAdd(&S.counters[P], 1ull);
+    item = __shfl_sync(FULL, item, 0);
+    if (item * 32 >= nb) break;
+    const i64 t = item * 32 + lane;
+    if (t >= nb) continue;
+    const int tau = S.tau[t];
+    if (tau < 0 || S.status[t] != 0) continue;
+    const TplRec& tp = sT.tpl[tau];
+    if (!(tp.pmask >> P & 1)) continue;
+    for (int c = 0; c < tp.C; ++c) {
+      const int32_t off = tp.crec[c];
+      if (crec_hdr(sT, off)->P != P) continue;
+      const PipeOut r = class_pipes_inl<P>(sT, off, load_split(S, c, tp.C, t));
+      S.Tc[c * S.nb + t] = r.T0;
+      cells += r.cells;
+    }
+  }
+  if (count) {
+    cells = warp_sum(cells);
+    if (lane == 0 && cells) atomicAdd(&S.counters[CNT_CELLS], (unsigned long long)cells);
+  }
+}
+
+// ---- K_deep: lane-per-stage wavefront for depth > FASTP --------------------------
+// Packs floor(32 / P) sub-classes (same class, same candidate) per pass.
+__device__ i64 warp_pipe_class(const Tables& T, int32_t off, const ClassSplit& cs, i64* cells) {
+  const int lane = threadIdx.x & 31;
+  const CrecHdr* h = crec_hdr(T, off);
+  const StageRec* st = crec_stages(T, off);
+  const int P = h->P, U = h->U;
+  const int nseg = 32 / P;
+  const int seg = lane / P, s = lane - seg * P;
+  // stage durations of this lane's stage (same for every sub-class)
+  LayerWalk lw = walk(T, h, cs.dig);
+  int l = 0;
+  for (int k = 0; k <= s && k < P; ++k) l = lw.next(st);
+  const i64 f = seg < nseg ? (i64)l * st[s].layer_f + st[s].fext : 0;
+  const i64 g = seg < nseg ? (i64)l * st[s].layer_b + st[s].gext : 0;
+  i64 best = 0;
+  for (int base = 0; base < U; base += nseg) {
+    const int u = base + seg;
+    const bool act = seg < nseg && u < U;
+    const i64* sub = crec_sub(T, off, P, act ? u : 0);
+    LanePipe lp;
+    lp.P = P; lp.s = s; lp.lane = lane;
+    lp.m = act ? mb_of(cs, sub[0]) : 0;
+    if (act && s == 0) *cells += 2 * P * lp.m;
+    lp.f = act ? f : 0;
+    lp.g = act ? g : 0;
+    lp.cR = act && s + 1 < P ? sub[1 + s] : 0;
+    lp.cL = act && s > 0 ? sub[s] : 0;
+    lp.X = 0;
+    lp.out = 0;
+    const i64 lo = 2 * P - 1;
+    const i64 hi = lp.m >= P ? 2 * lp.m : lo;
+    i64 totMax = act ? 2 * (lp.m + P - 1) : 0;
+    i64 hiMin = act ? hi : INT64_MAX;
+    for (int o = 16; o > 0; o >>= 1) {
+      totMax = imax(totMax, (i64)__shfl_xor_sync(FULL, (long long)totMax, o));
+      hiMin = imin(hiMin, (i64)__shfl_xor_sync(FULL, (long long)hiMin, o));
+    }
+    // per-lane constants of the two steady level parities (lo = 2P-1 is odd)
+    const bool oddS = s & 1;
+    const int srcO = oddS ? lane - 1 : lane + 1, srcE = oddS ? lane + 1 : lane - 1;
+    const i64 durO = oddS ? lp.f : lp.g, durE = oddS ? lp.g : lp.f;
+    const i64 cO = oddS ? lp.cR : lp.cL, cE = oddS ? lp.cL : lp.cR;
+    const i64 zO = (!oddS && s == P - 1) ? 0 : -1;
+    const i64 zE = (oddS ? s == P - 1 : s == 0) ? 0 : -1;
+    i64 lv = 0;
+    for (; lv < lo && lv < totMax; ++lv) lp.level(lv, false, 0, 0, 0, 0);
+    for (; lv + 1 < hiMin; lv += 2) {  // every job steady: one shuffle per level
+      {
+        const i64 v = shfl64(lp.out, srcO) & zO;
+        const i64 e = imax(lp.X, v) + durO;
+        lp.X = e;
+        lp.out = e + cO;
+      }
+      {
+        const i64 v = shfl64(lp.out, srcE) & zE;
+        const i64 e = imax(lp.X, v) + durE;
+        lp.X = e;
+        lp.out = e + cE;
+      }
+    }
+    for (; lv < totMax; ++lv) {
+      const bool odd = lv & 1;
+      lp.level(lv, lv >= lo && lv < hi, odd ? srcO : srcE, odd ? durO : durE, odd ? cO : cE, odd ? zO : zE);
+    }
+    // T_pipe of each job sits on its stage-0 lane
+    i64 v = act && s == 0 ? lp.X : 0;
+    for (int o = 16; o > 0; o >>= 1) v = imax(v, (i64)__shfl_xor_sync(FULL, (long long)v, o));
+    best = imax(best, v);
+  }
+  return best;
+}
+
+__global__ void __launch_bounds__(NT) k_deep(const Tables* __restrict__ gT, Scratch S, i64 nb, int count) {
+  __shared__ Tables sT;
+  load_tables(sT, gT);
+  const int lane = threadIdx.x & 31;
+  i64 cells = 0;
+  for (;;) {
+    i64 item = 0;
+    if (lane == 0) item = (i64)atomicAdd(&S.counters[CNT_DEEP], 1ull);
+    item = __shfl_sync(FULL, item, 0);
+    if (item * 32 >= nb) break;
+    const i64 t = item * 32 + lane;
+    bool has = false;
+    int tau = -1;
+    if (t < nb) {
+      tau = S.tau[t];
+      has = tau >= 0 && S.status[t] == 0 && (sT.tpl[tau].pmask >> (FASTP + 1)) != 0;
+    }
+    unsigned todo = __ballot_sync(FULL, has);
+    while (todo) {
+      const int jl = __ffs(todo) - 1;
+      todo &= todo - 1;
+      const i64 tj = item * 32 + jl;
+      const TplRec& tp = sT.tpl[__shfl_sync(FULL, tau, jl)];
+      for (int c = 0; c < tp.C; ++c) {
+        const int32_t off = tp.crec[c];
+        const int P = crec_hdr(sT, off)->P;
+        if (P <= FASTP) continue;
+        const ClassSplit cs = load_split(S, c, tp.C, tj);
+        i64 T0;
+        if (P <= 32) {
+          i64 cl = 0;
+          T0 = warp_pipe_class(sT, off, cs, &cl);
+          cells += cl;
+        } else {  // very deep (> 32 stages): one lane, per-thread arrays
+          PipeOut r{0, 0};
+          if (lane == 0) r = class_pipes_generic(sT, off, cs);
+          T0 = __shfl_sync(FULL, (long long)r.T0, 0);
+          cells += r.cells;
+        }
+        if (lane == 0) S.Tc[c * S.nb + tj] = T0;
+      }
+    }
+  }
+  if (count) {
+    cells = warp_sum(cells);
+    if (lane == 0 && cells) atomicAdd(&S.counters[CNT_CELLS], (unsigned long long)cells);
+  }
+}
+
+// ---- per-warp top-k list in global memory: [k times | k indices], sorted ----------
 struct WarpTopK {
   i64* wl;
   int k, cnt;
   i64 thrT, thrI;
 };
+
+__device__ void warp_topk_load(WarpTopK& w) {  // lists persist across batches (pad = LIST_PAD)
+  const int lane = threadIdx.x & 31;
+  int cnt = 0;
+  for (int base = 0; base < w.k; base += 32) {
+    const int a = base + lane;
+    cnt += __popc(__ballot_sync(FULL, a < w.k && w.wl[a] != LIST_PAD));
+  }
+  w.cnt = cnt;
+  w.thrT = w.thrI = KEY_INF;
+  if (cnt == w.k) { w.thrT = w.wl[w.k - 1]; w.thrI = w.wl[2 * w.k - 1]; }
+}
+
+__device__ __forceinline__ bool key_less(i64 t1, i64 i1, i64 t2, i64 i2) {
+  return t1 < t2 || (t1 == t2 && i1 < i2);
+}
 
 __device__ void warp_offer(WarpTopK& w, i64 t, i64 i, bool valid) {
   const int lane = threadIdx.x & 31;
@@ -140,62 +327,55 @@ __device__ void warp_offer(WarpTopK& w, i64 t, i64 i, bool valid) {
   }
 }
 
-__global__ void __launch_bounds__(NT, HSIM_MINB) k_eval(const Tables* __restrict__ gT, Cands c, i64 nr, i64* __restrict__ work,
+// ---- K_sync ------------------------------------------------------------------------
+__device__ i64 sync_any(const Tables& T, const TplRec& tp, const Scratch& S, i64 t, i64 T0) {
+  switch (tp.C) {
+    case 1: { ClassSplit cs[1] = {load_split(S, 0, 1, t)}; return grad_sync_c<1>(T, tp, cs, T0); }
+    case 2: { ClassSplit cs[2] = {load_split(S, 0, 2, t), load_split(S, 1, 2, t)}; return grad_sync_c<2>(T, tp, cs, T0); }
+    case 3: {
+      ClassSplit cs[3] = {load_split(S, 0, 3, t), load_split(S, 1, 3, t), load_split(S, 2, 3, t)};
+      return grad_sync_c<3>(T, tp, cs, T0);
+    }
+    default: {
+      ClassSplit cs[4] = {load_split(S, 0, 4, t), load_split(S, 1, 4, t), load_split(S, 2, 4, t), load_split(S, 3, 4, t)};
+      return grad_sync_c<4>(T, tp, cs, T0);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(NT) k_sync(const Tables* __restrict__ gT, Cands c, i64 t0, Scratch S, i64 nb,
                                              i64* __restrict__ out, int k, i64* __restrict__ lists) {
   __shared__ Tables sT;
   load_tables(sT, gT);
   const int lane = threadIdx.x & 31;
-  const i64 wid = (i64)blockIdx.x * WPB + (threadIdx.x >> 5);
-  WarpTopK tk{lists ? lists + wid * 2 * k : nullptr, k, 0, KEY_INF, KEY_INF};
-  const i64* c0 = work + 2;
-  const i64* pre = work + 2 + nr;
-  const i64 total = c.idx ? (c.n + 31) / 32 : work[1];
-  for (;;) {
-    i64 item = 0;
-    if (lane == 0) item = atomicAdd((unsigned long long*)work, 1ull);
-    item = __shfl_sync(FULL, item, 0);
-    if (item >= total) break;
-    i64 t = -1, i = -1, T = INT64_MIN, tau = -1;
-    bool valid;
-    if (c.idx) {
-      t = item * 32 + lane;
-      valid = t < c.n;
-      if (valid) {
-        i = c.idx[t];
-        if (i >= 0 && i < sT.N) tau = find_template(sT, i);
+  const i64 wid = (i64)blockIdx.x * (NT / 32) + (threadIdx.x >> 5);
+  WarpTopK tk{k ? lists + wid * 2 * k : nullptr, k, 0, KEY_INF, KEY_INF};
+  if (k) warp_topk_load(tk);
+  const i64 nw = (i64)gridDim.x * (NT / 32);
+  for (i64 base = wid * 32; base < nb; base += nw * 32) {
+    const i64 t = base + lane;
+    i64 T = INT64_MIN, i = -1;
+    if (t < nb) {
+      i = cand_index(c, t0 + t);
+      const int tau = S.tau[t];
+      if (tau >= 0) {
+        const int st = S.status[t];
+        if (st) {
+          T = st;
+        } else {
+          const TplRec& tp = sT.tpl[tau];
+          i64 T0 = 0;
+          for (int q = 0; q < tp.C; ++q) T0 = imax(T0, S.Tc[q * S.nb + t]);
+          T = tp.D == 1 ? T0 : sync_any(sT, tp, S, t, T0);
+        }
       }
-    } else {
-      const i64 r = bsearch_le(pre, nr, item);
-      const i64 g = c0[r] + (item - pre[r]);
-      tau = bsearch_le(sT.tpl_cprefix, sT.n_tpl, g);
-      const i64 lo = sT.tpl_prefix[tau] + (g - sT.tpl_cprefix[tau]) * CHUNK;
-      const i64 start = c.block ? c.first + r * c.stride : c.first;
-      const i64 len = c.block ? imin(c.block, c.n - r * c.block) : c.n;
-      const i64 end = imin(start + len, sT.tpl_prefix[tau + 1]);
-      i = lo + lane;
-      valid = i >= start && i < end;
-      if (valid) t = (c.block ? r * c.block : 0) + (i - start);
+      if (out) out[t0 + t] = T;
     }
-    // evaluate each template present in the warp with warp-uniform code
-    // (chunk mode: exactly one; explicit lists: lanes grouped by template)
-    unsigned todo = __ballot_sync(FULL, tau >= 0);
-    while (todo) {
-      const i64 tg = __shfl_sync(FULL, tau, __ffs(todo) - 1);
-      const bool in_g = tau == tg;
-      todo &= ~__ballot_sync(FULL, in_g);
-      const TplRec tp = sT.tpl[tg];
-      const i64 Tg = eval_group(sT, tp, i - tp.prefix, in_g);
-      if (in_g) T = Tg;
-    }
-    if (valid && out) out[t] = T;
-    if (k) warp_offer(tk, T, i, valid && T >= 0);
-  }
-  if (k) {  // pad the list
-    for (int a = tk.cnt + lane; a < k; a += 32) { tk.wl[a] = KEY_INF; tk.wl[k + a] = -1; }
+    if (k) warp_offer(tk, T, i, t < nb && T >= 0);
   }
 }
 
-// --- K3: shared-memory running top-k over sorted lists ----------------------------
+// ---- K_merge: shared-memory running top-k over sorted lists -------------------------
 struct TopK {
   i64 lt[KMAX], li[KMAX];   // sorted ascending, `count` valid
   i64 nt[KMAX], ni[KMAX];   // merge target
@@ -258,22 +438,32 @@ __device__ void topk_offer(TopK& s, int k, i64 t, i64 i, bool valid) {
   __syncthreads();
 }
 
+// lists: nblk x [k times | k indices], each sorted, padded with LIST_PAD or
+// (INT64_MAX, -1) (the all_gather layout of hsim_merge_topk)
 __global__ void __launch_bounds__(MT) k_merge(const i64* __restrict__ blk, int nblk, int k, i64* __restrict__ out_t,
                                               i64* __restrict__ out_i) {
   extern __shared__ __align__(16) unsigned char dyn[];
   TopK& tk = *reinterpret_cast<TopK*>(dyn);
   if (threadIdx.x == 0) tk.count = 0;
   __syncthreads();
-  for (int b = 0; b < nblk; ++b) {
+  // MT lists at a time: each thread walks down its (sorted) list while its
+  // head can still enter the running top-k
+  for (int lb = 0; lb < nblk; lb += MT) {
+    const int b = lb + threadIdx.x;
     const i64* bt = blk + (i64)b * 2 * k;
-    for (int a0 = 0; a0 < k; a0 += MT) {
-      // each list is sorted: stop at its first element that cannot enter
-      const i64 t0 = bt[a0], i0 = bt[k + a0];
-      if (t0 == KEY_INF) break;
-      if (tk.count >= k && !key_less(t0, i0, tk.lt[k - 1], tk.li[k - 1])) break;
-      const int a = a0 + threadIdx.x;
-      const bool v = a < k && bt[a] != KEY_INF;
-      topk_offer(tk, k, v ? bt[a] : 0, v ? bt[k + a] : 0, v);
+    bool alive = b < nblk;
+    int p = 0;
+    while (__syncthreads_or(alive)) {
+      i64 t = 0, i = 0;
+      bool cand = false;
+      if (alive && p < k) {
+        t = bt[p];
+        i = bt[k + p];
+        cand = t != KEY_INF && t != LIST_PAD && (tk.count < k || key_less(t, i, tk.lt[k - 1], tk.li[k - 1]));
+      }
+      alive = cand;
+      topk_offer(tk, k, t, i, cand);
+      if (cand) ++p;
     }
   }
   __syncthreads();
@@ -283,24 +473,15 @@ __global__ void __launch_bounds__(MT) k_merge(const i64* __restrict__ blk, int n
   }
 }
 
-__global__ void __launch_bounds__(256) k_count(const Tables* __restrict__ gT, i64 first, i64 n, unsigned long long* acc) {
-  __shared__ Tables sT;
-  load_tables(sT, gT);
-  unsigned long long local = 0;
-  const i64 step = (i64)gridDim.x * 256;
-  for (i64 t = (i64)blockIdx.x * 256 + threadIdx.x; t < n; t += step) {
-    i64 cells = 0;
-    if (eval_candidate(sT, first + t, &cells) >= 0) local += (unsigned long long)cells;
+// ---- launch ------------------------------------------------------------------------
+template <typename K>
+static int grid_of(const hsim_handle* h, K kern, int& cache) {
+  if (!cache) {
+    int per = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, NT, 0) != cudaSuccess || per < 1) per = 1;
+    cache = per;
   }
-  atomicAdd(acc, local);
-}
-
-static int eval_grid(const hsim_handle* h) {
-  static int per_sm = 0;
-  if (!per_sm) {
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_eval, NT, 0) != cudaSuccess || per_sm < 1) per_sm = 1;
-  }
-  return sm_count(h) * per_sm;
+  return sm_count(h) * cache;
 }
 
 static void merge_attr() {
@@ -311,32 +492,7 @@ static void merge_attr() {
   }
 }
 
-int launch_eval(hsim_handle* h, const Tables* dT, const hsim_cands* cc, int64_t n, int64_t* out_ns, int32_t k,
-                int64_t* out_t, int64_t* out_i, cudaStream_t st) {
-  Cands c{cc->idx, cc->first, cc->block, cc->stride, n};
-  const int grid = eval_grid(h);
-  const i64 nr = c.idx ? 0 : (c.block ? (n + c.block - 1) / c.block : 1);
-  i64* work = nullptr;
-  if (ensure_work_scratch(h, (size_t)(3 + 2 * nr), &work)) return HSIM_ENOMEM;
-  i64* lists = nullptr;
-  if (k && ensure_block_scratch(h, (size_t)grid * WPB * 2 * k, &lists)) return HSIM_ENOMEM;
-  int launches = 0;
-  if (n > 0) {
-    if (c.idx) {
-      cudaMemsetAsync(work, 0, 8, st);
-    } else {
-      k_plan<<<1, 1024, 0, st>>>(dT, c, nr, work);
-      ++launches;
-    }
-    k_eval<<<grid, NT, 0, st>>>(dT, c, nr, work, out_ns, k, lists);
-    ++launches;
-  }
-  if (k) {
-    merge_attr();
-    // n == 0 merges no list and only writes the (INT64_MAX, -1) padding
-    k_merge<<<1, MT, sizeof(TopK), st>>>(lists, n > 0 ? grid * WPB : 0, k, out_t, out_i);
-    ++launches;
-  }
+static int finish(hsim_handle* h, int launches) {
   set_launches(h, launches);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
@@ -344,6 +500,96 @@ int launch_eval(hsim_handle* h, const Tables* dT, const hsim_cands* cc, int64_t 
     return HSIM_ECUDA;
   }
   return HSIM_OK;
+}
+
+// Runs the phase kernels over all work items; out / top-k lists / cell count optional.
+static int run_phases(hsim_handle* h, const Tables* dT, const Cands& c, int64_t n, int64_t* out_ns, int32_t k, i64* lists,
+                      int count, unsigned long long** counters_out, cudaStream_t st, int& launches) {
+  static int g_split = 0, g_pipe[FASTP + 1] = {0}, g_deep = 0, g_sync = 0;
+  const i64 nb = n < NBMAX ? n : NBMAX;
+  // scratch: tau, status, rm (3 x i32), dig/q/seats/add (4 x MAXC x i32), Tc (MAXC x i64), counters
+  const size_t words = (size_t)((3 + 4 * MAXC) * nb + 1) / 2 + (size_t)MAXC * nb + 16 + 8;
+  i64* base = nullptr;
+  if (ensure_work_scratch(h, words, &base)) return HSIM_ENOMEM;
+  Scratch S;
+  S.nb = nb;
+  S.Tc = base;
+  S.counters = (unsigned long long*)(base + MAXC * nb);
+  int32_t* p32 = (int32_t*)(base + MAXC * nb + 16);
+  S.tau = p32;
+  S.status = p32 + nb;
+  S.rm = p32 + 2 * nb;
+  S.dig = (u32*)(p32 + 3 * nb);
+  S.q = p32 + (3 + MAXC) * nb;
+  S.seats = p32 + (3 + 2 * MAXC) * nb;
+  S.add = p32 + (3 + 3 * MAXC) * nb;
+  if (counters_out) *counters_out = S.counters;
+  const uint32_t pm = depth_mask(h);
+  const int gs = grid_of(h, k_split, g_split), gd = grid_of(h, k_deep, g_deep), gy = grid_of(h, k_sync, g_sync);
+  for (i64 t0 = 0; t0 < n; t0 += nb) {
+    const i64 m = n - t0 < nb ? n - t0 : nb;
+    k_split<<<gs, NT, 0, st>>>(dT, c, t0, S, m);
+    ++launches;
+#define HSIM_PIPE(P)                                                               \
+    if (P <= FASTP && (pm >> P & 1)) {                                             \
+      k_pipe<P><<<grid_of(h, k_pipe<P>, g_pipe[P]), NT, 0, st>>>(dT, S, m, count); \
+      ++launches;                                                                  \
+    }
+    HSIM_PIPE(1) HSIM_PIPE(2)
+#if HSIM_FASTP >= 3
+    HSIM_PIPE(3)
+#endif
+#if HSIM_FASTP >= 4
+    HSIM_PIPE(4)
+#endif
+#if HSIM_FASTP >= 5
+    HSIM_PIPE(5)
+#endif
+#if HSIM_FASTP >= 6
+    HSIM_PIPE(6)
+#endif
+#if HSIM_FASTP >= 7
+    HSIM_PIPE(7)
+#endif
+#if HSIM_FASTP >= 8
+    HSIM_PIPE(8)
+#endif
+#undef HSIM_PIPE
+    if (pm >> (FASTP + 1)) {
+      k_deep<<<gd, NT, 0, st>>>(dT, S, m, count);
+      ++launches;
+    }
+    if (!count) {
+      Cands cb = c;
+      k_sync<<<gy, NT, 0, st>>>(dT, cb, t0, S, m, out_ns, k, lists);
+      ++launches;
+    }
+  }
+  return HSIM_OK;
+}
+
+int launch_eval(hsim_handle* h, const Tables* dT, const hsim_cands* cc, int64_t n, int64_t* out_ns, int32_t k,
+                int64_t* out_t, int64_t* out_i, cudaStream_t st) {
+  Cands c{cc->idx, cc->first, cc->block, cc->stride};
+  static int g_sync = 0;
+  int launches = 0;
+  i64* lists = nullptr;
+  const int nlists = grid_of(h, k_sync, g_sync) * (NT / 32);
+  if (k) {
+    if (ensure_block_scratch(h, (size_t)nlists * 2 * k, &lists)) return HSIM_ENOMEM;
+    cudaMemsetAsync(lists, 0x7F, (size_t)nlists * 2 * k * 8, st);
+  }
+  if (n > 0) {
+    const int rc = run_phases(h, dT, c, n, out_ns, k, lists, 0, nullptr, st, launches);
+    if (rc) return rc;
+  }
+  if (k) {
+    merge_attr();
+    // n == 0 merges no list and only writes the (INT64_MAX, -1) padding
+    k_merge<<<1, MT, sizeof(TopK), st>>>(lists, n > 0 ? nlists : 0, k, out_t, out_i);
+    ++launches;
+  }
+  return finish(h, launches);
 }
 
 int launch_merge(const int64_t* lists, int32_t nlists, int32_t k, int64_t* out_t, int64_t* out_i, cudaStream_t st) {
@@ -357,15 +603,29 @@ int launch_merge(const int64_t* lists, int32_t nlists, int32_t k, int64_t* out_t
   return HSIM_OK;
 }
 
-int launch_count(const Tables* dT, int64_t first, int64_t n, int64_t* d_acc, cudaStream_t st) {
-  cudaMemsetAsync(d_acc, 0, 8, st);
-  if (n > 0) k_count<<<148 * 4, 256, 0, st>>>(dT, first, n, (unsigned long long*)d_acc);
-  cudaError_t e = cudaStreamSynchronize(st);
-  if (e == cudaSuccess) e = cudaGetLastError();
+int launch_count(hsim_handle* h, const Tables* dT, int64_t first, int64_t n, int64_t* d_acc, cudaStream_t st) {
+  Cands c{nullptr, first, 0, 0};
+  int launches = 0;
+  unsigned long long* counters = nullptr;
+  // batches reset the counters: accumulate per batch on the host side
+  i64 total = 0;
+  for (i64 t0 = 0; t0 < n; t0 += NBMAX) {
+    const i64 m = n - t0 < NBMAX ? n - t0 : NBMAX;
+    Cands cb{nullptr, first + t0, 0, 0};
+    const int rc = run_phases(h, dT, cb, m, nullptr, 0, nullptr, 1, &counters, st, launches);
+    if (rc) return rc;
+    unsigned long long v = 0;
+    cudaMemcpyAsync(&v, counters + CNT_CELLS, 8, cudaMemcpyDeviceToHost, st);
+    if (cudaStreamSynchronize(st) != cudaSuccess) break;
+    total += (i64)v;
+  }
+  (void)c;
+  cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     set_error(cudaGetErrorString(e));
     return HSIM_ECUDA;
   }
+  cudaMemcpy(d_acc, &total, 8, cudaMemcpyHostToDevice);
   return 0;
 }
 

@@ -8,6 +8,8 @@ from paper_2508_05370_b200 import build as B  # noqa: E402
 
 VARIANTS = {
     "f8_nb": ["-DHSIM_FASTP=8"],
+    "f8_b3": ["-DHSIM_FASTP=8", "-DHSIM_MINB=3"],
+    "f4_b4": ["-DHSIM_FASTP=4", "-DHSIM_MINB=4"],
     "f8_b4": ["-DHSIM_FASTP=8", "-DHSIM_MINB=4"],
     "f4_b6": ["-DHSIM_FASTP=4", "-DHSIM_MINB=6"],
     "f4_b8": ["-DHSIM_FASTP=4", "-DHSIM_MINB=8"],
