@@ -39,7 +39,7 @@ constexpr i64 NBMAX = 1 << 22;     // work items per batch
 constexpr i64 KEY_INF = INT64_MAX;
 constexpr i64 LIST_PAD = 0x7F7F7F7F7F7F7F7FLL;  // memset(0x7F) sentinel of the per-warp lists
 constexpr unsigned FULL = 0xffffffffu;
-constexpr int CNT_DEEP = 0, CNT_CELLS = 15;      // counter slots (slot P = K_pipe<P>)
+constexpr int CNT_DEEP = 0, CNT_NDEEP = 14, CNT_CELLS = 15;  // counter slots (slot P = K_pipe<P>)
 
 struct Cands {
   const i64* idx;
@@ -62,6 +62,7 @@ struct Scratch {
   int32_t* add;       // [MAXC][nb]
   int32_t* rm;        // [nb] (last class)
   i64* Tc;            // [MAXC][nb] max T_pipe over the class's sub-classes
+  int32_t* deep;      // [nb] items with a class deeper than FASTP (compacted by K_split)
   unsigned long long* counters;  // [16]
   i64 nb;
 };
@@ -88,7 +89,6 @@ __device__ void load_tables(Tables& sT, const Tables* __restrict__ gT) {
 __global__ void __launch_bounds__(NT) k_split(const Tables* __restrict__ gT, Cands c, i64 t0, Scratch S, i64 nb) {
   __shared__ Tables sT;
   load_tables(sT, gT);
-  if (blockIdx.x == 0 && threadIdx.x < 16) S.counters[threadIdx.x] = 0;
   for (i64 t = (i64)blockIdx.x * NT + threadIdx.x; t < nb; t += (i64)gridDim.x * NT) {
     const i64 i = cand_index(c, t0 + t);
     if (i < 0 || i >= sT.N) {
@@ -109,6 +109,7 @@ __global__ void __launch_bounds__(NT) k_split(const Tables* __restrict__ gT, Can
         S.add[k * S.nb + t] = (int32_t)cs[k].add;
       }
       S.rm[t] = (int32_t)cs[tp.C - 1].rm;
+      if (tp.pmask >> (FASTP + 1)) S.deep[atomicAdd(&S.counters[CNT_NDEEP], 1ull)] = (int32_t)t;
     }
   }
 }
@@ -223,47 +224,98 @@ __device__ i64 warp_pipe_class(const Tables& T, int32_t off, const ClassSplit& c
   return best;
 }
 
-__global__ void __launch_bounds__(NT) k_deep(const Tables* __restrict__ gT, Scratch S, i64 nb, int count) {
+// 32 < P <= 64: lane holds stages 2*lane and 2*lane+1 (generic levels only;
+// such pipelines are rare).  Stage 2l+1 reads its left input from the same
+// lane, stage 2l from lane-1's odd stage; B inputs mirror that.
+__device__ i64 warp_pipe_class2(const Tables& T, int32_t off, const ClassSplit& cs, i64* cells) {
+  const int lane = threadIdx.x & 31;
+  const CrecHdr* h = crec_hdr(T, off);
+  const StageRec* st = crec_stages(T, off);
+  const int P = h->P, U = h->U;
+  const int s0 = 2 * lane, s1 = 2 * lane + 1;
+  LayerWalk lw = walk(T, h, cs.dig);
+  int l0 = 0, l1 = 0;
+  for (int k = 0; k <= s1 && k < P; ++k) {
+    const int l = lw.next(st);
+    if (k == s0) l0 = l;
+    if (k == s1) l1 = l;
+  }
+  const bool a0 = s0 < P, a1 = s1 < P;
+  const i64 f0 = a0 ? (i64)l0 * st[s0].layer_f + st[s0].fext : 0, g0 = a0 ? (i64)l0 * st[s0].layer_b + st[s0].gext : 0;
+  const i64 f1 = a1 ? (i64)l1 * st[s1].layer_f + st[s1].fext : 0, g1 = a1 ? (i64)l1 * st[s1].layer_b + st[s1].gext : 0;
+  i64 best = 0;
+  for (int u = 0; u < U; ++u) {
+    const i64* sub = crec_sub(T, off, P, u);
+    const i64 m = mb_of(cs, sub[0]);
+    if (lane == 0) *cells += 2 * P * m;
+    const i64 c0R = a0 && s0 + 1 < P ? sub[1 + s0] : 0, c0L = a0 && s0 > 0 ? sub[s0] : 0;
+    const i64 c1R = a1 && s1 + 1 < P ? sub[1 + s1] : 0, c1L = a1 ? sub[s1] : 0;
+    i64 X0 = 0, X1 = 0, out0 = 0, out1 = 0;
+    const i64 total = 2 * (m + P - 1);
+    for (i64 lv = 0; lv < total; ++lv) {
+      // neighbour exports as of the previous level
+      const i64 fromLeft = __shfl_up_sync(FULL, (long long)out1, 1);    // stage 2l-1 (lane-1, odd)
+      const i64 fromRight = __shfl_down_sync(FULL, (long long)out0, 1); // stage 2l+2 (lane+1, even)
+      const i64 own0 = out0, own1 = out1;
+      // odd stage first (descending order): F reads stage s0's previous export
+      if (a1) {
+        const i64 js = lv - s1, jb = lv - (2 * P - 1 - s1);
+        const bool isF = (js >= 0 && lv <= P - 1 && js < m) || (lv >= 2 * P - s1 && !(js & 1) && (js >> 1) < m);
+        const bool isB = jb >= 0 && !(jb & 1) && (jb >> 1) < m;
+        if (isF || isB) {
+          const i64 v = isF ? own0 : (s1 == P - 1 ? 0 : fromRight);
+          const i64 e = imax(X1, v) + (isF ? f1 : g1);
+          X1 = e;
+          out1 = e + (isF ? c1R : c1L);
+        }
+      }
+      if (a0) {
+        const i64 js = lv - s0, jb = lv - (2 * P - 1 - s0);
+        const bool isF = (js >= 0 && lv <= P - 1 && js < m) || (lv >= 2 * P - s0 && !(js & 1) && (js >> 1) < m);
+        const bool isB = jb >= 0 && !(jb & 1) && (jb >> 1) < m;
+        if (isF || isB) {
+          const i64 v = isF ? (s0 == 0 ? 0 : fromLeft) : (s0 == P - 1 ? 0 : own1);
+          const i64 e = imax(X0, v) + (isF ? f0 : g0);
+          X0 = e;
+          out0 = e + (isF ? c0R : c0L);
+        }
+      }
+    }
+    best = imax(best, __shfl_sync(FULL, (long long)X0, 0));
+  }
+  return best;
+}
+
+// one warp per compacted deep item (its deep classes, sub-classes packed)
+__global__ void __launch_bounds__(NT) k_deep(const Tables* __restrict__ gT, Scratch S, int count) {
   __shared__ Tables sT;
   load_tables(sT, gT);
   const int lane = threadIdx.x & 31;
+  const i64 ndeep = (i64)S.counters[CNT_NDEEP];
   i64 cells = 0;
   for (;;) {
     i64 item = 0;
     if (lane == 0) item = (i64)atomicAdd(&S.counters[CNT_DEEP], 1ull);
     item = __shfl_sync(FULL, item, 0);
-    if (item * 32 >= nb) break;
-    const i64 t = item * 32 + lane;
-    bool has = false;
-    int tau = -1;
-    if (t < nb) {
-      tau = S.tau[t];
-      has = tau >= 0 && S.status[t] == 0 && (sT.tpl[tau].pmask >> (FASTP + 1)) != 0;
-    }
-    unsigned todo = __ballot_sync(FULL, has);
-    while (todo) {
-      const int jl = __ffs(todo) - 1;
-      todo &= todo - 1;
-      const i64 tj = item * 32 + jl;
-      const TplRec& tp = sT.tpl[__shfl_sync(FULL, tau, jl)];
-      for (int c = 0; c < tp.C; ++c) {
-        const int32_t off = tp.crec[c];
-        const int P = crec_hdr(sT, off)->P;
-        if (P <= FASTP) continue;
-        const ClassSplit cs = load_split(S, c, tp.C, tj);
-        i64 T0;
-        if (P <= 32) {
-          i64 cl = 0;
-          T0 = warp_pipe_class(sT, off, cs, &cl);
-          cells += cl;
-        } else {  // very deep (> 32 stages): one lane, per-thread arrays
-          PipeOut r{0, 0};
-          if (lane == 0) r = class_pipes_generic(sT, off, cs);
-          T0 = __shfl_sync(FULL, (long long)r.T0, 0);
-          cells += r.cells;
-        }
-        if (lane == 0) S.Tc[c * S.nb + tj] = T0;
+    if (item >= ndeep) break;
+    const i64 tj = S.deep[item];
+    const TplRec& tp = sT.tpl[S.tau[tj]];
+    for (int c = 0; c < tp.C; ++c) {
+      const int32_t off = tp.crec[c];
+      const int P = crec_hdr(sT, off)->P;
+      if (P <= FASTP) continue;
+      const ClassSplit cs = load_split(S, c, tp.C, tj);
+      i64 T0;
+      if (P <= 32) {
+        i64 cl = 0;
+        T0 = warp_pipe_class(sT, off, cs, &cl);
+        cells += cl;
+      } else {  // very deep (> 32 stages): two stages per lane
+        i64 cl = 0;
+        T0 = warp_pipe_class2(sT, off, cs, &cl);
+        cells += cl;
       }
+      if (lane == 0) S.Tc[c * S.nb + tj] = T0;
     }
   }
   if (count) {
@@ -473,6 +525,70 @@ __global__ void __launch_bounds__(MT) k_merge(const i64* __restrict__ blk, int n
   }
 }
 
+// K_merge for k <= 32: every warp keeps a sorted top-k in registers (lane j
+// holds the j-th entry) and walks the heads of its share of the lists; warp 0
+// then merges the per-warp results.  Same output as k_merge.
+constexpr int MW = 8;  // warps of k_merge_small
+struct RegTopK {
+  i64 t, i;  // this lane's entry
+  __device__ __forceinline__ void init() { t = KEY_INF; i = KEY_INF; }
+  __device__ __forceinline__ void insert(i64 xt, i64 xi) {
+    const int lane = threadIdx.x & 31;
+    const int pos = __popc(__ballot_sync(FULL, key_less(t, i, xt, xi)));
+    const i64 ut = __shfl_up_sync(FULL, (long long)t, 1), ui = __shfl_up_sync(FULL, (long long)i, 1);
+    if (lane == pos) { t = xt; i = xi; }
+    else if (lane > pos) { t = ut; i = ui; }
+  }
+};
+
+__global__ void __launch_bounds__(MW * 32) k_merge_small(const i64* __restrict__ blk, int nblk, int k,
+                                                          i64* __restrict__ out_t, i64* __restrict__ out_i) {
+  __shared__ i64 st[MW][32], si[MW][32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  RegTopK r;
+  r.init();
+  for (int g = w * 32; g < nblk; g += MW * 32) {
+    const int b = g + lane;
+    i64 ht = KEY_INF, hi = KEY_INF;
+    if (b < nblk) {
+      ht = blk[(i64)b * 2 * k];
+      hi = blk[(i64)b * 2 * k + k];
+      if (ht == LIST_PAD) ht = hi = KEY_INF;
+    }
+    const i64 tt = __shfl_sync(FULL, (long long)r.t, k - 1), ti = __shfl_sync(FULL, (long long)r.i, k - 1);
+    unsigned cand = __ballot_sync(FULL, ht != KEY_INF && key_less(ht, hi, tt, ti));
+    while (cand) {
+      const int src = __ffs(cand) - 1;
+      cand &= cand - 1;
+      const i64* L = blk + (i64)(g + src) * 2 * k;
+      for (int p = 0; p < k; ++p) {
+        const i64 xt = L[p], xi = L[k + p];
+        const i64 thT = __shfl_sync(FULL, (long long)r.t, k - 1), thI = __shfl_sync(FULL, (long long)r.i, k - 1);
+        if (xt == KEY_INF || xt == LIST_PAD || !key_less(xt, xi, thT, thI)) break;
+        r.insert(xt, xi);
+      }
+    }
+  }
+  st[w][lane] = r.t;
+  si[w][lane] = r.i;
+  __syncthreads();
+  if (w == 0) {
+    for (int o = 1; o < MW; ++o)
+      for (int p = 0; p < k; ++p) {
+        const i64 xt = st[o][p], xi = si[o][p];
+        const i64 thT = __shfl_sync(FULL, (long long)r.t, k - 1), thI = __shfl_sync(FULL, (long long)r.i, k - 1);
+        if (xt == KEY_INF || !key_less(xt, xi, thT, thI)) break;
+        r.insert(xt, xi);
+      }
+    if (lane < k) {
+      out_t[lane] = r.t;
+      out_i[lane] = r.t == KEY_INF ? -1 : r.i;
+    }
+  }
+}
+
+static void launch_merge_any(const i64* lists, int nlists, int k, i64* out_t, i64* out_i, cudaStream_t st);
+
 // ---- launch ------------------------------------------------------------------------
 template <typename K>
 static int grid_of(const hsim_handle* h, K kern, int& cache) {
@@ -508,7 +624,7 @@ static int run_phases(hsim_handle* h, const Tables* dT, const Cands& c, int64_t 
   static int g_split = 0, g_pipe[FASTP + 1] = {0}, g_deep = 0, g_sync = 0;
   const i64 nb = n < NBMAX ? n : NBMAX;
   // scratch: tau, status, rm (3 x i32), dig/q/seats/add (4 x MAXC x i32), Tc (MAXC x i64), counters
-  const size_t words = (size_t)((3 + 4 * MAXC) * nb + 1) / 2 + (size_t)MAXC * nb + 16 + 8;
+  const size_t words = (size_t)((4 + 4 * MAXC) * nb + 1) / 2 + (size_t)MAXC * nb + 16 + 8;
   i64* base = nullptr;
   if (ensure_work_scratch(h, words, &base)) return HSIM_ENOMEM;
   Scratch S;
@@ -523,11 +639,13 @@ static int run_phases(hsim_handle* h, const Tables* dT, const Cands& c, int64_t 
   S.q = p32 + (3 + MAXC) * nb;
   S.seats = p32 + (3 + 2 * MAXC) * nb;
   S.add = p32 + (3 + 3 * MAXC) * nb;
+  S.deep = p32 + (3 + 4 * MAXC) * nb;
   if (counters_out) *counters_out = S.counters;
   const uint32_t pm = depth_mask(h);
   const int gs = grid_of(h, k_split, g_split), gd = grid_of(h, k_deep, g_deep), gy = grid_of(h, k_sync, g_sync);
   for (i64 t0 = 0; t0 < n; t0 += nb) {
     const i64 m = n - t0 < nb ? n - t0 : nb;
+    cudaMemsetAsync(S.counters, 0, 16 * sizeof(unsigned long long), st);
     k_split<<<gs, NT, 0, st>>>(dT, c, t0, S, m);
     ++launches;
 #define HSIM_PIPE(P)                                                               \
@@ -556,7 +674,7 @@ static int run_phases(hsim_handle* h, const Tables* dT, const Cands& c, int64_t 
 #endif
 #undef HSIM_PIPE
     if (pm >> (FASTP + 1)) {
-      k_deep<<<gd, NT, 0, st>>>(dT, S, m, count);
+      k_deep<<<gd, NT, 0, st>>>(dT, S, count);
       ++launches;
     }
     if (!count) {
@@ -586,15 +704,23 @@ int launch_eval(hsim_handle* h, const Tables* dT, const hsim_cands* cc, int64_t 
   if (k) {
     merge_attr();
     // n == 0 merges no list and only writes the (INT64_MAX, -1) padding
-    k_merge<<<1, MT, sizeof(TopK), st>>>(lists, n > 0 ? nlists : 0, k, out_t, out_i);
+    launch_merge_any(lists, n > 0 ? nlists : 0, k, out_t, out_i, st);
     ++launches;
   }
   return finish(h, launches);
 }
 
+static void launch_merge_any(const i64* lists, int nlists, int k, i64* out_t, i64* out_i, cudaStream_t st) {
+  if (k <= 32) {
+    k_merge_small<<<1, MW * 32, 0, st>>>(lists, nlists, k, out_t, out_i);
+  } else {
+    merge_attr();
+    k_merge<<<1, MT, sizeof(TopK), st>>>(lists, nlists, k, out_t, out_i);
+  }
+}
+
 int launch_merge(const int64_t* lists, int32_t nlists, int32_t k, int64_t* out_t, int64_t* out_i, cudaStream_t st) {
-  merge_attr();
-  k_merge<<<1, MT, sizeof(TopK), st>>>(lists, nlists, k, out_t, out_i);
+  launch_merge_any(lists, nlists, k, out_t, out_i, st);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     set_error(cudaGetErrorString(e));

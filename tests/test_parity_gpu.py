@@ -142,9 +142,10 @@ def test_edge_cases(torch_cuda, oracle_mod):
 def test_launch_count_is_native(torch_cuda, oracle_mod):
     sim, _ = pair(oracle_mod, 2)
     sim.eval_batch(n=1000)
-    assert sim.last_launch_count() == 2      # K0 plan + K1 eval
+    n_eval = sim.last_launch_count()         # K_split + K_pipe<P> per depth + K_deep + K_sync
+    assert n_eval >= 3
     sim.topk(8, n=1000)
-    assert sim.last_launch_count() == 3      # + K3 merge
+    assert sim.last_launch_count() == n_eval + 1      # + K_merge
 
 
 @pytest.mark.skipif(os.environ.get("HSIM_FULL") != "1", reason="exhaustive run: set HSIM_FULL=1")
