@@ -75,19 +75,21 @@ struct hsim_handle {
   Dur& dur_at(int t, int lg, int bi) { return dur[((size_t)t * 4 + lg) * bs.size() + bi]; }
   u64 tp_mask[MAXT][4];
   // templates
-  std::vector<i64> prefix, cprefix;
+  std::vector<i64> prefix;
+  std::vector<int32_t> bucket;
   std::vector<TplRec> tpl;
   std::vector<i64> pool;
   std::map<std::vector<int>, int32_t> crec_of;
   std::vector<std::vector<int>> nodes_of_type;
   i64 n_of_type[MAXT] = {0, 0, 0, 0};
   uint32_t pmask_all = 0;   // union of template depth masks (which depth kernels to launch)
+  int pcnt_max[FASTP + 1] = {0};  // max #classes of depth P in one template (job-list capacity)
   i64 N = 0;
   Tables hT{};  // host pointers (for hsim_decode)
   // device
   Tables* dT = nullptr;
   i64* d_prefix = nullptr;
-  i64* d_cprefix = nullptr;
+  int32_t* d_bucket = nullptr;
   i64* d_work = nullptr;      // work counter + per-range plan (kernels.cu)
   size_t work_cap = 0;
   TplRec* d_tpl = nullptr;
@@ -461,6 +463,9 @@ void hsim_handle::enumerate() {
         r.crec[c] = crec((int)bi, (int)M, classes[c].first, classes[c].second);
         r.pmask |= 1u << std::min<int>((int)classes[c].second.size(), 31);
       }
+      int cnt[33] = {0};
+      for (auto& cl : classes) cnt[std::min<int>((int)cl.second.size(), 32)]++;
+      for (int q = 0; q <= FASTP; ++q) pcnt_max[q] = std::max(pcnt_max[q], cnt[q]);
       pmask_all |= r.pmask;
       const i64 R = radix_of(Ps);
       if (R >= ((i64)1 << 31)) fail(HSIM_ERANGE, "template radix exceeds 2^31");
@@ -556,11 +561,16 @@ void hsim_handle::prepare() {
   hT.n_lc = (int32_t)lcs.size();
   hT.n_nodes = cd.n_nodes;
   for (size_t k = 0; k < lcs.size(); ++k) hT.lc[k] = lcs[k];
-  cprefix.assign(prefix.size(), 0);
-  for (size_t k = 0; k + 1 < prefix.size(); ++k) cprefix[k + 1] = cprefix[k] + (prefix[k + 1] - prefix[k] + CHUNK - 1) / CHUNK;
-  hT.n_chunks = cprefix.back();
+  int shift = 0;
+  while ((N >> shift) > 65536) ++shift;
+  const i64 nbk = N > 0 ? ((N - 1) >> shift) + 1 : 1;
+  bucket.assign(nbk + 1, 0);
+  for (i64 b = 0; b <= nbk; ++b)
+    bucket[b] = (int32_t)bsearch_le(prefix.data(), (i64)tpl.size(), std::min((b << shift), N > 0 ? N - 1 : 0));
+  hT.n_bucket = nbk;
+  hT.bucket_shift = shift;
+  hT.tpl_bucket = bucket.data();
   hT.tpl_prefix = prefix.data();
-  hT.tpl_cprefix = cprefix.data();
   hT.tpl = tpl.data();
   hT.pool = pool.data();
   hT.node_type = node_type8.data();
@@ -572,9 +582,9 @@ void hsim_handle::upload() {
   };
   Tables dt = hT;
   ck(cudaMalloc(&d_prefix, prefix.size() * 8), "cudaMalloc prefix");
-  ck(cudaMalloc(&d_cprefix, cprefix.size() * 8), "cudaMalloc cprefix");
-  ck(cudaMemcpy(d_cprefix, cprefix.data(), cprefix.size() * 8, cudaMemcpyHostToDevice), "H2D cprefix");
-  dt.tpl_cprefix = d_cprefix;
+  ck(cudaMalloc(&d_bucket, bucket.size() * 4), "cudaMalloc bucket");
+  ck(cudaMemcpy(d_bucket, bucket.data(), bucket.size() * 4, cudaMemcpyHostToDevice), "H2D bucket");
+  dt.tpl_bucket = d_bucket;
   ck(cudaMalloc(&d_tpl, std::max<size_t>(1, tpl.size()) * sizeof(TplRec)), "cudaMalloc tpl");
   ck(cudaMalloc(&d_pool, std::max<size_t>(1, pool.size()) * 8), "cudaMalloc pool");
   ck(cudaMalloc(&d_node_type, node_type8.size()), "cudaMalloc nodes");
@@ -660,7 +670,7 @@ int hsim_create(const hsim_cluster_desc* cluster, const hsim_model_desc* model, 
 void hsim_destroy(hsim_handle* h) {
   if (!h) return;
   cudaFree(h->d_prefix);
-  cudaFree(h->d_cprefix);
+  cudaFree(h->d_bucket);
   cudaFree(h->d_work);
   cudaFree(h->d_tpl);
   cudaFree(h->d_pool);
@@ -799,6 +809,7 @@ int ensure_work_scratch(hsim_handle* h, size_t entries, int64_t** out) {
 }
 const Tables& host_tables(const hsim_handle* h) { return h->hT; }
 uint32_t depth_mask(const hsim_handle* h) { return h->pmask_all; }
+int depth_jobs_max(const hsim_handle* h, int P) { return P >= 0 && P <= FASTP ? h->pcnt_max[P] : 0; }
 int ensure_block_scratch(hsim_handle* h, size_t entries, int64_t** out) {
   if (entries > h->blk_cap) {
     cudaFree(h->d_blk);

@@ -79,9 +79,10 @@ struct Tables {
   i64 seg_last_bytes;     // (V*h*!tied + h)*bpe_grad (head + final norm with layer L-1)
   int32_t r_layer, r_batch;
   // templates
-  i64 n_tpl, N, n_chunks;
+  i64 n_tpl, N, n_bucket;
   const i64* tpl_prefix;  // [n_tpl + 1] first candidate of each template
-  const i64* tpl_cprefix; // [n_tpl + 1] first chunk of each template (chunks never straddle templates)
+  const int32_t* tpl_bucket;  // [n_bucket + 1] template of candidate b << bucket_shift (coarse index)
+  int32_t bucket_shift, _pad2;
   const TplRec* tpl;      // [n_tpl]
   const i64* pool;        // crec pool
   // links
@@ -134,7 +135,18 @@ HD i64 bsearch_le(const i64* a, i64 n, i64 x) {
   }
   return lo;
 }
-HD i64 find_template(const Tables& T, i64 i) { return bsearch_le(T.tpl_prefix, T.n_tpl, i); }
+// template of candidate i: max{tau : prefix[tau] <= i}; the coarse bucket
+// table narrows the binary search to the templates of one bucket
+HD i64 find_template(const Tables& T, i64 i) {
+  const i64 b = i >> T.bucket_shift;
+  i64 lo = T.tpl_bucket[b], hi = (i64)T.tpl_bucket[b + 1] + 1;
+  if (hi > T.n_tpl) hi = T.n_tpl;
+  while (hi - lo > 1) {
+    const i64 mid = (lo + hi) >> 1;
+    if (T.tpl_prefix[mid] <= i) lo = mid; else hi = mid;
+  }
+  return lo;
+}
 
 // Decoded + partitioned candidate, per class (steps a0 + a1), without
 // per-stage arrays: layer counts are re-derived from the class's digit block.

@@ -29,6 +29,7 @@ int ensure_block_scratch(hsim_handle* h, size_t entries, int64_t** out);
 int ensure_work_scratch(hsim_handle* h, size_t entries, int64_t** out);
 int sm_count(const hsim_handle* h);
 uint32_t depth_mask(const hsim_handle* h);
+int depth_jobs_max(const hsim_handle* h, int P);
 void set_launches(hsim_handle* h, int n);
 void set_error(const char* m);
 
@@ -39,7 +40,8 @@ constexpr i64 NBMAX = 1 << 22;     // work items per batch
 constexpr i64 KEY_INF = INT64_MAX;
 constexpr i64 LIST_PAD = 0x7F7F7F7F7F7F7F7FLL;  // memset(0x7F) sentinel of the per-warp lists
 constexpr unsigned FULL = 0xffffffffu;
-constexpr int CNT_DEEP = 0, CNT_NDEEP = 14, CNT_CELLS = 15;  // counter slots (slot P = K_pipe<P>)
+// counter slots: P = work counter of K_pipe<P>, 16 + P = #jobs of depth P
+constexpr int CNT_DEEP = 0, CNT_NDEEP = 14, CNT_CELLS = 15, CNT_JOBS = 16, NCNT = 32;
 
 struct Cands {
   const i64* idx;
@@ -63,6 +65,7 @@ struct Scratch {
   int32_t* rm;        // [nb] (last class)
   i64* Tc;            // [MAXC][nb] max T_pipe over the class's sub-classes
   int32_t* deep;      // [nb] items with a class deeper than FASTP (compacted by K_split)
+  int32_t* jobs[FASTP + 1];  // per depth: (item << 2 | class) jobs, compacted by K_split
   unsigned long long* counters;  // [16]
   i64 nb;
 };
@@ -86,30 +89,58 @@ __device__ void load_tables(Tables& sT, const Tables* __restrict__ gT) {
 }
 
 // ---- K_split -------------------------------------------------------------------
-__global__ void __launch_bounds__(NT) k_split(const Tables* __restrict__ gT, Cands c, i64 t0, Scratch S, i64 nb) {
+__global__ void __launch_bounds__(NT) k_split(const Tables* __restrict__ gT, Cands c, i64 t0, Scratch S, i64 nb,
+                                              uint32_t pm_all) {
   __shared__ Tables sT;
   load_tables(sT, gT);
-  for (i64 t = (i64)blockIdx.x * NT + threadIdx.x; t < nb; t += (i64)gridDim.x * NT) {
-    const i64 i = cand_index(c, t0 + t);
-    if (i < 0 || i >= sT.N) {
-      S.tau[t] = -1;
-      continue;
-    }
-    const i64 tau = find_template(sT, i);
-    const TplRec& tp = sT.tpl[tau];
-    ClassSplit cs[MAXC];
-    const int st = partition_any(sT, tp, i - tp.prefix, cs);
-    S.tau[t] = (int32_t)tau;
-    S.status[t] = st;
-    if (st == 0) {
-      for (int k = 0; k < tp.C; ++k) {
-        S.dig[k * S.nb + t] = cs[k].dig;
-        S.q[k * S.nb + t] = (int32_t)cs[k].q;
-        S.seats[k * S.nb + t] = (int32_t)cs[k].seats;
-        S.add[k * S.nb + t] = (int32_t)cs[k].add;
+  const int lane = threadIdx.x & 31;
+  const i64 nwarp = (i64)gridDim.x * (NT / 32);
+  for (i64 base = ((i64)blockIdx.x * (NT / 32) + (threadIdx.x >> 5)) * 32; base < nb; base += nwarp * 32) {
+    const i64 t = base + lane;
+    int st = 1;
+    const TplRec* tp = nullptr;
+    if (t < nb) {
+      const i64 i = cand_index(c, t0 + t);
+      if (i < 0 || i >= sT.N) {
+        S.tau[t] = -1;
+      } else {
+        const i64 tau = find_template(sT, i);
+        tp = &sT.tpl[tau];
+        ClassSplit cs[MAXC];
+        st = partition_any(sT, *tp, i - tp->prefix, cs);
+        S.tau[t] = (int32_t)tau;
+        S.status[t] = st;
+        if (st == 0) {
+          for (int k = 0; k < tp->C; ++k) {
+            S.dig[k * S.nb + t] = cs[k].dig;
+            S.q[k * S.nb + t] = (int32_t)cs[k].q;
+            S.seats[k * S.nb + t] = (int32_t)cs[k].seats;
+            S.add[k * S.nb + t] = (int32_t)cs[k].add;
+          }
+          S.rm[t] = (int32_t)cs[tp->C - 1].rm;
+          if (tp->pmask >> (FASTP + 1)) S.deep[atomicAdd(&S.counters[CNT_NDEEP], 1ull)] = (int32_t)t;
+        }
       }
-      S.rm[t] = (int32_t)cs[tp.C - 1].rm;
-      if (tp.pmask >> (FASTP + 1)) S.deep[atomicAdd(&S.counters[CNT_NDEEP], 1ull)] = (int32_t)t;
+    }
+    // per-depth job lists: one atomic per (warp, depth), jobs of a warp contiguous
+    const uint32_t mypm = st == 0 ? tp->pmask : 0;
+    for (int P = 1; P <= FASTP; ++P) {
+      if (!(pm_all >> P & 1)) continue;
+      int n = 0, cls[MAXC];
+      if (mypm >> P & 1)
+        for (int k = 0; k < tp->C; ++k)
+          if (crec_hdr(sT, tp->crec[k])->P == P) cls[n++] = k;
+      int incl = n;  // inclusive warp scan
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(FULL, incl, o);
+        if (lane >= o) incl += v;
+      }
+      const int total = __shfl_sync(FULL, incl, 31);
+      if (!total) continue;
+      unsigned long long off = 0;
+      if (lane == 31) off = atomicAdd(&S.counters[CNT_JOBS + P], (unsigned long long)total);
+      off = __shfl_sync(FULL, off, 31) + (incl - n);
+      for (int q = 0; q < n; ++q) S.jobs[P][off + q] = (int32_t)(t << 2 | cls[q]);
     }
   }
 }
@@ -121,29 +152,27 @@ __device__ __forceinline__ i64 warp_sum(i64 v) {
 
 // ---- K_pipe<P> -------------------------------------------------------------------
 template <int P>
-__global__ void __launch_bounds__(NT) k_pipe(const Tables* __restrict__ gT, Scratch S, i64 nb, int count) {
+__global__ void __launch_bounds__(NT) k_pipe(const Tables* __restrict__ gT, Scratch S, int count) {
   __shared__ Tables sT;
   load_tables(sT, gT);
   const int lane = threadIdx.x & 31;
+  const i64 njobs = (i64)S.counters[CNT_JOBS + P];
+  const int32_t* jobs = S.jobs[P];
   i64 cells = 0;
   for (;;) {
     i64 item = 0;
     if (lane == 0) item = (i64)atomicAdd(&S.counters[P], 1ull);
     item = __shfl_sync(FULL, item, 0);
-    if (item * 32 >= nb) break;
-    const i64 t = item * 32 + lane;
-    if (t >= nb) continue;
-    const int tau = S.tau[t];
-    if (tau < 0 || S.status[t] != 0) continue;
-    const TplRec& tp = sT.tpl[tau];
-    if (!(tp.pmask >> P & 1)) continue;
-    for (int c = 0; c < tp.C; ++c) {
-      const int32_t off = tp.crec[c];
-      if (crec_hdr(sT, off)->P != P) continue;
-      const PipeOut r = class_pipes_inl<P>(sT, off, load_split(S, c, tp.C, t));
-      S.Tc[c * S.nb + t] = r.T0;
-      cells += r.cells;
-    }
+    if (item * 32 >= njobs) break;
+    const i64 q = item * 32 + lane;
+    if (q >= njobs) continue;
+    const int job = jobs[q];
+    const i64 t = job >> 2;
+    const int c = job & 3;
+    const TplRec& tp = sT.tpl[S.tau[t]];
+    const PipeOut r = class_pipes_inl<P>(sT, tp.crec[c], load_split(S, c, tp.C, t));
+    S.Tc[c * S.nb + t] = r.T0;
+    cells += r.cells;
   }
   if (count) {
     cells = warp_sum(cells);
@@ -528,7 +557,7 @@ __global__ void __launch_bounds__(MT) k_merge(const i64* __restrict__ blk, int n
 // K_merge for k <= 32: every warp keeps a sorted top-k in registers (lane j
 // holds the j-th entry) and walks the heads of its share of the lists; warp 0
 // then merges the per-warp results.  Same output as k_merge.
-constexpr int MW = 8;  // warps of k_merge_small
+constexpr int MW = 32;  // warps of k_merge_small
 struct RegTopK {
   i64 t, i;  // this lane's entry
   __device__ __forceinline__ void init() { t = KEY_INF; i = KEY_INF; }
@@ -623,34 +652,48 @@ static int run_phases(hsim_handle* h, const Tables* dT, const Cands& c, int64_t 
                       int count, unsigned long long** counters_out, cudaStream_t st, int& launches) {
   static int g_split = 0, g_pipe[FASTP + 1] = {0}, g_deep = 0, g_sync = 0;
   const i64 nb = n < NBMAX ? n : NBMAX;
-  // scratch: tau, status, rm (3 x i32), dig/q/seats/add (4 x MAXC x i32), Tc (MAXC x i64), counters
-  const size_t words = (size_t)((4 + 4 * MAXC) * nb + 1) / 2 + (size_t)MAXC * nb + 16 + 8;
+  // scratch (int64 words): Tc [MAXC][nb] | counters [NCNT] | int32 arrays:
+  // tau, status, rm, deep [nb] each, dig / q / seats / add [MAXC][nb] each,
+  // jobs of depth P [cap_P * nb]
+  size_t n32 = (size_t)(4 + 4 * MAXC) * nb;
+  size_t cap[FASTP + 1];
+  for (int P = 1; P <= FASTP; ++P) {
+    cap[P] = (size_t)depth_jobs_max(h, P) * nb;
+    n32 += cap[P];
+  }
+  const size_t words = (size_t)MAXC * nb + NCNT + (n32 + 1) / 2 + 8;
   i64* base = nullptr;
   if (ensure_work_scratch(h, words, &base)) return HSIM_ENOMEM;
   Scratch S;
   S.nb = nb;
   S.Tc = base;
   S.counters = (unsigned long long*)(base + MAXC * nb);
-  int32_t* p32 = (int32_t*)(base + MAXC * nb + 16);
+  int32_t* p32 = (int32_t*)(base + MAXC * nb + NCNT);
   S.tau = p32;
   S.status = p32 + nb;
   S.rm = p32 + 2 * nb;
-  S.dig = (u32*)(p32 + 3 * nb);
-  S.q = p32 + (3 + MAXC) * nb;
-  S.seats = p32 + (3 + 2 * MAXC) * nb;
-  S.add = p32 + (3 + 3 * MAXC) * nb;
-  S.deep = p32 + (3 + 4 * MAXC) * nb;
+  S.deep = p32 + 3 * nb;
+  S.dig = (u32*)(p32 + 4 * nb);
+  S.q = p32 + (4 + MAXC) * nb;
+  S.seats = p32 + (4 + 2 * MAXC) * nb;
+  S.add = p32 + (4 + 3 * MAXC) * nb;
+  int32_t* pj = p32 + (4 + 4 * MAXC) * nb;
+  S.jobs[0] = nullptr;
+  for (int P = 1; P <= FASTP; ++P) {
+    S.jobs[P] = pj;
+    pj += cap[P];
+  }
   if (counters_out) *counters_out = S.counters;
   const uint32_t pm = depth_mask(h);
   const int gs = grid_of(h, k_split, g_split), gd = grid_of(h, k_deep, g_deep), gy = grid_of(h, k_sync, g_sync);
   for (i64 t0 = 0; t0 < n; t0 += nb) {
     const i64 m = n - t0 < nb ? n - t0 : nb;
-    cudaMemsetAsync(S.counters, 0, 16 * sizeof(unsigned long long), st);
-    k_split<<<gs, NT, 0, st>>>(dT, c, t0, S, m);
+    cudaMemsetAsync(S.counters, 0, NCNT * sizeof(unsigned long long), st);
+    k_split<<<gs, NT, 0, st>>>(dT, c, t0, S, m, pm);
     ++launches;
 #define HSIM_PIPE(P)                                                               \
     if (P <= FASTP && (pm >> P & 1)) {                                             \
-      k_pipe<P><<<grid_of(h, k_pipe<P>, g_pipe[P]), NT, 0, st>>>(dT, S, m, count); \
+      k_pipe<P><<<grid_of(h, k_pipe<P>, g_pipe[P]), NT, 0, st>>>(dT, S, count);    \
       ++launches;                                                                  \
     }
     HSIM_PIPE(1) HSIM_PIPE(2)
