@@ -100,6 +100,9 @@ struct hsim_handle {
   i64* d_blk = nullptr;
   size_t blk_cap = 0;
   i64* d_cells = nullptr;
+  static constexpr int NSIDE = 10;
+  cudaStream_t side[NSIDE] = {};     // fork/join streams: the depth kernels of a batch run concurrently
+  cudaEvent_t ev_fork = nullptr, ev_join[NSIDE] = {};
   int32_t last_launches = 0;
   int sm_count = 148;
 
@@ -602,6 +605,11 @@ void hsim_handle::upload() {
   int dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, dev);
+  ck(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming), "cudaEventCreate");
+  for (int q = 0; q < NSIDE; ++q) {
+    ck(cudaStreamCreateWithFlags(&side[q], cudaStreamNonBlocking), "cudaStreamCreate");
+    ck(cudaEventCreateWithFlags(&ev_join[q], cudaEventDisableTiming), "cudaEventCreate");
+  }
 }
 
 // =============================================================================
@@ -678,6 +686,11 @@ void hsim_destroy(hsim_handle* h) {
   cudaFree(h->dT);
   cudaFree(h->d_blk);
   cudaFree(h->d_cells);
+  for (int q = 0; q < hsim_handle::NSIDE; ++q) {
+    if (h->side[q]) cudaStreamDestroy(h->side[q]);
+    if (h->ev_join[q]) cudaEventDestroy(h->ev_join[q]);
+  }
+  if (h->ev_fork) cudaEventDestroy(h->ev_fork);
   delete h;
 }
 
@@ -809,6 +822,9 @@ int ensure_work_scratch(hsim_handle* h, size_t entries, int64_t** out) {
 }
 const Tables& host_tables(const hsim_handle* h) { return h->hT; }
 uint32_t depth_mask(const hsim_handle* h) { return h->pmask_all; }
+cudaStream_t side_stream(const hsim_handle* h, int q) { return h->side[q % hsim_handle::NSIDE]; }
+cudaEvent_t fork_event(const hsim_handle* h) { return h->ev_fork; }
+cudaEvent_t join_event(const hsim_handle* h, int q) { return h->ev_join[q % hsim_handle::NSIDE]; }
 int depth_jobs_max(const hsim_handle* h, int P) { return P >= 0 && P <= FASTP ? h->pcnt_max[P] : 0; }
 int ensure_block_scratch(hsim_handle* h, size_t entries, int64_t** out) {
   if (entries > h->blk_cap) {

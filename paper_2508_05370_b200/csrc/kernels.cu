@@ -30,6 +30,9 @@ int ensure_work_scratch(hsim_handle* h, size_t entries, int64_t** out);
 int sm_count(const hsim_handle* h);
 uint32_t depth_mask(const hsim_handle* h);
 int depth_jobs_max(const hsim_handle* h, int P);
+cudaStream_t side_stream(const hsim_handle* h, int q);
+cudaEvent_t fork_event(const hsim_handle* h);
+cudaEvent_t join_event(const hsim_handle* h, int q);
 void set_launches(hsim_handle* h, int n);
 void set_error(const char* m);
 
@@ -122,25 +125,21 @@ __global__ void __launch_bounds__(NT) k_split(const Tables* __restrict__ gT, Can
         }
       }
     }
-    // per-depth job lists: one atomic per (warp, depth), jobs of a warp contiguous
+    // per-depth job lists, class-major per warp (lanes of one K_pipe warp then
+    // share a class, so their micro-batch counts are close): one atomic per
+    // (warp, depth, class)
     const uint32_t mypm = st == 0 ? tp->pmask : 0;
     for (int P = 1; P <= FASTP; ++P) {
       if (!(pm_all >> P & 1)) continue;
-      int n = 0, cls[MAXC];
-      if (mypm >> P & 1)
-        for (int k = 0; k < tp->C; ++k)
-          if (crec_hdr(sT, tp->crec[k])->P == P) cls[n++] = k;
-      int incl = n;  // inclusive warp scan
-      for (int o = 1; o < 32; o <<= 1) {
-        const int v = __shfl_up_sync(FULL, incl, o);
-        if (lane >= o) incl += v;
+      for (int k = 0; k < MAXC; ++k) {
+        const int n = (mypm >> P & 1) && k < tp->C && crec_hdr(sT, tp->crec[k])->P == P ? 1 : 0;
+        const unsigned bal = __ballot_sync(FULL, n);
+        if (!bal) continue;
+        unsigned long long off = 0;
+        if (lane == 0) off = atomicAdd(&S.counters[CNT_JOBS + P], (unsigned long long)__popc(bal));
+        off = __shfl_sync(FULL, off, 0) + __popc(bal & ((1u << lane) - 1));
+        if (n) S.jobs[P][off] = (int32_t)(t << 2 | k);
       }
-      const int total = __shfl_sync(FULL, incl, 31);
-      if (!total) continue;
-      unsigned long long off = 0;
-      if (lane == 31) off = atomicAdd(&S.counters[CNT_JOBS + P], (unsigned long long)total);
-      off = __shfl_sync(FULL, off, 31) + (incl - n);
-      for (int q = 0; q < n; ++q) S.jobs[P][off + q] = (int32_t)(t << 2 | cls[q]);
     }
   }
 }
@@ -590,8 +589,9 @@ __global__ void __launch_bounds__(MW * 32) k_merge_small(const i64* __restrict__
       const int src = __ffs(cand) - 1;
       cand &= cand - 1;
       const i64* L = blk + (i64)(g + src) * 2 * k;
+      const i64 lt = lane < k ? L[lane] : KEY_INF, li = lane < k ? L[k + lane] : KEY_INF;  // whole list at once
       for (int p = 0; p < k; ++p) {
-        const i64 xt = L[p], xi = L[k + p];
+        const i64 xt = __shfl_sync(FULL, (long long)lt, p), xi = __shfl_sync(FULL, (long long)li, p);
         const i64 thT = __shfl_sync(FULL, (long long)r.t, k - 1), thI = __shfl_sync(FULL, (long long)r.i, k - 1);
         if (xt == KEY_INF || xt == LIST_PAD || !key_less(xt, xi, thT, thI)) break;
         r.insert(xt, xi);
@@ -691,34 +691,57 @@ static int run_phases(hsim_handle* h, const Tables* dT, const Cands& c, int64_t 
     cudaMemsetAsync(S.counters, 0, NCNT * sizeof(unsigned long long), st);
     k_split<<<gs, NT, 0, st>>>(dT, c, t0, S, m, pm);
     ++launches;
-#define HSIM_PIPE(P)                                                               \
-    if (P <= FASTP && (pm >> P & 1)) {                                             \
-      k_pipe<P><<<grid_of(h, k_pipe<P>, g_pipe[P]), NT, 0, st>>>(dT, S, count);    \
-      ++launches;                                                                  \
-    }
-    HSIM_PIPE(1) HSIM_PIPE(2)
+    // the depth kernels and K_deep are independent: fork them onto side
+    // streams (each is bounded by its longest 1F1B chains), join before K_sync
+    cudaEventRecord(fork_event(h), st);
+    int nside = 0;
+    auto side = [&]() {
+      cudaStream_t ss = side_stream(h, nside);
+      cudaStreamWaitEvent(ss, fork_event(h), 0);
+      return ss;
+    };
+    auto join = [&](cudaStream_t ss) {
+      cudaEventRecord(join_event(h, nside), ss);
+      cudaStreamWaitEvent(st, join_event(h, nside), 0);
+      ++nside;
+    };
+    static const int order[FASTP] = {4, 8, 2, 6, 5, 3, 7, 1};  // longest first
+    for (int oi = 0; oi < FASTP; ++oi) {
+      const int P = order[oi];
+      if (P > FASTP || !(pm >> P & 1)) continue;
+      cudaStream_t ss = side();
+      switch (P) {
+#define HSIM_PIPE(PP) case PP: k_pipe<PP><<<grid_of(h, k_pipe<PP>, g_pipe[PP]), NT, 0, ss>>>(dT, S, count); break;
+        HSIM_PIPE(1) HSIM_PIPE(2)
 #if HSIM_FASTP >= 3
-    HSIM_PIPE(3)
+        HSIM_PIPE(3)
 #endif
 #if HSIM_FASTP >= 4
-    HSIM_PIPE(4)
+        HSIM_PIPE(4)
 #endif
 #if HSIM_FASTP >= 5
-    HSIM_PIPE(5)
+        HSIM_PIPE(5)
 #endif
 #if HSIM_FASTP >= 6
-    HSIM_PIPE(6)
+        HSIM_PIPE(6)
 #endif
 #if HSIM_FASTP >= 7
-    HSIM_PIPE(7)
+        HSIM_PIPE(7)
 #endif
 #if HSIM_FASTP >= 8
-    HSIM_PIPE(8)
+        HSIM_PIPE(8)
 #endif
 #undef HSIM_PIPE
-    if (pm >> (FASTP + 1)) {
-      k_deep<<<gd, NT, 0, st>>>(dT, S, count);
+        default: break;
+      }
       ++launches;
+      join(ss);
+    }
+    if (pm >> (FASTP + 1)) {
+      cudaStream_t ss = side();
+      k_deep<<<gd, NT, 0, ss>>>(dT, S, count);
+      ++launches;
+      join(ss);
     }
     if (!count) {
       Cands cb = c;
