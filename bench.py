@@ -135,7 +135,7 @@ def run_reference(a):
     o = oracle.Oracle(cfg)
     cores = os.cpu_count() or 1
     N = o.space_size()
-    per_step = max(64, 16 * cores)  # bounded sample per step
+    per_step = max(512, 256 * cores)  # bounded sample per step (~0.05-0.2 s of host work)
     times = []
     for s in range(a.warmup + a.steps):
         idx = H.sample_indices(N, per_step, seed=H.PARITY_SEED + s)

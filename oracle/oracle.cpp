@@ -723,9 +723,9 @@ void orc_eval_many(void* h, const i64* idx, i64 first, i64 n, i64* out, int thre
   std::atomic<i64> next{0};
   auto work = [&]() {
     for (;;) {
-      i64 k = next.fetch_add(64);
+      i64 k = next.fetch_add(4);  // small grabs: per-candidate cost varies ~1000x
       if (k >= n) return;
-      for (i64 t = k; t < std::min(n, k + 64); ++t) out[t] = o->eval(idx ? idx[t] : first + t);
+      for (i64 t = k; t < std::min(n, k + 4); ++t) out[t] = o->eval(idx ? idx[t] : first + t);
     }
   };
   std::vector<std::thread> pool;

@@ -4,12 +4,12 @@ the k-entry lists over NVLink, merged by the hsim_merge_topk kernel
 (BASELINE.json north_star "merged by an NCCL allgather").
 
 torch.distributed is plumbing only (process group + the one collective); the
-evaluation and both top-k stages run in libhsim's kernels.
+evaluation and both top-k stages run in libhsim's kernels.  `merge` is
+injectable so the host-side sharding / gather logic can be exercised on CPU
+(gloo) by the tests.
 """
 import torch
 import torch.distributed as dist
-
-from .hsim import hsim_merge_topk
 
 DEFAULT_BLOCK = 1 << 16
 
@@ -25,7 +25,20 @@ def shard(n_space, rank, world, block=DEFAULT_BLOCK):
     return rank * block, n, block, stride
 
 
-def sweep(sim, k, group=None, block=DEFAULT_BLOCK, stream=None, out=None):
+def shard_indices(n_space, rank, world, block=DEFAULT_BLOCK):
+    """The explicit index list of a shard (for tests and reports)."""
+    first, n, blk, stride = shard(n_space, rank, world, block)
+    if blk == 0:
+        return list(range(first, first + n))
+    return [first + (t // blk) * stride + t % blk for t in range(n)]
+
+
+def _device_merge(gathered, k, out):
+    from .hsim import hsim_merge_topk
+    return hsim_merge_topk(gathered, k, out=out)
+
+
+def sweep(sim, k, group=None, block=DEFAULT_BLOCK, stream=None, out=None, merge=None, device=None):
     """Global top-k (times, indices) over the whole space of `sim`, identical
     on every rank.  Single process when torch.distributed is not initialised."""
     world = dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
@@ -33,8 +46,9 @@ def sweep(sim, k, group=None, block=DEFAULT_BLOCK, stream=None, out=None):
     first, n, blk, stride = shard(sim.space_size(), rank, world, block)
     if world == 1:
         return sim.topk(k, n=n, first=first, stream=stream, out=out)
-    local = torch.empty(2 * k, dtype=torch.int64, device="cuda")
+    device = device or "cuda"
+    local = torch.empty(2 * k, dtype=torch.int64, device=device)
     sim.topk(k, n=n, first=first, block=blk, stride=stride, stream=stream, out=(local[:k], local[k:]))
-    gathered = torch.empty(world, 2 * k, dtype=torch.int64, device="cuda")
+    gathered = torch.empty(world * 2 * k, dtype=torch.int64, device=device)
     dist.all_gather_into_tensor(gathered, local, group=group)
-    return hsim_merge_topk(gathered, k, out=out, stream=stream)
+    return (merge or _device_merge)(gathered.view(world, 2 * k), k, out)
