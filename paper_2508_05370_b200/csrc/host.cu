@@ -49,6 +49,20 @@ Link path_link(const hsim_path& p, i64 frame) {
 Link cat(const Link& a, const Link& b) { return Link{a.alpha + b.alpha, std::min(a.beta, b.beta)}; }
 i64 tau(const Link& e, i64 x) { return e.alpha + ceilq(x, e.beta); }
 
+// magic multiplier for floor(n / d), n < 2^53 (Granlund-Montgomery): sh = 53 +
+// ceil(log2 d), M = floor(2^sh / d) + 1 < 2^64; M*d - 2^sh < d <= 2^(sh-53)
+bool magic_for(u64 d, u64* M, int* sh) {
+  if (d == 0) return false;
+  int l = 0;
+  while (l < 63 && ((u64)1 << l) < d) ++l;
+  *sh = 53 + l;
+  const unsigned __int128 two = (unsigned __int128)1 << *sh;
+  const unsigned __int128 m = two / d + 1;
+  if (m >> 64) return false;
+  *M = (u64)m;
+  return m * d - two <= ((unsigned __int128)1 << (*sh - 53));
+}
+
 i64 hamilton_floor_rem(i64 n, i64 w, i64 W, i64* rem) {
   *rem = n * w % W;
   return n * w / W;
@@ -90,6 +104,8 @@ struct hsim_handle {
   Tables* dT = nullptr;
   i64* d_prefix = nullptr;
   int32_t* d_bucket = nullptr;
+  u64* d_xmask = nullptr;
+  std::vector<u64> xmask_cross, xmask_same;
   i64* d_work = nullptr;      // work counter + per-range plan (kernels.cu)
   size_t work_cap = 0;
   TplRec* d_tpl = nullptr;
@@ -461,6 +477,7 @@ void hsim_handle::enumerate() {
       if (M < Dt) return;
       TplRec r{};
       r.prefix = acc;
+      if (!magic_for((u64)Dt, &r.dM, &r.dsh)) fail(HSIM_ERANGE, "replica count");
       r.b = b; r.M = (int32_t)M; r.C = (int32_t)classes.size(); r.D = (int32_t)Dt;
       for (size_t c = 0; c < classes.size(); ++c) {
         r.crec[c] = crec((int)bi, (int)M, classes[c].first, classes[c].second);
@@ -564,6 +581,48 @@ void hsim_handle::prepare() {
   hT.n_lc = (int32_t)lcs.size();
   hT.n_nodes = cd.n_nodes;
   for (size_t k = 0; k < lcs.size(); ++k) hT.lc[k] = lcs[k];
+  // exact integer tau: beta = G / 2^k with every x << k < 2^52 (x <= total gradient bytes)
+  {
+    const i64 xmax = md.layers * hT.seg_layer_bytes + hT.seg_first_bytes + hT.seg_last_bytes;
+    bool exact = true;
+    for (size_t b = 0; b < lcs.size() && exact; ++b) {
+      bool found = false;
+      for (int k = 0; k <= 20 && !found; ++k) {
+        const double v = std::ldexp(lcs[b].beta, k);  // exact scaling by 2^k
+        if (v >= 1 && v < 2147483648.0 && v == std::floor(v) && (xmax < ((i64)1 << (52 - k)))) {
+          hT.lc_G[b] = (i64)v;
+          hT.lc_k[b] = (int8_t)k;
+          int sh = 0;
+          found = magic_for((u64)v, &hT.lc_M[b], &sh);
+          hT.lc_sh[b] = (int8_t)sh;
+        }
+      }
+      exact = found;
+    }
+    hT.lc_exact = exact ? 1 : 0;
+  }
+  // link classes of the q < 2^lg edges between two groups' bases (cross-class ring edges)
+  {
+    xmask_cross.assign((size_t)MAXT * MAXG * MAXT * MAXG * 4, 0);
+    xmask_same.assign((size_t)MAXT * MAXG * MAXG * 4, 0);
+    const int g = types[0].gpus_per_node;
+    for (int t1 = 0; t1 < nt; ++t1)
+      for (int b1 = 0; b1 < g; ++b1)
+        for (int b2 = 0; b2 < g; ++b2)
+          for (int lg = 0; lg < 4; ++lg) {
+            for (int t2 = 0; t2 < nt; ++t2) {
+              u64 m = 0;
+              for (int q = 0; q < (1 << lg) && b1 + q < g && b2 + q < g; ++q) m |= (u64)1 << hT.lc_cross[t1][b1 + q][t2][b2 + q];
+              xmask_cross[(((t1 * MAXG + b1) * MAXT + t2) * MAXG + b2) * 4 + lg] = m;
+            }
+            u64 m = 0;
+            for (int q = 0; q < (1 << lg) && b1 + q < g && b2 + q < g; ++q)
+              if (b1 + q != b2 + q) m |= (u64)1 << hT.lc_same[t1][b1 + q][b2 + q];
+            xmask_same[((t1 * MAXG + b1) * MAXG + b2) * 4 + lg] = m;
+          }
+    hT.xmask_cross = xmask_cross.data();
+    hT.xmask_same = xmask_same.data();
+  }
   int shift = 0;
   while ((N >> shift) > 65536) ++shift;
   const i64 nbk = N > 0 ? ((N - 1) >> shift) + 1 : 1;
@@ -588,6 +647,11 @@ void hsim_handle::upload() {
   ck(cudaMalloc(&d_bucket, bucket.size() * 4), "cudaMalloc bucket");
   ck(cudaMemcpy(d_bucket, bucket.data(), bucket.size() * 4, cudaMemcpyHostToDevice), "H2D bucket");
   dt.tpl_bucket = d_bucket;
+  ck(cudaMalloc(&d_xmask, (xmask_cross.size() + xmask_same.size()) * 8), "cudaMalloc xmask");
+  ck(cudaMemcpy(d_xmask, xmask_cross.data(), xmask_cross.size() * 8, cudaMemcpyHostToDevice), "H2D xmask");
+  ck(cudaMemcpy(d_xmask + xmask_cross.size(), xmask_same.data(), xmask_same.size() * 8, cudaMemcpyHostToDevice), "H2D xmask");
+  dt.xmask_cross = d_xmask;
+  dt.xmask_same = d_xmask + xmask_cross.size();
   ck(cudaMalloc(&d_tpl, std::max<size_t>(1, tpl.size()) * sizeof(TplRec)), "cudaMalloc tpl");
   ck(cudaMalloc(&d_pool, std::max<size_t>(1, pool.size()) * 8), "cudaMalloc pool");
   ck(cudaMalloc(&d_node_type, node_type8.size()), "cudaMalloc nodes");
@@ -679,6 +743,7 @@ void hsim_destroy(hsim_handle* h) {
   if (!h) return;
   cudaFree(h->d_prefix);
   cudaFree(h->d_bucket);
+  cudaFree(h->d_xmask);
   cudaFree(h->d_work);
   cudaFree(h->d_tpl);
   cudaFree(h->d_pool);

@@ -68,7 +68,8 @@ struct TplRec {
   int32_t b, M, C, D;     // micro-batch size, #micro-batches, classes, total replicas
   int32_t crec[MAXC];     // int64-offsets of the class records in the pool
   uint32_t pmask;         // bit min(P, 31) set for every class depth P
-  int32_t _pad;
+  int32_t dsh;            // magic division by D (ring chunk): shift
+  u64 dM;                 //   and multiplier
 };
 
 struct Tables {
@@ -88,6 +89,16 @@ struct Tables {
   // links
   int32_t n_lc, n_nodes;
   Link lc[MAXLC];
+  // exact integer form of tau (DESIGN.md C.0): when beta = G / 2^k exactly and
+  // every x << k < 2^53 with x / beta < 2^53 / (2G) (checked at create),
+  // ceil(RN(x / beta)) == ceil_div(x << k, G); floor division by G through a
+  // magic multiplier M with shift sh (Granlund-Montgomery, n < 2^53)
+  i64 lc_G[MAXLC];
+  u64 lc_M[MAXLC];
+  int8_t lc_k[MAXLC], lc_sh[MAXLC];
+  int32_t lc_exact, _pad3;
+  const u64* xmask_cross;  // [MAXT][MAXG][MAXT][MAXG][4] link classes of edges (t1, b1+q) -> (t2, b2+q), q < 2^lg
+  const u64* xmask_same;   // [MAXT][MAXG][MAXG][4] same node
   int8_t lc_same[MAXT][MAXG][MAXG];               // same node: link class of i -> j
   int8_t lc_cross[MAXT][MAXG][MAXT][MAXG];        // different nodes: (t1, r1) -> (t2, r2)
   const int8_t* node_type;                        // [n_nodes]
@@ -105,6 +116,28 @@ HD i64 ceil_div(i64 a, i64 b) { return (a + b - 1) / b; }
 HD i64 imax(i64 a, i64 b) { return a > b ? a : b; }
 HD i64 imin(i64 a, i64 b) { return a < b ? a : b; }
 
+HD u64 umulhi64(u64 a, u64 b) {
+#ifdef __CUDA_ARCH__
+  return __umul64hi(a, b);
+#else
+  return (u64)(((unsigned __int128)a * b) >> 64);
+#endif
+}
+// floor(n / d) for n < 2^53 given M = floor(2^sh / d) + 1, sh = 53 + ceil(log2 d)
+HD u64 div_magic(u64 n, u64 M, int sh) {
+  const u64 hi = umulhi64(n, M), lo = n * M;
+  return sh >= 64 ? hi >> (sh - 64) : (hi << (64 - sh)) | (lo >> sh);
+}
+HD i64 ceil_div_magic(i64 n, i64 d, u64 M, int sh) {
+  const u64 q = div_magic((u64)n, M, sh);
+  return (i64)q + ((i64)q * d != n ? 1 : 0);
+}
+// alpha_e + ceil(x / beta_e) of link class b (C.6 tau_e)
+HD i64 tau_lc(const Tables& T, int b, i64 x) {
+  if (T.lc_exact) return T.lc[b].alpha + ceil_div_magic(x << T.lc_k[b], T.lc_G[b], T.lc_M[b], T.lc_sh[b]);
+  return T.lc[b].alpha + ceilq(x, T.lc[b].beta);
+}
+
 // max over the link classes in `mask` of alpha + ceil(x / beta)  (C.6 tau_e)
 HD i64 eval_mask(const Tables& T, u64 mask, i64 x) {
   i64 best = 0;
@@ -115,7 +148,7 @@ HD i64 eval_mask(const Tables& T, u64 mask, i64 x) {
     int b = __builtin_ctzll(mask);
 #endif
     mask &= mask - 1;
-    best = imax(best, T.lc[b].alpha + ceilq(x, T.lc[b].beta));
+    best = imax(best, tau_lc(T, b, x));
   }
   return best;
 }
@@ -450,7 +483,7 @@ HD i64 grad_sync_c(const Tables& T, const TplRec& tp, const ClassSplit (&cs)[C],
       const int tpc = st[c][sc[c]].tp;
       if (tpc < tstar) { tstar = tpc; lg = st[c][sc[c]].lg_tp; }
     }
-    const i64 xs = ceil_div(S, tstar);
+    const i64 xs = (S + tstar - 1) >> lg;  // t* is a power of two
     u64 rsmask = 0, mask = 0;
 #pragma unroll
     for (int c = 0; c < C; ++c) {
@@ -462,13 +495,11 @@ HD i64 grad_sync_c(const Tables& T, const TplRec& tp, const ClassSplit (&cs)[C],
       const StageRec& t = st[c + 1 < C ? c + 1 : 0][sc[c + 1 < C ? c + 1 : 0]];
       const int n1 = s.last_node, n2 = t.first_node;
       const int t1 = T.node_type[n1], t2 = T.node_type[n2];
-      for (int q = 0; q < tstar; ++q) {
-        const int r1 = s.last_base + q, r2 = t.first_base + q;
-        mask |= (u64)1 << (n1 == n2 ? T.lc_same[t1][r1][r2] : T.lc_cross[t1][r1][t2][r2]);
-      }
+      mask |= n1 == n2 ? T.xmask_same[((t1 * MAXG + s.last_base) * MAXG + t.first_base) * 4 + lg]
+                       : T.xmask_cross[(((t1 * MAXG + s.last_base) * MAXT + t2) * MAXG + t.first_base) * 4 + lg];
     }
     const i64 RS = rsmask ? eval_mask(T, rsmask, xs) : 0;
-    const i64 AR = 2 * (i64)(tp.D - 1) * eval_mask(T, mask, ceil_div(xs, (i64)tp.D));
+    const i64 AR = 2 * (i64)(tp.D - 1) * eval_mask(T, mask, ceil_div_magic(xs, tp.D, tp.dM, tp.dsh));
     i64 start = 0;
 #pragma unroll
     for (int c = 0; c < C; ++c) start = imax(start, cur_free[c]);

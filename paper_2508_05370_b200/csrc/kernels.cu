@@ -69,6 +69,7 @@ struct Scratch {
   i64* Tc;            // [MAXC][nb] max T_pipe over the class's sub-classes
   int32_t* deep;      // [nb] items with a class deeper than FASTP (compacted by K_split)
   int32_t* jobs[FASTP + 1];  // per depth: (item << 2 | class) jobs, compacted by K_split
+  i64* extra;         // [nb] gradient-sync time beyond T0 (C.8), by K_sync
   unsigned long long* counters;  // [16]
   i64 nb;
 };
@@ -423,8 +424,24 @@ __device__ i64 sync_any(const Tables& T, const TplRec& tp, const Scratch& S, i64
   }
 }
 
-__global__ void __launch_bounds__(NT) k_sync(const Tables* __restrict__ gT, Cands c, i64 t0, Scratch S, i64 nb,
-                                             i64* __restrict__ out, int k, i64* __restrict__ lists) {
+// T_iter = T0 + extra with extra = max over runs of consecutive segments
+// sharing a group of sum(RS + AR): every segment starts at T0 or when the
+// previous one ends (C.8) -- so the sync runs concurrently with the 1F1B
+// kernels (grad_sync_c with T0 = 0).
+__global__ void __launch_bounds__(NT) k_sync(const Tables* __restrict__ gT, Scratch S, i64 nb) {
+  __shared__ Tables sT;
+  load_tables(sT, gT);
+  for (i64 t = (i64)blockIdx.x * NT + threadIdx.x; t < nb; t += (i64)gridDim.x * NT) {
+    const int tau = S.tau[t];
+    if (tau < 0 || S.status[t] != 0) continue;
+    const TplRec& tp = sT.tpl[tau];
+    S.extra[t] = tp.D == 1 ? 0 : sync_any(sT, tp, S, t, 0);
+  }
+}
+
+// final: T = max_c T_pipe + extra, coalesced store, per-warp top-k
+__global__ void __launch_bounds__(NT) k_final(const Tables* __restrict__ gT, Cands c, i64 t0, Scratch S, i64 nb,
+                                              i64* __restrict__ out, int k, i64* __restrict__ lists) {
   __shared__ Tables sT;
   load_tables(sT, gT);
   const int lane = threadIdx.x & 31;
@@ -443,10 +460,10 @@ __global__ void __launch_bounds__(NT) k_sync(const Tables* __restrict__ gT, Cand
         if (st) {
           T = st;
         } else {
-          const TplRec& tp = sT.tpl[tau];
+          const int C = sT.tpl[tau].C;
           i64 T0 = 0;
-          for (int q = 0; q < tp.C; ++q) T0 = imax(T0, S.Tc[q * S.nb + t]);
-          T = tp.D == 1 ? T0 : sync_any(sT, tp, S, t, T0);
+          for (int q = 0; q < C; ++q) T0 = imax(T0, S.Tc[q * S.nb + t]);
+          T = T0 + S.extra[t];
         }
       }
       if (out) out[t0 + t] = T;
@@ -650,7 +667,7 @@ static int finish(hsim_handle* h, int launches) {
 // Runs the phase kernels over all work items; out / top-k lists / cell count optional.
 static int run_phases(hsim_handle* h, const Tables* dT, const Cands& c, int64_t n, int64_t* out_ns, int32_t k, i64* lists,
                       int count, unsigned long long** counters_out, cudaStream_t st, int& launches) {
-  static int g_split = 0, g_pipe[FASTP + 1] = {0}, g_deep = 0, g_sync = 0;
+  static int g_split = 0, g_pipe[FASTP + 1] = {0}, g_deep = 0, g_sync = 0, g_final = 0;
   const i64 nb = n < NBMAX ? n : NBMAX;
   // scratch (int64 words): Tc [MAXC][nb] | counters [NCNT] | int32 arrays:
   // tau, status, rm, deep [nb] each, dig / q / seats / add [MAXC][nb] each,
@@ -661,14 +678,15 @@ static int run_phases(hsim_handle* h, const Tables* dT, const Cands& c, int64_t 
     cap[P] = (size_t)depth_jobs_max(h, P) * nb;
     n32 += cap[P];
   }
-  const size_t words = (size_t)MAXC * nb + NCNT + (n32 + 1) / 2 + 8;
+  const size_t words = (size_t)(MAXC + 1) * nb + NCNT + (n32 + 1) / 2 + 8;
   i64* base = nullptr;
   if (ensure_work_scratch(h, words, &base)) return HSIM_ENOMEM;
   Scratch S;
   S.nb = nb;
   S.Tc = base;
-  S.counters = (unsigned long long*)(base + MAXC * nb);
-  int32_t* p32 = (int32_t*)(base + MAXC * nb + NCNT);
+  S.extra = base + MAXC * nb;
+  S.counters = (unsigned long long*)(base + (MAXC + 1) * nb);
+  int32_t* p32 = (int32_t*)(base + (MAXC + 1) * nb + NCNT);
   S.tau = p32;
   S.status = p32 + nb;
   S.rm = p32 + 2 * nb;
@@ -685,7 +703,8 @@ static int run_phases(hsim_handle* h, const Tables* dT, const Cands& c, int64_t 
   }
   if (counters_out) *counters_out = S.counters;
   const uint32_t pm = depth_mask(h);
-  const int gs = grid_of(h, k_split, g_split), gd = grid_of(h, k_deep, g_deep), gy = grid_of(h, k_sync, g_sync);
+  const int gs = grid_of(h, k_split, g_split), gd = grid_of(h, k_deep, g_deep), gy = grid_of(h, k_sync, g_sync),
+            gf = grid_of(h, k_final, g_final);
   for (i64 t0 = 0; t0 < n; t0 += nb) {
     const i64 m = n - t0 < nb ? n - t0 : nb;
     cudaMemsetAsync(S.counters, 0, NCNT * sizeof(unsigned long long), st);
@@ -744,8 +763,13 @@ static int run_phases(hsim_handle* h, const Tables* dT, const Cands& c, int64_t 
       join(ss);
     }
     if (!count) {
-      Cands cb = c;
-      k_sync<<<gy, NT, 0, st>>>(dT, cb, t0, S, m, out_ns, k, lists);
+      cudaStream_t ss = side();
+      k_sync<<<gy, NT, 0, ss>>>(dT, S, m);
+      ++launches;
+      join(ss);
+    }
+    if (!count) {
+      k_final<<<gf, NT, 0, st>>>(dT, c, t0, S, m, out_ns, k, lists);
       ++launches;
     }
   }
@@ -755,10 +779,10 @@ static int run_phases(hsim_handle* h, const Tables* dT, const Cands& c, int64_t 
 int launch_eval(hsim_handle* h, const Tables* dT, const hsim_cands* cc, int64_t n, int64_t* out_ns, int32_t k,
                 int64_t* out_t, int64_t* out_i, cudaStream_t st) {
   Cands c{cc->idx, cc->first, cc->block, cc->stride};
-  static int g_sync = 0;
+  static int g_final = 0;
   int launches = 0;
   i64* lists = nullptr;
-  const int nlists = grid_of(h, k_sync, g_sync) * (NT / 32);
+  const int nlists = grid_of(h, k_final, g_final) * (NT / 32);
   if (k) {
     if (ensure_block_scratch(h, (size_t)nlists * 2 * k, &lists)) return HSIM_ENOMEM;
     cudaMemsetAsync(lists, 0x7F, (size_t)nlists * 2 * k * 8, st);
