@@ -91,6 +91,7 @@ struct hsim_handle {
   // templates
   std::vector<i64> prefix;
   std::vector<int32_t> bucket;
+  std::vector<i64> cprefix;
   std::vector<TplRec> tpl;
   std::vector<i64> pool;
   std::map<std::vector<int>, int32_t> crec_of;
@@ -104,6 +105,9 @@ struct hsim_handle {
   Tables* dT = nullptr;
   i64* d_prefix = nullptr;
   int32_t* d_bucket = nullptr;
+  i64* d_cprefix = nullptr;
+  i64* h_plan = nullptr;        // pinned host staging of the per-call chunk plan
+  size_t h_plan_cap = 0;
   u64* d_xmask = nullptr;
   std::vector<u64> xmask_cross, xmask_same;
   i64* d_work = nullptr;      // work counter + per-range plan (kernels.cu)
@@ -118,7 +122,7 @@ struct hsim_handle {
   i64* d_cells = nullptr;
   static constexpr int NSIDE = 10;
   cudaStream_t side[NSIDE] = {};     // fork/join streams: the depth kernels of a batch run concurrently
-  cudaEvent_t ev_fork = nullptr, ev_join[NSIDE] = {};
+  cudaEvent_t ev_fork = nullptr, ev_join[NSIDE] = {}, ev_plan = nullptr;
   int32_t last_launches = 0;
   int sm_count = 148;
 
@@ -632,6 +636,9 @@ void hsim_handle::prepare() {
   hT.n_bucket = nbk;
   hT.bucket_shift = shift;
   hT.tpl_bucket = bucket.data();
+  cprefix.assign(prefix.size(), 0);
+  for (size_t k = 0; k + 1 < prefix.size(); ++k) cprefix[k + 1] = cprefix[k] + (prefix[k + 1] - prefix[k] + CHUNK - 1) / CHUNK;
+  hT.tpl_cprefix = cprefix.data();
   hT.tpl_prefix = prefix.data();
   hT.tpl = tpl.data();
   hT.pool = pool.data();
@@ -647,6 +654,9 @@ void hsim_handle::upload() {
   ck(cudaMalloc(&d_bucket, bucket.size() * 4), "cudaMalloc bucket");
   ck(cudaMemcpy(d_bucket, bucket.data(), bucket.size() * 4, cudaMemcpyHostToDevice), "H2D bucket");
   dt.tpl_bucket = d_bucket;
+  ck(cudaMalloc(&d_cprefix, cprefix.size() * 8), "cudaMalloc cprefix");
+  ck(cudaMemcpy(d_cprefix, cprefix.data(), cprefix.size() * 8, cudaMemcpyHostToDevice), "H2D cprefix");
+  dt.tpl_cprefix = d_cprefix;
   ck(cudaMalloc(&d_xmask, (xmask_cross.size() + xmask_same.size()) * 8), "cudaMalloc xmask");
   ck(cudaMemcpy(d_xmask, xmask_cross.data(), xmask_cross.size() * 8, cudaMemcpyHostToDevice), "H2D xmask");
   ck(cudaMemcpy(d_xmask + xmask_cross.size(), xmask_same.data(), xmask_same.size() * 8, cudaMemcpyHostToDevice), "H2D xmask");
@@ -670,6 +680,7 @@ void hsim_handle::upload() {
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, dev);
   ck(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming), "cudaEventCreate");
+  ck(cudaEventCreateWithFlags(&ev_plan, cudaEventDisableTiming), "cudaEventCreate");
   for (int q = 0; q < NSIDE; ++q) {
     ck(cudaStreamCreateWithFlags(&side[q], cudaStreamNonBlocking), "cudaStreamCreate");
     ck(cudaEventCreateWithFlags(&ev_join[q], cudaEventDisableTiming), "cudaEventCreate");
@@ -743,6 +754,8 @@ void hsim_destroy(hsim_handle* h) {
   if (!h) return;
   cudaFree(h->d_prefix);
   cudaFree(h->d_bucket);
+  cudaFree(h->d_cprefix);
+  if (h->h_plan) cudaFreeHost(h->h_plan);
   cudaFree(h->d_xmask);
   cudaFree(h->d_work);
   cudaFree(h->d_tpl);
@@ -756,6 +769,7 @@ void hsim_destroy(hsim_handle* h) {
     if (h->ev_join[q]) cudaEventDestroy(h->ev_join[q]);
   }
   if (h->ev_fork) cudaEventDestroy(h->ev_fork);
+  if (h->ev_plan) cudaEventDestroy(h->ev_plan);
   delete h;
 }
 
@@ -886,9 +900,41 @@ int ensure_work_scratch(hsim_handle* h, size_t entries, int64_t** out) {
   return 0;
 }
 const Tables& host_tables(const hsim_handle* h) { return h->hT; }
+// chunk of candidate i (host copy of the template tables)
+static i64 host_chunk_of(const hsim_handle* h, i64 i) {
+  const i64 tau = find_template(h->hT, i);
+  return h->cprefix[tau] + (i - h->prefix[tau]) / CHUNK;
+}
+// Per-call chunk plan of a range / block-cyclic candidate list: for range r,
+// c0[r] = chunk of its first candidate and pre[r] = #chunks of ranges < r.
+// Written to a pinned host buffer [c0 (nr) | pre (nr + 1)]; returns the total.
+i64 host_plan(hsim_handle* h, i64 first, i64 block, i64 stride, i64 n, i64 nr, i64** buf) {
+  const size_t need = (size_t)(2 * nr + 1);
+  if (need > h->h_plan_cap) {
+    if (h->h_plan) cudaFreeHost(h->h_plan);
+    h->h_plan = nullptr;
+    h->h_plan_cap = 0;
+    if (cudaMallocHost(&h->h_plan, need * 8) != cudaSuccess) return -1;
+    h->h_plan_cap = need;
+  }
+  i64* c0 = h->h_plan;
+  i64* pre = h->h_plan + nr;
+  i64 acc = 0;
+  for (i64 r = 0; r < nr; ++r) {
+    const i64 start = block ? first + r * stride : first;
+    const i64 len = block ? std::min(block, n - r * block) : n;
+    c0[r] = host_chunk_of(h, start);
+    pre[r] = acc;
+    acc += host_chunk_of(h, start + len - 1) - c0[r] + 1;
+  }
+  pre[nr] = acc;
+  *buf = h->h_plan;
+  return acc;
+}
 uint32_t depth_mask(const hsim_handle* h) { return h->pmask_all; }
 cudaStream_t side_stream(const hsim_handle* h, int q) { return h->side[q % hsim_handle::NSIDE]; }
 cudaEvent_t fork_event(const hsim_handle* h) { return h->ev_fork; }
+cudaEvent_t plan_event(const hsim_handle* h) { return h->ev_plan; }
 cudaEvent_t join_event(const hsim_handle* h, int q) { return h->ev_join[q % hsim_handle::NSIDE]; }
 int depth_jobs_max(const hsim_handle* h, int P) { return P >= 0 && P <= FASTP ? h->pcnt_max[P] : 0; }
 int ensure_block_scratch(hsim_handle* h, size_t entries, int64_t** out) {

@@ -83,6 +83,7 @@ struct Tables {
   i64 n_tpl, N, n_bucket;
   const i64* tpl_prefix;  // [n_tpl + 1] first candidate of each template
   const int32_t* tpl_bucket;  // [n_bucket + 1] template of candidate b << bucket_shift (coarse index)
+  const i64* tpl_cprefix;     // [n_tpl + 1] first 32-candidate chunk of each template (chunks never straddle)
   int32_t bucket_shift, _pad2;
   const TplRec* tpl;      // [n_tpl]
   const i64* pool;        // crec pool

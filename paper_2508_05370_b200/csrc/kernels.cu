@@ -1,23 +1,28 @@
 // kernels.cu — the hot path on the B200 (sm_100a).
 //
-// A call (hsim_eval_batch / hsim_topk / hsim_count_cells) is processed in
-// batches of up to 2^22 work items t (candidate i = cands(t)).  Per batch, in
-// stream order, each phase a small kernel with its own register budget:
+// A call (hsim_eval_batch / hsim_topk / hsim_count_cells) maps its candidate
+// list onto 32-candidate chunks that never straddle a template (range and
+// block-cyclic lists; explicit lists use 32 consecutive entries) and runs in
+// batches of up to 2^17 chunks.  Per batch, each phase is a small kernel with
+// its own register budget; a chunk's 32 lanes occupy 32 scratch "slots":
 //
-//   K_split   thread per item: decode (template by binary search, mixed-radix
-//             digits) + step (1) partition -> compact per-class split in HBM.
-//   K_pipe<P> P = 1..8, one launch per depth present: lane = (item, class of
-//             depth P); register-resident 1F1B max-plus (step 4) with stage
-//             durations (step 2) and p2p costs (step 3) -> T_pipe per class.
-//             Warps pull 32-item chunks with one atomicAdd (cost varies ~1000x).
-//   K_deep    depth > 8: the warp sweeps the 1F1B anti-diagonal wavefront,
-//             lane = stage, __shfl max-plus (BASELINE north_star mapping).
-//   K_sync    thread per item: T0 = max over classes, step (5) gradient sync
-//             with reshard (step 3), coalesced int64 store, per-warp top-k.
+//   K_split   warp per chunk, lane per candidate: decode (mixed-radix digits)
+//             + step (1) partition -> compact per-class split in HBM; appends
+//             one job segment per (depth P, class) of the chunk's template.
+//   K_pipe<P> P = 1..8, one launch per depth present: warp per segment, lane =
+//             (candidate, class of depth P) of one template and class, so the
+//             32 lanes have near-equal micro-batch counts; register-resident
+//             1F1B max-plus (step 4) over stage durations (step 2) and p2p
+//             costs (step 3) -> T_pipe per class.
+//   K_deep    depth > 8: warp per candidate; the warp sweeps the 1F1B
+//             anti-diagonal wavefront, lane = stage, __shfl max-plus.
+//   K_sync    thread per candidate: step (5) gradient sync incl. reshard as the
+//             T0-independent "extra" (runs concurrently with the 1F1B kernels).
+//   K_final   T = max over classes of T_pipe + extra, coalesced int64 store,
+//             per-warp top-k lists with a global pruning bound.
 //   K_merge   (top-k only, once per call) merges the per-warp sorted lists.
-//
-// Scratch per item: template index, status, per-class split (20 B), per-class
-// T_pipe (8 B) — ~100 B, i.e. < 1 % of the time at HBM rates.
+// The depth kernels, K_deep and K_sync of a batch run concurrently on fork /
+// join side streams.
 #include <cuda_runtime.h>
 
 #include "hsim.h"
@@ -33,22 +38,26 @@ int depth_jobs_max(const hsim_handle* h, int P);
 cudaStream_t side_stream(const hsim_handle* h, int q);
 cudaEvent_t fork_event(const hsim_handle* h);
 cudaEvent_t join_event(const hsim_handle* h, int q);
+cudaEvent_t plan_event(const hsim_handle* h);
+i64 host_plan(hsim_handle* h, i64 first, i64 block, i64 stride, i64 n, i64 nr, i64** buf);
 void set_launches(hsim_handle* h, int n);
 void set_error(const char* m);
 
-constexpr int NT = 128;            // threads per block (phase kernels)
-constexpr int MT = 256;            // threads of K_merge
-constexpr int KMAX = 1024;         // max k
-constexpr i64 NBMAX = 1 << 22;     // work items per batch
+constexpr int NT = 128;              // threads per block (phase kernels)
+constexpr int MT = 256;              // threads of K_merge
+constexpr int KMAX = 1024;           // max k
+constexpr i64 CBMAX = 1 << 17;       // chunks per batch (2^22 slots)
 constexpr i64 KEY_INF = INT64_MAX;
 constexpr i64 LIST_PAD = 0x7F7F7F7F7F7F7F7FLL;  // memset(0x7F) sentinel of the per-warp lists
 constexpr unsigned FULL = 0xffffffffu;
-// counter slots: P = work counter of K_pipe<P>, 16 + P = #jobs of depth P
-constexpr int CNT_DEEP = 0, CNT_NDEEP = 14, CNT_CELLS = 15, CNT_JOBS = 16, NCNT = 32;
+// counter slots: P = work counter of K_pipe<P>, 16 + P = #segments of depth P
+constexpr int CNT_DEEP = 0, CNT_NDEEP = 14, CNT_CELLS = 15, CNT_SEGS = 16, NCNT = 32;
 
 struct Cands {
   const i64* idx;
-  i64 first, block, stride;
+  i64 first, block, stride, n;
+  const i64* plan;   // device [c0 (nr) | pre (nr + 1)] (range / block-cyclic)
+  i64 nr;
 };
 
 __device__ __forceinline__ i64 cand_index(const Cands& c, i64 t) {
@@ -57,29 +66,30 @@ __device__ __forceinline__ i64 cand_index(const Cands& c, i64 t) {
   return c.first + (t / c.block) * c.stride + (t % c.block);
 }
 
-// per-batch scratch (SoA; [MAXC][nb] arrays have row stride nb)
+// per-batch scratch, indexed by slot = (chunk - first chunk of the batch) * 32 + lane
 struct Scratch {
-  int32_t* tau;       // template index, -1 = index out of range
-  int32_t* status;    // 0 ok, -1 / -2 invalid split
-  u32* dig;           // [MAXC][nb]
-  int32_t* q;         // [MAXC][nb]
-  int32_t* seats;     // [MAXC][nb]
-  int32_t* add;       // [MAXC][nb]
-  int32_t* rm;        // [nb] (last class)
-  i64* Tc;            // [MAXC][nb] max T_pipe over the class's sub-classes
-  int32_t* deep;      // [nb] items with a class deeper than FASTP (compacted by K_split)
-  int32_t* jobs[FASTP + 1];  // per depth: (item << 2 | class) jobs, compacted by K_split
-  i64* extra;         // [nb] gradient-sync time beyond T0 (C.8), by K_sync
-  unsigned long long* counters;  // [16]
-  i64 nb;
+  i64* tpos;          // [ns] position t in the call's candidate list, -1 = empty slot
+  int32_t* tau;       // [ns] template index, -1 = none / index out of range
+  int32_t* status;    // [ns] 0 ok, -1 / -2 invalid split
+  u32* dig;           // [MAXC][ns]
+  int32_t* q;         // [MAXC][ns]
+  int32_t* seats;     // [MAXC][ns]
+  int32_t* add;       // [MAXC][ns]
+  int32_t* rm;        // [ns] (last class)
+  i64* Tc;            // [MAXC][ns] max T_pipe over the class's sub-classes
+  i64* extra;         // [ns] gradient-sync time beyond T0 (C.8), by K_sync
+  int32_t* deep;      // [ns] slots with a class deeper than FASTP (compacted)
+  i64* segs[FASTP + 1];  // per depth: segments (first slot << 2 | class)
+  unsigned long long* counters;  // [NCNT]
+  i64 ns;             // slot capacity (row stride of the [MAXC][ns] arrays)
 };
 
 __device__ __forceinline__ ClassSplit load_split(const Scratch& S, int c, int C, i64 t) {
   ClassSplit cs;
-  cs.dig = S.dig[c * S.nb + t];
-  cs.q = S.q[c * S.nb + t];
-  cs.seats = S.seats[c * S.nb + t];
-  cs.add = S.add[c * S.nb + t];
+  cs.dig = S.dig[c * S.ns + t];
+  cs.q = S.q[c * S.ns + t];
+  cs.seats = S.seats[c * S.ns + t];
+  cs.add = S.add[c * S.ns + t];
   cs.rm = c == C - 1 ? S.rm[t] : 0;
   return cs;
 }
@@ -92,62 +102,89 @@ __device__ void load_tables(Tables& sT, const Tables* __restrict__ gT) {
   __syncthreads();
 }
 
+__device__ __forceinline__ i64 warp_sum(i64 v) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, (long long)v, o);
+  return v;
+}
+
 // ---- K_split -------------------------------------------------------------------
-__global__ void __launch_bounds__(NT) k_split(const Tables* __restrict__ gT, Cands c, i64 t0, Scratch S, i64 nb,
+__global__ void __launch_bounds__(NT) k_split(const Tables* __restrict__ gT, Cands c, i64 ca, i64 cb, Scratch S,
                                               uint32_t pm_all) {
   __shared__ Tables sT;
   load_tables(sT, gT);
   const int lane = threadIdx.x & 31;
   const i64 nwarp = (i64)gridDim.x * (NT / 32);
-  for (i64 base = ((i64)blockIdx.x * (NT / 32) + (threadIdx.x >> 5)) * 32; base < nb; base += nwarp * 32) {
-    const i64 t = base + lane;
-    int st = 1;
-    const TplRec* tp = nullptr;
-    if (t < nb) {
-      const i64 i = cand_index(c, t0 + t);
-      if (i < 0 || i >= sT.N) {
-        S.tau[t] = -1;
+  for (i64 item = ca + (i64)blockIdx.x * (NT / 32) + (threadIdx.x >> 5); item < cb; item += nwarp) {
+    const i64 slot = (item - ca) * 32 + lane;
+    i64 t = -1, i = -1, tau = -1;
+    if (c.idx) {
+      t = item * 32 + lane;
+      if (t < c.n) {
+        i = c.idx[t];
+        if (i >= 0 && i < sT.N) tau = find_template(sT, i);
       } else {
-        const i64 tau = find_template(sT, i);
-        tp = &sT.tpl[tau];
-        ClassSplit cs[MAXC];
-        st = partition_any(sT, *tp, i - tp->prefix, cs);
-        S.tau[t] = (int32_t)tau;
-        S.status[t] = st;
-        if (st == 0) {
-          for (int k = 0; k < tp->C; ++k) {
-            S.dig[k * S.nb + t] = cs[k].dig;
-            S.q[k * S.nb + t] = (int32_t)cs[k].q;
-            S.seats[k * S.nb + t] = (int32_t)cs[k].seats;
-            S.add[k * S.nb + t] = (int32_t)cs[k].add;
-          }
-          S.rm[t] = (int32_t)cs[tp->C - 1].rm;
-          if (tp->pmask >> (FASTP + 1)) S.deep[atomicAdd(&S.counters[CNT_NDEEP], 1ull)] = (int32_t)t;
+        t = -1;
+      }
+    } else {
+      const i64* c0 = c.plan;
+      const i64* pre = c.plan + c.nr;
+      const i64 r = bsearch_le(pre, c.nr, item);
+      const i64 g = c0[r] + (item - pre[r]);
+      const i64 tg = bsearch_le(sT.tpl_cprefix, sT.n_tpl, g);
+      const i64 lo = sT.tpl_prefix[tg] + (g - sT.tpl_cprefix[tg]) * CHUNK;
+      const i64 start = c.block ? c.first + r * c.stride : c.first;
+      const i64 len = c.block ? imin(c.block, c.n - r * c.block) : c.n;
+      const i64 end = imin(start + len, sT.tpl_prefix[tg + 1]);
+      if (lo + lane >= start && lo + lane < end) {
+        i = lo + lane;
+        tau = tg;
+        t = (c.block ? r * c.block : 0) + (i - start);
+      }
+    }
+    S.tpos[slot] = t;
+    S.tau[slot] = (int32_t)tau;
+    int st = 1;
+    uint32_t mypm = 0;
+    if (tau >= 0) {
+      const TplRec& tp = sT.tpl[tau];
+      ClassSplit cs[MAXC];
+      st = partition_any(sT, tp, i - tp.prefix, cs);
+      S.status[slot] = st;
+      if (st == 0) {
+        for (int k = 0; k < tp.C; ++k) {
+          S.dig[k * S.ns + slot] = cs[k].dig;
+          S.q[k * S.ns + slot] = (int32_t)cs[k].q;
+          S.seats[k * S.ns + slot] = (int32_t)cs[k].seats;
+          S.add[k * S.ns + slot] = (int32_t)cs[k].add;
+        }
+        S.rm[slot] = (int32_t)cs[tp.C - 1].rm;
+        mypm = tp.pmask;
+      }
+    }
+    // deep candidates: compacted, warp-aggregated
+    const bool deep = (mypm >> (FASTP + 1)) != 0;
+    const unsigned dbal = __ballot_sync(FULL, deep);
+    if (dbal) {
+      unsigned long long off = 0;
+      if (lane == 0) off = atomicAdd(&S.counters[CNT_NDEEP], (unsigned long long)__popc(dbal));
+      off = __shfl_sync(FULL, off, 0) + __popc(dbal & ((1u << lane) - 1));
+      if (deep) S.deep[off] = (int32_t)slot;
+    }
+    // one segment per (depth, class) present in the chunk
+    const uint32_t wpm = __reduce_or_sync(FULL, mypm) & pm_all;
+    if (!wpm) continue;
+    for (int P = 1; P <= FASTP; ++P) {
+      if (!(wpm >> P & 1)) continue;
+      for (int k = 0; k < MAXC; ++k) {
+        const bool has = (mypm >> P & 1) && k < sT.tpl[tau].C && crec_hdr(sT, sT.tpl[tau].crec[k])->P == P;
+        if (!__any_sync(FULL, has)) continue;
+        if (lane == 0) {
+          const unsigned long long o = atomicAdd(&S.counters[CNT_SEGS + P], 1ull);
+          S.segs[P][o] = (item - ca) * 32 << 2 | k;
         }
       }
     }
-    // per-depth job lists, class-major per warp (lanes of one K_pipe warp then
-    // share a class, so their micro-batch counts are close): one atomic per
-    // (warp, depth, class)
-    const uint32_t mypm = st == 0 ? tp->pmask : 0;
-    for (int P = 1; P <= FASTP; ++P) {
-      if (!(pm_all >> P & 1)) continue;
-      for (int k = 0; k < MAXC; ++k) {
-        const int n = (mypm >> P & 1) && k < tp->C && crec_hdr(sT, tp->crec[k])->P == P ? 1 : 0;
-        const unsigned bal = __ballot_sync(FULL, n);
-        if (!bal) continue;
-        unsigned long long off = 0;
-        if (lane == 0) off = atomicAdd(&S.counters[CNT_JOBS + P], (unsigned long long)__popc(bal));
-        off = __shfl_sync(FULL, off, 0) + __popc(bal & ((1u << lane) - 1));
-        if (n) S.jobs[P][off] = (int32_t)(t << 2 | k);
-      }
-    }
   }
-}
-
-__device__ __forceinline__ i64 warp_sum(i64 v) {
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, (long long)v, o);
-  return v;
 }
 
 // ---- K_pipe<P> -------------------------------------------------------------------
@@ -156,22 +193,23 @@ __global__ void __launch_bounds__(NT) k_pipe(const Tables* __restrict__ gT, Scra
   __shared__ Tables sT;
   load_tables(sT, gT);
   const int lane = threadIdx.x & 31;
-  const i64 njobs = (i64)S.counters[CNT_JOBS + P];
-  const int32_t* jobs = S.jobs[P];
+  const i64 nseg = (i64)S.counters[CNT_SEGS + P];
+  const i64* segs = S.segs[P];
   i64 cells = 0;
   for (;;) {
     i64 item = 0;
     if (lane == 0) item = (i64)atomicAdd(&S.counters[P], 1ull);
     item = __shfl_sync(FULL, item, 0);
-    if (item * 32 >= njobs) break;
-    const i64 q = item * 32 + lane;
-    if (q >= njobs) continue;
-    const int job = jobs[q];
-    const i64 t = job >> 2;
-    const int c = job & 3;
-    const TplRec& tp = sT.tpl[S.tau[t]];
-    const PipeOut r = class_pipes_inl<P>(sT, tp.crec[c], load_split(S, c, tp.C, t));
-    S.Tc[c * S.nb + t] = r.T0;
+    if (item >= nseg) break;
+    const i64 sg = segs[item];
+    const int c = sg & 3;
+    const i64 slot = (sg >> 2) + lane;
+    const int tau = S.tau[slot];
+    if (tau < 0 || S.status[slot] != 0) continue;
+    const TplRec& tp = sT.tpl[tau];
+    if (c >= tp.C || crec_hdr(sT, tp.crec[c])->P != P) continue;  // explicit lists mix templates
+    const PipeOut r = class_pipes_inl<P>(sT, tp.crec[c], load_split(S, c, tp.C, slot));
+    S.Tc[c * S.ns + slot] = r.T0;
     cells += r.cells;
   }
   if (count) {
@@ -315,7 +353,7 @@ __device__ i64 warp_pipe_class2(const Tables& T, int32_t off, const ClassSplit& 
   return best;
 }
 
-// one warp per compacted deep item (its deep classes, sub-classes packed)
+// one warp per compacted deep candidate (its deep classes, sub-classes packed)
 __global__ void __launch_bounds__(NT) k_deep(const Tables* __restrict__ gT, Scratch S, int count) {
   __shared__ Tables sT;
   load_tables(sT, gT);
@@ -327,24 +365,17 @@ __global__ void __launch_bounds__(NT) k_deep(const Tables* __restrict__ gT, Scra
     if (lane == 0) item = (i64)atomicAdd(&S.counters[CNT_DEEP], 1ull);
     item = __shfl_sync(FULL, item, 0);
     if (item >= ndeep) break;
-    const i64 tj = S.deep[item];
-    const TplRec& tp = sT.tpl[S.tau[tj]];
+    const i64 sj = S.deep[item];
+    const TplRec& tp = sT.tpl[S.tau[sj]];
     for (int c = 0; c < tp.C; ++c) {
       const int32_t off = tp.crec[c];
       const int P = crec_hdr(sT, off)->P;
       if (P <= FASTP) continue;
-      const ClassSplit cs = load_split(S, c, tp.C, tj);
-      i64 T0;
-      if (P <= 32) {
-        i64 cl = 0;
-        T0 = warp_pipe_class(sT, off, cs, &cl);
-        cells += cl;
-      } else {  // very deep (> 32 stages): two stages per lane
-        i64 cl = 0;
-        T0 = warp_pipe_class2(sT, off, cs, &cl);
-        cells += cl;
-      }
-      if (lane == 0) S.Tc[c * S.nb + tj] = T0;
+      const ClassSplit cs = load_split(S, c, tp.C, sj);
+      i64 cl = 0;
+      const i64 T0 = P <= 32 ? warp_pipe_class(sT, off, cs, &cl) : warp_pipe_class2(sT, off, cs, &cl);
+      cells += cl;
+      if (lane == 0) S.Tc[c * S.ns + sj] = T0;
     }
   }
   if (count) {
@@ -358,6 +389,7 @@ struct WarpTopK {
   i64* wl;
   int k, cnt;
   i64 thrT, thrI;
+  unsigned long long* gthr;  // global bound: the k-th time of any full list (>= the global k-th)
 };
 
 __device__ void warp_topk_load(WarpTopK& w) {  // lists persist across batches (pad = LIST_PAD)
@@ -378,8 +410,10 @@ __device__ __forceinline__ bool key_less(i64 t1, i64 i1, i64 t2, i64 i2) {
 
 __device__ void warp_offer(WarpTopK& w, i64 t, i64 i, bool valid) {
   const int lane = threadIdx.x & 31;
-  const bool cand = valid && (w.cnt < w.k || key_less(t, i, w.thrT, w.thrI));
+  const i64 g = (i64)*(volatile unsigned long long*)w.gthr;
+  const bool cand = valid && t <= g && (w.cnt < w.k || key_less(t, i, w.thrT, w.thrI));
   unsigned mask = __ballot_sync(FULL, cand);
+  if (!mask) return;
   while (mask) {
     const int src = __ffs(mask) - 1;
     mask &= mask - 1;
@@ -406,9 +440,10 @@ __device__ void warp_offer(WarpTopK& w, i64 t, i64 i, bool valid) {
     if (w.cnt < w.k) w.cnt++;
     if (w.cnt == w.k) { w.thrT = w.wl[w.k - 1]; w.thrI = w.wl[2 * w.k - 1]; }
   }
+  if (w.cnt == w.k && lane == 0) atomicMin(w.gthr, (unsigned long long)w.thrT);
 }
 
-// ---- K_sync ------------------------------------------------------------------------
+// ---- K_sync / K_final -----------------------------------------------------------------
 __device__ i64 sync_any(const Tables& T, const TplRec& tp, const Scratch& S, i64 t, i64 T0) {
   switch (tp.C) {
     case 1: { ClassSplit cs[1] = {load_split(S, 0, 1, t)}; return grad_sync_c<1>(T, tp, cs, T0); }
@@ -428,10 +463,10 @@ __device__ i64 sync_any(const Tables& T, const TplRec& tp, const Scratch& S, i64
 // sharing a group of sum(RS + AR): every segment starts at T0 or when the
 // previous one ends (C.8) -- so the sync runs concurrently with the 1F1B
 // kernels (grad_sync_c with T0 = 0).
-__global__ void __launch_bounds__(NT) k_sync(const Tables* __restrict__ gT, Scratch S, i64 nb) {
+__global__ void __launch_bounds__(NT) k_sync(const Tables* __restrict__ gT, Scratch S, i64 ns) {
   __shared__ Tables sT;
   load_tables(sT, gT);
-  for (i64 t = (i64)blockIdx.x * NT + threadIdx.x; t < nb; t += (i64)gridDim.x * NT) {
+  for (i64 t = (i64)blockIdx.x * NT + threadIdx.x; t < ns; t += (i64)gridDim.x * NT) {
     const int tau = S.tau[t];
     if (tau < 0 || S.status[t] != 0) continue;
     const TplRec& tp = sT.tpl[tau];
@@ -439,36 +474,37 @@ __global__ void __launch_bounds__(NT) k_sync(const Tables* __restrict__ gT, Scra
   }
 }
 
-// final: T = max_c T_pipe + extra, coalesced store, per-warp top-k
-__global__ void __launch_bounds__(NT) k_final(const Tables* __restrict__ gT, Cands c, i64 t0, Scratch S, i64 nb,
+__global__ void __launch_bounds__(NT) k_final(const Tables* __restrict__ gT, Cands c, Scratch S, i64 ns,
                                               i64* __restrict__ out, int k, i64* __restrict__ lists) {
   __shared__ Tables sT;
   load_tables(sT, gT);
   const int lane = threadIdx.x & 31;
   const i64 wid = (i64)blockIdx.x * (NT / 32) + (threadIdx.x >> 5);
-  WarpTopK tk{k ? lists + wid * 2 * k : nullptr, k, 0, KEY_INF, KEY_INF};
-  if (k) warp_topk_load(tk);
   const i64 nw = (i64)gridDim.x * (NT / 32);
-  for (i64 base = wid * 32; base < nb; base += nw * 32) {
-    const i64 t = base + lane;
+  WarpTopK tk{k ? lists + wid * 2 * k : nullptr, k, 0, KEY_INF, KEY_INF,
+              k ? (unsigned long long*)(lists + nw * 2 * k) : nullptr};
+  if (k) warp_topk_load(tk);
+  for (i64 base = wid * 32; base < ns; base += nw * 32) {
+    const i64 slot = base + lane;
     i64 T = INT64_MIN, i = -1;
-    if (t < nb) {
-      i = cand_index(c, t0 + t);
-      const int tau = S.tau[t];
+    const i64 t = S.tpos[slot];
+    if (t >= 0) {
+      i = cand_index(c, t);
+      const int tau = S.tau[slot];
       if (tau >= 0) {
-        const int st = S.status[t];
+        const int st = S.status[slot];
         if (st) {
           T = st;
         } else {
           const int C = sT.tpl[tau].C;
           i64 T0 = 0;
-          for (int q = 0; q < C; ++q) T0 = imax(T0, S.Tc[q * S.nb + t]);
-          T = T0 + S.extra[t];
+          for (int q = 0; q < C; ++q) T0 = imax(T0, S.Tc[q * S.ns + slot]);
+          T = T0 + S.extra[slot];
         }
       }
-      if (out) out[t0 + t] = T;
+      if (out) out[t] = T;
     }
-    if (k) warp_offer(tk, T, i, t < nb && T >= 0);
+    if (k) warp_offer(tk, T, i, t >= 0 && T >= 0);
   }
 }
 
@@ -635,7 +671,6 @@ __global__ void __launch_bounds__(MW * 32) k_merge_small(const i64* __restrict__
 
 static void launch_merge_any(const i64* lists, int nlists, int k, i64* out_t, i64* out_i, cudaStream_t st);
 
-// ---- launch ------------------------------------------------------------------------
 template <typename K>
 static int grid_of(const hsim_handle* h, K kern, int& cache) {
   if (!cache) {
@@ -664,54 +699,78 @@ static int finish(hsim_handle* h, int launches) {
   return HSIM_OK;
 }
 
-// Runs the phase kernels over all work items; out / top-k lists / cell count optional.
-static int run_phases(hsim_handle* h, const Tables* dT, const Cands& c, int64_t n, int64_t* out_ns, int32_t k, i64* lists,
-                      int count, unsigned long long** counters_out, cudaStream_t st, int& launches) {
+// Runs the phase kernels over all chunks of the call; out / top-k lists / cell
+// count optional.
+static int run_phases(hsim_handle* h, const Tables* dT, Cands c, int64_t n, int64_t* out_ns, int32_t k, i64* lists,
+                      int count, i64* cells_out, cudaStream_t st, int& launches) {
   static int g_split = 0, g_pipe[FASTP + 1] = {0}, g_deep = 0, g_sync = 0, g_final = 0;
-  const i64 nb = n < NBMAX ? n : NBMAX;
-  // scratch (int64 words): Tc [MAXC][nb] | counters [NCNT] | int32 arrays:
-  // tau, status, rm, deep [nb] each, dig / q / seats / add [MAXC][nb] each,
-  // jobs of depth P [cap_P * nb]
-  size_t n32 = (size_t)(4 + 4 * MAXC) * nb;
-  size_t cap[FASTP + 1];
-  for (int P = 1; P <= FASTP; ++P) {
-    cap[P] = (size_t)depth_jobs_max(h, P) * nb;
-    n32 += cap[P];
+  // chunk plan
+  i64 nchunks;
+  i64* hplan = nullptr;
+  if (c.idx) {
+    nchunks = (n + 31) / 32;
+    c.nr = 0;
+  } else {
+    c.nr = c.block ? (n + c.block - 1) / c.block : 1;
+    cudaEventSynchronize(plan_event(h));  // the pinned plan buffer is free again
+    nchunks = host_plan(h, c.first, c.block, c.stride, n, c.nr, &hplan);
+    if (nchunks < 0) return HSIM_ENOMEM;
   }
-  const size_t words = (size_t)(MAXC + 1) * nb + NCNT + (n32 + 1) / 2 + 8;
+  const i64 cbatch = nchunks < CBMAX ? nchunks : CBMAX;
+  const i64 ns = cbatch * 32;
+  // scratch (int64 words): tpos, Tc [MAXC], extra | segs per depth | counters | plan |
+  // int32: tau, status, rm, deep, dig / q / seats / add [MAXC]
+  // segment capacity per depth: per chunk, #classes of that depth (any class for explicit lists)
+  const uint32_t pm = depth_mask(h);
+  size_t segcap[FASTP + 1], segw = 0;
+  for (int P = 1; P <= FASTP; ++P) {
+    segcap[P] = (pm >> P & 1) ? (size_t)(c.idx ? MAXC : depth_jobs_max(h, P)) * cbatch : 0;
+    segw += segcap[P];
+  }
+  const size_t planw = c.idx ? 0 : (size_t)(2 * c.nr + 1);
+  const size_t n32 = (size_t)(4 + 4 * MAXC) * ns;
+  const size_t words = (size_t)(MAXC + 2) * ns + segw + NCNT + planw + (n32 + 1) / 2 + 8;
   i64* base = nullptr;
   if (ensure_work_scratch(h, words, &base)) return HSIM_ENOMEM;
   Scratch S;
-  S.nb = nb;
-  S.Tc = base;
-  S.extra = base + MAXC * nb;
-  S.counters = (unsigned long long*)(base + (MAXC + 1) * nb);
-  int32_t* p32 = (int32_t*)(base + (MAXC + 1) * nb + NCNT);
-  S.tau = p32;
-  S.status = p32 + nb;
-  S.rm = p32 + 2 * nb;
-  S.deep = p32 + 3 * nb;
-  S.dig = (u32*)(p32 + 4 * nb);
-  S.q = p32 + (4 + MAXC) * nb;
-  S.seats = p32 + (4 + 2 * MAXC) * nb;
-  S.add = p32 + (4 + 3 * MAXC) * nb;
-  int32_t* pj = p32 + (4 + 4 * MAXC) * nb;
-  S.jobs[0] = nullptr;
+  S.ns = ns;
+  S.tpos = base;
+  S.Tc = base + ns;
+  S.extra = base + (MAXC + 1) * ns;
+  i64* pw = base + (MAXC + 2) * ns;
+  S.segs[0] = nullptr;
   for (int P = 1; P <= FASTP; ++P) {
-    S.jobs[P] = pj;
-    pj += cap[P];
+    S.segs[P] = pw;
+    pw += segcap[P];
   }
-  if (counters_out) *counters_out = S.counters;
-  const uint32_t pm = depth_mask(h);
+  S.counters = (unsigned long long*)pw;
+  pw += NCNT;
+  if (!c.idx) {
+    cudaMemcpyAsync(pw, hplan, planw * 8, cudaMemcpyHostToDevice, st);
+    cudaEventRecord(plan_event(h), st);
+    c.plan = pw;
+    pw += planw;
+  }
+  int32_t* p32 = (int32_t*)pw;
+  S.tau = p32;
+  S.status = p32 + ns;
+  S.rm = p32 + 2 * ns;
+  S.deep = p32 + 3 * ns;
+  S.dig = (u32*)(p32 + 4 * ns);
+  S.q = p32 + (4 + MAXC) * ns;
+  S.seats = p32 + (4 + 2 * MAXC) * ns;
+  S.add = p32 + (4 + 3 * MAXC) * ns;
   const int gs = grid_of(h, k_split, g_split), gd = grid_of(h, k_deep, g_deep), gy = grid_of(h, k_sync, g_sync),
             gf = grid_of(h, k_final, g_final);
-  for (i64 t0 = 0; t0 < n; t0 += nb) {
-    const i64 m = n - t0 < nb ? n - t0 : nb;
+  i64 cells = 0;
+  for (i64 ca = 0; ca < nchunks; ca += cbatch) {
+    const i64 cb = ca + cbatch < nchunks ? ca + cbatch : nchunks;
+    const i64 nsb = (cb - ca) * 32;
     cudaMemsetAsync(S.counters, 0, NCNT * sizeof(unsigned long long), st);
-    k_split<<<gs, NT, 0, st>>>(dT, c, t0, S, m, pm);
+    k_split<<<gs, NT, 0, st>>>(dT, c, ca, cb, S, pm);
     ++launches;
-    // the depth kernels and K_deep are independent: fork them onto side
-    // streams (each is bounded by its longest 1F1B chains), join before K_sync
+    // the depth kernels, K_deep and K_sync are independent: fork them onto
+    // side streams (each is bounded by its longest chains), join before K_final
     cudaEventRecord(fork_event(h), st);
     int nside = 0;
     auto side = [&]() {
@@ -724,8 +783,8 @@ static int run_phases(hsim_handle* h, const Tables* dT, const Cands& c, int64_t 
       cudaStreamWaitEvent(st, join_event(h, nside), 0);
       ++nside;
     };
-    static const int order[FASTP] = {4, 8, 2, 6, 5, 3, 7, 1};  // longest first
-    for (int oi = 0; oi < FASTP; ++oi) {
+    static const int order[8] = {4, 8, 2, 6, 5, 3, 7, 1};  // longest first
+    for (int oi = 0; oi < 8; ++oi) {
       const int P = order[oi];
       if (P > FASTP || !(pm >> P & 1)) continue;
       cudaStream_t ss = side();
@@ -762,42 +821,24 @@ static int run_phases(hsim_handle* h, const Tables* dT, const Cands& c, int64_t 
       ++launches;
       join(ss);
     }
-    if (!count) {
+    if (count) {
+      unsigned long long v = 0;
+      cudaMemcpyAsync(&v, S.counters + CNT_CELLS, 8, cudaMemcpyDeviceToHost, st);
+      if (cudaStreamSynchronize(st) != cudaSuccess) break;
+      cells += (i64)v;
+      continue;
+    }
+    {
       cudaStream_t ss = side();
-      k_sync<<<gy, NT, 0, ss>>>(dT, S, m);
+      k_sync<<<gy, NT, 0, ss>>>(dT, S, nsb);
       ++launches;
       join(ss);
     }
-    if (!count) {
-      k_final<<<gf, NT, 0, st>>>(dT, c, t0, S, m, out_ns, k, lists);
-      ++launches;
-    }
-  }
-  return HSIM_OK;
-}
-
-int launch_eval(hsim_handle* h, const Tables* dT, const hsim_cands* cc, int64_t n, int64_t* out_ns, int32_t k,
-                int64_t* out_t, int64_t* out_i, cudaStream_t st) {
-  Cands c{cc->idx, cc->first, cc->block, cc->stride};
-  static int g_final = 0;
-  int launches = 0;
-  i64* lists = nullptr;
-  const int nlists = grid_of(h, k_final, g_final) * (NT / 32);
-  if (k) {
-    if (ensure_block_scratch(h, (size_t)nlists * 2 * k, &lists)) return HSIM_ENOMEM;
-    cudaMemsetAsync(lists, 0x7F, (size_t)nlists * 2 * k * 8, st);
-  }
-  if (n > 0) {
-    const int rc = run_phases(h, dT, c, n, out_ns, k, lists, 0, nullptr, st, launches);
-    if (rc) return rc;
-  }
-  if (k) {
-    merge_attr();
-    // n == 0 merges no list and only writes the (INT64_MAX, -1) padding
-    launch_merge_any(lists, n > 0 ? nlists : 0, k, out_t, out_i, st);
+    k_final<<<gf, NT, 0, st>>>(dT, c, S, nsb, out_ns, k, lists);
     ++launches;
   }
-  return finish(h, launches);
+  if (cells_out) *cells_out = cells;
+  return HSIM_OK;
 }
 
 static void launch_merge_any(const i64* lists, int nlists, int k, i64* out_t, i64* out_i, cudaStream_t st) {
@@ -819,23 +860,37 @@ int launch_merge(const int64_t* lists, int32_t nlists, int32_t k, int64_t* out_t
   return HSIM_OK;
 }
 
-int launch_count(hsim_handle* h, const Tables* dT, int64_t first, int64_t n, int64_t* d_acc, cudaStream_t st) {
-  Cands c{nullptr, first, 0, 0};
+int launch_eval(hsim_handle* h, const Tables* dT, const hsim_cands* cc, int64_t n, int64_t* out_ns, int32_t k,
+                int64_t* out_t, int64_t* out_i, cudaStream_t st) {
+  Cands c{cc->idx, cc->first, cc->block, cc->stride, n, nullptr, 0};
+  static int g_final = 0;
   int launches = 0;
-  unsigned long long* counters = nullptr;
-  // batches reset the counters: accumulate per batch on the host side
-  i64 total = 0;
-  for (i64 t0 = 0; t0 < n; t0 += NBMAX) {
-    const i64 m = n - t0 < NBMAX ? n - t0 : NBMAX;
-    Cands cb{nullptr, first + t0, 0, 0};
-    const int rc = run_phases(h, dT, cb, m, nullptr, 0, nullptr, 1, &counters, st, launches);
-    if (rc) return rc;
-    unsigned long long v = 0;
-    cudaMemcpyAsync(&v, counters + CNT_CELLS, 8, cudaMemcpyDeviceToHost, st);
-    if (cudaStreamSynchronize(st) != cudaSuccess) break;
-    total += (i64)v;
+  i64* lists = nullptr;
+  const int nlists = grid_of(h, k_final, g_final) * (NT / 32);
+  if (k) {
+    if (ensure_block_scratch(h, (size_t)nlists * 2 * k + 1, &lists)) return HSIM_ENOMEM;
+    cudaMemsetAsync(lists, 0x7F, ((size_t)nlists * 2 * k + 1) * 8, st);  // lists + global bound word
   }
-  (void)c;
+  if (n > 0) {
+    const int rc = run_phases(h, dT, c, n, out_ns, k, lists, 0, nullptr, st, launches);
+    if (rc) return rc;
+  }
+  if (k) {
+    // n == 0 merges no list and only writes the (INT64_MAX, -1) padding
+    launch_merge_any(lists, n > 0 ? nlists : 0, k, out_t, out_i, st);
+    ++launches;
+  }
+  return finish(h, launches);
+}
+
+int launch_count(hsim_handle* h, const Tables* dT, int64_t first, int64_t n, int64_t* d_acc, cudaStream_t st) {
+  Cands c{nullptr, first, 0, 0, n, nullptr, 0};
+  int launches = 0;
+  i64 total = 0;
+  if (n > 0) {
+    const int rc = run_phases(h, dT, c, n, nullptr, 0, nullptr, 1, &total, st, launches);
+    if (rc) return rc;
+  }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     set_error(cudaGetErrorString(e));
