@@ -313,63 +313,94 @@ HD i64 pipeline_generic(int P, i64 m, const i64* f, const i64* g, const i64* c) 
   return X[0];
 }
 
-// compile-time depth: every array is register-resident; the steady phase
-// (levels [2P-1, 2m), every stage busy, F iff level = s mod 2) has no
-// per-cell bookkeeping: one int64 max and two int64 adds per cell.
+// compile-time depth: every array is register-resident.  Clocks are kept in
+// offset coordinates X_s = end_s - o_s with o_s = c_0 + ... + c_{s-1}: then
+// the F message of stage s-1 arrives at X_{s-1} (no add), the B message of
+// stage s+1 at X_{s+1} + 2 c_s, stage 0's F input (time 0) and the last
+// stage's B input (its own F) never exceed the stage clock, and
+// T_pipe = end(B(0, m-1)) = X_0.  Every input is the neighbour's clock as of
+// the previous level (its most recent op is the one consumed, C.7), so a
+// level is computed from the previous level's clocks.
+// m >= P: warm-up levels [0, 2P-1) and cool-down levels [2m, 2m+2P-2) have a
+// fixed op pattern (unrolled, no bookkeeping); the steady levels [2P-1, 2m)
+// alternate F (s = level mod 2) / B.  m < P: closed-form levels at run time.
 template <int P>
 struct Pipe {
-  i64 f[P], g[P], c[P], X[P], R[P], Lb[P], lastF;
+  i64 f[P], g[P], c[P], X[P];  // c[s] = 2 * (p2p cost of boundary s -> s+1)
 
-  HD void generic_level(i64 lv, i64 m) {
+  // op of stage s at level lv: +1 F, -1 B, 0 none
+  HD static int op_at(i64 lv, int s, i64 m) {
+    const i64 js = lv - s, jb = lv - (2 * P - 1 - s);
+    if ((js >= 0 && lv <= P - 1 && js < m) || (lv >= 2 * P - s && !(js & 1) && (js >> 1) < m)) return 1;
+    if (jb >= 0 && !(jb & 1) && (jb >> 1) < m) return -1;
+    return 0;
+  }
+  HD i64 fop(const i64 (&old)[P], int s) const {
+    return s == 0 ? old[0] + f[0] : imax(old[s], old[s == 0 ? 0 : s - 1]) + f[s];
+  }
+  HD i64 bop(const i64 (&old)[P], int s) const {
+    return s == P - 1 ? old[s] + g[s] : imax(old[s], old[s == P - 1 ? s : s + 1] + c[s]) + g[s];
+  }
+  HD void level_rt(i64 lv, i64 m) {  // run-time ops
+    i64 old[P];
 #pragma unroll
-    for (int s = P - 1; s >= 0; --s) {
-      const i64 js = lv - s, jb = lv - (2 * P - 1 - s);
-      const bool isF = (js >= 0 && lv <= P - 1 && js < m) || (lv >= 2 * P - s && !(js & 1) && (js >> 1) < m);
-      const bool isB = jb >= 0 && !(jb & 1) && (jb >> 1) < m;
-      if (isF) {
-        const i64 e = imax(X[s], s == 0 ? (i64)0 : R[s == 0 ? 0 : s - 1]) + f[s];
-        X[s] = e;
-        if (s < P - 1) R[s] = e + c[s]; else lastF = e;
-      } else if (isB) {
-        const i64 e = imax(X[s], s == P - 1 ? lastF : Lb[s == P - 1 ? s : s + 1]) + g[s];
-        X[s] = e;
-        if (s > 0) Lb[s] = e + c[s == 0 ? 0 : s - 1];
-      }
+    for (int s = 0; s < P; ++s) old[s] = X[s];
+#pragma unroll
+    for (int s = 0; s < P; ++s) {
+      const int o = op_at(lv, s, m);
+      if (o > 0) X[s] = fop(old, s);
+      else if (o < 0) X[s] = bop(old, s);
+    }
+  }
+  // m >= P: ops of warm-up level lv (compile-time after unrolling)
+  HD void level_warm(int lv) {
+    i64 old[P];
+#pragma unroll
+    for (int s = 0; s < P; ++s) old[s] = X[s];
+#pragma unroll
+    for (int s = 0; s < P; ++s) {
+      const int js = lv - s, jb = lv - (2 * P - 1 - s);
+      if ((js >= 0 && lv <= P - 1) || (lv >= 2 * P - s && !(js & 1))) X[s] = fop(old, s);
+      else if (jb >= 0 && !(jb & 1)) X[s] = bop(old, s);
+    }
+  }
+  // m >= P: ops of cool-down level 2m + d
+  HD void level_cool(int d) {
+    i64 old[P];
+#pragma unroll
+    for (int s = 0; s < P; ++s) old[s] = X[s];
+#pragma unroll
+    for (int s = 0; s < P; ++s) {
+      if (d < s && !((d - s) & 1)) X[s] = fop(old, s);
+      else if (d < 2 * P - 1 - s && !((d + 1 + s) & 1)) X[s] = bop(old, s);
     }
   }
   // one steady level of parity par: stages with s % 2 == par run F, the others B
   template <int par>
   HD void steady_level() {
+    i64 old[P];
 #pragma unroll
-    for (int s = P - 1; s >= 0; --s) {
-      if ((s & 1) == par) {
-        const i64 e = imax(X[s], s == 0 ? (i64)0 : R[s == 0 ? 0 : s - 1]) + f[s];
-        X[s] = e;
-        if (s < P - 1) R[s] = e + c[s]; else lastF = e;
-      } else {
-        const i64 e = imax(X[s], s == P - 1 ? lastF : Lb[s == P - 1 ? s : s + 1]) + g[s];
-        X[s] = e;
-        if (s > 0) Lb[s] = e + c[s == 0 ? 0 : s - 1];
-      }
-    }
+    for (int s = 0; s < P; ++s) old[s] = X[s];
+#pragma unroll
+    for (int s = 0; s < P; ++s) X[s] = (s & 1) == par ? fop(old, s) : bop(old, s);
   }
   HD i64 run(i64 m) {
 #pragma unroll
-    for (int s = 0; s < P; ++s) X[s] = R[s] = Lb[s] = 0;
-    lastF = 0;
-    const i64 total = 2 * (m + P - 1);
-    const i64 lo = 2 * P - 1;
-    const i64 hi = m >= P ? 2 * m : lo;
-    const i64 e1 = lo < total ? lo : total;
-    for (i64 lv = 0; lv < e1; ++lv) generic_level(lv, m);
-    if (hi > lo) {
-      steady_level<1>();  // level 2P-1 is odd
-      for (int k = 0, kn = (int)(m - P); k < kn; ++k) {
-        steady_level<0>();
+    for (int s = 0; s < P; ++s) X[s] = 0;
+    if (m >= P) {
+#pragma unroll
+      for (int lv = 0; lv < 2 * P - 1; ++lv) level_warm(lv);
+      for (int k = 0, kn = (int)(m - P); k < kn; ++k) {  // levels [2P-1, 2m): (odd, even) pairs
         steady_level<1>();
+        steady_level<0>();
       }
+      steady_level<1>();  // level 2m-1
+#pragma unroll
+      for (int d = 0; d < 2 * P - 2; ++d) level_cool(d);
+    } else {
+      const i64 total = 2 * (m + P - 1);
+      for (i64 lv = 0; lv < total; ++lv) level_rt(lv, m);
     }
-    for (i64 lv = hi > lo ? hi : lo; lv < total; ++lv) generic_level(lv, m);
     return X[0];
   }
 };
@@ -393,7 +424,7 @@ HD PipeOut class_pipes_inl(const Tables& T, int32_t off, const ClassSplit& cs) {
   for (int u = 0; u < h->U; ++u) {
     const i64* sub = crec_sub(T, off, P, u);
 #pragma unroll
-    for (int s = 0; s + 1 < P; ++s) p.c[s] = sub[1 + s];
+    for (int s = 0; s + 1 < P; ++s) p.c[s] = 2 * sub[1 + s];
     const i64 m = mb_of(cs, sub[0]);
     r.cells += 2 * P * m;
     r.T0 = imax(r.T0, p.run(m));

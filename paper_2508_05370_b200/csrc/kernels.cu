@@ -170,18 +170,21 @@ __global__ void __launch_bounds__(NT) k_split(const Tables* __restrict__ gT, Can
       off = __shfl_sync(FULL, off, 0) + __popc(dbal & ((1u << lane) - 1));
       if (deep) S.deep[off] = (int32_t)slot;
     }
-    // one segment per (depth, class) present in the chunk
-    const uint32_t wpm = __reduce_or_sync(FULL, mypm) & pm_all;
-    if (!wpm) continue;
-    for (int P = 1; P <= FASTP; ++P) {
-      if (!(wpm >> P & 1)) continue;
-      for (int k = 0; k < MAXC; ++k) {
-        const bool has = (mypm >> P & 1) && k < sT.tpl[tau].C && crec_hdr(sT, sT.tpl[tau].crec[k])->P == P;
-        if (!__any_sync(FULL, has)) continue;
-        if (lane == 0) {
-          const unsigned long long o = atomicAdd(&S.counters[CNT_SEGS + P], 1ull);
-          S.segs[P][o] = (item - ca) * 32 << 2 | k;
-        }
+    // one segment per (depth, class) present in the chunk: bit (P-1)*4 + class
+    uint32_t combos = 0;
+    if (mypm)
+      for (int k = 0; k < sT.tpl[tau].C; ++k) {
+        const int P = crec_hdr(sT, sT.tpl[tau].crec[k])->P;
+        if (P <= FASTP) combos |= 1u << ((P - 1) * 4 + k);
+      }
+    uint32_t all = __reduce_or_sync(FULL, combos);
+    while (all) {
+      const int bit = __ffs(all) - 1;
+      all &= all - 1;
+      const int P = bit / 4 + 1, k = bit & 3;
+      if (lane == 0) {
+        const unsigned long long o = atomicAdd(&S.counters[CNT_SEGS + P], 1ull);
+        S.segs[P][o] = (item - ca) * 32 << 2 | k;
       }
     }
   }
