@@ -50,8 +50,9 @@ constexpr i64 CBMAX = 1 << 17;       // chunks per batch (2^22 slots)
 constexpr i64 KEY_INF = INT64_MAX;
 constexpr i64 LIST_PAD = 0x7F7F7F7F7F7F7F7FLL;  // memset(0x7F) sentinel of the per-warp lists
 constexpr unsigned FULL = 0xffffffffu;
-// counter slots: P = work counter of K_pipe<P>, 16 + P = #segments of depth P
-constexpr int CNT_DEEP = 0, CNT_NDEEP = 14, CNT_CELLS = 15, CNT_SEGS = 16, NCNT = 32;
+// counter slots: P = work counter of K_pipe<P>, 16 + P = #jobs of depth P in
+// full (32-aligned) chunks, 32 + P = #jobs of depth P from partial chunks
+constexpr int CNT_DEEP = 0, CNT_NDEEP = 14, CNT_CELLS = 15, CNT_FULL = 16, CNT_PART = 32, NCNT = 48;
 
 struct Cands {
   const i64* idx;
@@ -79,7 +80,8 @@ struct Scratch {
   i64* Tc;            // [MAXC][ns] max T_pipe over the class's sub-classes
   i64* extra;         // [ns] gradient-sync time beyond T0 (C.8), by K_sync
   int32_t* deep;      // [ns] slots with a class deeper than FASTP (compacted)
-  i64* segs[FASTP + 1];  // per depth: segments (first slot << 2 | class)
+  int32_t* full[FASTP + 1];  // per depth: jobs (slot << 2 | class) of full chunks, 32-aligned groups
+  int32_t* part[FASTP + 1];  // per depth: jobs of partial chunks, packed
   unsigned long long* counters;  // [NCNT]
   i64 ns;             // slot capacity (row stride of the [MAXC][ns] arrays)
 };
@@ -108,7 +110,7 @@ __device__ __forceinline__ i64 warp_sum(i64 v) {
 }
 
 // ---- K_split -------------------------------------------------------------------
-__global__ void __launch_bounds__(NT) k_split(const Tables* __restrict__ gT, Cands c, i64 ca, i64 cb, Scratch S,
+__global__ void __launch_bounds__(NT, 6) k_split(const Tables* __restrict__ gT, Cands c, i64 ca, i64 cb, Scratch S,
                                               uint32_t pm_all) {
   __shared__ Tables sT;
   load_tables(sT, gT);
@@ -170,7 +172,10 @@ __global__ void __launch_bounds__(NT) k_split(const Tables* __restrict__ gT, Can
       off = __shfl_sync(FULL, off, 0) + __popc(dbal & ((1u << lane) - 1));
       if (deep) S.deep[off] = (int32_t)slot;
     }
-    // one segment per (depth, class) present in the chunk: bit (P-1)*4 + class
+    // jobs per (depth, class) present in the chunk: a full chunk (32 jobs of one
+    // template and class) keeps its own aligned group of 32, so a K_pipe warp's
+    // lanes have near-equal micro-batch counts; partial chunks (small-radix
+    // templates) are packed densely
     uint32_t combos = 0;
     if (mypm)
       for (int k = 0; k < sT.tpl[tau].C; ++k) {
@@ -182,10 +187,13 @@ __global__ void __launch_bounds__(NT) k_split(const Tables* __restrict__ gT, Can
       const int bit = __ffs(all) - 1;
       all &= all - 1;
       const int P = bit / 4 + 1, k = bit & 3;
-      if (lane == 0) {
-        const unsigned long long o = atomicAdd(&S.counters[CNT_SEGS + P], 1ull);
-        S.segs[P][o] = (item - ca) * 32 << 2 | k;
-      }
+      const bool has = combos >> bit & 1;
+      const unsigned bal = __ballot_sync(FULL, has);
+      const int cnt = __popc(bal);
+      unsigned long long o = 0;
+      if (lane == 0) o = atomicAdd(&S.counters[(cnt == 32 ? CNT_FULL : CNT_PART) + P], (unsigned long long)cnt);
+      o = __shfl_sync(FULL, o, 0) + __popc(bal & ((1u << lane) - 1));
+      if (has) (cnt == 32 ? S.full[P] : S.part[P])[o] = (int32_t)(slot << 2 | k);
     }
   }
 }
@@ -196,21 +204,22 @@ __global__ void __launch_bounds__(NT) k_pipe(const Tables* __restrict__ gT, Scra
   __shared__ Tables sT;
   load_tables(sT, gT);
   const int lane = threadIdx.x & 31;
-  const i64 nseg = (i64)S.counters[CNT_SEGS + P];
-  const i64* segs = S.segs[P];
+  const i64 nfull = (i64)S.counters[CNT_FULL + P], npart = (i64)S.counters[CNT_PART + P];
+  const i64 gfull = nfull / 32, items = gfull + (npart + 31) / 32;
   i64 cells = 0;
   for (;;) {
     i64 item = 0;
     if (lane == 0) item = (i64)atomicAdd(&S.counters[P], 1ull);
     item = __shfl_sync(FULL, item, 0);
-    if (item >= nseg) break;
-    const i64 sg = segs[item];
-    const int c = sg & 3;
-    const i64 slot = (sg >> 2) + lane;
+    if (item >= items) break;
+    const i64 q = item < gfull ? item * 32 + lane : (item - gfull) * 32 + lane;
+    if (item >= gfull && q >= npart) continue;
+    const int job = item < gfull ? S.full[P][q] : S.part[P][q];
+    const int c = job & 3;
+    const i64 slot = job >> 2;
     const int tau = S.tau[slot];
     if (tau < 0 || S.status[slot] != 0) continue;
     const TplRec& tp = sT.tpl[tau];
-    if (c >= tp.C || crec_hdr(sT, tp.crec[c])->P != P) continue;  // explicit lists mix templates
     const PipeOut r = class_pipes_inl<P>(sT, tp.crec[c], load_split(S, c, tp.C, slot));
     S.Tc[c * S.ns + slot] = r.T0;
     cells += r.cells;
@@ -706,7 +715,7 @@ static int finish(hsim_handle* h, int launches) {
 // count optional.
 static int run_phases(hsim_handle* h, const Tables* dT, Cands c, int64_t n, int64_t* out_ns, int32_t k, i64* lists,
                       int count, i64* cells_out, cudaStream_t st, int& launches) {
-  static int g_split = 0, g_pipe[FASTP + 1] = {0}, g_deep = 0, g_sync = 0, g_final = 0;
+  static int g_split = 0, g_pipe[FASTP + 1] = {0}, g_deep = 0, g_sync = 0;
   // chunk plan
   i64 nchunks;
   i64* hplan = nullptr;
@@ -723,16 +732,16 @@ static int run_phases(hsim_handle* h, const Tables* dT, Cands c, int64_t n, int6
   const i64 ns = cbatch * 32;
   // scratch (int64 words): tpos, Tc [MAXC], extra | segs per depth | counters | plan |
   // int32: tau, status, rm, deep, dig / q / seats / add [MAXC]
-  // segment capacity per depth: per chunk, #classes of that depth (any class for explicit lists)
+  // job capacity per depth: #classes of that depth per template x slots (x2: full / partial lists)
   const uint32_t pm = depth_mask(h);
-  size_t segcap[FASTP + 1], segw = 0;
+  size_t jobcap[FASTP + 1], jobw = 0;
   for (int P = 1; P <= FASTP; ++P) {
-    segcap[P] = (pm >> P & 1) ? (size_t)(c.idx ? MAXC : depth_jobs_max(h, P)) * cbatch : 0;
-    segw += segcap[P];
+    jobcap[P] = (pm >> P & 1) ? (size_t)depth_jobs_max(h, P) * ns : 0;
+    jobw += 2 * jobcap[P];
   }
   const size_t planw = c.idx ? 0 : (size_t)(2 * c.nr + 1);
-  const size_t n32 = (size_t)(4 + 4 * MAXC) * ns;
-  const size_t words = (size_t)(MAXC + 2) * ns + segw + NCNT + planw + (n32 + 1) / 2 + 8;
+  const size_t n32 = (size_t)(4 + 4 * MAXC) * ns + jobw;
+  const size_t words = (size_t)(MAXC + 2) * ns + NCNT + planw + (n32 + 1) / 2 + 8;
   i64* base = nullptr;
   if (ensure_work_scratch(h, words, &base)) return HSIM_ENOMEM;
   Scratch S;
@@ -741,11 +750,6 @@ static int run_phases(hsim_handle* h, const Tables* dT, Cands c, int64_t n, int6
   S.Tc = base + ns;
   S.extra = base + (MAXC + 1) * ns;
   i64* pw = base + (MAXC + 2) * ns;
-  S.segs[0] = nullptr;
-  for (int P = 1; P <= FASTP; ++P) {
-    S.segs[P] = pw;
-    pw += segcap[P];
-  }
   S.counters = (unsigned long long*)pw;
   pw += NCNT;
   if (!c.idx) {
@@ -763,8 +767,15 @@ static int run_phases(hsim_handle* h, const Tables* dT, Cands c, int64_t n, int6
   S.q = p32 + (4 + MAXC) * ns;
   S.seats = p32 + (4 + 2 * MAXC) * ns;
   S.add = p32 + (4 + 3 * MAXC) * ns;
+  int32_t* pj = p32 + (4 + 4 * MAXC) * ns;
+  S.full[0] = S.part[0] = nullptr;
+  for (int P = 1; P <= FASTP; ++P) {
+    S.full[P] = pj;
+    S.part[P] = pj + jobcap[P];
+    pj += 2 * jobcap[P];
+  }
   const int gs = grid_of(h, k_split, g_split), gd = grid_of(h, k_deep, g_deep), gy = grid_of(h, k_sync, g_sync),
-            gf = grid_of(h, k_final, g_final);
+            gf = sm_count(h) * 2;  // few per-warp top-k lists: cheap final merge
   i64 cells = 0;
   for (i64 ca = 0; ca < nchunks; ca += cbatch) {
     const i64 cb = ca + cbatch < nchunks ? ca + cbatch : nchunks;
@@ -866,10 +877,9 @@ int launch_merge(const int64_t* lists, int32_t nlists, int32_t k, int64_t* out_t
 int launch_eval(hsim_handle* h, const Tables* dT, const hsim_cands* cc, int64_t n, int64_t* out_ns, int32_t k,
                 int64_t* out_t, int64_t* out_i, cudaStream_t st) {
   Cands c{cc->idx, cc->first, cc->block, cc->stride, n, nullptr, 0};
-  static int g_final = 0;
   int launches = 0;
   i64* lists = nullptr;
-  const int nlists = grid_of(h, k_final, g_final) * (NT / 32);
+  const int nlists = sm_count(h) * 2 * (NT / 32);  // = K_final grid x warps
   if (k) {
     if (ensure_block_scratch(h, (size_t)nlists * 2 * k + 1, &lists)) return HSIM_ENOMEM;
     cudaMemsetAsync(lists, 0x7F, ((size_t)nlists * 2 * k + 1) * 8, st);  // lists + global bound word
