@@ -486,6 +486,97 @@ __global__ void __launch_bounds__(NT) k_sync(const Tables* __restrict__ gT, Scra
   }
 }
 
+constexpr int MW = 32;  // warps of k_merge_small
+struct RegTopK {
+  i64 t, i;  // this lane's entry
+  __device__ __forceinline__ void init() { t = KEY_INF; i = KEY_INF; }
+  __device__ __forceinline__ void insert(i64 xt, i64 xi) {
+    const int lane = threadIdx.x & 31;
+    const int pos = __popc(__ballot_sync(FULL, key_less(t, i, xt, xi)));
+    const i64 ut = __shfl_up_sync(FULL, (long long)t, 1), ui = __shfl_up_sync(FULL, (long long)i, 1);
+    if (lane == pos) { t = xt; i = xi; }
+    else if (lane > pos) { t = ut; i = ui; }
+  }
+};
+
+// T of one slot (K_final)
+__device__ __forceinline__ i64 final_T(const Tables& sT, const Cands& c, const Scratch& S, i64 slot, i64* t_out, i64* i_out) {
+  i64 T = INT64_MIN, i = -1;
+  const i64 t = S.tpos[slot];
+  if (t >= 0) {
+    i = cand_index(c, t);
+    const int tau = S.tau[slot];
+    if (tau >= 0) {
+      const int st = S.status[slot];
+      if (st) {
+        T = st;
+      } else {
+        const int C = sT.tpl[tau].C;
+        i64 T0 = 0;
+        for (int q = 0; q < C; ++q) T0 = imax(T0, S.Tc[q * S.ns + slot]);
+        T = T0 + S.extra[slot];
+      }
+    }
+  }
+  *t_out = t;
+  *i_out = i;
+  return T;
+}
+
+// k <= 32: each warp keeps its top-k in registers (lane j = j-th entry), warps
+// share a global pruning bound, and each block merges its warps into one list
+// (lists[block], kept across batches) at the end.
+__global__ void __launch_bounds__(NT) k_final_small(const Tables* __restrict__ gT, Cands c, Scratch S, i64 ns,
+                                                    i64* __restrict__ out, int k, i64* __restrict__ lists) {
+  __shared__ Tables sT;
+  __shared__ i64 bt[NT / 32][32], bi[NT / 32][32];
+  load_tables(sT, gT);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const i64 wid = (i64)blockIdx.x * (NT / 32) + w;
+  const i64 nw = (i64)gridDim.x * (NT / 32);
+  i64* blist = lists + (i64)blockIdx.x * 2 * k;
+  unsigned long long* gthr = (unsigned long long*)(lists + (i64)gridDim.x * 2 * k);
+  RegTopK r;
+  r.init();
+  if (w == 0 && lane < k && blist[lane] != LIST_PAD && blist[lane] != KEY_INF) { r.t = blist[lane]; r.i = blist[k + lane]; }
+  for (i64 base = wid * 32; base < ns; base += nw * 32) {
+    i64 t, i;
+    const i64 T = final_T(sT, c, S, base + lane, &t, &i);
+    if (out && t >= 0) out[t] = T;
+    const i64 g = (i64)*(volatile unsigned long long*)gthr;
+    i64 thT = __shfl_sync(FULL, (long long)r.t, k - 1), thI = __shfl_sync(FULL, (long long)r.i, k - 1);
+    unsigned cand = __ballot_sync(FULL, t >= 0 && T >= 0 && T <= g && key_less(T, i, thT, thI));
+    if (!cand) continue;
+    while (cand) {
+      const int src = __ffs(cand) - 1;
+      cand &= cand - 1;
+      const i64 xt = __shfl_sync(FULL, (long long)T, src), xi = __shfl_sync(FULL, (long long)i, src);
+      if (key_less(xt, xi, thT, thI)) {
+        r.insert(xt, xi);
+        thT = __shfl_sync(FULL, (long long)r.t, k - 1);
+        thI = __shfl_sync(FULL, (long long)r.i, k - 1);
+      }
+    }
+    if (lane == 0 && thT != KEY_INF) atomicMin(gthr, (unsigned long long)thT);
+  }
+  bt[w][lane] = r.t;
+  bi[w][lane] = r.i;
+  __syncthreads();
+  if (w == 0) {
+    for (int o = 1; o < NT / 32; ++o)
+      for (int p = 0; p < k; ++p) {
+        const i64 xt = bt[o][p], xi = bi[o][p];
+        const i64 thT = __shfl_sync(FULL, (long long)r.t, k - 1), thI = __shfl_sync(FULL, (long long)r.i, k - 1);
+        if (xt == KEY_INF || !key_less(xt, xi, thT, thI)) break;
+        r.insert(xt, xi);
+      }
+    if (lane < k) {
+      blist[lane] = r.t;
+      blist[k + lane] = r.t == KEY_INF ? -1 : r.i;
+    }
+  }
+}
+
 __global__ void __launch_bounds__(NT) k_final(const Tables* __restrict__ gT, Cands c, Scratch S, i64 ns,
                                               i64* __restrict__ out, int k, i64* __restrict__ lists) {
   __shared__ Tables sT;
@@ -621,19 +712,6 @@ __global__ void __launch_bounds__(MT) k_merge(const i64* __restrict__ blk, int n
 // K_merge for k <= 32: every warp keeps a sorted top-k in registers (lane j
 // holds the j-th entry) and walks the heads of its share of the lists; warp 0
 // then merges the per-warp results.  Same output as k_merge.
-constexpr int MW = 32;  // warps of k_merge_small
-struct RegTopK {
-  i64 t, i;  // this lane's entry
-  __device__ __forceinline__ void init() { t = KEY_INF; i = KEY_INF; }
-  __device__ __forceinline__ void insert(i64 xt, i64 xi) {
-    const int lane = threadIdx.x & 31;
-    const int pos = __popc(__ballot_sync(FULL, key_less(t, i, xt, xi)));
-    const i64 ut = __shfl_up_sync(FULL, (long long)t, 1), ui = __shfl_up_sync(FULL, (long long)i, 1);
-    if (lane == pos) { t = xt; i = xi; }
-    else if (lane > pos) { t = ut; i = ui; }
-  }
-};
-
 __global__ void __launch_bounds__(MW * 32) k_merge_small(const i64* __restrict__ blk, int nblk, int k,
                                                           i64* __restrict__ out_t, i64* __restrict__ out_i) {
   __shared__ i64 st[MW][32], si[MW][32];
@@ -711,6 +789,8 @@ static int finish(hsim_handle* h, int launches) {
   return HSIM_OK;
 }
 
+static int final_grid(const hsim_handle* h, int k) { return sm_count(h) * (k && k <= 32 ? 8 : 2); }
+
 // Runs the phase kernels over all chunks of the call; out / top-k lists / cell
 // count optional.
 static int run_phases(hsim_handle* h, const Tables* dT, Cands c, int64_t n, int64_t* out_ns, int32_t k, i64* lists,
@@ -775,7 +855,7 @@ static int run_phases(hsim_handle* h, const Tables* dT, Cands c, int64_t n, int6
     pj += 2 * jobcap[P];
   }
   const int gs = grid_of(h, k_split, g_split), gd = grid_of(h, k_deep, g_deep), gy = grid_of(h, k_sync, g_sync),
-            gf = sm_count(h) * 2;  // few per-warp top-k lists: cheap final merge
+            gf = final_grid(h, k);
   i64 cells = 0;
   for (i64 ca = 0; ca < nchunks; ca += cbatch) {
     const i64 cb = ca + cbatch < nchunks ? ca + cbatch : nchunks;
@@ -848,7 +928,8 @@ static int run_phases(hsim_handle* h, const Tables* dT, Cands c, int64_t n, int6
       ++launches;
       join(ss);
     }
-    k_final<<<gf, NT, 0, st>>>(dT, c, S, nsb, out_ns, k, lists);
+    if (k && k <= 32) k_final_small<<<gf, NT, 0, st>>>(dT, c, S, nsb, out_ns, k, lists);
+    else k_final<<<gf, NT, 0, st>>>(dT, c, S, nsb, out_ns, k, lists);
     ++launches;
   }
   if (cells_out) *cells_out = cells;
@@ -879,7 +960,7 @@ int launch_eval(hsim_handle* h, const Tables* dT, const hsim_cands* cc, int64_t 
   Cands c{cc->idx, cc->first, cc->block, cc->stride, n, nullptr, 0};
   int launches = 0;
   i64* lists = nullptr;
-  const int nlists = sm_count(h) * 2 * (NT / 32);  // = K_final grid x warps
+  const int nlists = final_grid(h, k) * (k <= 32 ? 1 : NT / 32);  // per block (k <= 32) or per warp
   if (k) {
     if (ensure_block_scratch(h, (size_t)nlists * 2 * k + 1, &lists)) return HSIM_ENOMEM;
     cudaMemsetAsync(lists, 0x7F, ((size_t)nlists * 2 * k + 1) * 8, st);  // lists + global bound word
