@@ -49,20 +49,6 @@ Link path_link(const hsim_path& p, i64 frame) {
 Link cat(const Link& a, const Link& b) { return Link{a.alpha + b.alpha, std::min(a.beta, b.beta)}; }
 i64 tau(const Link& e, i64 x) { return e.alpha + ceilq(x, e.beta); }
 
-// magic multiplier for floor(n / d), n < 2^53 (Granlund-Montgomery): sh = 53 +
-// ceil(log2 d), M = floor(2^sh / d) + 1 < 2^64; M*d - 2^sh < d <= 2^(sh-53)
-bool magic_for(u64 d, u64* M, int* sh) {
-  if (d == 0) return false;
-  int l = 0;
-  while (l < 63 && ((u64)1 << l) < d) ++l;
-  *sh = 53 + l;
-  const unsigned __int128 two = (unsigned __int128)1 << *sh;
-  const unsigned __int128 m = two / d + 1;
-  if (m >> 64) return false;
-  *M = (u64)m;
-  return m * d - two <= ((unsigned __int128)1 << (*sh - 53));
-}
-
 i64 hamilton_floor_rem(i64 n, i64 w, i64 W, i64* rem) {
   *rem = n * w % W;
   return n * w / W;
@@ -481,7 +467,7 @@ void hsim_handle::enumerate() {
       if (M < Dt) return;
       TplRec r{};
       r.prefix = acc;
-      if (!magic_for((u64)Dt, &r.dM, &r.dsh)) fail(HSIM_ERANGE, "replica count");
+      r.rD = 1.0 / (double)Dt;
       r.b = b; r.M = (int32_t)M; r.C = (int32_t)classes.size(); r.D = (int32_t)Dt;
       for (size_t c = 0; c < classes.size(); ++c) {
         r.crec[c] = crec((int)bi, (int)M, classes[c].first, classes[c].second);
@@ -596,14 +582,19 @@ void hsim_handle::prepare() {
         if (v >= 1 && v < 2147483648.0 && v == std::floor(v) && (xmax < ((i64)1 << (52 - k)))) {
           hT.lc_G[b] = (i64)v;
           hT.lc_k[b] = (int8_t)k;
-          int sh = 0;
-          found = magic_for((u64)v, &hT.lc_M[b], &sh);
-          hT.lc_sh[b] = (int8_t)sh;
+          hT.lc_rG[b] = 1.0 / v;
+          found = true;
         }
       }
       exact = found;
     }
     hT.lc_exact = exact ? 1 : 0;
+    // dominance: tau_b(x) >= tau_a(x) for all x when alpha_b >= alpha_a and beta_b <= beta_a
+    for (size_t b = 0; b < lcs.size(); ++b) {
+      hT.lc_dom[b] = 0;
+      for (size_t a = 0; a < lcs.size(); ++a)
+        if (a != b && lcs[b].alpha >= lcs[a].alpha && lcs[b].beta <= lcs[a].beta) hT.lc_dom[b] |= (u64)1 << a;
+    }
   }
   // link classes of the q < 2^lg edges between two groups' bases (cross-class ring edges)
   {

@@ -68,8 +68,8 @@ struct TplRec {
   int32_t b, M, C, D;     // micro-batch size, #micro-batches, classes, total replicas
   int32_t crec[MAXC];     // int64-offsets of the class records in the pool
   uint32_t pmask;         // bit min(P, 31) set for every class depth P
-  int32_t dsh;            // magic division by D (ring chunk): shift
-  u64 dM;                 //   and multiplier
+  int32_t _pad;
+  double rD;              // 1.0 / D (ring chunk: ceil division by D with exact fix-up)
 };
 
 struct Tables {
@@ -91,12 +91,12 @@ struct Tables {
   int32_t n_lc, n_nodes;
   Link lc[MAXLC];
   // exact integer form of tau (DESIGN.md C.0): when beta = G / 2^k exactly and
-  // every x << k < 2^53 with x / beta < 2^53 / (2G) (checked at create),
-  // ceil(RN(x / beta)) == ceil_div(x << k, G); floor division by G through a
-  // magic multiplier M with shift sh (Granlund-Montgomery, n < 2^53)
+  // every x << k < 2^52 (checked at create), ceil(RN(x / beta)) ==
+  // ceil_div(x << k, G), computed from a reciprocal estimate + exact fix-up
   i64 lc_G[MAXLC];
-  u64 lc_M[MAXLC];
-  int8_t lc_k[MAXLC], lc_sh[MAXLC];
+  double lc_rG[MAXLC];     // 1.0 / G (floor estimate, then exact integer fix-up)
+  u64 lc_dom[MAXLC];       // link classes with alpha <= and beta >= this one's (never the max of tau)
+  int8_t lc_k[MAXLC], _pad4[MAXLC];
   int32_t lc_exact, _pad3;
   const u64* xmask_cross;  // [MAXT][MAXG][MAXT][MAXG][4] link classes of edges (t1, b1+q) -> (t2, b2+q), q < 2^lg
   const u64* xmask_same;   // [MAXT][MAXG][MAXG][4] same node
@@ -117,31 +117,33 @@ HD i64 ceil_div(i64 a, i64 b) { return (a + b - 1) / b; }
 HD i64 imax(i64 a, i64 b) { return a > b ? a : b; }
 HD i64 imin(i64 a, i64 b) { return a < b ? a : b; }
 
-HD u64 umulhi64(u64 a, u64 b) {
-#ifdef __CUDA_ARCH__
-  return __umul64hi(a, b);
-#else
-  return (u64)(((unsigned __int128)a * b) >> 64);
-#endif
-}
-// floor(n / d) for n < 2^53 given M = floor(2^sh / d) + 1, sh = 53 + ceil(log2 d)
-HD u64 div_magic(u64 n, u64 M, int sh) {
-  const u64 hi = umulhi64(n, M), lo = n * M;
-  return sh >= 64 ? hi >> (sh - 64) : (hi << (64 - sh)) | (lo >> sh);
-}
-HD i64 ceil_div_magic(i64 n, i64 d, u64 M, int sh) {
-  const u64 q = div_magic((u64)n, M, sh);
-  return (i64)q + ((i64)q * d != n ? 1 : 0);
+// ceil(n / d) for 0 <= n < 2^52, 1 <= d < 2^31: floor estimate in fp64 from the
+// reciprocal (|error| < 1), then an exact integer fix-up of the remainder
+HD i64 ceil_div_rcp(i64 n, i64 d, double rd) {
+  i64 q = (i64)((double)n * rd);
+  i64 r = n - q * d;
+  if (r < 0) { q -= 1; r += d; }
+  if (r >= d) { q += 1; r -= d; }
+  return q + (r != 0 ? 1 : 0);
 }
 // alpha_e + ceil(x / beta_e) of link class b (C.6 tau_e)
 HD i64 tau_lc(const Tables& T, int b, i64 x) {
-  if (T.lc_exact) return T.lc[b].alpha + ceil_div_magic(x << T.lc_k[b], T.lc_G[b], T.lc_M[b], T.lc_sh[b]);
+  if (T.lc_exact) return T.lc[b].alpha + ceil_div_rcp(x << T.lc_k[b], T.lc_G[b], T.lc_rG[b]);
   return T.lc[b].alpha + ceilq(x, T.lc[b].beta);
 }
 
-// max over the link classes in `mask` of alpha + ceil(x / beta)  (C.6 tau_e)
+// max over the link classes in `mask` of alpha + ceil(x / beta)  (C.6 tau_e);
+// classes dominated by another class of the mask are skipped first
+HD int ffs64(u64 m) {
+#ifdef __CUDA_ARCH__
+  return __ffsll((long long)m) - 1;
+#else
+  return __builtin_ctzll(m);
+#endif
+}
 HD i64 eval_mask(const Tables& T, u64 mask, i64 x) {
   i64 best = 0;
+  for (u64 m = mask; m; m &= m - 1) mask &= ~T.lc_dom[ffs64(m)];
   while (mask) {
 #ifdef __CUDA_ARCH__
     int b = __ffsll((long long)mask) - 1;
@@ -531,7 +533,7 @@ HD i64 grad_sync_c(const Tables& T, const TplRec& tp, const ClassSplit (&cs)[C],
                        : T.xmask_cross[(((t1 * MAXG + s.last_base) * MAXT + t2) * MAXG + t.first_base) * 4 + lg];
     }
     const i64 RS = rsmask ? eval_mask(T, rsmask, xs) : 0;
-    const i64 AR = 2 * (i64)(tp.D - 1) * eval_mask(T, mask, ceil_div_magic(xs, tp.D, tp.dM, tp.dsh));
+    const i64 AR = 2 * (i64)(tp.D - 1) * eval_mask(T, mask, ceil_div_rcp(xs, tp.D, tp.rD));
     i64 start = 0;
 #pragma unroll
     for (int c = 0; c < C; ++c) start = imax(start, cur_free[c]);

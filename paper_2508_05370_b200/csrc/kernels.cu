@@ -712,8 +712,8 @@ __global__ void __launch_bounds__(MT) k_merge(const i64* __restrict__ blk, int n
 // K_merge for k <= 32: every warp keeps a sorted top-k in registers (lane j
 // holds the j-th entry) and walks the heads of its share of the lists; warp 0
 // then merges the per-warp results.  Same output as k_merge.
-__global__ void __launch_bounds__(MW * 32) k_merge_small(const i64* __restrict__ blk, int nblk, int k,
-                                                          i64* __restrict__ out_t, i64* __restrict__ out_i) {
+__device__ void merge_small_body(const i64* __restrict__ blk, int nblk, int k, i64* __restrict__ out_t,
+                                 i64* __restrict__ out_i) {
   __shared__ i64 st[MW][32], si[MW][32];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   RegTopK r;
@@ -756,6 +756,65 @@ __global__ void __launch_bounds__(MW * 32) k_merge_small(const i64* __restrict__
       out_t[lane] = r.t;
       out_i[lane] = r.t == KEY_INF ? -1 : r.i;
     }
+  }
+}
+
+__global__ void __launch_bounds__(MW * 32) k_merge_small(const i64* __restrict__ blk, int nblk, int k,
+                                                          i64* __restrict__ out_t, i64* __restrict__ out_i) {
+  merge_small_body(blk, nblk, k, out_t, out_i);
+}
+
+// k <= 32 with a global bound g >= the k-th smallest time (K_final's): only
+// list entries with time <= g can be in the top-k -- a few k of them -- so
+// compact those into shared memory and bitonic-sort them; fall back to the
+// register merge if more than CAP survive (massive ties).
+constexpr int CAP = 1024;
+__global__ void __launch_bounds__(1024) k_merge_thresh(const i64* __restrict__ blk, int nblk, int k,
+                                                      const unsigned long long* __restrict__ gthr,
+                                                      i64* __restrict__ out_t, i64* __restrict__ out_i) {
+  __shared__ i64 ct[CAP], ci[CAP];
+  __shared__ int cnt;
+  const int tid = threadIdx.x;
+  const i64 g = (i64)*gthr;
+  if (tid == 0) cnt = 0;
+  __syncthreads();
+  const i64 tot = (i64)nblk * k;
+  for (i64 e = tid; e < tot; e += 1024) {
+    const i64 b = e / k, p = e - b * k;
+    const i64 t = blk[b * 2 * k + p];
+    if (t != LIST_PAD && t != KEY_INF && t <= g) {
+      const int pos = atomicAdd(&cnt, 1);
+      if (pos < CAP) {
+        ct[pos] = t;
+        ci[pos] = blk[b * 2 * k + k + p];
+      }
+    }
+  }
+  __syncthreads();
+  const int n = cnt;
+  if (n > CAP) {  // uniform branch
+    merge_small_body(blk, nblk, k, out_t, out_i);
+    return;
+  }
+  int np = 1;
+  while (np < n) np <<= 1;
+  for (int e = n + tid; e < np; e += 1024) { ct[e] = KEY_INF; ci[e] = KEY_INF; }
+  __syncthreads();
+  for (int size = 2; size <= np; size <<= 1)
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int e = tid; e < np; e += 1024) {
+        const int j = e ^ stride;
+        if (j > e) {
+          const bool up = (e & size) == 0;
+          const i64 a = ct[e], ai = ci[e], b = ct[j], bi = ci[j];
+          if (key_less(b, bi, a, ai) == up) { ct[e] = b; ci[e] = bi; ct[j] = a; ci[j] = ai; }
+        }
+      }
+      __syncthreads();
+    }
+  if (tid < k) {
+    out_t[tid] = tid < n ? ct[tid] : KEY_INF;
+    out_i[tid] = tid < n ? ci[tid] : -1;
   }
 }
 
@@ -971,7 +1030,11 @@ int launch_eval(hsim_handle* h, const Tables* dT, const hsim_cands* cc, int64_t 
   }
   if (k) {
     // n == 0 merges no list and only writes the (INT64_MAX, -1) padding
-    launch_merge_any(lists, n > 0 ? nlists : 0, k, out_t, out_i, st);
+    if (n > 0 && k <= 32)
+      k_merge_thresh<<<1, 1024, 0, st>>>(lists, nlists, k, (const unsigned long long*)(lists + (size_t)nlists * 2 * k),
+                                         out_t, out_i);
+    else
+      launch_merge_any(lists, n > 0 ? nlists : 0, k, out_t, out_i, st);
     ++launches;
   }
   return finish(h, launches);
