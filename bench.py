@@ -231,7 +231,7 @@ def run_ours(a):
     if os.path.exists(prof):
         try:
             with open(prof) as f:
-                traffic = json.load(f).get("k_eval_dram_bytes_per_launch")
+                traffic = json.load(f).get("sweep_dram_bytes")
         except (OSError, ValueError):
             traffic = None
 
@@ -278,7 +278,8 @@ def run_ours(a):
                            "parallelism": f"block-cyclic shard x{world}" + (" + NCCL all_gather" if world > 1 else "")},
                 "roofline": {"bound": "alu", "achieved": round(achieved, 1), "peak": round(peak_gops, 1),
                              "unit": "Gop/s", "frac": round(achieved / peak_gops, 4), "traffic": traffic,
-                             "kernel": "k_eval (+k_merge in the same interval)",
+                             "kernel": "one hsim_topk sweep = K_split, K_pipe<P>, K_deep, K_sync (concurrent "
+                                       "fork/join streams), K_final, K_merge; per-kernel shares in profiles/",
                              "ops_per_launch": OPS_PER_CELL * cells, "cells_per_launch": cells,
                              "peak_from": f"{SMS} SMs x {LANES_PER_SM} lanes x {sm_max:.0f} MHz (issue slots)"},
                 "gpu_launches": launches_per_step * a.steps,

@@ -778,15 +778,15 @@ __global__ void __launch_bounds__(1024) k_merge_thresh(const i64* __restrict__ b
   const i64 g = (i64)*gthr;
   if (tid == 0) cnt = 0;
   __syncthreads();
-  const i64 tot = (i64)nblk * k;
-  for (i64 e = tid; e < tot; e += 1024) {
-    const i64 b = e / k, p = e - b * k;
-    const i64 t = blk[b * 2 * k + p];
+  const int tot = nblk * k;
+  for (int e = tid; e < tot; e += 1024) {
+    const int b = e / k, p = e - b * k;
+    const i64 t = blk[(i64)b * 2 * k + p];
     if (t != LIST_PAD && t != KEY_INF && t <= g) {
       const int pos = atomicAdd(&cnt, 1);
       if (pos < CAP) {
         ct[pos] = t;
-        ci[pos] = blk[b * 2 * k + k + p];
+        ci[pos] = blk[(i64)b * 2 * k + k + p];
       }
     }
   }
