@@ -84,6 +84,8 @@ struct hsim_handle {
   std::vector<std::vector<int>> nodes_of_type;
   i64 n_of_type[MAXT] = {0, 0, 0, 0};
   uint32_t pmask_all = 0;   // union of template depth masks (which depth kernels to launch)
+  i64 layer_fb_max = 0, ext_max = 0, c_max = 0;  // bound of every 1F1B time (fp64-exact pipelines, < 2^52)
+  int depth_max = 0;
   int pcnt_max[FASTP + 1] = {0};  // max #classes of depth P in one template (job-list capacity)
   i64 N = 0;
   Tables hT{};  // host pointers (for hsim_decode)
@@ -376,6 +378,8 @@ int32_t hsim_handle::crec(int bi, int M, int D, const std::vector<std::pair<int,
     if (s == P - 1) { r.fext += d.head_f; r.gext += d.head_b; r.wext += d.head_f + d.head_b; }
     r.tp_mask = tp_mask[t][lg];
     w[s] = ((i64)1 << 40) / r.tcomp;
+    layer_fb_max = std::max(layer_fb_max, r.layer_f + r.layer_b);
+    ext_max = std::max(ext_max, r.fext + r.gext);
   }
   // base layer split: Hamilton of L with weights floor(2^40 / tcomp) (C.4)
   {
@@ -407,7 +411,9 @@ int32_t hsim_handle::crec(int bi, int M, int D, const std::vector<std::pair<int,
       for (int q = 0; q < np; ++q)
         c = std::max(c, tau(link(pl[r][s].first, pl[r][s].second + q, pl[r][s + 1].first, pl[r][s + 1].second + q), A));
       cv[r][s] = c;
+      c_max = std::max(c_max, c);
     }
+  depth_max = std::max(depth_max, P);
   // sub-classes (A13): replicas with identical p2p vectors, ordered by lowest replica
   std::vector<int> rep;
   std::map<std::vector<i64>, int> seen;
@@ -724,6 +730,12 @@ int hsim_create(const hsim_cluster_desc* cluster, const hsim_model_desc* model, 
         fail(HSIM_ERANGE, "a stage's compute time reaches 2^40 ns");
     h->enumerate();
     if (h->N <= 0) fail(HSIM_EINVAL, "InsufficientDevices: the candidate space is empty");
+    {  // every 1F1B time <= sum of all op and message weights <= m (L max layer f+g + 2 max emb/head f+g
+       // + 2 P max p2p), m <= global batch
+      const double bound = (double)model->global_batch *
+                           ((double)model->layers * h->layer_fb_max + 2.0 * h->ext_max + 2.0 * h->depth_max * (double)h->c_max);
+      if (bound >= 4503599627370496.0) fail(HSIM_ERANGE, "1F1B times may reach 2^52 ns");
+    }
     h->prepare();
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) == cudaSuccess && ndev > 0) h->upload();  // else: host-only handle

@@ -328,7 +328,10 @@ HD i64 pipeline_generic(int P, i64 m, const i64* f, const i64* g, const i64* c) 
 // alternate F (s = level mod 2) / B.  m < P: closed-form levels at run time.
 template <int P>
 struct Pipe {
-  i64 f[P], g[P], c[P], X[P];  // c[s] = 2 * (p2p cost of boundary s -> s+1)
+  // Times are exact integers held in doubles (all < 2^52, checked at create):
+  // the max-plus cell then runs on the fp64 pipe (DSETP + DADD) with the
+  // selects on the ALU pipe, about half the ALU-pipe work of int64 max/add.
+  double f[P], g[P], c[P], X[P];  // c[s] = 2 * (p2p cost of boundary s -> s+1)
 
   // op of stage s at level lv: +1 F, -1 B, 0 none
   HD static int op_at(i64 lv, int s, i64 m) {
@@ -337,14 +340,15 @@ struct Pipe {
     if (jb >= 0 && !(jb & 1) && (jb >> 1) < m) return -1;
     return 0;
   }
-  HD i64 fop(const i64 (&old)[P], int s) const {
-    return s == 0 ? old[0] + f[0] : imax(old[s], old[s == 0 ? 0 : s - 1]) + f[s];
+  HD static double dmax(double a, double b) { return a > b ? a : b; }
+  HD double fop(const double (&old)[P], int s) const {
+    return s == 0 ? old[0] + f[0] : dmax(old[s], old[s == 0 ? 0 : s - 1]) + f[s];
   }
-  HD i64 bop(const i64 (&old)[P], int s) const {
-    return s == P - 1 ? old[s] + g[s] : imax(old[s], old[s == P - 1 ? s : s + 1] + c[s]) + g[s];
+  HD double bop(const double (&old)[P], int s) const {
+    return s == P - 1 ? old[s] + g[s] : dmax(old[s], old[s == P - 1 ? s : s + 1] + c[s]) + g[s];
   }
   HD void level_rt(i64 lv, i64 m) {  // run-time ops
-    i64 old[P];
+    double old[P];
 #pragma unroll
     for (int s = 0; s < P; ++s) old[s] = X[s];
 #pragma unroll
@@ -356,7 +360,7 @@ struct Pipe {
   }
   // m >= P: ops of warm-up level lv (compile-time after unrolling)
   HD void level_warm(int lv) {
-    i64 old[P];
+    double old[P];
 #pragma unroll
     for (int s = 0; s < P; ++s) old[s] = X[s];
 #pragma unroll
@@ -368,7 +372,7 @@ struct Pipe {
   }
   // m >= P: ops of cool-down level 2m + d
   HD void level_cool(int d) {
-    i64 old[P];
+    double old[P];
 #pragma unroll
     for (int s = 0; s < P; ++s) old[s] = X[s];
 #pragma unroll
@@ -380,7 +384,7 @@ struct Pipe {
   // one steady level of parity par: stages with s % 2 == par run F, the others B
   template <int par>
   HD void steady_level() {
-    i64 old[P];
+    double old[P];
 #pragma unroll
     for (int s = 0; s < P; ++s) old[s] = X[s];
 #pragma unroll
@@ -403,7 +407,7 @@ struct Pipe {
       const i64 total = 2 * (m + P - 1);
       for (i64 lv = 0; lv < total; ++lv) level_rt(lv, m);
     }
-    return X[0];
+    return (i64)X[0];
   }
 };
 
@@ -419,14 +423,14 @@ HD PipeOut class_pipes_inl(const Tables& T, int32_t off, const ClassSplit& cs) {
 #pragma unroll
   for (int s = 0; s < P; ++s) {
     const i64 l = lw.next(st);
-    p.f[s] = l * st[s].layer_f + st[s].fext;
-    p.g[s] = l * st[s].layer_b + st[s].gext;
+    p.f[s] = (double)(l * st[s].layer_f + st[s].fext);
+    p.g[s] = (double)(l * st[s].layer_b + st[s].gext);
   }
   PipeOut r{0, 0};
   for (int u = 0; u < h->U; ++u) {
     const i64* sub = crec_sub(T, off, P, u);
 #pragma unroll
-    for (int s = 0; s + 1 < P; ++s) p.c[s] = 2 * sub[1 + s];
+    for (int s = 0; s + 1 < P; ++s) p.c[s] = (double)(2 * sub[1 + s]);
     const i64 m = mb_of(cs, sub[0]);
     r.cells += 2 * P * m;
     r.T0 = imax(r.T0, p.run(m));
