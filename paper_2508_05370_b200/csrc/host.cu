@@ -78,6 +78,7 @@ struct hsim_handle {
   std::vector<i64> prefix;
   std::vector<int32_t> bucket;
   std::vector<i64> cprefix;
+  std::vector<int32_t> cbucket;
   std::vector<TplRec> tpl;
   std::vector<i64> pool;
   std::map<std::vector<int>, int32_t> crec_of;
@@ -94,6 +95,7 @@ struct hsim_handle {
   i64* d_prefix = nullptr;
   int32_t* d_bucket = nullptr;
   i64* d_cprefix = nullptr;
+  int32_t* d_cbucket = nullptr;
   i64* h_plan = nullptr;        // pinned host staging of the per-call chunk plan
   size_t h_plan_cap = 0;
   u64* d_xmask = nullptr;
@@ -636,6 +638,18 @@ void hsim_handle::prepare() {
   cprefix.assign(prefix.size(), 0);
   for (size_t k = 0; k + 1 < prefix.size(); ++k) cprefix[k + 1] = cprefix[k] + (prefix[k + 1] - prefix[k] + CHUNK - 1) / CHUNK;
   hT.tpl_cprefix = cprefix.data();
+  {
+    const i64 nch = cprefix.back();
+    int cs = 0;
+    while ((nch >> cs) > 65536) ++cs;
+    const i64 ncb = nch > 0 ? ((nch - 1) >> cs) + 1 : 1;
+    cbucket.assign(ncb + 1, 0);
+    for (i64 b = 0; b <= ncb; ++b)
+      cbucket[b] = (int32_t)bsearch_le(cprefix.data(), (i64)tpl.size(), std::min((b << cs), nch > 0 ? nch - 1 : 0));
+    hT.n_cbucket = ncb;
+    hT.cbucket_shift = cs;
+    hT.tpl_cbucket = cbucket.data();
+  }
   hT.tpl_prefix = prefix.data();
   hT.tpl = tpl.data();
   hT.pool = pool.data();
@@ -654,6 +668,9 @@ void hsim_handle::upload() {
   ck(cudaMalloc(&d_cprefix, cprefix.size() * 8), "cudaMalloc cprefix");
   ck(cudaMemcpy(d_cprefix, cprefix.data(), cprefix.size() * 8, cudaMemcpyHostToDevice), "H2D cprefix");
   dt.tpl_cprefix = d_cprefix;
+  ck(cudaMalloc(&d_cbucket, cbucket.size() * 4), "cudaMalloc cbucket");
+  ck(cudaMemcpy(d_cbucket, cbucket.data(), cbucket.size() * 4, cudaMemcpyHostToDevice), "H2D cbucket");
+  dt.tpl_cbucket = d_cbucket;
   ck(cudaMalloc(&d_xmask, (xmask_cross.size() + xmask_same.size()) * 8), "cudaMalloc xmask");
   ck(cudaMemcpy(d_xmask, xmask_cross.data(), xmask_cross.size() * 8, cudaMemcpyHostToDevice), "H2D xmask");
   ck(cudaMemcpy(d_xmask + xmask_cross.size(), xmask_same.data(), xmask_same.size() * 8, cudaMemcpyHostToDevice), "H2D xmask");
@@ -758,6 +775,7 @@ void hsim_destroy(hsim_handle* h) {
   cudaFree(h->d_prefix);
   cudaFree(h->d_bucket);
   cudaFree(h->d_cprefix);
+  cudaFree(h->d_cbucket);
   if (h->h_plan) cudaFreeHost(h->h_plan);
   cudaFree(h->d_xmask);
   cudaFree(h->d_work);

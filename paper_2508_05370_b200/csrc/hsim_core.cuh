@@ -84,6 +84,9 @@ struct Tables {
   const i64* tpl_prefix;  // [n_tpl + 1] first candidate of each template
   const int32_t* tpl_bucket;  // [n_bucket + 1] template of candidate b << bucket_shift (coarse index)
   const i64* tpl_cprefix;     // [n_tpl + 1] first 32-candidate chunk of each template (chunks never straddle)
+  const int32_t* tpl_cbucket; // [n_cbucket + 1] template of chunk b << cbucket_shift (coarse index)
+  i64 n_cbucket;
+  int32_t cbucket_shift, _pad5;
   int32_t bucket_shift, _pad2;
   const TplRec* tpl;      // [n_tpl]
   const i64* pool;        // crec pool
@@ -173,6 +176,17 @@ HD i64 bsearch_le(const i64* a, i64 n, i64 x) {
 }
 // template of candidate i: max{tau : prefix[tau] <= i}; the coarse bucket
 // table narrows the binary search to the templates of one bucket
+// template of chunk g (chunks of 32 candidates never straddle templates)
+HD i64 find_template_of_chunk(const Tables& T, i64 g) {
+  const i64 b = g >> T.cbucket_shift;
+  i64 lo = T.tpl_cbucket[b], hi = (i64)T.tpl_cbucket[b + 1] + 1;
+  if (hi > T.n_tpl) hi = T.n_tpl;
+  while (hi - lo > 1) {
+    const i64 mid = (lo + hi) >> 1;
+    if (T.tpl_cprefix[mid] <= g) lo = mid; else hi = mid;
+  }
+  return lo;
+}
 HD i64 find_template(const Tables& T, i64 i) {
   const i64 b = i >> T.bucket_shift;
   i64 lo = T.tpl_bucket[b], hi = (i64)T.tpl_bucket[b + 1] + 1;
@@ -579,17 +593,22 @@ __device__ __forceinline__ int nth_set_lane(unsigned mask, int n) {
   return __ffs(mask) - 1;
 }
 
+// Times as exact integers in doubles (< 2^52, checked at create): fp64 max/add.
+__device__ __forceinline__ double shfl_d(double v, int src) { return __shfl_sync(0xffffffffu, v, src); }
+__device__ __forceinline__ double dmax2(double a, double b) { return a > b ? a : b; }
+
 struct LanePipe {
   int P, s, lane;
-  i64 m, f, g, cR, cL;  // cR = c_s (0 on the last stage), cL = c_{s-1}
-  i64 X, out;
+  i64 m;
+  double f, g, cR, cL;  // cR = c_s (0 on the last stage), cL = c_{s-1}
+  double X, out;
   // one level; every lane of the warp must call it (it shuffles).  In the
   // steady range the op is given by the parity constants, else by the
   // closed-form levels of F(s,j) / B(s,j).
-  __device__ __forceinline__ void level(i64 lv, bool steady, int srcS, i64 durS, i64 cS, i64 zS) {
+  __device__ __forceinline__ void level(i64 lv, bool steady, int srcS, double durS, double cS, bool keepS) {
     int src = srcS;
-    i64 dur = durS, cc = cS, z = zS;
-    bool doOp = true;
+    double dur = durS, cc = cS;
+    bool keep = keepS, doOp = true;
     if (!steady) {
       const i64 js = lv - s, jb = lv - (2 * P - 1 - s);
       const bool isF = (js >= 0 && lv <= P - 1 && js < m) || (lv >= 2 * P - s && !(js & 1) && (js >> 1) < m);
@@ -598,11 +617,12 @@ struct LanePipe {
       src = isF ? lane - 1 : lane + 1;
       dur = isF ? f : g;
       cc = isF ? cR : cL;
-      z = (isF && s == 0) || (isB && s == P - 1) ? 0 : -1;  // stage-0 input / B right after own F
+      keep = !((isF && s == 0) || (isB && s == P - 1));  // stage-0 input / B right after own F
     }
-    const i64 v = shfl64(out, src) & z;
+    const double v0 = shfl_d(out, src);
+    const double v = keep ? v0 : 0.0;
     if (doOp) {
-      const i64 e = imax(X, v) + dur;
+      const double e = dmax2(X, v) + dur;
       X = e;
       out = e + cc;
     }

@@ -132,7 +132,7 @@ __global__ void __launch_bounds__(NT, 6) k_split(const Tables* __restrict__ gT, 
       const i64* pre = c.plan + c.nr;
       const i64 r = bsearch_le(pre, c.nr, item);
       const i64 g = c0[r] + (item - pre[r]);
-      const i64 tg = bsearch_le(sT.tpl_cprefix, sT.n_tpl, g);
+      const i64 tg = find_template_of_chunk(sT, g);
       const i64 lo = sT.tpl_prefix[tg] + (g - sT.tpl_cprefix[tg]) * CHUNK;
       const i64 start = c.block ? c.first + r * c.stride : c.first;
       const i64 len = c.block ? imin(c.block, c.n - r * c.block) : c.n;
@@ -243,9 +243,9 @@ __device__ i64 warp_pipe_class(const Tables& T, int32_t off, const ClassSplit& c
   LayerWalk lw = walk(T, h, cs.dig);
   int l = 0;
   for (int k = 0; k <= s && k < P; ++k) l = lw.next(st);
-  const i64 f = seg < nseg ? (i64)l * st[s].layer_f + st[s].fext : 0;
-  const i64 g = seg < nseg ? (i64)l * st[s].layer_b + st[s].gext : 0;
-  i64 best = 0;
+  const double f = seg < nseg ? (double)((i64)l * st[s].layer_f + st[s].fext) : 0.0;
+  const double g = seg < nseg ? (double)((i64)l * st[s].layer_b + st[s].gext) : 0.0;
+  double best = 0;
   for (int base = 0; base < U; base += nseg) {
     const int u = base + seg;
     const bool act = seg < nseg && u < U;
@@ -254,10 +254,10 @@ __device__ i64 warp_pipe_class(const Tables& T, int32_t off, const ClassSplit& c
     lp.P = P; lp.s = s; lp.lane = lane;
     lp.m = act ? mb_of(cs, sub[0]) : 0;
     if (act && s == 0) *cells += 2 * P * lp.m;
-    lp.f = act ? f : 0;
-    lp.g = act ? g : 0;
-    lp.cR = act && s + 1 < P ? sub[1 + s] : 0;
-    lp.cL = act && s > 0 ? sub[s] : 0;
+    lp.f = act ? f : 0.0;
+    lp.g = act ? g : 0.0;
+    lp.cR = act && s + 1 < P ? (double)sub[1 + s] : 0.0;
+    lp.cL = act && s > 0 ? (double)sub[s] : 0.0;
     lp.X = 0;
     lp.out = 0;
     const i64 lo = 2 * P - 1;
@@ -271,36 +271,36 @@ __device__ i64 warp_pipe_class(const Tables& T, int32_t off, const ClassSplit& c
     // per-lane constants of the two steady level parities (lo = 2P-1 is odd)
     const bool oddS = s & 1;
     const int srcO = oddS ? lane - 1 : lane + 1, srcE = oddS ? lane + 1 : lane - 1;
-    const i64 durO = oddS ? lp.f : lp.g, durE = oddS ? lp.g : lp.f;
-    const i64 cO = oddS ? lp.cR : lp.cL, cE = oddS ? lp.cL : lp.cR;
-    const i64 zO = (!oddS && s == P - 1) ? 0 : -1;
-    const i64 zE = (oddS ? s == P - 1 : s == 0) ? 0 : -1;
+    const double durO = oddS ? lp.f : lp.g, durE = oddS ? lp.g : lp.f;
+    const double cO = oddS ? lp.cR : lp.cL, cE = oddS ? lp.cL : lp.cR;
+    const bool kO = !(!oddS && s == P - 1);
+    const bool kE = !(oddS ? s == P - 1 : s == 0);
     i64 lv = 0;
-    for (; lv < lo && lv < totMax; ++lv) lp.level(lv, false, 0, 0, 0, 0);
+    for (; lv < lo && lv < totMax; ++lv) lp.level(lv, false, 0, 0, 0, true);
     for (; lv + 1 < hiMin; lv += 2) {  // every job steady: one shuffle per level
       {
-        const i64 v = shfl64(lp.out, srcO) & zO;
-        const i64 e = imax(lp.X, v) + durO;
+        const double v0 = shfl_d(lp.out, srcO);
+        const double e = dmax2(lp.X, kO ? v0 : 0.0) + durO;
         lp.X = e;
         lp.out = e + cO;
       }
       {
-        const i64 v = shfl64(lp.out, srcE) & zE;
-        const i64 e = imax(lp.X, v) + durE;
+        const double v0 = shfl_d(lp.out, srcE);
+        const double e = dmax2(lp.X, kE ? v0 : 0.0) + durE;
         lp.X = e;
         lp.out = e + cE;
       }
     }
     for (; lv < totMax; ++lv) {
       const bool odd = lv & 1;
-      lp.level(lv, lv >= lo && lv < hi, odd ? srcO : srcE, odd ? durO : durE, odd ? cO : cE, odd ? zO : zE);
+      lp.level(lv, lv >= lo && lv < hi, odd ? srcO : srcE, odd ? durO : durE, odd ? cO : cE, odd ? kO : kE);
     }
     // T_pipe of each job sits on its stage-0 lane
-    i64 v = act && s == 0 ? lp.X : 0;
-    for (int o = 16; o > 0; o >>= 1) v = imax(v, (i64)__shfl_xor_sync(FULL, (long long)v, o));
-    best = imax(best, v);
+    double v = act && s == 0 ? lp.X : 0.0;
+    for (int o = 16; o > 0; o >>= 1) v = dmax2(v, __shfl_xor_sync(FULL, v, o));
+    best = dmax2(best, v);
   }
-  return best;
+  return (i64)best;
 }
 
 // 32 < P <= 64: lane holds stages 2*lane and 2*lane+1 (generic levels only;
