@@ -21,7 +21,7 @@
 #define HDN static
 #endif
 #ifndef HSIM_FASTP
-#define HSIM_FASTP 8   // deepest pipeline evaluated register-resident (compile-time P)
+#define HSIM_FASTP 16  // deepest pipeline evaluated register-resident (compile-time P): 8 or 16
 #endif
 
 namespace hsim {
@@ -304,31 +304,6 @@ HD int partition_c(const Tables& T, const TplRec& tp, i64 local, ClassSplit (&cs
 HD i64 level_F(int P, int s, i64 j) { return j <= P - 1 - s ? s + j : 2 * j + s; }
 HD i64 level_B(int P, int s, i64 j) { return 2 * P - 1 - s + 2 * j; }
 
-// generic depth (P <= MAXP), per-thread arrays
-HD i64 pipeline_generic(int P, i64 m, const i64* f, const i64* g, const i64* c) {
-  i64 X[MAXP], R[MAXP], Lb[MAXP];
-  i64 lastF = 0;
-  for (int s = 0; s < P; ++s) X[s] = R[s] = Lb[s] = 0;
-  const i64 levels = 2 * (m + P - 1);
-  for (i64 lv = 0; lv < levels; ++lv) {
-    for (int s = P - 1; s >= 0; --s) {
-      const i64 jw = lv - s, js = lv - s, jb = lv - (2 * P - 1 - s);
-      const bool isF = (jw >= 0 && lv <= P - 1 && jw < m) || (lv >= 2 * P - s && !(js & 1) && (js >> 1) < m);
-      const bool isB = jb >= 0 && !(jb & 1) && (jb >> 1) < m;
-      if (isF) {
-        const i64 e = imax(X[s], s == 0 ? 0 : R[s - 1]) + f[s];
-        X[s] = e;
-        if (s < P - 1) R[s] = e + c[s]; else lastF = e;
-      } else if (isB) {
-        const i64 e = imax(X[s], s == P - 1 ? lastF : Lb[s + 1]) + g[s];
-        X[s] = e;
-        if (s > 0) Lb[s] = e + c[s - 1];
-      }
-    }
-  }
-  return X[0];
-}
-
 // compile-time depth: every array is register-resident.  Clocks are kept in
 // offset coordinates X_s = end_s - o_s with o_s = c_0 + ... + c_{s-1}: then
 // the F message of stage s-1 arrives at X_{s-1} (no add), the B message of
@@ -450,56 +425,6 @@ HD PipeOut class_pipes_inl(const Tables& T, int32_t off, const ClassSplit& cs) {
     r.T0 = imax(r.T0, p.run(m));
   }
   return r;
-}
-
-template <int P>
-HDN PipeOut class_pipes(const Tables& T, int32_t off, const ClassSplit cs) { return class_pipes_inl<P>(T, off, cs); }
-
-HDN PipeOut class_pipes_generic(const Tables& T, int32_t off, const ClassSplit cs) {
-  const CrecHdr* h = crec_hdr(T, off);
-  const StageRec* st = crec_stages(T, off);
-  const int P = h->P;
-  i64 f[MAXP], g[MAXP];
-  LayerWalk lw = walk(T, h, cs.dig);
-  for (int s = 0; s < P; ++s) {
-    const i64 l = lw.next(st);
-    f[s] = l * st[s].layer_f + st[s].fext;
-    g[s] = l * st[s].layer_b + st[s].gext;
-  }
-  PipeOut r{0, 0};
-  for (int u = 0; u < h->U; ++u) {
-    const i64* sub = crec_sub(T, off, P, u);
-    const i64 m = mb_of(cs, sub[0]);
-    r.cells += 2 * P * m;
-    r.T0 = imax(r.T0, pipeline_generic(P, m, f, g, sub + 1));
-  }
-  return r;
-}
-
-HD PipeOut thread_pipes(const Tables& T, int32_t off, const ClassSplit& cs) {
-  switch (crec_hdr(T, off)->P) {
-    case 1: return class_pipes<1>(T, off, cs);
-    case 2: return class_pipes<2>(T, off, cs);
-#if HSIM_FASTP >= 3
-    case 3: return class_pipes<3>(T, off, cs);
-#endif
-#if HSIM_FASTP >= 4
-    case 4: return class_pipes<4>(T, off, cs);
-#endif
-#if HSIM_FASTP >= 5
-    case 5: return class_pipes<5>(T, off, cs);
-#endif
-#if HSIM_FASTP >= 6
-    case 6: return class_pipes<6>(T, off, cs);
-#endif
-#if HSIM_FASTP >= 7
-    case 7: return class_pipes<7>(T, off, cs);
-#endif
-#if HSIM_FASTP >= 8
-    case 8: return class_pipes<8>(T, off, cs);
-#endif
-    default: return class_pipes_generic(T, off, cs);
-  }
 }
 
 // --- step a5: gradient sync (C.6, C.8) -----------------------------------------

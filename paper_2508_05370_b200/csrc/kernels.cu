@@ -50,9 +50,10 @@ constexpr i64 CBMAX = 1 << 17;       // chunks per batch (2^22 slots)
 constexpr i64 KEY_INF = INT64_MAX;
 constexpr i64 LIST_PAD = 0x7F7F7F7F7F7F7F7FLL;  // memset(0x7F) sentinel of the per-warp lists
 constexpr unsigned FULL = 0xffffffffu;
-// counter slots: P = work counter of K_pipe<P>, 16 + P = #jobs of depth P in
-// full (32-aligned) chunks, 32 + P = #jobs of depth P from partial chunks
-constexpr int CNT_DEEP = 0, CNT_NDEEP = 14, CNT_CELLS = 15, CNT_FULL = 16, CNT_PART = 32, NCNT = 48;
+// counter slots: P (1..FASTP) = work counter of K_pipe<P>; CNT_FULL + P = #jobs of
+// depth P in full (32-aligned) chunks, CNT_PART + P = #jobs from partial chunks
+constexpr int CNT_DEEP = 17, CNT_NDEEP = 18, CNT_CELLS = 19, CNT_FULL = 20, CNT_PART = 40, NCNT = 64;
+static_assert(FASTP <= 16, "counter layout");
 
 struct Cands {
   const i64* idx;
@@ -176,15 +177,15 @@ __global__ void __launch_bounds__(NT, 6) k_split(const Tables* __restrict__ gT, 
     // template and class) keeps its own aligned group of 32, so a K_pipe warp's
     // lanes have near-equal micro-batch counts; partial chunks (small-radix
     // templates) are packed densely
-    uint32_t combos = 0;
+    u64 combos = 0;
     if (mypm)
       for (int k = 0; k < sT.tpl[tau].C; ++k) {
         const int P = crec_hdr(sT, sT.tpl[tau].crec[k])->P;
-        if (P <= FASTP) combos |= 1u << ((P - 1) * 4 + k);
+        if (P <= FASTP) combos |= (u64)1 << ((P - 1) * 4 + k);
       }
-    uint32_t all = __reduce_or_sync(FULL, combos);
+    u64 all = (u64)__reduce_or_sync(FULL, (unsigned)combos) | (u64)__reduce_or_sync(FULL, (unsigned)(combos >> 32)) << 32;
     while (all) {
-      const int bit = __ffs(all) - 1;
+      const int bit = __ffsll((long long)all) - 1;
       all &= all - 1;
       const int P = bit / 4 + 1, k = bit & 3;
       const bool has = combos >> bit & 1;
@@ -936,31 +937,16 @@ static int run_phases(hsim_handle* h, const Tables* dT, Cands c, int64_t n, int6
       cudaStreamWaitEvent(st, join_event(h, nside), 0);
       ++nside;
     };
-    static const int order[8] = {4, 8, 2, 6, 5, 3, 7, 1};  // longest first
-    for (int oi = 0; oi < 8; ++oi) {
+    static const int order[16] = {4, 8, 16, 2, 6, 5, 3, 12, 10, 7, 9, 11, 13, 14, 15, 1};  // longest first
+    for (int oi = 0; oi < 16; ++oi) {
       const int P = order[oi];
       if (P > FASTP || !(pm >> P & 1)) continue;
       cudaStream_t ss = side();
       switch (P) {
 #define HSIM_PIPE(PP) case PP: k_pipe<PP><<<grid_of(h, k_pipe<PP>, g_pipe[PP]), NT, 0, ss>>>(dT, S, count); break;
-        HSIM_PIPE(1) HSIM_PIPE(2)
-#if HSIM_FASTP >= 3
-        HSIM_PIPE(3)
-#endif
-#if HSIM_FASTP >= 4
-        HSIM_PIPE(4)
-#endif
-#if HSIM_FASTP >= 5
-        HSIM_PIPE(5)
-#endif
-#if HSIM_FASTP >= 6
-        HSIM_PIPE(6)
-#endif
-#if HSIM_FASTP >= 7
-        HSIM_PIPE(7)
-#endif
-#if HSIM_FASTP >= 8
-        HSIM_PIPE(8)
+        HSIM_PIPE(1) HSIM_PIPE(2) HSIM_PIPE(3) HSIM_PIPE(4) HSIM_PIPE(5) HSIM_PIPE(6) HSIM_PIPE(7) HSIM_PIPE(8)
+#if HSIM_FASTP >= 16
+        HSIM_PIPE(9) HSIM_PIPE(10) HSIM_PIPE(11) HSIM_PIPE(12) HSIM_PIPE(13) HSIM_PIPE(14) HSIM_PIPE(15) HSIM_PIPE(16)
 #endif
 #undef HSIM_PIPE
         default: break;
