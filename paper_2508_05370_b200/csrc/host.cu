@@ -110,9 +110,9 @@ struct hsim_handle {
   i64* d_blk = nullptr;
   size_t blk_cap = 0;
   i64* d_cells = nullptr;
-  static constexpr int NSIDE = 10;
-  cudaStream_t side[NSIDE] = {};     // fork/join streams: the depth kernels of a batch run concurrently
-  cudaEvent_t ev_fork = nullptr, ev_join[NSIDE] = {}, ev_plan = nullptr;
+  static constexpr int NSIDE = 20, NEV = 48;
+  cudaStream_t side[NSIDE] = {};     // one stream per phase-kernel type + the final stream
+  cudaEvent_t ev_fork = nullptr, ev_join[NSIDE] = {}, ev_plan = nullptr, ev_pool[NEV] = {};
   int32_t last_launches = 0;
   int sm_count = 148;
 
@@ -695,6 +695,7 @@ void hsim_handle::upload() {
   cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, dev);
   ck(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming), "cudaEventCreate");
   ck(cudaEventCreateWithFlags(&ev_plan, cudaEventDisableTiming), "cudaEventCreate");
+  for (int q = 0; q < NEV; ++q) ck(cudaEventCreateWithFlags(&ev_pool[q], cudaEventDisableTiming), "cudaEventCreate");
   for (int q = 0; q < NSIDE; ++q) {
     ck(cudaStreamCreateWithFlags(&side[q], cudaStreamNonBlocking), "cudaStreamCreate");
     ck(cudaEventCreateWithFlags(&ev_join[q], cudaEventDisableTiming), "cudaEventCreate");
@@ -791,6 +792,8 @@ void hsim_destroy(hsim_handle* h) {
   }
   if (h->ev_fork) cudaEventDestroy(h->ev_fork);
   if (h->ev_plan) cudaEventDestroy(h->ev_plan);
+  for (int q = 0; q < hsim_handle::NEV; ++q)
+    if (h->ev_pool[q]) cudaEventDestroy(h->ev_pool[q]);
   delete h;
 }
 
@@ -956,6 +959,7 @@ uint32_t depth_mask(const hsim_handle* h) { return h->pmask_all; }
 cudaStream_t side_stream(const hsim_handle* h, int q) { return h->side[q % hsim_handle::NSIDE]; }
 cudaEvent_t fork_event(const hsim_handle* h) { return h->ev_fork; }
 cudaEvent_t plan_event(const hsim_handle* h) { return h->ev_plan; }
+cudaEvent_t pool_event(const hsim_handle* h, int q) { return h->ev_pool[q % hsim_handle::NEV]; }
 cudaEvent_t join_event(const hsim_handle* h, int q) { return h->ev_join[q % hsim_handle::NSIDE]; }
 int depth_jobs_max(const hsim_handle* h, int P) { return P >= 0 && P <= FASTP ? h->pcnt_max[P] : 0; }
 int ensure_block_scratch(hsim_handle* h, size_t entries, int64_t** out) {

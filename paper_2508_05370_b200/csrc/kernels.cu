@@ -39,6 +39,8 @@ cudaStream_t side_stream(const hsim_handle* h, int q);
 cudaEvent_t fork_event(const hsim_handle* h);
 cudaEvent_t join_event(const hsim_handle* h, int q);
 cudaEvent_t plan_event(const hsim_handle* h);
+cudaEvent_t pool_event(const hsim_handle* h, int q);
+constexpr int NSTREAM_FINAL = 19;
 i64 host_plan(hsim_handle* h, i64 first, i64 block, i64 stride, i64 n, i64 nr, i64** buf);
 void set_launches(hsim_handle* h, int n);
 void set_error(const char* m);
@@ -200,8 +202,17 @@ __global__ void __launch_bounds__(NT, 6) k_split(const Tables* __restrict__ gT, 
 }
 
 // ---- K_pipe<P> -------------------------------------------------------------------
+#ifndef HSIM_NBATCH
+#define HSIM_NBATCH 2  // target number of pipelined batches per call
+#endif
+#ifndef HSIM_PIPE_MINB
+#define HSIM_PIPE_MINB 8
+#endif
+#ifndef HSIM_SYNC_MINB
+#define HSIM_SYNC_MINB 6
+#endif
 template <int P>
-__global__ void __launch_bounds__(NT) k_pipe(const Tables* __restrict__ gT, Scratch S, int count) {
+__global__ void __launch_bounds__(NT, P <= 4 ? HSIM_PIPE_MINB : 1) k_pipe(const Tables* __restrict__ gT, Scratch S, int count) {
   __shared__ Tables sT;
   load_tables(sT, gT);
   const int lane = threadIdx.x & 31;
@@ -476,7 +487,7 @@ __device__ i64 sync_any(const Tables& T, const TplRec& tp, const Scratch& S, i64
 // sharing a group of sum(RS + AR): every segment starts at T0 or when the
 // previous one ends (C.8) -- so the sync runs concurrently with the 1F1B
 // kernels (grad_sync_c with T0 = 0).
-__global__ void __launch_bounds__(NT) k_sync(const Tables* __restrict__ gT, Scratch S, i64 ns) {
+__global__ void __launch_bounds__(NT, HSIM_SYNC_MINB) k_sync(const Tables* __restrict__ gT, Scratch S, i64 ns) {
   __shared__ Tables sT;
   load_tables(sT, gT);
   for (i64 t = (i64)blockIdx.x * NT + threadIdx.x; t < ns; t += (i64)gridDim.x * NT) {
@@ -868,11 +879,15 @@ static int run_phases(hsim_handle* h, const Tables* dT, Cands c, int64_t n, int6
     nchunks = host_plan(h, c.first, c.block, c.stride, n, c.nr, &hplan);
     if (nchunks < 0) return HSIM_ENOMEM;
   }
-  const i64 cbatch = nchunks < CBMAX ? nchunks : CBMAX;
+  // batches of chunks, double-buffered: batch b+1's K_split overlaps batch b's
+  // depth kernels, batch b's K_final overlaps batch b+1's depth kernels
+  i64 cbatch = (nchunks + HSIM_NBATCH - 1) / HSIM_NBATCH;
+  if (cbatch < 2048) cbatch = nchunks < 2048 ? nchunks : 2048;
+  if (cbatch > CBMAX) cbatch = CBMAX;
   const i64 ns = cbatch * 32;
-  // scratch (int64 words): tpos, Tc [MAXC], extra | segs per depth | counters | plan |
-  // int32: tau, status, rm, deep, dig / q / seats / add [MAXC]
-  // job capacity per depth: #classes of that depth per template x slots (x2: full / partial lists)
+  const int NBUF = count ? 1 : 2;
+  // scratch per buffer (int64 words): tpos, Tc [MAXC], extra | counters | int32: tau,
+  // status, rm, deep, dig / q / seats / add [MAXC], job lists (x2: full / partial)
   const uint32_t pm = depth_mask(h);
   size_t jobcap[FASTP + 1], jobw = 0;
   for (int P = 1; P <= FASTP; ++P) {
@@ -881,67 +896,75 @@ static int run_phases(hsim_handle* h, const Tables* dT, Cands c, int64_t n, int6
   }
   const size_t planw = c.idx ? 0 : (size_t)(2 * c.nr + 1);
   const size_t n32 = (size_t)(4 + 4 * MAXC) * ns + jobw;
-  const size_t words = (size_t)(MAXC + 2) * ns + NCNT + planw + (n32 + 1) / 2 + 8;
+  const size_t bufw = (size_t)(MAXC + 2) * ns + NCNT + (n32 + 1) / 2 + 8;
   i64* base = nullptr;
-  if (ensure_work_scratch(h, words, &base)) return HSIM_ENOMEM;
-  Scratch S;
-  S.ns = ns;
-  S.tpos = base;
-  S.Tc = base + ns;
-  S.extra = base + (MAXC + 1) * ns;
-  i64* pw = base + (MAXC + 2) * ns;
-  S.counters = (unsigned long long*)pw;
-  pw += NCNT;
+  if (ensure_work_scratch(h, NBUF * bufw + planw + 8, &base)) return HSIM_ENOMEM;
+  Scratch SB[2];
+  for (int q = 0; q < NBUF; ++q) {
+    Scratch& S = SB[q];
+    i64* b0 = base + q * bufw;
+    S.ns = ns;
+    S.tpos = b0;
+    S.Tc = b0 + ns;
+    S.extra = b0 + (MAXC + 1) * ns;
+    S.counters = (unsigned long long*)(b0 + (MAXC + 2) * ns);
+    int32_t* p32 = (int32_t*)(b0 + (MAXC + 2) * ns + NCNT);
+    S.tau = p32;
+    S.status = p32 + ns;
+    S.rm = p32 + 2 * ns;
+    S.deep = p32 + 3 * ns;
+    S.dig = (u32*)(p32 + 4 * ns);
+    S.q = p32 + (4 + MAXC) * ns;
+    S.seats = p32 + (4 + 2 * MAXC) * ns;
+    S.add = p32 + (4 + 3 * MAXC) * ns;
+    int32_t* pj = p32 + (4 + 4 * MAXC) * ns;
+    S.full[0] = S.part[0] = nullptr;
+    for (int P = 1; P <= FASTP; ++P) {
+      S.full[P] = pj;
+      S.part[P] = pj + jobcap[P];
+      pj += 2 * jobcap[P];
+    }
+  }
   if (!c.idx) {
+    i64* pw = base + NBUF * bufw;
     cudaMemcpyAsync(pw, hplan, planw * 8, cudaMemcpyHostToDevice, st);
     cudaEventRecord(plan_event(h), st);
     c.plan = pw;
-    pw += planw;
-  }
-  int32_t* p32 = (int32_t*)pw;
-  S.tau = p32;
-  S.status = p32 + ns;
-  S.rm = p32 + 2 * ns;
-  S.deep = p32 + 3 * ns;
-  S.dig = (u32*)(p32 + 4 * ns);
-  S.q = p32 + (4 + MAXC) * ns;
-  S.seats = p32 + (4 + 2 * MAXC) * ns;
-  S.add = p32 + (4 + 3 * MAXC) * ns;
-  int32_t* pj = p32 + (4 + 4 * MAXC) * ns;
-  S.full[0] = S.part[0] = nullptr;
-  for (int P = 1; P <= FASTP; ++P) {
-    S.full[P] = pj;
-    S.part[P] = pj + jobcap[P];
-    pj += 2 * jobcap[P];
   }
   const int gs = grid_of(h, k_split, g_split), gd = grid_of(h, k_deep, g_deep), gy = grid_of(h, k_sync, g_sync),
             gf = final_grid(h, k);
+  static const int order[16] = {4, 8, 16, 2, 6, 5, 3, 12, 10, 7, 9, 11, 13, 14, 15, 1};  // longest first
+  cudaStream_t fin = side_stream(h, NSTREAM_FINAL);
   i64 cells = 0;
-  for (i64 ca = 0; ca < nchunks; ca += cbatch) {
+  int b = 0;
+  for (i64 ca = 0; ca < nchunks; ca += cbatch, ++b) {
+    const int q = b % NBUF;
+    Scratch& S = SB[q];
     const i64 cb = ca + cbatch < nchunks ? ca + cbatch : nchunks;
     const i64 nsb = (cb - ca) * 32;
+    if (b >= NBUF && !count) cudaStreamWaitEvent(st, pool_event(h, 2 + q), 0);  // buffer free: final(b-2) done
     cudaMemsetAsync(S.counters, 0, NCNT * sizeof(unsigned long long), st);
     k_split<<<gs, NT, 0, st>>>(dT, c, ca, cb, S, pm);
     ++launches;
-    // the depth kernels, K_deep and K_sync are independent: fork them onto
-    // side streams (each is bounded by its longest chains), join before K_final
-    cudaEventRecord(fork_event(h), st);
-    int nside = 0;
-    auto side = [&]() {
-      cudaStream_t ss = side_stream(h, nside);
-      cudaStreamWaitEvent(ss, fork_event(h), 0);
+    cudaEventRecord(pool_event(h, q), st);
+    // the depth kernels, K_deep and K_sync of a batch are independent: each on
+    // its own stream after K_split, all joined by K_final
+    int j = 0;
+    auto side = [&](int sid) {
+      cudaStream_t ss = side_stream(h, sid);
+      cudaStreamWaitEvent(ss, pool_event(h, q), 0);
       return ss;
     };
     auto join = [&](cudaStream_t ss) {
-      cudaEventRecord(join_event(h, nside), ss);
-      cudaStreamWaitEvent(st, join_event(h, nside), 0);
-      ++nside;
+      cudaEvent_t e = pool_event(h, 4 + q * 20 + j);
+      cudaEventRecord(e, ss);
+      cudaStreamWaitEvent(count ? st : fin, e, 0);
+      ++j;
     };
-    static const int order[16] = {4, 8, 16, 2, 6, 5, 3, 12, 10, 7, 9, 11, 13, 14, 15, 1};  // longest first
     for (int oi = 0; oi < 16; ++oi) {
       const int P = order[oi];
       if (P > FASTP || !(pm >> P & 1)) continue;
-      cudaStream_t ss = side();
+      cudaStream_t ss = side(P);
       switch (P) {
 #define HSIM_PIPE(PP) case PP: k_pipe<PP><<<grid_of(h, k_pipe<PP>, g_pipe[PP]), NT, 0, ss>>>(dT, S, count); break;
         HSIM_PIPE(1) HSIM_PIPE(2) HSIM_PIPE(3) HSIM_PIPE(4) HSIM_PIPE(5) HSIM_PIPE(6) HSIM_PIPE(7) HSIM_PIPE(8)
@@ -955,7 +978,7 @@ static int run_phases(hsim_handle* h, const Tables* dT, Cands c, int64_t n, int6
       join(ss);
     }
     if (pm >> (FASTP + 1)) {
-      cudaStream_t ss = side();
+      cudaStream_t ss = side(17);
       k_deep<<<gd, NT, 0, ss>>>(dT, S, count);
       ++launches;
       join(ss);
@@ -968,15 +991,17 @@ static int run_phases(hsim_handle* h, const Tables* dT, Cands c, int64_t n, int6
       continue;
     }
     {
-      cudaStream_t ss = side();
+      cudaStream_t ss = side(18);
       k_sync<<<gy, NT, 0, ss>>>(dT, S, nsb);
       ++launches;
       join(ss);
     }
-    if (k && k <= 32) k_final_small<<<gf, NT, 0, st>>>(dT, c, S, nsb, out_ns, k, lists);
-    else k_final<<<gf, NT, 0, st>>>(dT, c, S, nsb, out_ns, k, lists);
+    if (k && k <= 32) k_final_small<<<gf, NT, 0, fin>>>(dT, c, S, nsb, out_ns, k, lists);
+    else k_final<<<gf, NT, 0, fin>>>(dT, c, S, nsb, out_ns, k, lists);
     ++launches;
+    cudaEventRecord(pool_event(h, 2 + q), fin);
   }
+  if (!count && b > 0) cudaStreamWaitEvent(st, pool_event(h, 2 + (b - 1) % NBUF), 0);  // join the final stream
   if (cells_out) *cells_out = cells;
   return HSIM_OK;
 }

@@ -7,6 +7,14 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2508_05370_b200 import build as B  # noqa: E402
 
 VARIANTS = {
+    "p8s6": ["-DHSIM_PIPE_MINB=8", "-DHSIM_SYNC_MINB=6"],
+    "nb1": ["-DHSIM_NBATCH=1"],
+    "nb2": ["-DHSIM_NBATCH=2"],
+    "nb3": ["-DHSIM_NBATCH=3"],
+    "nb6": ["-DHSIM_NBATCH=6"],
+    "nb8": ["-DHSIM_NBATCH=8"],
+    "p6s5": ["-DHSIM_PIPE_MINB=6", "-DHSIM_SYNC_MINB=5"],
+    "p7s4": ["-DHSIM_PIPE_MINB=7", "-DHSIM_SYNC_MINB=4"],
     "f8_nb": ["-DHSIM_FASTP=8"],
     "f8_b3": ["-DHSIM_FASTP=8", "-DHSIM_MINB=3"],
     "f4_b4": ["-DHSIM_FASTP=4", "-DHSIM_MINB=4"],
