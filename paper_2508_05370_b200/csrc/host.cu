@@ -227,7 +227,24 @@ void hsim_handle::derive_links() {
       l = cat(l, path_link(types[b].gpu_nic, fr));
       rail[a][b] = l;
     }
-  // every link the kernels may meet gets a class id
+  // every link the kernels may meet gets a class id, ids in (beta ascending,
+  // alpha descending) order: eval_mask walks a mask from its slowest class
+  {
+    std::vector<Link> all;
+    for (int t = 0; t < nt; ++t)
+      for (int i = 0; i < types[t].gpus_per_node; ++i)
+        for (int j = 0; j < types[t].gpus_per_node; ++j)
+          if (i != j) all.push_back(intra[t][i][j]);
+    for (int a = 0; a < nt; ++a)
+      for (int i = 0; i < types[a].gpus_per_node; ++i)
+        for (int b = 0; b < nt; ++b)
+          for (int j = 0; j < types[b].gpus_per_node; ++j)
+            all.push_back(i == j ? rail[a][b] : cat(intra[a][i][j], rail[a][b]));
+    std::stable_sort(all.begin(), all.end(), [](const Link& x, const Link& y) {
+      return x.beta != y.beta ? x.beta < y.beta : x.alpha > y.alpha;
+    });
+    for (const Link& l : all) lc(l);
+  }
   std::memset(hT.lc_same, 0, sizeof(hT.lc_same));
   std::memset(hT.lc_cross, 0, sizeof(hT.lc_cross));
   for (int t = 0; t < nt; ++t)
@@ -431,6 +448,7 @@ int32_t hsim_handle::crec(int bi, int M, int D, const std::vector<std::pair<int,
   hd.nd = P <= md.pmax_perturb ? P - 1 : 0;
   hd.pw = 1;
   for (int q = 0; q < hd.nd; ++q) hd.pw *= (u32)(2 * md.r_layer + 1);
+  hd.pwdiv = make_fastdiv(hd.pw);
   pool.resize(off + HDR_WORDS + 16 * P + rep.size() * P);
   std::memcpy(&pool[off], &hd, sizeof hd);
   std::memcpy(&pool[off + HDR_WORDS], sr.data(), sizeof(StageRec) * P);
@@ -574,6 +592,8 @@ void hsim_handle::prepare() {
     fail(HSIM_ERANGE, "gradient bytes reach 2^53");
   hT.r_layer = md.r_layer;
   hT.r_batch = md.r_batch;
+  hT.ldiv = make_fastdiv((u32)(2 * md.r_layer + 1));
+  hT.bdiv = make_fastdiv((u32)(2 * md.r_batch + 1));
   hT.n_tpl = (i64)tpl.size();
   hT.N = N;
   hT.n_lc = (int32_t)lcs.size();
@@ -597,11 +617,14 @@ void hsim_handle::prepare() {
       exact = found;
     }
     hT.lc_exact = exact ? 1 : 0;
-    // dominance: tau_b(x) >= tau_a(x) for all x when alpha_b >= alpha_a and beta_b <= beta_a
+    // classes after b (beta >= beta_b) that b does not dominate: alpha_a > alpha_b
+    // (tau_b(x) >= tau_a(x) for all x when alpha_b >= alpha_a and beta_b <= beta_a)
     for (size_t b = 0; b < lcs.size(); ++b) {
-      hT.lc_dom[b] = 0;
-      for (size_t a = 0; a < lcs.size(); ++a)
-        if (a != b && lcs[b].alpha >= lcs[a].alpha && lcs[b].beta <= lcs[a].beta) hT.lc_dom[b] |= (u64)1 << a;
+      if (b > 0 && !(lcs[b - 1].beta < lcs[b].beta || (lcs[b - 1].beta == lcs[b].beta && lcs[b - 1].alpha > lcs[b].alpha)))
+        fail(HSIM_EINVAL, "internal: link classes not in (beta, -alpha) order");
+      hT.lc_up[b] = 0;
+      for (size_t a = b + 1; a < lcs.size(); ++a)
+        if (lcs[a].alpha > lcs[b].alpha) hT.lc_up[b] |= (u64)1 << a;
     }
   }
   // link classes of the q < 2^lg edges between two groups' bases (cross-class ring edges)

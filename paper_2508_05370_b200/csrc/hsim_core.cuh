@@ -54,10 +54,23 @@ struct StageRec {
 };
 static_assert(sizeof(StageRec) == 128, "StageRec layout");
 
+// n / d for 0 <= n < 2^31 as ((u64)n * m) >> sh with l = ceil(log2 d),
+// m = floor(2^(31+l) / d) + 1 < 2^32, sh = 31 + l (Granlund-Montgomery, N = 31)
+struct FastDiv {
+  u32 m, sh;
+  HD u32 div(u32 n) const { return (u32)(((u64)n * m) >> sh); }
+};
+inline FastDiv make_fastdiv(u32 d) {
+  u32 l = 0;
+  while (((u64)1 << l) < d) ++l;
+  return FastDiv{(u32)((((u64)1 << (31 + l)) / d) + 1), 31 + l};
+}
+
 struct CrecHdr {
   int32_t P, D, U, nd;    // stages, replicas, sub-classes, #layer digits
   u32 pw;                 // (2 r_layer + 1)^nd: radix of the class's digit block
-  int32_t _pad[3];
+  FastDiv pwdiv;          // division by pw
+  int32_t _pad;
 };
 static_assert(sizeof(CrecHdr) == 32, "CrecHdr layout");
 // crec layout in the int64 pool: CrecHdr (4 x i64) | StageRec[P] (16 x i64 each) | U x (i64 k_u, i64 c[P-1])
@@ -79,6 +92,7 @@ struct Tables {
   i64 seg_first_bytes;    // V*h*bpe_grad (embedding with layer 0)
   i64 seg_last_bytes;     // (V*h*!tied + h)*bpe_grad (head + final norm with layer L-1)
   int32_t r_layer, r_batch;
+  FastDiv ldiv, bdiv;     // division by 2 r_layer + 1 / 2 r_batch + 1
   // templates
   i64 n_tpl, N, n_bucket;
   const i64* tpl_prefix;  // [n_tpl + 1] first candidate of each template
@@ -98,7 +112,7 @@ struct Tables {
   // ceil_div(x << k, G), computed from a reciprocal estimate + exact fix-up
   i64 lc_G[MAXLC];
   double lc_rG[MAXLC];     // 1.0 / G (floor estimate, then exact integer fix-up)
-  u64 lc_dom[MAXLC];       // link classes with alpha <= and beta >= this one's (never the max of tau)
+  u64 lc_up[MAXLC];       // classes after this one (ids sorted by beta asc, alpha desc) with a larger alpha
   int8_t lc_k[MAXLC], _pad4[MAXLC];
   int32_t lc_exact, _pad3;
   const u64* xmask_cross;  // [MAXT][MAXG][MAXT][MAXG][4] link classes of edges (t1, b1+q) -> (t2, b2+q), q < 2^lg
@@ -135,8 +149,10 @@ HD i64 tau_lc(const Tables& T, int b, i64 x) {
   return T.lc[b].alpha + ceilq(x, T.lc[b].beta);
 }
 
-// max over the link classes in `mask` of alpha + ceil(x / beta)  (C.6 tau_e);
-// classes dominated by another class of the mask are skipped first
+// max over the link classes in `mask` of alpha + ceil(x / beta)  (C.6 tau_e).
+// Class ids are sorted by (beta ascending, alpha descending), so the lowest bit
+// is the slowest class; every later class with alpha <= its alpha is dominated
+// (tau never larger) and dropped: the walk visits only the mask's Pareto front.
 HD int ffs64(u64 m) {
 #ifdef __CUDA_ARCH__
   return __ffsll((long long)m) - 1;
@@ -146,15 +162,10 @@ HD int ffs64(u64 m) {
 }
 HD i64 eval_mask(const Tables& T, u64 mask, i64 x) {
   i64 best = 0;
-  for (u64 m = mask; m; m &= m - 1) mask &= ~T.lc_dom[ffs64(m)];
   while (mask) {
-#ifdef __CUDA_ARCH__
-    int b = __ffsll((long long)mask) - 1;
-#else
-    int b = __builtin_ctzll(mask);
-#endif
-    mask &= mask - 1;
+    const int b = ffs64(mask);
     best = imax(best, tau_lc(T, b, x));
+    mask &= T.lc_up[b];
   }
   return best;
 }
@@ -218,9 +229,14 @@ struct LayerWalk {
   int nd, dprev, s;
   u32 bl;
   int r;
+  FastDiv dv;
   HD int next(const StageRec* st) {
     int d = 0;
-    if (s < nd) { d = (int)(dig % bl) - r; dig /= bl; }
+    if (s < nd) {
+      const u32 qd = dv.div(dig);
+      d = (int)(dig - qd * bl) - r;
+      dig = qd;
+    }
     int l = st[s].l0 + d - dprev;
     dprev = d;
     ++s;
@@ -228,7 +244,7 @@ struct LayerWalk {
   }
 };
 HD LayerWalk walk(const Tables& T, const CrecHdr* h, u32 dig) {
-  return LayerWalk{dig, h->nd, 0, 0, (u32)(2 * T.r_layer + 1), T.r_layer};
+  return LayerWalk{dig, h->nd, 0, 0, (u32)(2 * T.r_layer + 1), T.r_layer, T.ldiv};
 }
 
 // Digits are least-significant first: class 0's boundaries, class 1's, ...,
@@ -246,8 +262,9 @@ HD int partition_c(const Tables& T, const TplRec& tp, i64 local, ClassSplit (&cs
     const CrecHdr* h = crec_hdr(T, tp.crec[c]);
     const StageRec* st = crec_stages(T, tp.crec[c]);
     D[c] = h->D;
-    cs[c].dig = loc % h->pw;
-    loc /= h->pw;
+    const u32 lq = h->pwdiv.div(loc);
+    cs[c].dig = loc - lq * h->pw;
+    loc = lq;
     LayerWalk lw = walk(T, h, cs[c].dig);
     i64 worst = 0;
     for (int s = 0; s < h->P; ++s) {
@@ -269,8 +286,9 @@ HD int partition_c(const Tables& T, const TplRec& tp, i64 local, ClassSplit (&cs
     cs[c].seats = 0;
     cs[c].rm = 0;
     if (c < C - 1) {
-      cs[c].add = (i64)(loc % bb) - T.r_batch;
-      loc /= bb;
+      const u32 lq = T.bdiv.div(loc);
+      cs[c].add = (i64)(loc - lq * bb) - T.r_batch;
+      loc = lq;
       R -= D[c] * cs[c].add;
     }
   }
@@ -379,16 +397,51 @@ struct Pipe {
 #pragma unroll
     for (int s = 0; s < P; ++s) X[s] = (s & 1) == par ? fop(old, s) : bop(old, s);
   }
-  HD i64 run(i64 m) {
+  HD void steady_pair() {
+    steady_level<1>();
+    steady_level<0>();
+  }
+  // T_pipe; `skipped` = steady level pairs not executed (periodic regime).
+  HD i64 run(i64 m, i64& skipped) {
 #pragma unroll
     for (int s = 0; s < P; ++s) X[s] = 0;
+    skipped = 0;
     if (m >= P) {
 #pragma unroll
       for (int lv = 0; lv < 2 * P - 1; ++lv) level_warm(lv);
-      for (int k = 0, kn = (int)(m - P); k < kn; ++k) {  // levels [2P-1, 2m): (odd, even) pairs
-        steady_level<1>();
-        steady_level<0>();
+      // levels [2P-1, 2m): (odd, even) pairs, each the same max-plus map A
+      // (per-stage constants).  Once one pair moves every X[s] by the same d,
+      // X(k+1) = X(k) + d and homogeneity of A (A(x + d) = A(x) + d) gives
+      // X(k+r) = X(k) + r*d exactly: the remaining pairs are one multiply-add
+      // (integers < 2^52, exact in fp64).  Checked every 4th pair.
+      const int kn = (int)(m - P);
+      int k = 0;
+      for (; k + 4 <= kn; k += 4) {
+        steady_pair();
+        steady_pair();
+        steady_pair();
+        double o[P];
+#pragma unroll
+        for (int s = 0; s < P; ++s) o[s] = X[s];
+        steady_pair();
+        const double d = X[0] - o[0];
+        bool per = true;
+#pragma unroll
+        for (int s = 1; s < P; ++s) per = per && (X[s] - o[s] == d);
+#ifdef HSIM_NOSKIP
+        per = false;
+#endif
+        if (per) {
+          const int r = kn - k - 4;
+          const double rd = (double)r * d;
+#pragma unroll
+          for (int s = 0; s < P; ++s) X[s] += rd;
+          skipped = r;
+          k = kn;
+          break;
+        }
       }
+      for (; k < kn; ++k) steady_pair();
       steady_level<1>();  // level 2m-1
 #pragma unroll
       for (int d = 0; d < 2 * P - 2; ++d) level_cool(d);
@@ -400,6 +453,9 @@ struct Pipe {
   }
 };
 
+#ifdef HSIM_DIAG
+__device__ unsigned long long g_diag[17][16];
+#endif
 // T_pipe of every sub-class of a class (compile-time depth), max-reduced.
 struct PipeOut { i64 T0, cells; };
 
@@ -421,8 +477,18 @@ HD PipeOut class_pipes_inl(const Tables& T, int32_t off, const ClassSplit& cs) {
 #pragma unroll
     for (int s = 0; s + 1 < P; ++s) p.c[s] = (double)(2 * sub[1 + s]);
     const i64 m = mb_of(cs, sub[0]);
-    r.cells += 2 * P * m;
-    r.T0 = imax(r.T0, p.run(m));
+    i64 sk;
+    r.T0 = imax(r.T0, p.run(m, sk));
+    r.cells += 2 * P * (m - sk);  // cells executed
+#if defined(HSIM_DIAG) && defined(__CUDA_ARCH__)
+    {  // histogram of executed steady pairs in units of P; bucket 7 = not detected
+      const i64 kn = m >= P ? m - P : 0, ex = kn - sk;
+      const int bk = sk > 0 ? (int)imin(ex / P, 6) : 7;
+      atomicAdd(&g_diag[P][bk], 1ull);
+      atomicAdd(&g_diag[P][8], (unsigned long long)ex);
+      atomicAdd(&g_diag[P][9], (unsigned long long)kn);
+    }
+#endif
   }
   return r;
 }

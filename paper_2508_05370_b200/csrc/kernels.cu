@@ -23,6 +23,7 @@
 //   K_merge   (top-k only, once per call) merges the per-warp sorted lists.
 // The depth kernels, K_deep and K_sync of a batch run concurrently on fork /
 // join side streams.
+#include <cstdio>
 #include <cuda_runtime.h>
 
 #include "hsim.h"
@@ -234,7 +235,11 @@ __global__ void __launch_bounds__(NT, P <= 4 ? HSIM_PIPE_MINB : 1) k_pipe(const 
     const TplRec& tp = sT.tpl[tau];
     const PipeOut r = class_pipes_inl<P>(sT, tp.crec[c], load_split(S, c, tp.C, slot));
     S.Tc[c * S.ns + slot] = r.T0;
+#ifdef HSIM_WARPCELLS  // diagnostic: count mode reports warp-slot cells (32 x warp max)
+    cells += 32 * __reduce_max_sync(__activemask(), (unsigned)r.cells);
+#else
     cells += r.cells;
+#endif
   }
   if (count) {
     cells = warp_sum(cells);
@@ -289,7 +294,7 @@ __device__ i64 warp_pipe_class(const Tables& T, int32_t off, const ClassSplit& c
     const bool kE = !(oddS ? s == P - 1 : s == 0);
     i64 lv = 0;
     for (; lv < lo && lv < totMax; ++lv) lp.level(lv, false, 0, 0, 0, true);
-    for (; lv + 1 < hiMin; lv += 2) {  // every job steady: one shuffle per level
+    auto pair = [&]() {  // levels (odd, even) of the steady range: one shuffle per level
       {
         const double v0 = shfl_d(lp.out, srcO);
         const double e = dmax2(lp.X, kO ? v0 : 0.0) + durO;
@@ -302,7 +307,27 @@ __device__ i64 warp_pipe_class(const Tables& T, int32_t off, const ClassSplit& c
         lp.X = e;
         lp.out = e + cE;
       }
+    };
+    // P > 16 here, so one job per warp (nseg == 1): the periodic-regime skip of
+    // Pipe<P>::run applies to the whole warp (X and out = X + cE all move by d)
+    for (; lv + 7 < hiMin; lv += 8) {
+      pair();
+      pair();
+      pair();
+      const double xo = lp.X;
+      pair();
+      const double dd = lp.X - xo, d0 = __shfl_sync(FULL, dd, 0);
+      if (__all_sync(FULL, !act || dd == d0)) {
+        const i64 r = (hiMin - (lv + 8)) >> 1;  // remaining whole pairs
+        const double rd = (double)r * d0;
+        lp.X += rd;
+        lp.out += rd;
+        lv += 8 + 2 * r;
+        if (act && s == 0) *cells -= 2 * P * r;
+        break;
+      }
     }
+    for (; lv + 1 < hiMin; lv += 2) pair();
     for (; lv < totMax; ++lv) {
       const bool odd = lv & 1;
       lp.level(lv, lv >= lo && lv < hi, odd ? srcO : srcE, odd ? durO : durE, odd ? cO : cE, odd ? kO : kE);
@@ -1003,6 +1028,22 @@ static int run_phases(hsim_handle* h, const Tables* dT, Cands c, int64_t n, int6
   }
   if (!count && b > 0) cudaStreamWaitEvent(st, pool_event(h, 2 + (b - 1) % NBUF), 0);  // join the final stream
   if (cells_out) *cells_out = cells;
+#ifdef HSIM_DIAG
+  if (count) {
+    unsigned long long hd[17][16];
+    cudaMemcpyFromSymbol(hd, g_diag, sizeof hd);
+    for (int P = 1; P <= 16; ++P) {
+      unsigned long long t = 0;
+      for (int b = 0; b < 8; ++b) t += hd[P][b];
+      if (!t) continue;
+      fprintf(stderr, "P=%2d jobs %llu exec/kn pairs %.3f | hist", P, t, (double)hd[P][8] / (double)(hd[P][9] ? hd[P][9] : 1));
+      for (int b = 0; b < 8; ++b) fprintf(stderr, " %.3f", (double)hd[P][b] / t);
+      fprintf(stderr, "\n");
+    }
+    unsigned long long z[17][16] = {};
+    cudaMemcpyToSymbol(g_diag, z, sizeof z);
+  }
+#endif
   return HSIM_OK;
 }
 

@@ -9,6 +9,10 @@ from paper_2508_05370_b200 import build as B  # noqa: E402
 VARIANTS = {
     "p8s6": ["-DHSIM_PIPE_MINB=8", "-DHSIM_SYNC_MINB=6"],
     "nb1": ["-DHSIM_NBATCH=1"],
+    "wcells": ["-DHSIM_WARPCELLS"],
+    "diag": ["-DHSIM_DIAG"],
+    "noskip": ["-DHSIM_NOSKIP"],
+    "noskip_wc": ["-DHSIM_NOSKIP", "-DHSIM_WARPCELLS"],
     "nb2": ["-DHSIM_NBATCH=2"],
     "nb3": ["-DHSIM_NBATCH=3"],
     "nb6": ["-DHSIM_NBATCH=6"],
