@@ -11,6 +11,7 @@
 // division (__ddiv_rn on the device; host built with -ffp-contract=off), the
 // rest int64 + / max.  Device code is compiled with -fmad=false.
 #pragma once
+#include <math.h>
 #include <stdint.h>
 
 #ifdef __CUDACC__
@@ -19,6 +20,12 @@
 #else
 #define HD inline
 #define HDN static
+#endif
+#ifndef HSIM_AFFINE_MAXP
+#define HSIM_AFFINE_MAXP 8  // deepest register-resident pipeline with the affine-regime jump
+#endif
+#ifndef HSIM_UNROLL_MAXP
+#define HSIM_UNROLL_MAXP 16  // deepest pipeline whose 1F1B warm-up / cool-down levels are fully unrolled
 #endif
 #ifndef HSIM_FASTP
 #define HSIM_FASTP 16  // deepest pipeline evaluated register-resident (compile-time P): 8 or 16
@@ -401,50 +408,155 @@ struct Pipe {
     steady_level<1>();
     steady_level<0>();
   }
+  // --- exact acceleration of the steady regime ------------------------------
+  // Levels [2P-1, 2m) form (odd, even) pairs, each the same max-plus map A with
+  // per-stage constants, so X(k+1) = A(X(k)) and A(x + d) = A(x) + d.
+  //
+  // Affine regime (AFF): with d = X(k) - X(k-1), evaluate the next pair on
+  // (value, slope d) operands.  Every max keeps the operand that wins now
+  // (ties: the one growing faster); the pair is then the fixed selection
+  // X' = Pi X + w for as long as no losing operand that grows faster has
+  // caught up -- H pairs (a safe lower bound, see sym_cell).  If that pair
+  // moves X by exactly d and Pi d = d (slopes reproduce), then
+  // X(k + t) = X(k) + t d for t <= H: a transient in which different stages
+  // advance at different rates (balanced stages of unequal speed) is crossed
+  // in one multiply-add per stage, exactly (integers < 2^52 in fp64).  A
+  // uniform d is the periodic regime of cyclicity 1 (H infinite).
+  // Cyclic regime (WHOLE): X moved by the same d over a whole block of BL
+  // pairs -> cyclicity c | BL: X(k + q BL) = X(k) + q d.
+  HD static void sym_cell(double a, double sa, double b, double sb, double dur, double& x, double& sl, double& H) {
+    const bool bw = b > a || (b == a && sb > sa);
+    const double w = bw ? b : a, sw = bw ? sb : sa, l = bw ? a : b, sL = bw ? sa : sb;
+    // the loser overtakes after (w - l) / (sL - sw) pairs: RN quotient of exact
+    // integers < 2^52 is within 1 of the true one, so floor - 1 is safe
+    if (sL > sw) H = fmin(H, floor((w - l) / (sL - sw)) - 1.0);
+    x = w + dur;
+    sl = sw;
+  }
+  template <int par>
+  HD void sym_level(double (&x)[P], double (&sl)[P], double& H) const {
+    double ox[P], os[P];
+#pragma unroll
+    for (int s = 0; s < P; ++s) { ox[s] = x[s]; os[s] = sl[s]; }
+#pragma unroll
+    for (int s = 0; s < P; ++s) {
+      if ((s & 1) == par) {  // F
+        if (s == 0) { x[0] = ox[0] + f[0]; sl[0] = os[0]; }
+        else sym_cell(ox[s], os[s], ox[s == 0 ? 0 : s - 1], os[s == 0 ? 0 : s - 1], f[s], x[s], sl[s], H);
+      } else {               // B
+        if (s == P - 1) { x[s] = ox[s] + g[s]; sl[s] = os[s]; }
+        else sym_cell(ox[s], os[s], ox[s == P - 1 ? s : s + 1] + c[s], os[s == P - 1 ? s : s + 1], g[s], x[s], sl[s], H);
+      }
+    }
+  }
+  // horizon H >= 1 of the affine regime with increments d, or < 1 if none
+  HD double affine_horizon(const double (&d)[P]) const {
+    double x[P], sl[P], H = 1e300;
+#pragma unroll
+    for (int s = 0; s < P; ++s) { x[s] = X[s]; sl[s] = d[s]; }
+    sym_level<1>(x, sl, H);
+    sym_level<0>(x, sl, H);
+    bool ok = true;
+#pragma unroll
+    for (int s = 0; s < P; ++s) ok = ok && x[s] - X[s] == d[s] && sl[s] == d[s];
+    return ok ? H : 0.0;
+  }
+  // One block of BL steady pairs, then the checks above.  Returns true when
+  // the remaining steady pairs are settled (the caller runs the leftovers).
+  template <int BL, bool WHOLE, bool AFF>
+  HD bool block(int& k, int kn, i64& skipped) {
+    double o0[P], o1[P];
+#pragma unroll
+    for (int s = 0; s < P; ++s) o0[s] = X[s];
+#pragma unroll 1
+    for (int b = 0; b < BL - 1; ++b) steady_pair();
+#pragma unroll
+    for (int s = 0; s < P; ++s) o1[s] = X[s];
+    steady_pair();
+    k += BL;
+#ifndef HSIM_NOSKIP
+    if (AFF) {
+      double d[P];
+#pragma unroll
+      for (int s = 0; s < P; ++s) d[s] = X[s] - o1[s];
+      const double H = affine_horizon(d);
+      if (H >= 1.0) {
+        const int t = (int)fmin(H, (double)(kn - k));
+#pragma unroll
+        for (int s = 0; s < P; ++s) X[s] += (double)t * d[s];
+        skipped += t;
+        k += t;
+        return k == kn;
+      }
+    } else {
+      const double d = X[0] - o1[0];
+      bool per = true;
+#pragma unroll
+      for (int s = 1; s < P; ++s) per = per && (X[s] - o1[s] == d);
+      if (per) {
+        const int r = kn - k;
+        const double rd = (double)r * d;
+#pragma unroll
+        for (int s = 0; s < P; ++s) X[s] += rd;
+        skipped += r;
+        k = kn;
+        return true;
+      }
+    }
+    if (WHOLE) {
+      const double d = X[0] - o0[0];
+      bool per = true;
+#pragma unroll
+      for (int s = 1; s < P; ++s) per = per && (X[s] - o0[s] == d);
+      if (per) {
+        const int q = (kn - k) / BL;
+        const double qd = (double)q * d;
+#pragma unroll
+        for (int s = 0; s < P; ++s) X[s] += qd;
+        skipped += (i64)q * BL;
+        k += q * BL;
+        return true;
+      }
+    }
+#endif
+    return false;
+  }
   // T_pipe; `skipped` = steady level pairs not executed (periodic regime).
   HD i64 run(i64 m, i64& skipped) {
 #pragma unroll
     for (int s = 0; s < P; ++s) X[s] = 0;
     skipped = 0;
     if (m >= P) {
+      // warm-up levels [0, 2P-1): unrolled (compile-time op pattern) for
+      // shallow pipelines; deeper ones loop over levels with run-time ops so the
+      // kernel's straight-line code stays within the instruction cache
+      if (P <= HSIM_UNROLL_MAXP) {
 #pragma unroll
-      for (int lv = 0; lv < 2 * P - 1; ++lv) level_warm(lv);
-      // levels [2P-1, 2m): (odd, even) pairs, each the same max-plus map A
-      // (per-stage constants).  Once one pair moves every X[s] by the same d,
-      // X(k+1) = X(k) + d and homogeneity of A (A(x + d) = A(x) + d) gives
-      // X(k+r) = X(k) + r*d exactly: the remaining pairs are one multiply-add
-      // (integers < 2^52, exact in fp64).  Checked every 4th pair.
+        for (int lv = 0; lv < 2 * P - 1; ++lv) level_warm(lv);
+      } else {
+#pragma unroll 1
+        for (int lv = 0; lv < 2 * P - 1; ++lv) level_rt(lv, m);
+      }
+      // steady pairs: a first block of 4, then blocks of 12 (P <= 8) or 4;
+      // after each, the affine check (P <= HSIM_AFFINE_MAXP; else only the
+      // uniform-increment case) and, for P <= 8, the cyclic c | BL check
+      // (deeper pipelines: the extra snapshots would not fit the registers)
+      constexpr bool EXT = P <= 8, AFF = P <= HSIM_AFFINE_MAXP;
+      constexpr int BLK = EXT ? 12 : 4;
       const int kn = (int)(m - P);
       int k = 0;
-      for (; k + 4 <= kn; k += 4) {
-        steady_pair();
-        steady_pair();
-        steady_pair();
-        double o[P];
-#pragma unroll
-        for (int s = 0; s < P; ++s) o[s] = X[s];
-        steady_pair();
-        const double d = X[0] - o[0];
-        bool per = true;
-#pragma unroll
-        for (int s = 1; s < P; ++s) per = per && (X[s] - o[s] == d);
-#ifdef HSIM_NOSKIP
-        per = false;
-#endif
-        if (per) {
-          const int r = kn - k - 4;
-          const double rd = (double)r * d;
-#pragma unroll
-          for (int s = 0; s < P; ++s) X[s] += rd;
-          skipped = r;
-          k = kn;
-          break;
+      if (kn >= 4 && !block<4, EXT, AFF>(k, kn, skipped))
+        while (k + BLK <= kn && !block<BLK, EXT, AFF>(k, kn, skipped)) {
         }
-      }
       for (; k < kn; ++k) steady_pair();
       steady_level<1>();  // level 2m-1
+      if (P <= HSIM_UNROLL_MAXP) {
 #pragma unroll
-      for (int d = 0; d < 2 * P - 2; ++d) level_cool(d);
+        for (int d = 0; d < 2 * P - 2; ++d) level_cool(d);
+      } else {
+#pragma unroll 1
+        for (int d = 0; d < 2 * P - 2; ++d) level_rt(2 * m + d, m);
+      }
     } else {
       const i64 total = 2 * (m + P - 1);
       for (i64 lv = 0; lv < total; ++lv) level_rt(lv, m);

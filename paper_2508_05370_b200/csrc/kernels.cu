@@ -24,6 +24,7 @@
 // The depth kernels, K_deep and K_sync of a batch run concurrently on fork /
 // join side streams.
 #include <cstdio>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 #include "hsim.h"
@@ -45,6 +46,54 @@ constexpr int NSTREAM_FINAL = 19;
 i64 host_plan(hsim_handle* h, i64 first, i64 block, i64 stride, i64 n, i64 nr, i64** buf);
 void set_launches(hsim_handle* h, int n);
 void set_error(const char* m);
+
+// Optional timeline (env HSIM_TRACE=1, diagnostics only): timing events around
+// every launch of a call, printed to stderr as (kernel, stream, start, end) us.
+struct Trace {
+  static constexpr int MAXE = 256;
+  bool on = false;
+  int n = 0;
+  cudaEvent_t e0[MAXE], e1[MAXE];
+  const char* name[MAXE];
+  int sid[MAXE];
+  cudaEvent_t t0;
+  void begin(cudaStream_t st) {
+    static int env = -1;
+    if (env < 0) env = getenv("HSIM_TRACE") ? 1 : 0;
+    on = env == 1;
+    n = 0;
+    if (!on) return;
+    cudaEventCreate(&t0);
+    cudaEventRecord(t0, st);
+  }
+  int pre(const char* nm, int s, cudaStream_t st) {
+    if (!on || n >= MAXE) return -1;
+    cudaEventCreate(&e0[n]);
+    cudaEventCreate(&e1[n]);
+    name[n] = nm;
+    sid[n] = s;
+    cudaEventRecord(e0[n], st);
+    return n++;
+  }
+  void post(int q, cudaStream_t st) {
+    if (q >= 0) cudaEventRecord(e1[q], st);
+  }
+  void dump() {
+    if (!on) return;
+    cudaDeviceSynchronize();
+    for (int q = 0; q < n; ++q) {
+      float a = 0, b = 0;
+      cudaEventElapsedTime(&a, t0, e0[q]);
+      cudaEventElapsedTime(&b, t0, e1[q]);
+      fprintf(stderr, "TRACE %-16s s%-2d %9.1f %9.1f %8.1f\n", name[q], sid[q], a * 1e3, b * 1e3, (b - a) * 1e3);
+      cudaEventDestroy(e0[q]);
+      cudaEventDestroy(e1[q]);
+    }
+    cudaEventDestroy(t0);
+    n = 0;
+  }
+};
+static Trace g_trace;
 
 constexpr int NT = 128;              // threads per block (phase kernels)
 constexpr int MT = 256;              // threads of K_merge
@@ -309,24 +358,40 @@ __device__ i64 warp_pipe_class(const Tables& T, int32_t off, const ClassSplit& c
       }
     };
     // P > 16 here, so one job per warp (nseg == 1): the periodic-regime skip of
-    // Pipe<P>::run applies to the whole warp (X and out = X + cE all move by d)
-    for (; lv + 7 < hiMin; lv += 8) {
+    // Pipe<P>::block applies to the whole warp (X and out = X + cE all move by
+    // d): a first block of 4 pairs tests cyclicity 1 and c | 4, later blocks of
+    // 12 pairs test c = 1 and c | 12.
+    auto blk = [&](int BL) {
+      const double x0 = lp.X;
+      for (int b = 0; b < BL - 1; ++b) pair();
+      const double x1 = lp.X;
       pair();
-      pair();
-      pair();
-      const double xo = lp.X;
-      pair();
-      const double dd = lp.X - xo, d0 = __shfl_sync(FULL, dd, 0);
+      lv += 2 * BL;
+#ifdef HSIM_NOSKIP
+      return false;
+#endif
+      const i64 left = (hiMin - lv) >> 1;  // remaining whole pairs
+      double dd = lp.X - x1, d0 = __shfl_sync(FULL, dd, 0);
+      i64 q = -1, len = 1;  // q periods of len pairs, each adding d0
       if (__all_sync(FULL, !act || dd == d0)) {
-        const i64 r = (hiMin - (lv + 8)) >> 1;  // remaining whole pairs
-        const double rd = (double)r * d0;
-        lp.X += rd;
-        lp.out += rd;
-        lv += 8 + 2 * r;
-        if (act && s == 0) *cells -= 2 * P * r;
-        break;
+        q = left;
+      } else {
+        dd = lp.X - x0;
+        d0 = __shfl_sync(FULL, dd, 0);
+        if (__all_sync(FULL, !act || dd == d0)) { q = left / BL; len = BL; }
       }
-    }
+      if (q < 0) return false;
+      const i64 r = q * len;
+      const double rd = (double)q * d0;
+      lp.X += rd;
+      lp.out += rd;
+      lv += 2 * r;
+      if (act && s == 0) *cells -= 2 * P * r;
+      return true;
+    };
+    if (lv + 7 < hiMin && !blk(4))
+      while (lv + 23 < hiMin && !blk(12)) {
+      }
     for (; lv + 1 < hiMin; lv += 2) pair();
     for (; lv < totMax; ++lv) {
       const bool odd = lv & 1;
@@ -969,7 +1034,9 @@ static int run_phases(hsim_handle* h, const Tables* dT, Cands c, int64_t n, int6
     const i64 nsb = (cb - ca) * 32;
     if (b >= NBUF && !count) cudaStreamWaitEvent(st, pool_event(h, 2 + q), 0);  // buffer free: final(b-2) done
     cudaMemsetAsync(S.counters, 0, NCNT * sizeof(unsigned long long), st);
+    int tq = g_trace.pre("k_split", 0, st);
     k_split<<<gs, NT, 0, st>>>(dT, c, ca, cb, S, pm);
+    g_trace.post(tq, st);
     ++launches;
     cudaEventRecord(pool_event(h, q), st);
     // the depth kernels, K_deep and K_sync of a batch are independent: each on
@@ -990,6 +1057,8 @@ static int run_phases(hsim_handle* h, const Tables* dT, Cands c, int64_t n, int6
       const int P = order[oi];
       if (P > FASTP || !(pm >> P & 1)) continue;
       cudaStream_t ss = side(P);
+      static const char* pn[17] = {"", "k_pipe<1>", "k_pipe<2>", "k_pipe<3>", "k_pipe<4>", "k_pipe<5>", "k_pipe<6>", "k_pipe<7>", "k_pipe<8>", "k_pipe<9>", "k_pipe<10>", "k_pipe<11>", "k_pipe<12>", "k_pipe<13>", "k_pipe<14>", "k_pipe<15>", "k_pipe<16>"};
+      tq = g_trace.pre(pn[P], P, ss);
       switch (P) {
 #define HSIM_PIPE(PP) case PP: k_pipe<PP><<<grid_of(h, k_pipe<PP>, g_pipe[PP]), NT, 0, ss>>>(dT, S, count); break;
         HSIM_PIPE(1) HSIM_PIPE(2) HSIM_PIPE(3) HSIM_PIPE(4) HSIM_PIPE(5) HSIM_PIPE(6) HSIM_PIPE(7) HSIM_PIPE(8)
@@ -999,12 +1068,15 @@ static int run_phases(hsim_handle* h, const Tables* dT, Cands c, int64_t n, int6
 #undef HSIM_PIPE
         default: break;
       }
+      g_trace.post(tq, ss);
       ++launches;
       join(ss);
     }
     if (pm >> (FASTP + 1)) {
       cudaStream_t ss = side(17);
+      tq = g_trace.pre("k_deep", 17, ss);
       k_deep<<<gd, NT, 0, ss>>>(dT, S, count);
+      g_trace.post(tq, ss);
       ++launches;
       join(ss);
     }
@@ -1017,12 +1089,16 @@ static int run_phases(hsim_handle* h, const Tables* dT, Cands c, int64_t n, int6
     }
     {
       cudaStream_t ss = side(18);
+      tq = g_trace.pre("k_sync", 18, ss);
       k_sync<<<gy, NT, 0, ss>>>(dT, S, nsb);
+      g_trace.post(tq, ss);
       ++launches;
       join(ss);
     }
+    tq = g_trace.pre("k_final", NSTREAM_FINAL, fin);
     if (k && k <= 32) k_final_small<<<gf, NT, 0, fin>>>(dT, c, S, nsb, out_ns, k, lists);
     else k_final<<<gf, NT, 0, fin>>>(dT, c, S, nsb, out_ns, k, lists);
+    g_trace.post(tq, fin);
     ++launches;
     cudaEventRecord(pool_event(h, 2 + q), fin);
   }
@@ -1076,19 +1152,23 @@ int launch_eval(hsim_handle* h, const Tables* dT, const hsim_cands* cc, int64_t 
     if (ensure_block_scratch(h, (size_t)nlists * 2 * k + 1, &lists)) return HSIM_ENOMEM;
     cudaMemsetAsync(lists, 0x7F, ((size_t)nlists * 2 * k + 1) * 8, st);  // lists + global bound word
   }
+  g_trace.begin(st);
   if (n > 0) {
     const int rc = run_phases(h, dT, c, n, out_ns, k, lists, 0, nullptr, st, launches);
     if (rc) return rc;
   }
   if (k) {
     // n == 0 merges no list and only writes the (INT64_MAX, -1) padding
+    const int tq = g_trace.pre("k_merge", 0, st);
     if (n > 0 && k <= 32)
       k_merge_thresh<<<1, 1024, 0, st>>>(lists, nlists, k, (const unsigned long long*)(lists + (size_t)nlists * 2 * k),
                                          out_t, out_i);
     else
       launch_merge_any(lists, n > 0 ? nlists : 0, k, out_t, out_i, st);
+    g_trace.post(tq, st);
     ++launches;
   }
+  g_trace.dump();
   return finish(h, launches);
 }
 

@@ -7,6 +7,16 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2508_05370_b200 import build as B  # noqa: E402
 
 VARIANTS = {
+    "pm6": ["-DHSIM_PIPE_MINB=6"],
+    "pm5": ["-DHSIM_PIPE_MINB=5"],
+    "pm4": ["-DHSIM_PIPE_MINB=4"],
+    "noaff": ["-DHSIM_AFFINE_MAXP=0"],
+    "aff4": ["-DHSIM_AFFINE_MAXP=4", "-DHSIM_PIPE_MINB=6"],
+    "aff12": ["-DHSIM_AFFINE_MAXP=12", "-DHSIM_PIPE_MINB=6"],
+    "u4": ["-DHSIM_UNROLL_MAXP=4"],
+    "u6": ["-DHSIM_UNROLL_MAXP=6"],
+    "u16": ["-DHSIM_UNROLL_MAXP=16"],
+    "nb1": ["-DHSIM_NBATCH=1"],
     "p8s6": ["-DHSIM_PIPE_MINB=8", "-DHSIM_SYNC_MINB=6"],
     "nb1": ["-DHSIM_NBATCH=1"],
     "wcells": ["-DHSIM_WARPCELLS"],
