@@ -296,6 +296,17 @@ __global__ void __launch_bounds__(NT, P <= 4 ? HSIM_PIPE_MINB : 1) k_pipe(const 
   }
 }
 
+// max of (a, slope sa) and (b, slope sb) keeping the operand that wins now
+// (ties: the faster-growing one); H = min(H, pairs before the loser catches up)
+// -- the symbolic cell of Pipe<P>::sym_cell for the lane-per-stage layout
+__device__ __forceinline__ void sym_max(double& a, double& sa, double b, double sb, double& H) {
+  const bool bw = b > a || (b == a && sb > sa);
+  const double w = bw ? b : a, sw = bw ? sb : sa, l = bw ? a : b, sL = bw ? sa : sb;
+  if (sL > sw) H = fmin(H, floor((w - l) / (sL - sw)) - 1.0);
+  a = w;
+  sa = sw;
+}
+
 // ---- K_deep: lane-per-stage wavefront for depth > FASTP --------------------------
 // Packs floor(32 / P) sub-classes (same class, same candidate) per pass.
 __device__ i64 warp_pipe_class(const Tables& T, int32_t off, const ClassSplit& cs, i64* cells) {
@@ -357,10 +368,12 @@ __device__ i64 warp_pipe_class(const Tables& T, int32_t off, const ClassSplit& c
         lp.out = e + cE;
       }
     };
-    // P > 16 here, so one job per warp (nseg == 1): the periodic-regime skip of
-    // Pipe<P>::block applies to the whole warp (X and out = X + cE all move by
-    // d): a first block of 4 pairs tests cyclicity 1 and c | 4, later blocks of
-    // 12 pairs test c = 1 and c | 12.
+    // periodic-regime skip (Pipe<P>::block): the nseg sub-classes of the warp
+    // skip the same number of pairs, each with its own increment d (read from
+    // its stage-0 lane; X and out = X + cE all move by d): a first block of 4
+    // pairs tests cyclicity 1 and c | 4, later blocks of 12 pairs c = 1 and
+    // c | 12 -- for every active segment at once.
+    const int lead = seg < nseg ? seg * P : lane;
     auto blk = [&](int BL) {
       const double x0 = lp.X;
       for (int b = 0; b < BL - 1; ++b) pair();
@@ -371,13 +384,40 @@ __device__ i64 warp_pipe_class(const Tables& T, int32_t off, const ClassSplit& c
       return false;
 #endif
       const i64 left = (hiMin - lv) >> 1;  // remaining whole pairs
-      double dd = lp.X - x1, d0 = __shfl_sync(FULL, dd, 0);
+      double dd = lp.X - x1, d0 = __shfl_sync(FULL, dd, lead);
+      {
+        // affine regime (Pipe<P>::affine_horizon, lane = stage): the next pair
+        // on (value, slope dd) operands must move X by exactly dd with the
+        // slopes reproduced; H = pairs before a losing operand catches up
+        double x = lp.X, sx = dd, H = 1e300;
+        {
+          const double v = shfl_d(lp.out, srcO), sv = shfl_d(sx, srcO);
+          if (kO) sym_max(x, sx, v, sv, H);
+          x += durO;
+        }
+        {
+          const double v = shfl_d(x + cO, srcE), sv = shfl_d(sx, srcE);
+          if (kE) sym_max(x, sx, v, sv, H);
+          x += durE;
+        }
+        if (!act) H = 1e300;
+        for (int k = 16; k > 0; k >>= 1) H = fmin(H, __shfl_xor_sync(FULL, H, k));
+        if (__all_sync(FULL, !act || (x - lp.X == dd && sx == dd)) && H >= 1.0) {
+          const i64 t = (i64)fmin(H, (double)left);
+          const double td = (double)t * dd;
+          lp.X += td;
+          lp.out += td;
+          lv += 2 * t;
+          if (act && s == 0) *cells -= 2 * P * t;
+          return t == left;
+        }
+      }
       i64 q = -1, len = 1;  // q periods of len pairs, each adding d0
       if (__all_sync(FULL, !act || dd == d0)) {
         q = left;
       } else {
         dd = lp.X - x0;
-        d0 = __shfl_sync(FULL, dd, 0);
+        d0 = __shfl_sync(FULL, dd, lead);
         if (__all_sync(FULL, !act || dd == d0)) { q = left / BL; len = BL; }
       }
       if (q < 0) return false;
