@@ -105,6 +105,30 @@ class Clocks:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def overhead_ops(sim, first, n, blk, stride, world):
+    """SURVEY §8(d) per-candidate non-cell work: 50 ops per stage (partition +
+    stage sums), 26 per gradient-sync segment (J = sum P_c - C + 1, the most the
+    common refinement can have), 100 for the decode -- summed over this rank's
+    candidates template by template (host decode of each template's first
+    candidate; outside the timed region)."""
+    tot = 0
+    nt = sim.n_templates()
+    bounds = [sim.template_first(k) for k in range(nt + 1)]
+    ranges = [(first, first + n)] if world == 1 else \
+        [(b0, min(b0 + blk, sim.space_size())) for b0 in range(first, sim.space_size(), stride)]
+    import bisect
+    for lo, hi in ranges:
+        k = bisect.bisect_right(bounds, lo) - 1
+        while k < nt and bounds[k] < hi:
+            cnt = min(hi, bounds[k + 1]) - max(lo, bounds[k])
+            d = sim.decode(bounds[k])
+            sp = sum(len(c["stages"]) for c in d["classes"])
+            J = sp - len(d["classes"]) + 1
+            tot += cnt * (50 * sp + 26 * J + 100)
+            k += 1
+    return tot
+
+
 def cpu_baseline(cfg, seconds=15.0):
     """The oracle as it stands, on all host cores, on a seeded sample of the
     workload sized to ~`seconds` of wall time (rank 0, N=1 only)."""
@@ -220,18 +244,33 @@ def run_ours(a):
     launches_per_step = sim.last_launch_count() + (1 if world > 1 else 0)
     value = N * a.steps / (tot_ms / 1e3)
 
-    # roofline of the dominant kernel (k_eval; K3 merge included in the interval)
+    # roofline of the sweep: SURVEY §8(d)'s per-unit figures --
+    # 8 int32-equivalent ops per EXECUTED 1F1B cell (the steady-regime jumps
+    # skip cells; skipped cells are not counted) + per candidate ~50 ops per
+    # stage (partition + stage sums), ~26 per sync segment (J <= sum P - C + 1),
+    # ~100 for the decode -- over the ALU issue peak
     pk = peaks()
     sm_max = float(pk.get("sm_max_mhz", 1965.0))
     peak_gops = SMS * LANES_PER_SM * sm_max * 1e6 / 1e9
     my_ms = sum(ms) / a.steps
-    achieved = OPS_PER_CELL * cells / (my_ms / 1e3) / 1e9
-    traffic = None
+    over = overhead_ops(sim, first, n, blk, stride, world)
+    ops = OPS_PER_CELL * cells + over
+    achieved = ops / (my_ms / 1e3) / 1e9
+    traffic, issue = None, None
     prof = os.path.join(ROOT, "profiles", "ncu_summary.json")
     if os.path.exists(prof):
         try:
             with open(prof) as f:
-                traffic = json.load(f).get("sweep_dram_bytes")
+                js = json.load(f)
+            if js.get("config") == a.config and world == 1:
+                traffic = js.get("sweep_dram_bytes")
+                wi = js.get("sweep_warp_inst")
+                if wi:  # ncu warp instructions of one sweep / (live sweep time x issue slots)
+                    rate = wi / (my_ms / 1e3) / 1e9
+                    issue = {"achieved": round(rate, 1), "peak": round(SMS * 4 * sm_max * 1e6 / 1e9, 1),
+                             "unit": "Gwarp-inst/s", "frac": round(rate / (SMS * 4 * sm_max * 1e-3), 4),
+                             "from": "profiles/ncu_summary.json sweep_warp_inst (ncu launch list of one sweep) / "
+                                     "this run's mean sweep time; peak = 148 SMs x 4 schedulers x clock"}
         except (OSError, ValueError):
             traffic = None
 
@@ -278,9 +317,10 @@ def run_ours(a):
                            "parallelism": f"block-cyclic shard x{world}" + (" + NCCL all_gather" if world > 1 else "")},
                 "roofline": {"bound": "alu", "achieved": round(achieved, 1), "peak": round(peak_gops, 1),
                              "unit": "Gop/s", "frac": round(achieved / peak_gops, 4), "traffic": traffic,
+                             "issue_slots": issue, "ops_cells": OPS_PER_CELL * cells, "ops_overhead": over,
                              "kernel": "one hsim_topk sweep = K_split, K_pipe<P>, K_deep, K_sync (concurrent "
                                        "fork/join streams), K_final, K_merge; per-kernel shares in profiles/",
-                             "ops_per_launch": OPS_PER_CELL * cells, "cells_per_launch": cells,
+                             "ops_per_launch": ops, "cells_per_launch": cells,
                              "peak_from": f"{SMS} SMs x {LANES_PER_SM} lanes x {sm_max:.0f} MHz (issue slots)"},
                 "gpu_launches": launches_per_step * a.steps,
                 "clocks": clk}

@@ -7,6 +7,10 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2508_05370_b200 import build as B  # noqa: E402
 
 VARIANTS = {
+    "fm4": ["-DHSIM_FINAL_MULT=4"],
+    "fm2": ["-DHSIM_FINAL_MULT=2"],
+    "aff11": ["-DHSIM_AFFINE_MAXP=11"],
+    "aff16": ["-DHSIM_AFFINE_MAXP=16"],
     "pm6": ["-DHSIM_PIPE_MINB=6"],
     "pm5": ["-DHSIM_PIPE_MINB=5"],
     "pm4": ["-DHSIM_PIPE_MINB=4"],

@@ -23,6 +23,8 @@ ids = sorted(launch)
 half = ids[len(ids) // 2:]
 tot_ns = sum(launch[i]["gpu__time_duration.sum"] for i in half)
 dram = sum(launch[i].get("dram__bytes_read.sum", 0) + launch[i].get("dram__bytes_write.sum", 0) for i in half)
+winst = sum(launch[i].get("smsp__inst_executed.sum", 0) for i in half)
+tinst = sum(launch[i].get("smsp__thread_inst_executed.sum", 0) for i in half)
 kern = []
 for i in half:
     L = launch[i]
@@ -61,10 +63,12 @@ for rep, rx in (("prof_pipe4.ncu-rep", "k_pipe"), ("prof_phases.ncu-rep", "k_"))
             full[name]["top_stalls_per_issue"] = {k.replace("smsp__average_warps_issue_stalled_", "").replace("_per_issue_active.ratio", ""): d[k] for k in st}
 summary = {"round": tag, "workload": "config 2 full sweep (873192 candidates) -> top-16, one hsim_topk call",
            "how": "ncu --metrics ... --clock-control none (cold, serialised: shares, not absolutes); second of two sweeps",
-           "serialised_sum_us": round(tot_ns / 1e3, 1), "sweep_dram_bytes": int(dram), "kernels": kern, "full_captures": full}
+           "serialised_sum_us": round(tot_ns / 1e3, 1), "sweep_dram_bytes": int(dram),
+           "sweep_warp_inst": int(winst), "sweep_thread_inst": int(tinst), "kernels": kern, "full_captures": full}
 os.makedirs(prof, exist_ok=True)
 json.dump(summary, open(os.path.join(prof, f"ncu_summary_{tag}.json"), "w"), indent=1)
-json.dump({"sweep_dram_bytes": int(dram), "round": tag}, open(os.path.join(prof, "ncu_summary.json"), "w"), indent=1)
+json.dump({"sweep_dram_bytes": int(dram) or None, "sweep_warp_inst": int(winst), "sweep_thread_inst": int(tinst) or None,
+           "config": 2, "round": tag}, open(os.path.join(prof, "ncu_summary.json"), "w"), indent=1)
 subprocess.run(["cp", os.path.join(go, "launches.csv"), os.path.join(prof, f"launches_{tag}.csv")])
 for k in kern:
     print(k)
