@@ -157,3 +157,15 @@ def with_changes(cfg, **paths):
         else:
             node[last] = val
     return out
+
+
+def with_mem_check(cfg, mem_bytes=None):
+    """Copy of cfg with the memory-feasibility check on (SURVEY.md §8(f) f2,
+    DESIGN.md M.1); optionally per-type capacities in bytes (plain data)."""
+    out = copy.deepcopy(cfg)
+    out["search"]["mem_check"] = 1
+    if mem_bytes is not None:
+        for t, v in zip(out["cluster"]["types"], mem_bytes):
+            t["mem_bytes"] = int(v)
+    out["name"] = out["name"] + "-memcheck"
+    return out

@@ -23,7 +23,8 @@
 //
 // Pins (tests/test_oracle_pins.py): Table 4 delays, ring all-reduce and 1F1B
 // closed forms, DAG longest path, Hamilton / Fig 3 shares, Table 1 payload,
-// parameter counts, brute-force tiny spaces, invariants.  Absolute iteration
+// parameter counts, brute-force tiny spaces, invariants; the memory-feasibility
+// row (DESIGN M.1) in tests/test_memory_pins.py.  Absolute iteration
 // times are "parity unpinned" (the paper prints none).
 
 #include <algorithm>
@@ -72,6 +73,7 @@ struct orc_input {
   int32_t n_tp[8], tpset[8][8];
   int32_t n_p, pset[16];
   int32_t homo, mixed, use_all, r_layer, pmax, r_batch;
+  int32_t mem_check;  // prune candidates that do not fit (status -3, DESIGN M.1)
 };
 }
 
@@ -494,6 +496,52 @@ struct Oracle {
         if (v < 1) p.status = -2;
   }
 
+  // --- f2 / DESIGN M.1: memory feasibility -------------------------------------
+  // The paper never gates on memory (SPEC.md:104 makes it a warning); this row
+  // follows SURVEY §8(f) f2: "params + grads + optimizer + 1F1B in-flight
+  // activations <= capacity", read as follows, for one device of every stage
+  // group of every replica:
+  //   params  = l_s * ceil(W_layer / t) + [s = 0] ceil(V h / t)
+  //             + [s = P-1] ceil((V h [!tied] + h) / t)          (C.6's W_layer)
+  //   static  = params * (bpe_act + bpe_grad + 12)   weights, gradients (A7), and
+  //             Adam's fp32 master copy + two moments (4 + 4 + 4 bytes)
+  //   act     = b s h (10 + 24/t) bytes per layer and in-flight micro-batch
+  //             (Korthikanti et al. 2022, TP without sequence parallelism,
+  //             16-bit, attention scores recomputed -- their "selective
+  //             recomputation", i.e. no 5 a s^2 b term), as one integer
+  //             ceil(b s h (10 t + 24) / t)
+  //   in flight = min(P - s, m_r): 1F1B's warm-up depth of stage s
+  //   need    = static + in_flight * l_s * act  <=  mem_bytes(type)
+  // Any device over capacity -> -3.  Checked after the layer / batch split
+  // (-1 / -2 take precedence).
+  i64 device_bytes(const StageSpec& ss, int P, int s, i64 l, i64 m, int b) const {
+    const i64 t = ss.tp, h = in.h, S = in.seq;
+    const i64 hkv = in.kv_heads * h / in.heads;
+    const i64 Wlayer = h * (2 * h + 2 * hkv) + in.nm * h * in.ffn * in.E + (in.E > 1 ? h * in.E : 0) + 2 * h;
+    i64 params = l * ceil_div(Wlayer, t);
+    if (s == 0) params += ceil_div(in.V * h, t);
+    if (s == P - 1) params += ceil_div(in.V * h * (in.tied ? 0 : 1) + h, t);
+    const i64 stat = params * (in.bpe_act + in.bpe_grad + 12);
+    const i64 act = ceil_div((i64)b * S * h * (10 * t + 24), t);
+    const i64 inflight = std::min((i64)(P - s), m);
+    return stat + inflight * l * act;
+  }
+  void check_memory(Plan& p) const {
+    if (!in.mem_check || p.status) return;
+    const auto& cls = p.tpl->cls;
+    for (size_t c = 0; c < cls.size(); ++c) {
+      const int P = (int)cls[c].st.size();
+      for (int r = 0; r < cls[c].D; ++r)
+        for (int s = 0; s < P; ++s) {
+          const StageSpec& ss = cls[c].st[s];
+          if (device_bytes(ss, P, s, p.layers[c][s], p.mb[c][r], p.tpl->b) > types[ss.type].mem_bytes) {
+            p.status = -3;
+            return;
+          }
+        }
+    }
+  }
+
   // --- C.7 / C.11: event-driven 1F1B over every replica ------------------------
   struct SimGroup {
     int P, s, m;
@@ -568,6 +616,7 @@ struct Oracle {
     Plan p = decode(i);
     place(p);
     partition(p);
+    check_memory(p);
     if (p.status) return p.status;
     const auto& cls = p.tpl->cls;
     const int C = (int)cls.size(), b = p.tpl->b;
@@ -740,6 +789,7 @@ int orc_describe(void* h, i64 i, char* buf, int cap) {
   Plan p = o->decode(i);
   o->place(p);
   o->partition(p);
+  o->check_memory(p);
   std::string s = "{\"b\":" + std::to_string(p.tpl->b) + ",\"status\":" + std::to_string(p.status) + ",\"classes\":[";
   for (size_t c = 0; c < p.tpl->cls.size(); ++c) {
     const ClassSpec& cs = p.tpl->cls[c];
@@ -768,6 +818,10 @@ int orc_describe(void* h, i64 i, char* buf, int cap) {
 }
 
 // --- building blocks exposed for the pin tests -------------------------------
+// DESIGN M.1: bytes needed on one device of stage s (of P) with l layers, m micro-batches
+i64 orc_device_bytes(void* h, int type, int tp, int P, int s, i64 l, i64 m, int b) {
+  return ((Oracle*)h)->device_bytes(StageSpec{type, tp}, P, s, l, m, b);
+}
 // per-hop delay before rounding: frame*8 / uni Gbps
 double orc_hop_delay_exact(double gbps, int bidir, i64 frame) {
   orc_hop hp{gbps, bidir, 0};

@@ -61,7 +61,8 @@ class _Input(C.Structure):
                 ("n_tp", C.c_int32 * 8), ("tpset", (C.c_int32 * 8) * 8),
                 ("n_p", C.c_int32), ("pset", C.c_int32 * 16),
                 ("homo", C.c_int32), ("mixed", C.c_int32), ("use_all", C.c_int32),
-                ("r_layer", C.c_int32), ("pmax", C.c_int32), ("r_batch", C.c_int32)]
+                ("r_layer", C.c_int32), ("pmax", C.c_int32), ("r_batch", C.c_int32),
+                ("mem_check", C.c_int32)]
 
 
 def _path(hops):
@@ -110,6 +111,8 @@ def lib():
         L.orc_segment_bytes.argtypes = [C.c_void_p, C.c_int64, C.c_int, C.c_int]
         L.orc_act_bytes.restype = C.c_int64
         L.orc_act_bytes.argtypes = [C.c_void_p, C.c_int]
+        L.orc_device_bytes.restype = C.c_int64
+        L.orc_device_bytes.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int64, C.c_int64, C.c_int]
     return _lib
 
 
@@ -166,6 +169,7 @@ class Oracle:
             I.pset[q] = v
         I.homo, I.mixed, I.use_all = se["homo"], se["mixed"], se["use_all"]
         I.r_layer, I.pmax, I.r_batch = se["r_layer"], se["pmax_perturb"], se["r_batch"]
+        I.mem_check = int(se.get("mem_check", 0))
         self._in = I
         self.h = lib().orc_create(C.byref(I))
         if not self.h:
@@ -222,6 +226,10 @@ class Oracle:
 
     def segment_bytes(self, n_layers, has_first, has_last):
         return lib().orc_segment_bytes(self.h, n_layers, int(has_first), int(has_last))
+
+    def device_bytes(self, type_idx, tp, P, s, layers, mb, b):
+        """DESIGN M.1: bytes one device of stage s (of P) needs (f2 memory check)."""
+        return lib().orc_device_bytes(self.h, type_idx, tp, P, s, layers, mb, b)
 
     def act_bytes(self, b):
         return lib().orc_act_bytes(self.h, b)
