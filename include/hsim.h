@@ -31,7 +31,8 @@
  *     SPEC.md:335).
  *   - Per-candidate status is in-band in the int64 result: >= 0 iteration time
  *     in ns; -1 a stage received < 1 layer; -2 a replica received < 1
- *     micro-batch; (-3 reserved: memory feasibility, DESIGN.md §8 NEXT).
+ *     micro-batch; -3 some device exceeds its memory capacity (only when
+ *     hsim_model_desc.mem_check = 1; DESIGN.md M.1).
  */
 #ifndef HSIM_H
 #define HSIM_H
@@ -77,7 +78,7 @@ typedef struct {
   double hbm_bytes_per_ns;          /* HBM bandwidth, B/ns (= GB/s)                   */
   double eff_flop[HSIM_NKIND];      /* achieved fraction per layer kind, (0, 1]       */
   double eff_mem[HSIM_NKIND];
-  int64_t mem_bytes;                /* capacity (reserved for memory pruning)         */
+  int64_t mem_bytes;                /* capacity in bytes (memory pruning, mem_check)  */
   int32_t gpus_per_node;            /* 1, 2, 4 or 8; == NICs per node (rail-only)     */
   int32_t n_link_kinds;             /* 1..4                                           */
   hsim_path link_kinds[HSIM_MAX_LINK_KINDS];
@@ -112,6 +113,12 @@ typedef struct {
   int32_t homo, mixed;                        /* families: type-homogeneous / mixed pipelines */
   int32_t use_all;                            /* every used type fully used                   */
   int32_t r_layer, pmax_perturb, r_batch;     /* perturbation radii / max perturbed depth     */
+  /* memory-feasibility pruning (the paper never gates on
+   * memory): 1 = a candidate any of whose devices needs more than
+   * its type's mem_bytes -- parameters x (bpe_act + bpe_grad + 12 B Adam state)
+   * + min(P - s, m) in-flight micro-batches x layers x s b h (10 + 24/t) B of
+   * activations (DESIGN.md M.1) -- gets status -3.  0 = off (default). */
+  int32_t mem_check, _pad_mc;
 } hsim_model_desc;
 
 /* Which candidates the t-th work item (t = 0..n-1) evaluates. */

@@ -590,6 +590,28 @@ void hsim_handle::prepare() {
   hT.seg_last_bytes = ((i64)md.vocab * h * (md.tied ? 0 : 1) + h) * md.bpe_grad;
   if (md.layers * hT.seg_layer_bytes + hT.seg_first_bytes + hT.seg_last_bytes >= TWO53)
     fail(HSIM_ERANGE, "gradient bytes reach 2^53");
+  // memory feasibility (DESIGN.md M.1)
+  hT.mem_check = md.mem_check ? 1 : 0;
+  {
+    const i64 bst = (i64)md.bpe_act + md.bpe_grad + 12;  // weights + gradients + Adam fp32 master / m / v
+    double worst = 0, bmax = 1;
+    for (int q = 0; q < md.n_bset && q < 8; ++q) bmax = std::max(bmax, (double)md.bset[q]);
+    for (int lg = 0; lg < 4; ++lg) {
+      const i64 t = (i64)1 << lg;
+      hT.mem_layer[lg] = (Wlayer + t - 1) / t * bst;
+      hT.mem_emb[lg] = ((i64)md.vocab * h + t - 1) / t * bst;
+      hT.mem_head[lg] = ((i64)md.vocab * h * (md.tied ? 0 : 1) + h + t - 1) / t * bst;
+      hT.mem_K[lg] = (i64)md.seq * h * (10 * t + 24);
+      // largest need any candidate can have: all layers, deepest in-flight, largest b
+      worst = std::max(worst, (double)md.layers * hT.mem_layer[lg] + hT.mem_emb[lg] + hT.mem_head[lg] +
+                                  (double)MAXP * md.layers * (bmax * hT.mem_K[lg]));
+    }
+    if (md.mem_check && worst >= 9.0e18) fail(HSIM_ERANGE, "memory need may overflow int64");
+    for (int k = 0; k < MAXT; ++k) hT.mem_cap[k] = k < cd.n_device_types ? cd.device_types[k].mem_bytes : 0;
+    if (md.mem_check)
+      for (int k = 0; k < cd.n_device_types; ++k)
+        if (cd.device_types[k].mem_bytes <= 0) fail(HSIM_EINVAL, "InvalidValue: mem_bytes must be > 0 with mem_check");
+  }
   hT.r_layer = md.r_layer;
   hT.r_batch = md.r_batch;
   hT.ldiv = make_fastdiv((u32)(2 * md.r_layer + 1));

@@ -127,6 +127,12 @@ struct Tables {
   int8_t lc_same[MAXT][MAXG][MAXG];               // same node: link class of i -> j
   int8_t lc_cross[MAXT][MAXG][MAXT][MAXG];        // different nodes: (t1, r1) -> (t2, r2)
   const int8_t* node_type;                        // [n_nodes]
+  // memory feasibility (DESIGN.md M.1), per lg = log2(tp): bytes of state per
+  // layer / for the embedding / for the head on one device, and
+  // K[lg] = s h (10 t + 24) (activation bytes per layer = ceil(b K / t))
+  int32_t mem_check, _pad6;
+  i64 mem_layer[4], mem_emb[4], mem_head[4], mem_K[4];
+  i64 mem_cap[MAXT];
 };
 
 // --- C.0 --------------------------------------------------------------------
@@ -316,6 +322,27 @@ HD int partition_c(const Tables& T, const TplRec& tp, i64 local, ClassSplit (&cs
 #pragma unroll
   for (int c = 0; c < C; ++c)
     if (mb_of(cs[c], D[c] - 1) < 1) return -2;  // m non-increasing in k
+  if (T.mem_check) {
+    // DESIGN.md M.1: every device of every stage fits; replica 0 has the most
+    // micro-batches (m non-increasing in k) and need is non-decreasing in m
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      const CrecHdr* h = crec_hdr(T, tp.crec[c]);
+      const StageRec* st = crec_stages(T, tp.crec[c]);
+      const i64 m0 = mb_of(cs[c], 0);
+      LayerWalk lw = walk(T, h, cs[c].dig);
+      for (int s = 0; s < h->P; ++s) {
+        const i64 l = lw.next(st);
+        const int lg = st[s].lg_tp;
+        const i64 act = ((i64)tp.b * T.mem_K[lg] + st[s].tp - 1) >> lg;
+        const i64 fl = imin((i64)(h->P - s), m0);
+        i64 need = l * T.mem_layer[lg] + fl * l * act;
+        if (s == 0) need += T.mem_emb[lg];
+        if (s == h->P - 1) need += T.mem_head[lg];
+        if (need > T.mem_cap[st[s].type]) return -3;
+      }
+    }
+  }
   return 0;
 }
 

@@ -65,7 +65,8 @@ class hsim_model_desc(C.Structure):
                 ("tpset_mask", C.c_int32 * 4),
                 ("n_pset", C.c_int32), ("pset", C.c_int32 * 16),
                 ("homo", C.c_int32), ("mixed", C.c_int32), ("use_all", C.c_int32),
-                ("r_layer", C.c_int32), ("pmax_perturb", C.c_int32), ("r_batch", C.c_int32)]
+                ("r_layer", C.c_int32), ("pmax_perturb", C.c_int32), ("r_batch", C.c_int32),
+                ("mem_check", C.c_int32), ("_pad_mc", C.c_int32)]
 
 
 class hsim_cands(C.Structure):
@@ -161,6 +162,7 @@ def descriptors(cfg):
         m.pset[q] = v
     for k in ("homo", "mixed", "use_all", "r_layer", "pmax_perturb", "r_batch"):
         setattr(m, k, se[k])
+    m.mem_check = int(se.get("mem_check", 0))
     return cd, m, (types, nodes)
 
 
