@@ -169,3 +169,12 @@ def with_mem_check(cfg, mem_bytes=None):
             t["mem_bytes"] = int(v)
     out["name"] = out["name"] + "-memcheck"
     return out
+
+
+def with_sync_overlap(cfg):
+    """Copy of cfg with the gradient sync overlapped with the backward pass
+    (DESIGN.md S.1) instead of after the barrier (C.8)."""
+    out = copy.deepcopy(cfg)
+    out["search"]["sync_overlap"] = 1
+    out["name"] = out["name"] + "-overlap"
+    return out

@@ -74,6 +74,7 @@ struct orc_input {
   int32_t n_p, pset[16];
   int32_t homo, mixed, use_all, r_layer, pmax, r_batch;
   int32_t mem_check;  // prune candidates that do not fit (status -3, DESIGN M.1)
+  int32_t sync_overlap;  // gradient sync overlapped with the backward (DESIGN S.1)
 };
 }
 
@@ -549,6 +550,7 @@ struct Oracle {
     std::vector<std::pair<bool, int>> ops;  // (is_fwd, micro-batch)
     size_t next = 0;
     bool busy = false;
+    i64 done = 0;  // end of the group's last op (its last backward, C.7)
     std::vector<char> inF, inB;
   };
   struct Ev {
@@ -595,6 +597,7 @@ struct Oracle {
       if (e.kind == 0) {
         auto op = g.ops[g.next];
         g.busy = false;
+        g.done = e.t;
         g.next++;
         if (op.first) {
           if (g.s < g.P - 1) q.push(Ev{e.t + g.c_next, seq++, 1, e.grp + 1, op.second});
@@ -678,10 +681,9 @@ struct Oracle {
     cuts.erase(std::unique(cuts.begin(), cuts.end()), cuts.end());
     const i64 hkv = in.kv_heads * in.h / in.heads;
     const i64 Wlayer = in.h * (2 * in.h + 2 * hkv) + in.nm * in.h * in.ffn * in.E + (in.E > 1 ? in.h * in.E : 0) + 2 * in.h;
-    // free time per stage group of every replica, all from the barrier
-    std::vector<std::vector<std::vector<i64>>> freet(C);
-    for (int c = 0; c < C; ++c) freet[c].assign(cls[c].D, std::vector<i64>(cls[c].st.size(), T0));
-    i64 Titer = T0;
+    // per segment: RS_j + AR_j and the stage of every class holding it
+    std::vector<i64> cost;
+    std::vector<std::vector<int>> seg_sc;
     for (size_t j = 0; j + 1 < cuts.size(); ++j) {
       const i64 a = cuts[j], z = cuts[j + 1];
       i64 S = (z - a) * Wlayer * in.bpe_grad;
@@ -718,13 +720,50 @@ struct Oracle {
         }
         AR = std::max(AR, ring_sim(taus, (int)(2 * (D - 1))));
       }
-      i64 st = 0;
-      for (int c = 0; c < C; ++c)
-        for (int r = 0; r < cls[c].D; ++r) st = std::max(st, freet[c][r][sc[c]]);
-      const i64 en = st + RS + AR;
-      for (int c = 0; c < C; ++c)
-        for (int r = 0; r < cls[c].D; ++r) freet[c][r][sc[c]] = en;
-      Titer = std::max(Titer, en);
+      cost.push_back(RS + AR);
+      seg_sc.push_back(sc);
+    }
+    const int J = (int)cost.size();
+    // stage groups of every replica; FIFO per group (C.8 / S.1)
+    std::vector<std::vector<std::vector<i64>>> freet(C);
+    i64 Titer = T0;
+    if (!in.sync_overlap) {
+      // C.8: barrier at T0, segments in ascending layer order
+      for (int c = 0; c < C; ++c) freet[c].assign(cls[c].D, std::vector<i64>(cls[c].st.size(), T0));
+      for (int j = 0; j < J; ++j) {
+        i64 st = 0;
+        for (int c = 0; c < C; ++c)
+          for (int r = 0; r < cls[c].D; ++r) st = std::max(st, freet[c][r][seg_sc[j][c]]);
+        const i64 en = st + cost[j];
+        for (int c = 0; c < C; ++c)
+          for (int r = 0; r < cls[c].D; ++r) freet[c][r][seg_sc[j][c]] = en;
+        Titer = std::max(Titer, en);
+      }
+    } else {
+      // S.1 (Table 1: DP sync is exposed in the backward pass,
+      // PAPER.md:100-101): no barrier -- segment j is ready once every group
+      // holding its layers, in every replica, has ended its last backward op;
+      // segments are issued in descending layer order (the order backward
+      // produces gradients), FIFO per group.
+      size_t gi = 0;
+      std::vector<std::vector<std::vector<i64>>> lastB(C);
+      for (int c = 0; c < C; ++c) {
+        const int P = (int)cls[c].st.size();
+        lastB[c].assign(cls[c].D, std::vector<i64>(P, 0));
+        for (int r = 0; r < cls[c].D; ++r)
+          for (int s = 0; s < P; ++s) lastB[c][r][s] = G[gi++].done;
+        freet[c].assign(cls[c].D, std::vector<i64>(P, 0));
+      }
+      for (int j = J - 1; j >= 0; --j) {
+        i64 st = 0;
+        for (int c = 0; c < C; ++c)
+          for (int r = 0; r < cls[c].D; ++r)
+            st = std::max(st, std::max(lastB[c][r][seg_sc[j][c]], freet[c][r][seg_sc[j][c]]));
+        const i64 en = st + cost[j];
+        for (int c = 0; c < C; ++c)
+          for (int r = 0; r < cls[c].D; ++r) freet[c][r][seg_sc[j][c]] = en;
+        Titer = std::max(Titer, en);
+      }
     }
     return Titer;
   }

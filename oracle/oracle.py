@@ -62,7 +62,7 @@ class _Input(C.Structure):
                 ("n_p", C.c_int32), ("pset", C.c_int32 * 16),
                 ("homo", C.c_int32), ("mixed", C.c_int32), ("use_all", C.c_int32),
                 ("r_layer", C.c_int32), ("pmax", C.c_int32), ("r_batch", C.c_int32),
-                ("mem_check", C.c_int32)]
+                ("mem_check", C.c_int32), ("sync_overlap", C.c_int32)]
 
 
 def _path(hops):
@@ -170,6 +170,7 @@ class Oracle:
         I.homo, I.mixed, I.use_all = se["homo"], se["mixed"], se["use_all"]
         I.r_layer, I.pmax, I.r_batch = se["r_layer"], se["pmax_perturb"], se["r_batch"]
         I.mem_check = int(se.get("mem_check", 0))
+        I.sync_overlap = int(se.get("sync_overlap", 0))
         self._in = I
         self.h = lib().orc_create(C.byref(I))
         if not self.h:
