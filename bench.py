@@ -48,6 +48,10 @@ def parse():
     ap.add_argument("--k", type=int, default=TOPK)
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--mem-check", action="store_true",
+                    help="SURVEY 8(f) f2 row: prune candidates over device memory (status -3, DESIGN M.1)")
+    ap.add_argument("--sync-overlap", action="store_true",
+                    help="SURVEY 8(f) f1 row: gradient sync overlapped with the backward (DESIGN S.1)")
     return ap.parse_args()
 
 
@@ -147,7 +151,16 @@ def cpu_baseline(cfg, seconds=15.0):
     dt = time.perf_counter() - t
     return {"value": round(len(idx) / dt, 3), "unit": "configs/s", "cores": cores, "kind": "oracle",
             "sample": f"{len(idx)} seeded (splitmix64 0x5EED2508) uniform candidates of the {N}-candidate "
-                      f"config-{CONFIG} space, compact event-driven oracle, {dt:.1f} s wall"}
+                      f"{cfg['name']} space, compact event-driven oracle, {dt:.1f} s wall"}
+
+
+def workload(a):
+    cfg = H.get(a.config)
+    if a.mem_check:
+        cfg = H.with_mem_check(cfg)
+    if a.sync_overlap:
+        cfg = H.with_sync_overlap(cfg)
+    return cfg
 
 
 def run_reference(a):
@@ -155,7 +168,7 @@ def run_reference(a):
     if rank != 0:
         return
     import oracle
-    cfg = H.get(a.config)
+    cfg = workload(a)
     o = oracle.Oracle(cfg)
     cores = os.cpu_count() or 1
     N = o.space_size()
@@ -197,7 +210,7 @@ def run_ours(a):
         pbuild.build()
     if world > 1:
         dist.barrier()
-    cfg = H.get(a.config)
+    cfg = workload(a)
     sim = Sim(cfg)
     N = sim.space_size()
     first, n, blk, stride = shard(N, rank, world)
@@ -262,7 +275,7 @@ def run_ours(a):
         try:
             with open(prof) as f:
                 js = json.load(f)
-            if js.get("config") == a.config and world == 1:
+            if js.get("config") == a.config and world == 1 and not (a.mem_check or a.sync_overlap):
                 traffic = js.get("sweep_dram_bytes")
                 wi = js.get("sweep_warp_inst")
                 if wi:  # ncu warp instructions of one sweep / (live sweep time x issue slots)

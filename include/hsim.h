@@ -118,7 +118,14 @@ typedef struct {
    * its type's mem_bytes -- parameters x (bpe_act + bpe_grad + 12 B Adam state)
    * + min(P - s, m) in-flight micro-batches x layers x s b h (10 + 24/t) B of
    * activations (DESIGN.md M.1) -- gets status -3.  0 = off (default). */
-  int32_t mem_check, _pad_mc;
+  int32_t mem_check;
+  /* gradient-sync schedule: 0 = after the barrier at T0,
+   * segments in ascending layer order (DESIGN.md C.8, default); 1 = overlapped
+   * with the backward: a segment starts once every stage group holding its
+   * layers has ended its last backward, segments in descending layer order,
+   * FIFO per group (DESIGN.md S.1; Table 1: DP sync is
+   * exposed in the backward pass). */
+  int32_t sync_overlap;
 } hsim_model_desc;
 
 /* Which candidates the t-th work item (t = 0..n-1) evaluates. */

@@ -87,6 +87,7 @@ struct hsim_handle {
   uint32_t pmask_all = 0;   // union of template depth masks (which depth kernels to launch)
   i64 layer_fb_max = 0, ext_max = 0, c_max = 0;  // bound of every 1F1B time (fp64-exact pipelines, < 2^52)
   int depth_max = 0;
+  int stages_max = 0;       // max over templates of the stages of all classes (S.1 scratch rows)
   int pcnt_max[FASTP + 1] = {0};  // max #classes of depth P in one template (job-list capacity)
   i64 N = 0;
   Tables hT{};  // host pointers (for hsim_decode)
@@ -503,6 +504,11 @@ void hsim_handle::enumerate() {
       for (auto& cl : classes) cnt[std::min<int>((int)cl.second.size(), 32)]++;
       for (int q = 0; q <= FASTP; ++q) pcnt_max[q] = std::max(pcnt_max[q], cnt[q]);
       pmask_all |= r.pmask;
+      {
+        int sp = 0;
+        for (int P : Ps) sp += P;
+        stages_max = std::max(stages_max, sp);
+      }
       const i64 R = radix_of(Ps);
       if (R >= ((i64)1 << 31)) fail(HSIM_ERANGE, "template radix exceeds 2^31");
       tpl.push_back(r);
@@ -590,8 +596,10 @@ void hsim_handle::prepare() {
   hT.seg_last_bytes = ((i64)md.vocab * h * (md.tied ? 0 : 1) + h) * md.bpe_grad;
   if (md.layers * hT.seg_layer_bytes + hT.seg_first_bytes + hT.seg_last_bytes >= TWO53)
     fail(HSIM_ERANGE, "gradient bytes reach 2^53");
-  // memory feasibility (DESIGN.md M.1)
+  // memory feasibility (DESIGN.md M.1); overlapped sync (DESIGN.md S.1)
   hT.mem_check = md.mem_check ? 1 : 0;
+  hT.sync_overlap = md.sync_overlap ? 1 : 0;
+  if (md.sync_overlap && md.layers > 32767) fail(HSIM_ERANGE, "sync_overlap needs layers < 2^15");
   {
     const i64 bst = (i64)md.bpe_act + md.bpe_grad + 12;  // weights + gradients + Adam fp32 master / m / v
     double worst = 0, bmax = 1;
@@ -1007,6 +1015,8 @@ cudaEvent_t plan_event(const hsim_handle* h) { return h->ev_plan; }
 cudaEvent_t pool_event(const hsim_handle* h, int q) { return h->ev_pool[q % hsim_handle::NEV]; }
 cudaEvent_t join_event(const hsim_handle* h, int q) { return h->ev_join[q % hsim_handle::NSIDE]; }
 int depth_jobs_max(const hsim_handle* h, int P) { return P >= 0 && P <= FASTP ? h->pcnt_max[P] : 0; }
+int stages_max(const hsim_handle* h) { return h->stages_max; }
+int sync_overlap(const hsim_handle* h) { return h->md.sync_overlap; }
 int ensure_block_scratch(hsim_handle* h, size_t entries, int64_t** out) {
   if (entries > h->blk_cap) {
     cudaFree(h->d_blk);

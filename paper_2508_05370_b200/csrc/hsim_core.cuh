@@ -130,7 +130,7 @@ struct Tables {
   // memory feasibility (DESIGN.md M.1), per lg = log2(tp): bytes of state per
   // layer / for the embedding / for the head on one device, and
   // K[lg] = s h (10 t + 24) (activation bytes per layer = ceil(b K / t))
-  int32_t mem_check, _pad6;
+  int32_t mem_check, sync_overlap;
   i64 mem_layer[4], mem_emb[4], mem_head[4], mem_K[4];
   i64 mem_cap[MAXT];
 };
@@ -598,8 +598,10 @@ __device__ unsigned long long g_diag[17][16];
 // T_pipe of every sub-class of a class (compile-time depth), max-reduced.
 struct PipeOut { i64 T0, cells; };
 
+// R (S.1, overlap mode only; else nullptr): R[s * rs] = max over sub-classes
+// of the end of stage s's last op (its last backward) in real time
 template <int P>
-HD PipeOut class_pipes_inl(const Tables& T, int32_t off, const ClassSplit& cs) {
+HD PipeOut class_pipes_inl(const Tables& T, int32_t off, const ClassSplit& cs, i64* R = nullptr, i64 rs = 0) {
   const CrecHdr* h = crec_hdr(T, off);
   const StageRec* st = crec_stages(T, off);
   Pipe<P> p;
@@ -619,6 +621,15 @@ HD PipeOut class_pipes_inl(const Tables& T, int32_t off, const ClassSplit& cs) {
     i64 sk;
     r.T0 = imax(r.T0, p.run(m, sk));
     r.cells += 2 * P * (m - sk);  // cells executed
+    if (R) {  // offset coordinates -> real ends: end_s = X_s + c_0 + ... + c_{s-1}
+      double o = 0;
+#pragma unroll
+      for (int s = 0; s < P; ++s) {
+        const i64 e = (i64)(p.X[s] + o);
+        R[s * rs] = u == 0 ? e : imax(R[s * rs], e);
+        if (s + 1 < P) o += 0.5 * p.c[s];
+      }
+    }
 #if defined(HSIM_DIAG) && defined(__CUDA_ARCH__)
     {  // histogram of executed steady pairs in units of P; bucket 7 = not detected
       const i64 kn = m >= P ? m - P : 0, ex = kn - sk;
@@ -633,9 +644,42 @@ HD PipeOut class_pipes_inl(const Tables& T, int32_t off, const ClassSplit& cs) {
 }
 
 // --- step a5: gradient sync (C.6, C.8) -----------------------------------------
-// Segments = common refinement of the classes' layer boundaries, in ascending
-// layer order, list-scheduled FIFO per (class, stage) group from T0: a
-// segment starts when every group it uses is free (all classes take part).
+// RS_j + AR_j of the segment [a, z) whose layers sit in stage sc[c] of every
+// class c: reshard (A14) over the TP rings of groups with tp != t*, then the
+// DP ring all-reduce over all replicas (class asc, replica asc, wrap), rings
+// through device base + q, q < t*.
+template <int C>
+HD i64 seg_cost_c(const Tables& T, const TplRec& tp, const StageRec* const (&st)[C], const int (&sc)[C], i64 a, i64 z) {
+  const i64 S = (z - a) * T.seg_layer_bytes + (a == 0 ? T.seg_first_bytes : 0) + (z == T.L ? T.seg_last_bytes : 0);
+  int tstar = 1 << 30, lg = 0;
+#pragma unroll
+  for (int c = 0; c < C; ++c) {
+    const int tpc = st[c][sc[c]].tp;
+    if (tpc < tstar) { tstar = tpc; lg = st[c][sc[c]].lg_tp; }
+  }
+  const i64 xs = (S + tstar - 1) >> lg;  // t* is a power of two
+  u64 rsmask = 0, mask = 0;
+#pragma unroll
+  for (int c = 0; c < C; ++c) {
+    const StageRec& s = st[c][sc[c]];
+    if (s.tp != tstar) rsmask |= s.tp_mask;  // reshard over this group's TP ring (A14)
+    mask |= s.dp_mask[lg];
+    // edge from the last replica of class c to the first replica of the next
+    // class (wrap: class C-1 -> class 0), ring q through device base + q
+    const StageRec& t = st[c + 1 < C ? c + 1 : 0][sc[c + 1 < C ? c + 1 : 0]];
+    const int n1 = s.last_node, n2 = t.first_node;
+    const int t1 = T.node_type[n1], t2 = T.node_type[n2];
+    mask |= n1 == n2 ? T.xmask_same[((t1 * MAXG + s.last_base) * MAXG + t.first_base) * 4 + lg]
+                     : T.xmask_cross[(((t1 * MAXG + s.last_base) * MAXT + t2) * MAXG + t.first_base) * 4 + lg];
+  }
+  const i64 RS = rsmask ? eval_mask(T, rsmask, xs) : 0;
+  const i64 AR = 2 * (i64)(tp.D - 1) * eval_mask(T, mask, ceil_div_rcp(xs, tp.D, tp.rD));
+  return RS + AR;
+}
+
+// C.8: segments = common refinement of the classes' layer boundaries, in
+// ascending layer order, list-scheduled FIFO per (class, stage) group from T0:
+// a segment starts when every group it uses is free (all classes take part).
 template <int C>
 HD i64 grad_sync_c(const Tables& T, const TplRec& tp, const ClassSplit (&cs)[C], i64 T0) {
   int sc[C], P[C];
@@ -658,34 +702,11 @@ HD i64 grad_sync_c(const Tables& T, const TplRec& tp, const ClassSplit (&cs)[C],
     i64 z = T.L;
 #pragma unroll
     for (int c = 0; c < C; ++c) z = imin(z, nextcut[c]);
-    const i64 S = (z - a) * T.seg_layer_bytes + (a == 0 ? T.seg_first_bytes : 0) + (z == T.L ? T.seg_last_bytes : 0);
-    int tstar = 1 << 30, lg = 0;
-#pragma unroll
-    for (int c = 0; c < C; ++c) {
-      const int tpc = st[c][sc[c]].tp;
-      if (tpc < tstar) { tstar = tpc; lg = st[c][sc[c]].lg_tp; }
-    }
-    const i64 xs = (S + tstar - 1) >> lg;  // t* is a power of two
-    u64 rsmask = 0, mask = 0;
-#pragma unroll
-    for (int c = 0; c < C; ++c) {
-      const StageRec& s = st[c][sc[c]];
-      if (s.tp != tstar) rsmask |= s.tp_mask;  // reshard over this group's TP ring (A14)
-      mask |= s.dp_mask[lg];
-      // edge from the last replica of class c to the first replica of the next
-      // class (wrap: class C-1 -> class 0), ring q through device base + q
-      const StageRec& t = st[c + 1 < C ? c + 1 : 0][sc[c + 1 < C ? c + 1 : 0]];
-      const int n1 = s.last_node, n2 = t.first_node;
-      const int t1 = T.node_type[n1], t2 = T.node_type[n2];
-      mask |= n1 == n2 ? T.xmask_same[((t1 * MAXG + s.last_base) * MAXG + t.first_base) * 4 + lg]
-                       : T.xmask_cross[(((t1 * MAXG + s.last_base) * MAXT + t2) * MAXG + t.first_base) * 4 + lg];
-    }
-    const i64 RS = rsmask ? eval_mask(T, rsmask, xs) : 0;
-    const i64 AR = 2 * (i64)(tp.D - 1) * eval_mask(T, mask, ceil_div_rcp(xs, tp.D, tp.rD));
+    const i64 cost = seg_cost_c<C>(T, tp, st, sc, a, z);
     i64 start = 0;
 #pragma unroll
     for (int c = 0; c < C; ++c) start = imax(start, cur_free[c]);
-    const i64 end = start + RS + AR;
+    const i64 end = start + cost;
     Titer = imax(Titer, end);
 #pragma unroll
     for (int c = 0; c < C; ++c) {  // advance classes whose stage ends at z
@@ -698,6 +719,59 @@ HD i64 grad_sync_c(const Tables& T, const TplRec& tp, const ClassSplit (&cs)[C],
       }
     }
     a = z;
+  }
+  return Titer;
+}
+
+// S.1: no barrier.  Segment j is ready when every group
+// holding its layers has ended its last backward -- R[coff_c + s] = max over
+// the class's replicas of that stage's end (written by the 1F1B kernels,
+// row stride rs) -- and segments are issued in descending layer order (the
+// order backward produces gradients), FIFO per group: a class entering a new
+// stage meets a group that has not synchronised yet.
+template <int C>
+HD i64 grad_sync_overlap_c(const Tables& T, const TplRec& tp, const ClassSplit (&cs)[C], const i64* R, i64 rs,
+                           i64 T0) {
+  int sc[C], coff[C];
+  int16_t start[C][MAXP];
+  i64 cur_free[C];
+  const StageRec* st[C];
+  int off = 0;
+#pragma unroll
+  for (int c = 0; c < C; ++c) {
+    const CrecHdr* h = crec_hdr(T, tp.crec[c]);
+    st[c] = crec_stages(T, tp.crec[c]);
+    LayerWalk lw = walk(T, h, cs[c].dig);
+    int a = 0;
+    for (int s = 0; s < h->P; ++s) {
+      start[c][s] = (int16_t)a;
+      a += lw.next(st[c]);
+    }
+    sc[c] = h->P - 1;
+    coff[c] = off;
+    off += h->P;
+    cur_free[c] = 0;
+  }
+  i64 z = T.L, Titer = T0;
+  while (z > 0) {
+    i64 a = 0, ready = 0, begin = 0;
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      a = imax(a, (i64)start[c][sc[c]]);
+      ready = imax(ready, R[(i64)(coff[c] + sc[c]) * rs]);
+      begin = imax(begin, cur_free[c]);
+    }
+    const i64 end = imax(begin, ready) + seg_cost_c<C>(T, tp, st, sc, a, z);
+    Titer = imax(Titer, end);
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      cur_free[c] = end;
+      if (a > 0 && start[c][sc[c]] == a) {
+        sc[c]--;
+        cur_free[c] = 0;
+      }
+    }
+    z = a;
   }
   return Titer;
 }

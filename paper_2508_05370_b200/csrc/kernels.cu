@@ -37,6 +37,8 @@ int ensure_work_scratch(hsim_handle* h, size_t entries, int64_t** out);
 int sm_count(const hsim_handle* h);
 uint32_t depth_mask(const hsim_handle* h);
 int depth_jobs_max(const hsim_handle* h, int P);
+int stages_max(const hsim_handle* h);
+int sync_overlap(const hsim_handle* h);
 cudaStream_t side_stream(const hsim_handle* h, int q);
 cudaEvent_t fork_event(const hsim_handle* h);
 cudaEvent_t join_event(const hsim_handle* h, int q);
@@ -132,6 +134,7 @@ struct Scratch {
   int32_t* rm;        // [ns] (last class)
   i64* Tc;            // [MAXC][ns] max T_pipe over the class's sub-classes
   i64* extra;         // [ns] gradient-sync time beyond T0 (C.8), by K_sync
+  i64* Rs;            // [spmax][ns] overlap mode (S.1): end of each stage's last backward; else nullptr
   int32_t* deep;      // [ns] slots with a class deeper than FASTP (compacted)
   int32_t* full[FASTP + 1];  // per depth: jobs (slot << 2 | class) of full chunks, 32-aligned groups
   int32_t* part[FASTP + 1];  // per depth: jobs of partial chunks, packed
@@ -147,6 +150,13 @@ __device__ __forceinline__ ClassSplit load_split(const Scratch& S, int c, int C,
   cs.add = S.add[c * S.ns + t];
   cs.rm = c == C - 1 ? S.rm[t] : 0;
   return cs;
+}
+
+// first stage of class c among the template's stages (row of S.Rs)
+__device__ __forceinline__ int class_stage_off(const Tables& T, const TplRec& tp, int c) {
+  int off = 0;
+  for (int q = 0; q < c; ++q) off += crec_hdr(T, tp.crec[q])->P;
+  return off;
 }
 
 __device__ void load_tables(Tables& sT, const Tables* __restrict__ gT) {
@@ -282,7 +292,8 @@ __global__ void __launch_bounds__(NT, P <= 4 ? HSIM_PIPE_MINB : 1) k_pipe(const 
     const int tau = S.tau[slot];
     if (tau < 0 || S.status[slot] != 0) continue;
     const TplRec& tp = sT.tpl[tau];
-    const PipeOut r = class_pipes_inl<P>(sT, tp.crec[c], load_split(S, c, tp.C, slot));
+    i64* R = S.Rs ? S.Rs + (i64)class_stage_off(sT, tp, c) * S.ns + slot : nullptr;
+    const PipeOut r = class_pipes_inl<P>(sT, tp.crec[c], load_split(S, c, tp.C, slot), R, S.ns);
     S.Tc[c * S.ns + slot] = r.T0;
 #ifdef HSIM_WARPCELLS  // diagnostic: count mode reports warp-slot cells (32 x warp max)
     cells += 32 * __reduce_max_sync(__activemask(), (unsigned)r.cells);
@@ -309,7 +320,7 @@ __device__ __forceinline__ void sym_max(double& a, double& sa, double b, double 
 
 // ---- K_deep: lane-per-stage wavefront for depth > FASTP --------------------------
 // Packs floor(32 / P) sub-classes (same class, same candidate) per pass.
-__device__ i64 warp_pipe_class(const Tables& T, int32_t off, const ClassSplit& cs, i64* cells) {
+__device__ i64 warp_pipe_class(const Tables& T, int32_t off, const ClassSplit& cs, i64* cells, i64* R, i64 rs) {
   const int lane = threadIdx.x & 31;
   const CrecHdr* h = crec_hdr(T, off);
   const StageRec* st = crec_stages(T, off);
@@ -437,6 +448,11 @@ __device__ i64 warp_pipe_class(const Tables& T, int32_t off, const ClassSplit& c
       const bool odd = lv & 1;
       lp.level(lv, lv >= lo && lv < hi, odd ? srcO : srcE, odd ? durO : durE, odd ? cO : cE, odd ? kO : kE);
     }
+    if (R) {  // S.1: end of each stage's last op, max over this pass's sub-classes
+      double e = act ? lp.X : 0.0;
+      for (int q = 1; q < nseg; ++q) e = dmax2(e, __shfl_sync(FULL, act ? lp.X : 0.0, (s + q * P) & 31));
+      if (seg == 0) R[s * rs] = base == 0 ? (i64)e : imax(R[s * rs], (i64)e);
+    }
     // T_pipe of each job sits on its stage-0 lane
     double v = act && s == 0 ? lp.X : 0.0;
     for (int o = 16; o > 0; o >>= 1) v = dmax2(v, __shfl_xor_sync(FULL, v, o));
@@ -448,7 +464,7 @@ __device__ i64 warp_pipe_class(const Tables& T, int32_t off, const ClassSplit& c
 // 32 < P <= 64: lane holds stages 2*lane and 2*lane+1 (generic levels only;
 // such pipelines are rare).  Stage 2l+1 reads its left input from the same
 // lane, stage 2l from lane-1's odd stage; B inputs mirror that.
-__device__ i64 warp_pipe_class2(const Tables& T, int32_t off, const ClassSplit& cs, i64* cells) {
+__device__ i64 warp_pipe_class2(const Tables& T, int32_t off, const ClassSplit& cs, i64* cells, i64* R, i64 rs) {
   const int lane = threadIdx.x & 31;
   const CrecHdr* h = crec_hdr(T, off);
   const StageRec* st = crec_stages(T, off);
@@ -502,6 +518,10 @@ __device__ i64 warp_pipe_class2(const Tables& T, int32_t off, const ClassSplit& 
         }
       }
     }
+    if (R) {  // S.1: end of each stage's last op, max over sub-classes
+      if (a0) R[s0 * rs] = u == 0 ? X0 : imax(R[s0 * rs], X0);
+      if (a1) R[s1 * rs] = u == 0 ? X1 : imax(R[s1 * rs], X1);
+    }
     best = imax(best, __shfl_sync(FULL, (long long)X0, 0));
   }
   return best;
@@ -527,7 +547,8 @@ __global__ void __launch_bounds__(NT) k_deep(const Tables* __restrict__ gT, Scra
       if (P <= FASTP) continue;
       const ClassSplit cs = load_split(S, c, tp.C, sj);
       i64 cl = 0;
-      const i64 T0 = P <= 32 ? warp_pipe_class(sT, off, cs, &cl) : warp_pipe_class2(sT, off, cs, &cl);
+      i64* R = S.Rs ? S.Rs + (i64)class_stage_off(sT, tp, c) * S.ns + sj : nullptr;
+      const i64 T0 = P <= 32 ? warp_pipe_class(sT, off, cs, &cl, R, S.ns) : warp_pipe_class2(sT, off, cs, &cl, R, S.ns);
       cells += cl;
       if (lane == 0) S.Tc[c * S.ns + sj] = T0;
     }
@@ -625,6 +646,41 @@ __global__ void __launch_bounds__(NT, HSIM_SYNC_MINB) k_sync(const Tables* __res
     if (tau < 0 || S.status[t] != 0) continue;
     const TplRec& tp = sT.tpl[tau];
     S.extra[t] = tp.D == 1 ? 0 : sync_any(sT, tp, S, t, 0);
+  }
+}
+
+// S.1 (overlap mode): after the 1F1B kernels; extra = T_iter - T0 with T_iter
+// from the overlapped schedule over the stages' last-backward ends (S.Rs)
+__device__ i64 sync_overlap_any(const Tables& T, const TplRec& tp, const Scratch& S, i64 t, i64 T0) {
+  const i64* R = S.Rs + t;
+  switch (tp.C) {
+    case 1: { ClassSplit cs[1] = {load_split(S, 0, 1, t)}; return grad_sync_overlap_c<1>(T, tp, cs, R, S.ns, T0); }
+    case 2: {
+      ClassSplit cs[2] = {load_split(S, 0, 2, t), load_split(S, 1, 2, t)};
+      return grad_sync_overlap_c<2>(T, tp, cs, R, S.ns, T0);
+    }
+    case 3: {
+      ClassSplit cs[3] = {load_split(S, 0, 3, t), load_split(S, 1, 3, t), load_split(S, 2, 3, t)};
+      return grad_sync_overlap_c<3>(T, tp, cs, R, S.ns, T0);
+    }
+    default: {
+      ClassSplit cs[4] = {load_split(S, 0, 4, t), load_split(S, 1, 4, t), load_split(S, 2, 4, t), load_split(S, 3, 4, t)};
+      return grad_sync_overlap_c<4>(T, tp, cs, R, S.ns, T0);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(NT) k_sync_overlap(const Tables* __restrict__ gT, Scratch S, i64 ns) {
+  __shared__ Tables sT;
+  load_tables(sT, gT);
+  for (i64 t = (i64)blockIdx.x * NT + threadIdx.x; t < ns; t += (i64)gridDim.x * NT) {
+    const int tau = S.tau[t];
+    if (tau < 0 || S.status[t] != 0) continue;
+    const TplRec& tp = sT.tpl[tau];
+    if (tp.D == 1) { S.extra[t] = 0; continue; }
+    i64 T0 = 0;
+    for (int q = 0; q < tp.C; ++q) T0 = imax(T0, S.Tc[q * S.ns + t]);
+    S.extra[t] = sync_overlap_any(sT, tp, S, t, T0) - T0;
   }
 }
 
@@ -1044,6 +1100,11 @@ static int run_phases(hsim_handle* h, const Tables* dT, Cands c, int64_t n, int6
   i64 cbatch = (nchunks + HSIM_NBATCH - 1) / HSIM_NBATCH;
   if (cbatch < 2048) cbatch = nchunks < 2048 ? nchunks : 2048;
   if (cbatch > CBMAX) cbatch = CBMAX;
+  // S.1 overlap mode: per-stage last-backward ends, stages_max rows of ns
+  // int64 per buffer, kept under ~256 MiB
+  const bool overlap = sync_overlap(h) && !count;
+  const i64 spmax = overlap ? stages_max(h) : 0;
+  if (overlap && cbatch * 32 * spmax * 8 > ((i64)1 << 28)) cbatch = imax(1, ((i64)1 << 28) / (32 * 8 * spmax));
   const i64 ns = cbatch * 32;
   const int NBUF = count ? 1 : 2;
   // scratch per buffer (int64 words): tpos, Tc [MAXC], extra | counters | int32: tau,
@@ -1056,7 +1117,8 @@ static int run_phases(hsim_handle* h, const Tables* dT, Cands c, int64_t n, int6
   }
   const size_t planw = c.idx ? 0 : (size_t)(2 * c.nr + 1);
   const size_t n32 = (size_t)(4 + 4 * MAXC) * ns + jobw;
-  const size_t bufw = (size_t)(MAXC + 2) * ns + NCNT + (n32 + 1) / 2 + 8;
+  const size_t bufw0 = (size_t)(MAXC + 2) * ns + NCNT + (n32 + 1) / 2 + 8;
+  const size_t bufw = bufw0 + (size_t)spmax * ns;
   i64* base = nullptr;
   if (ensure_work_scratch(h, NBUF * bufw + planw + 8, &base)) return HSIM_ENOMEM;
   Scratch SB[2];
@@ -1067,6 +1129,7 @@ static int run_phases(hsim_handle* h, const Tables* dT, Cands c, int64_t n, int6
     S.tpos = b0;
     S.Tc = b0 + ns;
     S.extra = b0 + (MAXC + 1) * ns;
+    S.Rs = overlap ? b0 + bufw0 : nullptr;
     S.counters = (unsigned long long*)(b0 + (MAXC + 2) * ns);
     int32_t* p32 = (int32_t*)(b0 + (MAXC + 2) * ns + NCNT);
     S.tau = p32;
@@ -1157,7 +1220,12 @@ static int run_phases(hsim_handle* h, const Tables* dT, Cands c, int64_t n, int6
       cells += (i64)v;
       continue;
     }
-    {
+    if (overlap) {  // S.1: needs the stages' last-backward ends -> after the 1F1B kernels
+      tq = g_trace.pre("k_sync_overlap", NSTREAM_FINAL, fin);
+      k_sync_overlap<<<gy, NT, 0, fin>>>(dT, S, nsb);
+      g_trace.post(tq, fin);
+      ++launches;
+    } else {
       cudaStream_t ss = side(18);
       tq = g_trace.pre("k_sync", 18, ss);
       k_sync<<<gy, NT, 0, ss>>>(dT, S, nsb);

@@ -66,7 +66,7 @@ class hsim_model_desc(C.Structure):
                 ("n_pset", C.c_int32), ("pset", C.c_int32 * 16),
                 ("homo", C.c_int32), ("mixed", C.c_int32), ("use_all", C.c_int32),
                 ("r_layer", C.c_int32), ("pmax_perturb", C.c_int32), ("r_batch", C.c_int32),
-                ("mem_check", C.c_int32), ("_pad_mc", C.c_int32)]
+                ("mem_check", C.c_int32), ("sync_overlap", C.c_int32)]
 
 
 class hsim_cands(C.Structure):
@@ -163,6 +163,7 @@ def descriptors(cfg):
     for k in ("homo", "mixed", "use_all", "r_layer", "pmax_perturb", "r_batch"):
         setattr(m, k, se[k])
     m.mem_check = int(se.get("mem_check", 0))
+    m.sync_overlap = int(se.get("sync_overlap", 0))
     return cd, m, (types, nodes)
 
 
