@@ -749,8 +749,18 @@ void hsim_handle::upload() {
   ck(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming), "cudaEventCreate");
   ck(cudaEventCreateWithFlags(&ev_plan, cudaEventDisableTiming), "cudaEventCreate");
   for (int q = 0; q < NEV; ++q) ck(cudaEventCreateWithFlags(&ev_pool[q], cudaEventDisableTiming), "cudaEventCreate");
+  // latency-bound phase kernels (deep 1F1B chains: K_pipe<P >= 9> on streams
+  // 9..16, K_deep on 17) get the highest stream priority so their few
+  // long-running blocks are resident before the throughput kernels fill the SMs
+  int prio_lo = 0, prio_hi = 0;
+  cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
   for (int q = 0; q < NSIDE; ++q) {
-    ck(cudaStreamCreateWithFlags(&side[q], cudaStreamNonBlocking), "cudaStreamCreate");
+#ifndef HSIM_NOPRIO
+    const int prio = (q >= 9 && q <= 17) ? prio_hi : prio_lo;
+#else
+    const int prio = prio_lo;
+#endif
+    ck(cudaStreamCreateWithPriority(&side[q], cudaStreamNonBlocking, prio), "cudaStreamCreate");
     ck(cudaEventCreateWithFlags(&ev_join[q], cudaEventDisableTiming), "cudaEventCreate");
   }
 }

@@ -21,6 +21,9 @@
 #define HD inline
 #define HDN static
 #endif
+#ifndef HSIM_WHOLE_MAXP
+#define HSIM_WHOLE_MAXP 12  // deepest register-resident pipeline with the cyclic c | BL check
+#endif
 #ifndef HSIM_AFFINE_MAXP
 #define HSIM_AFFINE_MAXP 8  // deepest register-resident pipeline with the affine-regime jump
 #endif
@@ -564,11 +567,11 @@ struct Pipe {
 #pragma unroll 1
         for (int lv = 0; lv < 2 * P - 1; ++lv) level_rt(lv, m);
       }
-      // steady pairs: a first block of 4, then blocks of 12 (P <= 8) or 4;
-      // after each, the affine check (P <= HSIM_AFFINE_MAXP; else only the
-      // uniform-increment case) and, for P <= 8, the cyclic c | BL check
-      // (deeper pipelines: the extra snapshots would not fit the registers)
-      constexpr bool EXT = P <= 8, AFF = P <= HSIM_AFFINE_MAXP;
+      // steady pairs: a first block of 4, then blocks of 12 (P <= HSIM_WHOLE_MAXP)
+      // or 4; after each, the affine check (P <= HSIM_AFFINE_MAXP; else only
+      // the uniform-increment case) and, for P <= HSIM_WHOLE_MAXP, the cyclic
+      // c | BL check (deeper pipelines: the snapshot would not fit the registers)
+      constexpr bool EXT = P <= HSIM_WHOLE_MAXP, AFF = P <= HSIM_AFFINE_MAXP;
       constexpr int BLK = EXT ? 12 : 4;
       const int kn = (int)(m - P);
       int k = 0;

@@ -7,6 +7,10 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2508_05370_b200 import build as B  # noqa: E402
 
 VARIANTS = {
+    "noprio": ["-DHSIM_NOPRIO"],
+    "deepfirst": ["-DHSIM_DEEPFIRST"],
+    "w8": ["-DHSIM_WHOLE_MAXP=8"],
+    "w16": ["-DHSIM_WHOLE_MAXP=16"],
     "fm4": ["-DHSIM_FINAL_MULT=4"],
     "fm2": ["-DHSIM_FINAL_MULT=2"],
     "aff11": ["-DHSIM_AFFINE_MAXP=11"],
