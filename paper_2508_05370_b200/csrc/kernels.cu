@@ -440,9 +440,45 @@ __device__ i64 warp_pipe_class(const Tables& T, int32_t off, const ClassSplit& c
       if (act && s == 0) *cells -= 2 * P * r;
       return true;
     };
-    if (lv + 7 < hiMin && !blk(4))
-      while (lv + 23 < hiMin && !blk(12)) {
+    // lag scan: record X after each of HL pairs (one register per lag per
+    // lane), then take the smallest lag c <= HL - 1 over which every active
+    // stage moved by its segment's same d (cyclicity c, e.g. c = 7 for seven
+    // identical consecutive stages, which c | 4 / c | 12 miss) and jump
+    constexpr int HL = 16;
+    auto lagscan = [&]() {
+      double hx[HL];
+#pragma unroll
+      for (int b = 0; b < HL; ++b) {
+        pair();
+        hx[b] = lp.X;
       }
+      lv += 2 * HL;
+#ifdef HSIM_NOSKIP
+      return false;
+#endif
+      const i64 left = (hiMin - lv) >> 1;
+#pragma unroll
+      for (int cc = 1; cc < HL; ++cc) {
+        const double dd = hx[HL - 1] - hx[HL - 1 - cc], d0 = __shfl_sync(FULL, dd, lead);
+        if (__all_sync(FULL, !act || dd == d0)) {
+          const i64 q = left / cc;
+          const double rd = (double)q * d0;
+          lp.X += rd;
+          lp.out += rd;
+          lv += 2 * q * cc;
+          if (act && s == 0) *cells -= 2 * P * q * cc;
+          return true;
+        }
+      }
+      return false;
+    };
+    if (lv + 7 < hiMin && !blk(4)) {
+      bool done = false;
+      while (!done && lv + 23 < hiMin) {
+        done = blk(12);
+        if (!done && lv + 2 * HL - 1 < hiMin) done = lagscan();
+      }
+    }
     for (; lv + 1 < hiMin; lv += 2) pair();
     for (; lv < totMax; ++lv) {
       const bool odd = lv & 1;
