@@ -641,6 +641,8 @@ void hsim_handle::prepare() {
           hT.lc_G[b] = (i64)v;
           hT.lc_k[b] = (int8_t)k;
           hT.lc_rG[b] = 1.0 / v;
+          hT.lc_Gd[b] = v;
+          hT.lc_pw[b] = std::ldexp(1.0, k);
           found = true;
         }
       }

@@ -122,6 +122,8 @@ struct Tables {
   // ceil_div(x << k, G), computed from a reciprocal estimate + exact fix-up
   i64 lc_G[MAXLC];
   double lc_rG[MAXLC];     // 1.0 / G (floor estimate, then exact integer fix-up)
+  double lc_Gd[MAXLC];     // G as a double
+  double lc_pw[MAXLC];     // 2^k as a double
   u64 lc_up[MAXLC];       // classes after this one (ids sorted by beta asc, alpha desc) with a larger alpha
   int8_t lc_k[MAXLC], _pad4[MAXLC];
   int32_t lc_exact, _pad3;
@@ -152,16 +154,38 @@ HD i64 imin(i64 a, i64 b) { return a < b ? a : b; }
 
 // ceil(n / d) for 0 <= n < 2^52, 1 <= d < 2^31: floor estimate in fp64 from the
 // reciprocal (|error| < 1), then an exact integer fix-up of the remainder
+#ifdef __CUDA_ARCH__
+// Device form, all in fp64: n < 2^52 and d < 2^31 are exact doubles, the
+// truncated estimate q is within 1 of n / d, and the remainder n - q d is an
+// integer below 2^33 in magnitude, so one explicit FMA computes it exactly
+// (an exact integer result -- no contraction of a rounded expression).
+__device__ __forceinline__ i64 ceil_div_rcp_d(double n, double d, double rd) {
+  double q = trunc(n * rd);
+  double r = fma(-q, d, n);
+  if (r < 0.0) { q -= 1.0; r += d; }
+  if (r >= d) { q += 1.0; r -= d; }
+  return (i64)q + (r != 0.0 ? 1 : 0);
+}
+#endif
 HD i64 ceil_div_rcp(i64 n, i64 d, double rd) {
+#ifdef __CUDA_ARCH__
+  return ceil_div_rcp_d((double)n, (double)d, rd);
+#else
   i64 q = (i64)((double)n * rd);
   i64 r = n - q * d;
   if (r < 0) { q -= 1; r += d; }
   if (r >= d) { q += 1; r -= d; }
   return q + (r != 0 ? 1 : 0);
+#endif
 }
 // alpha_e + ceil(x / beta_e) of link class b (C.6 tau_e)
 HD i64 tau_lc(const Tables& T, int b, i64 x) {
+#ifdef __CUDA_ARCH__
+  // x << k as an exact power-of-two scaling in fp64 (x << k < 2^52)
+  if (T.lc_exact) return T.lc[b].alpha + ceil_div_rcp_d((double)x * T.lc_pw[b], T.lc_Gd[b], T.lc_rG[b]);
+#else
   if (T.lc_exact) return T.lc[b].alpha + ceil_div_rcp(x << T.lc_k[b], T.lc_G[b], T.lc_rG[b]);
+#endif
   return T.lc[b].alpha + ceilq(x, T.lc[b].beta);
 }
 
@@ -671,7 +695,7 @@ HD i64 seg_cost_c(const Tables& T, const TplRec& tp, const StageRec* const (&st)
     // class (wrap: class C-1 -> class 0), ring q through device base + q
     const StageRec& t = st[c + 1 < C ? c + 1 : 0][sc[c + 1 < C ? c + 1 : 0]];
     const int n1 = s.last_node, n2 = t.first_node;
-    const int t1 = T.node_type[n1], t2 = T.node_type[n2];
+    const int t1 = s.type, t2 = t.type;  // a node's type is its devices' type (C.1)
     mask |= n1 == n2 ? T.xmask_same[((t1 * MAXG + s.last_base) * MAXG + t.first_base) * 4 + lg]
                      : T.xmask_cross[(((t1 * MAXG + s.last_base) * MAXT + t2) * MAXG + t.first_base) * 4 + lg];
   }
