@@ -172,6 +172,24 @@ __device__ __forceinline__ i64 warp_sum(i64 v) {
   return v;
 }
 
+// steps a0 + a1 for a C-class template; stores the compact split of each class
+template <int C>
+__device__ __forceinline__ int split_store(const Tables& T, const TplRec& tp, i64 local, const Scratch& S, i64 slot) {
+  ClassSplit cs[C];
+  const int st = partition_c<C>(T, tp, local, cs);
+  if (st == 0) {
+#pragma unroll
+    for (int k = 0; k < C; ++k) {
+      S.dig[k * S.ns + slot] = cs[k].dig;
+      S.q[k * S.ns + slot] = (int32_t)cs[k].q;
+      S.seats[k * S.ns + slot] = (int32_t)cs[k].seats;
+      S.add[k * S.ns + slot] = (int32_t)cs[k].add;
+    }
+    S.rm[slot] = (int32_t)cs[C - 1].rm;
+  }
+  return st;
+}
+
 // ---- K_split -------------------------------------------------------------------
 __global__ void __launch_bounds__(NT, 6) k_split(const Tables* __restrict__ gT, Cands c, i64 ca, i64 cb, Scratch S,
                                               uint32_t pm_all) {
@@ -212,19 +230,15 @@ __global__ void __launch_bounds__(NT, 6) k_split(const Tables* __restrict__ gT, 
     uint32_t mypm = 0;
     if (tau >= 0) {
       const TplRec& tp = sT.tpl[tau];
-      ClassSplit cs[MAXC];
-      st = partition_any(sT, tp, i - tp.prefix, cs);
-      S.status[slot] = st;
-      if (st == 0) {
-        for (int k = 0; k < tp.C; ++k) {
-          S.dig[k * S.ns + slot] = cs[k].dig;
-          S.q[k * S.ns + slot] = (int32_t)cs[k].q;
-          S.seats[k * S.ns + slot] = (int32_t)cs[k].seats;
-          S.add[k * S.ns + slot] = (int32_t)cs[k].add;
-        }
-        S.rm[slot] = (int32_t)cs[tp.C - 1].rm;
-        mypm = tp.pmask;
+      // class count specialised: the per-class split stays in registers
+      switch (tp.C) {
+        case 1: st = split_store<1>(sT, tp, i - tp.prefix, S, slot); break;
+        case 2: st = split_store<2>(sT, tp, i - tp.prefix, S, slot); break;
+        case 3: st = split_store<3>(sT, tp, i - tp.prefix, S, slot); break;
+        default: st = split_store<4>(sT, tp, i - tp.prefix, S, slot); break;
       }
+      S.status[slot] = st;
+      if (st == 0) mypm = tp.pmask;
     }
     // deep candidates: compacted, warp-aggregated
     const bool deep = (mypm >> (FASTP + 1)) != 0;

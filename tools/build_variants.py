@@ -7,6 +7,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2508_05370_b200 import build as B  # noqa: E402
 
 VARIANTS = {
+    "s4": ["-DHSIM_SYNC_MINB=4"],
+    "s5": ["-DHSIM_SYNC_MINB=5"],
     "noprio": ["-DHSIM_NOPRIO"],
     "deepfirst": ["-DHSIM_DEEPFIRST"],
     "w8": ["-DHSIM_WHOLE_MAXP=8"],
