@@ -749,20 +749,29 @@ struct RegTopK {
 
 // T of one slot (K_final)
 __device__ __forceinline__ i64 final_T(const Tables& sT, const Cands& c, const Scratch& S, i64 slot, i64* t_out, i64* i_out) {
+  // every scratch word of the slot is loaded up front (independent loads, one
+  // memory latency instead of a chain); rows / words that do not apply to the
+  // slot (empty slot, invalid split, classes >= C) are read but ignored
+  const i64 t = __ldcs(&S.tpos[slot]);
+  const int tau = __ldcs(&S.tau[slot]);
+  const int st = __ldcs(&S.status[slot]);
+  const i64 ex = __ldcs(&S.extra[slot]);
+  i64 tc[MAXC];
+#pragma unroll
+  for (int q = 0; q < MAXC; ++q) tc[q] = __ldcs(&S.Tc[q * S.ns + slot]);
   i64 T = INT64_MIN, i = -1;
-  const i64 t = S.tpos[slot];
   if (t >= 0) {
     i = cand_index(c, t);
-    const int tau = S.tau[slot];
     if (tau >= 0) {
-      const int st = S.status[slot];
       if (st) {
         T = st;
       } else {
         const int C = sT.tpl[tau].C;
         i64 T0 = 0;
-        for (int q = 0; q < C; ++q) T0 = imax(T0, S.Tc[q * S.ns + slot]);
-        T = T0 + S.extra[slot];
+#pragma unroll
+        for (int q = 0; q < MAXC; ++q)
+          if (q < C) T0 = imax(T0, tc[q]);
+        T = T0 + ex;
       }
     }
   }
