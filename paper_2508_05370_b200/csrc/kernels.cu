@@ -277,7 +277,7 @@ __global__ void __launch_bounds__(NT, 6) k_split(const Tables* __restrict__ gT, 
 
 // ---- K_pipe<P> -------------------------------------------------------------------
 #ifndef HSIM_NBATCH
-#define HSIM_NBATCH 2  // target number of pipelined batches per call
+#define HSIM_NBATCH 1  // target number of batches per call (more only when the scratch cap forces it; measured: 1 beats 2 and 3 on config 2 once the deep tails were fixed)
 #endif
 #ifndef HSIM_PIPE_MINB
 #define HSIM_PIPE_MINB 8

@@ -7,6 +7,11 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2508_05370_b200 import build as B  # noqa: E402
 
 VARIANTS = {
+    "pm6": ["-DHSIM_PIPE_MINB=6"],
+    "pm7": ["-DHSIM_PIPE_MINB=7"],
+    "nb3": ["-DHSIM_NBATCH=3"],
+    "nb1": ["-DHSIM_NBATCH=1"],
+    "s7": ["-DHSIM_SYNC_MINB=7"],
     "s4": ["-DHSIM_SYNC_MINB=4"],
     "s5": ["-DHSIM_SYNC_MINB=5"],
     "noprio": ["-DHSIM_NOPRIO"],
