@@ -599,9 +599,21 @@ struct Pipe {
       constexpr int BLK = EXT ? 12 : 4;
       const int kn = (int)(m - P);
       int k = 0;
-      if (kn >= 4 && !block<4, EXT, AFF>(k, kn, skipped))
-        while (k + BLK <= kn && !block<BLK, EXT, AFF>(k, kn, skipped)) {
+      // with the cyclic check (P >= 5), block lengths cycle 12, 28, 20 so that
+      // c | 12, c | 28 (c = 7: seven identical consecutive stages) and c | 20
+      // (c = 5) are all caught within about one cycle after the transient
+      if (kn >= 4 && !block<4, EXT, AFF>(k, kn, skipped)) {
+        if (EXT && P >= 5) {
+          for (;;) {
+            if (k + 12 > kn || block<12, EXT, AFF>(k, kn, skipped)) break;
+            if (k + 28 > kn || block<28, EXT, AFF>(k, kn, skipped)) break;
+            if (k + 20 > kn || block<20, EXT, AFF>(k, kn, skipped)) break;
+          }
+        } else {
+          while (k + BLK <= kn && !block<BLK, EXT, AFF>(k, kn, skipped)) {
+          }
         }
+      }
       for (; k < kn; ++k) steady_pair();
       steady_level<1>();  // level 2m-1
       if (P <= HSIM_UNROLL_MAXP) {

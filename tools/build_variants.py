@@ -7,6 +7,10 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2508_05370_b200 import build as B  # noqa: E402
 
 VARIANTS = {
+    "s4": ["-DHSIM_SYNC_MINB=4"],
+    "s5": ["-DHSIM_SYNC_MINB=5"],
+    "s3": ["-DHSIM_SYNC_MINB=3"],
+    "w16": ["-DHSIM_WHOLE_MAXP=16"],
     "pm6": ["-DHSIM_PIPE_MINB=6"],
     "pm7": ["-DHSIM_PIPE_MINB=7"],
     "nb3": ["-DHSIM_NBATCH=3"],
