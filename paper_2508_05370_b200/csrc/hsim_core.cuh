@@ -22,7 +22,7 @@
 #define HDN static
 #endif
 #ifndef HSIM_WHOLE_MAXP
-#define HSIM_WHOLE_MAXP 12  // deepest register-resident pipeline with the cyclic c | BL check
+#define HSIM_WHOLE_MAXP 16  // deepest register-resident pipeline with the cyclic c | BL check
 #endif
 #ifndef HSIM_AFFINE_MAXP
 #define HSIM_AFFINE_MAXP 8  // deepest register-resident pipeline with the affine-regime jump
@@ -599,13 +599,14 @@ struct Pipe {
       constexpr int BLK = EXT ? 12 : 4;
       const int kn = (int)(m - P);
       int k = 0;
-      // with the cyclic check (P >= 5), block lengths cycle 12, 28, 20 so that
-      // c | 12, c | 28 (c = 7: seven identical consecutive stages) and c | 20
-      // (c = 5) are all caught within about one cycle after the transient
+      // with the cyclic check (P >= 5), block lengths cycle 24, 28, 20 so that
+      // c | 24 (c = 8: two runs of eight identical stages), c | 28 (c = 7:
+      // seven identical consecutive stages) and c | 20 (c = 5) are all caught
+      // within about one cycle after the transient
       if (kn >= 4 && !block<4, EXT, AFF>(k, kn, skipped)) {
         if (EXT && P >= 5) {
           for (;;) {
-            if (k + 12 > kn || block<12, EXT, AFF>(k, kn, skipped)) break;
+            if (k + 24 > kn || block<24, EXT, AFF>(k, kn, skipped)) break;
             if (k + 28 > kn || block<28, EXT, AFF>(k, kn, skipped)) break;
             if (k + 20 > kn || block<20, EXT, AFF>(k, kn, skipped)) break;
           }
