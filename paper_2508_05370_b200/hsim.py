@@ -240,6 +240,36 @@ class Sim:
             _err(rc)
         return out
 
+    def eval_host(self, idx_host, out_host, chunks=2, stream=None):
+        """End-to-end evaluation of an index list in pinned host memory into a
+        pinned host result buffer (the same hsim_eval_batch calls, chunked):
+        the H2D copy of chunk c+1 and the D2H copy of chunk c-1 overlap the
+        evaluation of chunk c (two copy streams + events).  On return the
+        caller's stream has every copy queued before its next work."""
+        import torch
+        n = idx_host.numel()
+        assert idx_host.dtype == torch.int64 and out_host.dtype == torch.int64 and out_host.numel() >= n
+        comp = stream or torch.cuda.current_stream()
+        if getattr(self, "_host_buf", None) is None or self._host_buf[0].numel() < n:
+            self._host_buf = (torch.empty(n, dtype=torch.int64, device="cuda"),
+                              torch.empty(n, dtype=torch.int64, device="cuda"),
+                              torch.cuda.Stream(), torch.cuda.Stream())
+        idx_dev, out_dev, s_in, s_out = self._host_buf
+        s_in.wait_stream(comp)   # buffers free: earlier work on the caller's stream is done
+        s_out.wait_stream(comp)
+        step = max(1, -(-n // max(1, chunks)))
+        for c0 in range(0, n, step):
+            c1 = min(n, c0 + step)
+            with torch.cuda.stream(s_in):
+                idx_dev[c0:c1].copy_(idx_host[c0:c1], non_blocking=True)
+            comp.wait_stream(s_in)
+            self.eval_batch(idx=idx_dev[c0:c1], out=out_dev[c0:c1], stream=comp)
+            s_out.wait_stream(comp)
+            with torch.cuda.stream(s_out):
+                out_host[c0:c1].copy_(out_dev[c0:c1], non_blocking=True)
+        comp.wait_stream(s_out)
+        return out_host
+
     def topk(self, k, n=None, first=0, idx=None, block=0, stride=0, out_ns=None, stream=None, out=None):
         """Top-k (time asc, index asc) over the candidates; returns device tensors (t_ns, idx)."""
         import torch

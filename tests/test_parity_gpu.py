@@ -155,3 +155,16 @@ def test_config2_exhaustive(torch_cuda, oracle_mod):
     got = sim.eval_batch(n=N).cpu().numpy()
     want = o.eval_many(first=0, n=N, threads=THREADS)
     assert_equal(np.arange(N), got, want)
+
+
+def test_eval_host_chunked_overlap(torch_cuda, oracle_mod):
+    """Sim.eval_host (pinned host in/out, chunked H2D / eval / D2H overlap) gives
+    the oracle's values for a shuffled index list with a ragged last chunk."""
+    torch = torch_cuda
+    sim, o = pair(oracle_mod, 2)
+    idx = H.sample_indices(o.space_size(), 20011, seed=H.PARITY_SEED + 77)
+    idx_host = torch.as_tensor(idx).pin_memory()
+    out_host = torch.empty(len(idx), dtype=torch.int64).pin_memory()
+    sim.eval_host(idx_host, out_host, chunks=7)
+    torch.cuda.synchronize()
+    assert_equal(idx, out_host.numpy(), o.eval_many(idx, threads=THREADS))
