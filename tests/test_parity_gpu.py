@@ -168,3 +168,32 @@ def test_eval_host_chunked_overlap(torch_cuda, oracle_mod):
     sim.eval_host(idx_host, out_host, chunks=7)
     torch.cuda.synchronize()
     assert_equal(idx, out_host.numpy(), o.eval_many(idx, threads=THREADS))
+
+
+def test_full_sweep_topk_config2_equals_oracle_brute_force(torch_cuda, oracle_mod):
+    """The bench's launch configuration (hsim_topk over the whole config-2 space,
+    range mode, one call) against the oracle's brute-force top-16 over all
+    873 192 candidates (about 10 s of host cores)."""
+    sim, o = pair(oracle_mod, 2)
+    t, i = sim.topk(16)
+    wt, wi = o.topk(16, threads=THREADS)
+    assert np.array_equal(t.cpu().numpy(), wt) and np.array_equal(i.cpu().numpy(), wi)
+
+
+@pytest.mark.parametrize("n", [3, 4, 5])
+def test_full_sweep_topk_properties(torch_cuda, oracle_mod, n):
+    """Full-space sweeps of configs 3-5 (6.2e7 / 1.1e7 / 1.2e9 candidates, the
+    bench's launch configuration): every reported entry is exact (oracle
+    re-evaluation), the list is sorted by (T, i), and no seeded sample of the
+    space beats the k-th entry unless it is in the list."""
+    sim, o = pair(oracle_mod, n)
+    k = 16
+    t, i = sim.topk(k)
+    t, i = t.cpu().numpy(), i.cpu().numpy()
+    assert np.array_equal(o.eval_many(i, threads=THREADS), t)
+    assert all((t[j], i[j]) < (t[j + 1], i[j + 1]) for j in range(k - 1))
+    idx = H.sample_indices(o.space_size(), 3000, seed=H.PARITY_SEED + 90 + n)
+    v = o.eval_many(idx, threads=THREADS)
+    ok = v >= 0
+    beat = ok & ((v < t[-1]) | ((v == t[-1]) & (idx < i[-1])))
+    assert set(idx[beat].tolist()) <= set(i.tolist())
