@@ -641,8 +641,7 @@ void hsim_handle::prepare() {
           hT.lc_G[b] = (i64)v;
           hT.lc_k[b] = (int8_t)k;
           hT.lc_rG[b] = 1.0 / v;
-          hT.lc_Gd[b] = v;
-          hT.lc_pw[b] = std::ldexp(1.0, k);
+          hT.lc_rb[b] = 1.0 / lcs[b].beta;
           found = true;
         }
       }

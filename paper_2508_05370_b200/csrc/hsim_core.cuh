@@ -122,8 +122,7 @@ struct Tables {
   // ceil_div(x << k, G), computed from a reciprocal estimate + exact fix-up
   i64 lc_G[MAXLC];
   double lc_rG[MAXLC];     // 1.0 / G (floor estimate, then exact integer fix-up)
-  double lc_Gd[MAXLC];     // G as a double
-  double lc_pw[MAXLC];     // 2^k as a double
+  double lc_rb[MAXLC];     // RN(1 / beta) (device ceil division by beta = G / 2^k)
   u64 lc_up[MAXLC];       // classes after this one (ids sorted by beta asc, alpha desc) with a larger alpha
   int8_t lc_k[MAXLC], _pad4[MAXLC];
   int32_t lc_exact, _pad3;
@@ -181,8 +180,10 @@ HD i64 ceil_div_rcp(i64 n, i64 d, double rd) {
 // alpha_e + ceil(x / beta_e) of link class b (C.6 tau_e)
 HD i64 tau_lc(const Tables& T, int b, i64 x) {
 #ifdef __CUDA_ARCH__
-  // x << k as an exact power-of-two scaling in fp64 (x << k < 2^52)
-  if (T.lc_exact) return T.lc[b].alpha + ceil_div_rcp_d((double)x * T.lc_pw[b], T.lc_Gd[b], T.lc_rG[b]);
+  // ceil(x / beta) with beta = G / 2^k itself: x / beta = (x << k) / G < 2^52
+  // keeps the truncated estimate within 1, and x - q beta = (x 2^k - q G) / 2^k
+  // has under 33 significant bits, so the FMA remainder is exact
+  if (T.lc_exact) return T.lc[b].alpha + ceil_div_rcp_d((double)x, T.lc[b].beta, T.lc_rb[b]);
 #else
   if (T.lc_exact) return T.lc[b].alpha + ceil_div_rcp(x << T.lc_k[b], T.lc_G[b], T.lc_rG[b]);
 #endif
