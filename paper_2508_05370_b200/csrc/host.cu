@@ -89,6 +89,7 @@ struct hsim_handle {
   int depth_max = 0;
   int stages_max = 0;       // max over templates of the stages of all classes (S.1 scratch rows)
   int pcnt_max[FASTP + 1] = {0};  // max #classes of depth P in one template (job-list capacity)
+  i64 depth_jobs_space[FASTP + 1] = {0};  // class-jobs of depth P over the whole space
   i64 N = 0;
   Tables hT{};  // host pointers (for hsim_decode)
   // device
@@ -503,6 +504,8 @@ void hsim_handle::enumerate() {
       int cnt[33] = {0};
       for (auto& cl : classes) cnt[std::min<int>((int)cl.second.size(), 32)]++;
       for (int q = 0; q <= FASTP; ++q) pcnt_max[q] = std::max(pcnt_max[q], cnt[q]);
+      const i64 Rt = radix_of(Ps);
+      for (int q = 0; q <= FASTP; ++q) depth_jobs_space[q] += Rt * cnt[q];
       pmask_all |= r.pmask;
       {
         int sp = 0;
@@ -1026,6 +1029,7 @@ cudaEvent_t plan_event(const hsim_handle* h) { return h->ev_plan; }
 cudaEvent_t pool_event(const hsim_handle* h, int q) { return h->ev_pool[q % hsim_handle::NEV]; }
 cudaEvent_t join_event(const hsim_handle* h, int q) { return h->ev_join[q % hsim_handle::NSIDE]; }
 int depth_jobs_max(const hsim_handle* h, int P) { return P >= 0 && P <= FASTP ? h->pcnt_max[P] : 0; }
+int64_t depth_jobs_space(const hsim_handle* h, int P) { return P >= 0 && P <= FASTP ? h->depth_jobs_space[P] : 0; }
 int stages_max(const hsim_handle* h) { return h->stages_max; }
 int sync_overlap(const hsim_handle* h) { return h->md.sync_overlap; }
 int ensure_block_scratch(hsim_handle* h, size_t entries, int64_t** out) {

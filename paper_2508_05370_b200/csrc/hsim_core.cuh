@@ -395,6 +395,20 @@ HD i64 level_B(int P, int s, i64 j) { return 2 * P - 1 - s + 2 * j; }
 // m >= P: warm-up levels [0, 2P-1) and cool-down levels [2m, 2m+2P-2) have a
 // fixed op pattern (unrolled, no bookkeeping); the steady levels [2P-1, 2m)
 // alternate F (s = level mod 2) / B.  m < P: closed-form levels at run time.
+// Lane compaction: a register-resident lane whose pipeline has
+// not settled after the first block re-queues its (slot, sub-class, class) to
+// a dense list of its depth and moves on; K_pipe_cont<P> re-runs those jobs 32
+// per warp, so a warp's easy jobs no longer wait for its one hard job.
+#ifndef HSIM_DEFER_MIN
+#define HSIM_DEFER_MIN 16  // re-queue only with at least this many steady pairs left
+#endif
+struct DeferCtx {
+  i64* list;                   // items slot << 16 | u << 4 | class
+  unsigned long long* counter;
+  i64 cap;
+  i64 item;                    // slot << 16 | class (the sub-class is or'ed in)
+};
+
 template <int P>
 struct Pipe {
   // Times are exact integers held in doubles (all < 2^52, checked at create):
@@ -577,7 +591,8 @@ struct Pipe {
     return false;
   }
   // T_pipe; `skipped` = steady level pairs not executed (periodic regime).
-  HD i64 run(i64 m, i64& skipped) {
+  // T_pipe; with dc (device): -1 if the job was re-queued for K_pipe_cont
+  HD i64 run(i64 m, i64& skipped, const DeferCtx* dc = nullptr, int u = 0) {
 #pragma unroll
     for (int s = 0; s < P; ++s) X[s] = 0;
     skipped = 0;
@@ -605,6 +620,16 @@ struct Pipe {
       // seven identical consecutive stages) and c | 20 (c = 5) are all caught
       // within about one cycle after the transient
       if (kn >= 4 && !block<4, EXT, AFF>(k, kn, skipped)) {
+#ifdef __CUDA_ARCH__
+        if (dc && kn - k >= HSIM_DEFER_MIN) {
+          const unsigned long long q = atomicAdd(dc->counter, 1ull);
+          if ((i64)q < dc->cap) {
+            dc->list[q] = dc->item | (i64)u << 4;
+            skipped = kn - k;  // executed here: warm-up + the first block
+            return -1;
+          }
+        }
+#endif
         if (EXT && P >= 5) {
           for (;;) {
             if (k + 24 > kn || block<24, EXT, AFF>(k, kn, skipped)) break;
@@ -641,8 +666,12 @@ struct PipeOut { i64 T0, cells; };
 
 // R (S.1, overlap mode only; else nullptr): R[s * rs] = max over sub-classes
 // of the end of stage s's last op (its last backward) in real time
+// dc (device): re-queue context or nullptr (a re-queued sub-class contributes
+// 0 here; K_pipe_cont<P> max's its exact T_pipe and stage ends in).
+// only_u >= 0: evaluate that sub-class alone (K_pipe_cont).
 template <int P>
-HD PipeOut class_pipes_inl(const Tables& T, int32_t off, const ClassSplit& cs, i64* R = nullptr, i64 rs = 0) {
+HD PipeOut class_pipes_inl(const Tables& T, int32_t off, const ClassSplit& cs, i64* R = nullptr, i64 rs = 0,
+                           const DeferCtx* dc = nullptr, int only_u = -1) {
   const CrecHdr* h = crec_hdr(T, off);
   const StageRec* st = crec_stages(T, off);
   Pipe<P> p;
@@ -654,20 +683,26 @@ HD PipeOut class_pipes_inl(const Tables& T, int32_t off, const ClassSplit& cs, i
     p.g[s] = (double)(l * st[s].layer_b + st[s].gext);
   }
   PipeOut r{0, 0};
-  for (int u = 0; u < h->U; ++u) {
+  const int u0 = only_u >= 0 ? only_u : 0, u1 = only_u >= 0 ? only_u + 1 : h->U;
+  for (int u = u0; u < u1; ++u) {
     const i64* sub = crec_sub(T, off, P, u);
 #pragma unroll
     for (int s = 0; s + 1 < P; ++s) p.c[s] = (double)(2 * sub[1 + s]);
     const i64 m = mb_of(cs, sub[0]);
     i64 sk;
-    r.T0 = imax(r.T0, p.run(m, sk));
+    const i64 tp = p.run(m, sk, dc, u);
+    r.T0 = imax(r.T0, tp);
     r.cells += 2 * P * (m - sk);  // cells executed
     if (R) {  // offset coordinates -> real ends: end_s = X_s + c_0 + ... + c_{s-1}
       double o = 0;
 #pragma unroll
       for (int s = 0; s < P; ++s) {
-        const i64 e = (i64)(p.X[s] + o);
-        R[s * rs] = u == 0 ? e : imax(R[s * rs], e);
+        const i64 e = tp < 0 ? 0 : (i64)(p.X[s] + o);
+#ifdef __CUDA_ARCH__
+        if (only_u >= 0) atomicMax((unsigned long long*)&R[s * rs], (unsigned long long)e);
+        else
+#endif
+          R[s * rs] = u == 0 ? e : imax(R[s * rs], e);
         if (s + 1 < P) o += 0.5 * p.c[s];
       }
     }

@@ -37,6 +37,7 @@ int ensure_work_scratch(hsim_handle* h, size_t entries, int64_t** out);
 int sm_count(const hsim_handle* h);
 uint32_t depth_mask(const hsim_handle* h);
 int depth_jobs_max(const hsim_handle* h, int P);
+int64_t depth_jobs_space(const hsim_handle* h, int P);
 int stages_max(const hsim_handle* h);
 int sync_overlap(const hsim_handle* h);
 cudaStream_t side_stream(const hsim_handle* h, int q);
@@ -106,7 +107,18 @@ constexpr i64 LIST_PAD = 0x7F7F7F7F7F7F7F7FLL;  // memset(0x7F) sentinel of the 
 constexpr unsigned FULL = 0xffffffffu;
 // counter slots: P (1..FASTP) = work counter of K_pipe<P>; CNT_FULL + P = #jobs of
 // depth P in full (32-aligned) chunks, CNT_PART + P = #jobs from partial chunks
-constexpr int CNT_DEEP = 17, CNT_NDEEP = 18, CNT_CELLS = 19, CNT_FULL = 20, CNT_PART = 40, NCNT = 64;
+constexpr int CNT_DEEP = 17, CNT_NDEEP = 18, CNT_CELLS = 19, CNT_FULL = 20, CNT_PART = 40, CNT_REQ = 55, NCNT = 64;
+// re-queued jobs of depth P (lane compaction), P in [2, HSIM_REQ_MAXP]: count at CNT_REQ + P
+#ifndef HSIM_REQ_MAXP
+#define HSIM_REQ_MAXP 8
+#endif
+#ifndef HSIM_REQ_MINP
+#define HSIM_REQ_MINP 5  // measured: re-queueing P <= 4 costs config 2 more than it saves
+#endif
+#ifndef HSIM_REQ_MINJOBS
+#define HSIM_REQ_MINJOBS (1LL << 20)  // ... and depths with few jobs in the space (extra launch, no gain)
+#endif
+static_assert(CNT_REQ + HSIM_REQ_MAXP < NCNT, "counter layout");
 static_assert(FASTP <= 16, "counter layout");
 
 struct Cands {
@@ -135,6 +147,8 @@ struct Scratch {
   i64* Tc;            // [MAXC][ns] max T_pipe over the class's sub-classes
   i64* extra;         // [ns] gradient-sync time beyond T0 (C.8), by K_sync
   i64* Rs;            // [spmax][ns] overlap mode (S.1): end of each stage's last backward; else nullptr
+  i64* req[HSIM_REQ_MAXP + 1];  // per depth: re-queued jobs (slot << 16 | u << 4 | class)
+  i64 req_cap[HSIM_REQ_MAXP + 1];
   int32_t* deep;      // [ns] slots with a class deeper than FASTP (compacted)
   int32_t* full[FASTP + 1];  // per depth: jobs (slot << 2 | class) of full chunks, 32-aligned groups
   int32_t* part[FASTP + 1];  // per depth: jobs of partial chunks, packed
@@ -307,7 +321,12 @@ __global__ void __launch_bounds__(NT, P <= 4 ? HSIM_PIPE_MINB : 1) k_pipe(const 
     if (tau < 0 || S.status[slot] != 0) continue;
     const TplRec& tp = sT.tpl[tau];
     i64* R = S.Rs ? S.Rs + (i64)class_stage_off(sT, tp, c) * S.ns + slot : nullptr;
-    const PipeOut r = class_pipes_inl<P>(sT, tp.crec[c], load_split(S, c, tp.C, slot), R, S.ns);
+    // depths gated off on the host have req_cap 0: the re-queue attempt fails
+    // and the lane continues in place (rare: only unsettled jobs try)
+    constexpr bool rq = P >= HSIM_REQ_MINP && P <= HSIM_REQ_MAXP;
+    const DeferCtx dc{rq ? S.req[rq ? P : 0] : nullptr, &S.counters[CNT_REQ + (rq ? P : 0)], rq ? S.req_cap[rq ? P : 0] : 0,
+                      slot << 16 | c};
+    const PipeOut r = class_pipes_inl<P>(sT, tp.crec[c], load_split(S, c, tp.C, slot), R, S.ns, rq ? &dc : nullptr);
     S.Tc[c * S.ns + slot] = r.T0;
 #ifdef HSIM_WARPCELLS  // diagnostic: count mode reports warp-slot cells (32 x warp max)
     cells += 32 * __reduce_max_sync(__activemask(), (unsigned)r.cells);
@@ -330,6 +349,29 @@ __device__ __forceinline__ void sym_max(double& a, double& sa, double b, double 
   if (sL > sw) H = fmin(H, floor((w - l) / (sL - sw)) - 1.0);
   a = w;
   sa = sw;
+}
+
+// ---- K_pipe_cont<P>: the re-queued jobs of depth P, 32 per warp ------------------
+template <int P>
+__global__ void __launch_bounds__(NT, P <= 4 ? HSIM_PIPE_MINB : 1) k_pipe_cont(const Tables* __restrict__ gT, Scratch S, int count) {
+  __shared__ Tables sT;
+  load_tables(sT, gT);
+  const i64 n = imin((i64)S.counters[CNT_REQ + P], S.req_cap[P]);
+  i64 cells = 0;
+  for (i64 q = (i64)blockIdx.x * NT + threadIdx.x; q < n; q += (i64)gridDim.x * NT) {
+    const i64 v = S.req[P][q];
+    const i64 slot = v >> 16;
+    const int u = (int)(v >> 4) & 0xfff, c = (int)v & 15;
+    const TplRec& tp = sT.tpl[S.tau[slot]];
+    i64* R = S.Rs ? S.Rs + (i64)class_stage_off(sT, tp, c) * S.ns + slot : nullptr;
+    const PipeOut r = class_pipes_inl<P>(sT, tp.crec[c], load_split(S, c, tp.C, slot), R, S.ns, nullptr, u);
+    atomicMax((unsigned long long*)&S.Tc[c * S.ns + slot], (unsigned long long)r.T0);
+    cells += r.cells;
+  }
+  if (count) {
+    cells = warp_sum(cells);
+    if ((threadIdx.x & 31) == 0 && cells) atomicAdd(&S.counters[CNT_CELLS], (unsigned long long)cells);
+  }
 }
 
 // ---- K_deep: lane-per-stage wavefront for depth > FASTP --------------------------
@@ -1141,7 +1183,7 @@ static int final_grid(const hsim_handle* h, int k) { return sm_count(h) * (k && 
 // count optional.
 static int run_phases(hsim_handle* h, const Tables* dT, Cands c, int64_t n, int64_t* out_ns, int32_t k, i64* lists,
                       int count, i64* cells_out, cudaStream_t st, int& launches) {
-  static int g_split = 0, g_pipe[FASTP + 1] = {0}, g_deep = 0, g_sync = 0;
+  static int g_split = 0, g_pipe[FASTP + 1] = {0}, g_cont[FASTP + 1] = {0}, g_deep = 0, g_sync = 0;
   // chunk plan
   i64 nchunks;
   i64* hplan = nullptr;
@@ -1177,7 +1219,13 @@ static int run_phases(hsim_handle* h, const Tables* dT, Cands c, int64_t n, int6
   const size_t planw = c.idx ? 0 : (size_t)(2 * c.nr + 1);
   const size_t n32 = (size_t)(4 + 4 * MAXC) * ns + jobw;
   const size_t bufw0 = (size_t)(MAXC + 2) * ns + NCNT + (n32 + 1) / 2 + 8;
-  const size_t bufw = bufw0 + (size_t)spmax * ns;
+  size_t reqw = 0, reqcap[HSIM_REQ_MAXP + 1] = {0};
+  for (int P = HSIM_REQ_MINP; P <= HSIM_REQ_MAXP && P <= FASTP; ++P) {
+    if (depth_jobs_space(h, P) < HSIM_REQ_MINJOBS) continue;
+    reqcap[P] = jobcap[P];  // a depth's jobs (re-queued at most once each)
+    reqw += reqcap[P];
+  }
+  const size_t bufw = bufw0 + (size_t)spmax * ns + reqw;
   i64* base = nullptr;
   if (ensure_work_scratch(h, NBUF * bufw + planw + 8, &base)) return HSIM_ENOMEM;
   Scratch SB[2];
@@ -1189,6 +1237,14 @@ static int run_phases(hsim_handle* h, const Tables* dT, Cands c, int64_t n, int6
     S.Tc = b0 + ns;
     S.extra = b0 + (MAXC + 1) * ns;
     S.Rs = overlap ? b0 + bufw0 : nullptr;
+    {
+      i64* rp = b0 + bufw0 + (size_t)spmax * ns;
+      for (int P = 0; P <= HSIM_REQ_MAXP; ++P) {
+        S.req[P] = reqcap[P] ? rp : nullptr;
+        S.req_cap[P] = (i64)reqcap[P];
+        rp += reqcap[P];
+      }
+    }
     S.counters = (unsigned long long*)(b0 + (MAXC + 2) * ns);
     int32_t* p32 = (int32_t*)(b0 + (MAXC + 2) * ns + NCNT);
     S.tau = p32;
@@ -1280,6 +1336,15 @@ static int run_phases(hsim_handle* h, const Tables* dT, Cands c, int64_t n, int6
 #endif
 #undef HSIM_PIPE
         default: break;
+      }
+      if (P >= HSIM_REQ_MINP && P <= HSIM_REQ_MAXP && reqcap[P]) {  // the re-queued jobs of this depth, densely
+        switch (P) {
+#define HSIM_CONT(PP) case PP: k_pipe_cont<PP><<<grid_of(h, k_pipe_cont<PP>, g_cont[PP]), NT, 0, ss>>>(dT, S, count); break;
+          HSIM_CONT(2) HSIM_CONT(3) HSIM_CONT(4) HSIM_CONT(5) HSIM_CONT(6) HSIM_CONT(7) HSIM_CONT(8)
+#undef HSIM_CONT
+          default: break;
+        }
+        ++launches;
       }
       g_trace.post(tq, ss);
       ++launches;

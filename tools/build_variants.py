@@ -7,6 +7,11 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2508_05370_b200 import build as B  # noqa: E402
 
 VARIANTS = {
+    "rq1": ["-DHSIM_DEFER_MIN=1", "-DHSIM_REQ_MINP=2", "-DHSIM_REQ_MINJOBS=0"],
+    "norq": ["-DHSIM_REQ_MAXP=1"],
+    "rq64": ["-DHSIM_DEFER_MIN=64"],
+    "rqmin2": ["-DHSIM_REQ_MINP=2"],
+    "rqmin4": ["-DHSIM_REQ_MINP=4"],
     "s4": ["-DHSIM_SYNC_MINB=4"],
     "s5": ["-DHSIM_SYNC_MINB=5"],
     "s3": ["-DHSIM_SYNC_MINB=3"],
