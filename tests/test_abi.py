@@ -44,6 +44,8 @@ def _create(cfg):
     (lambda c: c["cluster"]["types"][0].update(nic_gbps=0.0), hsim.HSIM_EINVAL, "NonPositiveBandwidth"),
     (lambda c: c["cluster"]["types"][1]["link_kinds"][0][0].update(gbps=-1.0), hsim.HSIM_EINVAL, "NonPositiveBandwidth"),
     (lambda c: c["model"].update(seq=1 << 20, vocab=1 << 20), hsim.HSIM_ERANGE, "2^53"),
+    (lambda c: (c["search"].update(mem_check=1), c["cluster"]["types"][0].update(mem_bytes=0)),
+     hsim.HSIM_EINVAL, "mem_bytes"),
 ])
 def test_validation_errors(L, mutate, code, kind):
     cfg = H.get(1)
@@ -110,3 +112,16 @@ def test_eval_without_gpu_fails_loudly(L):
     assert rc == hsim.HSIM_ECUDA
     with pytest.raises(RuntimeError):
         hsim.Sim(H.get(1))
+
+
+@pytest.mark.parametrize("n", [2, 4, 5])
+def test_host_decode_memcheck_status_matches_oracle(oracle_mod, L, n):
+    """With mem_check on (DESIGN.md M.1) the product's host-side split (the same
+    HD code the kernels run) and the oracle agree on every sampled status."""
+    cfg = H.with_mem_check(H.get(n))
+    s = hsim.Sim(cfg, host_only=True)
+    o = oracle_mod.Oracle(cfg)
+    idx = H.sample_indices(s.space_size(), 300, seed=H.PARITY_SEED + 60 + n)
+    got = [s.decode(int(i))["status"] for i in idx]
+    want = [o.describe(int(i))["status"] for i in idx]
+    assert got == want and -3 in got
