@@ -250,6 +250,22 @@ HD i64 find_template(const Tables& T, i64 i) {
   return lo;
 }
 
+// floor(n / d) and n mod d for 0 <= n < 2^63, 0 < d, quotient < 2^40: on the
+// device an fp64 estimate (relative error < 2^-51, so within 1 of the true
+// quotient) fixed up with one exact int64 remainder -- no 64-bit division
+// subroutine; on the host the plain operators.  Exact either way.
+HD void divmod_est(i64 n, i64 d, i64& q, i64& r) {
+#ifdef __CUDA_ARCH__
+  q = (i64)floor((double)n / (double)d);
+  r = n - q * d;
+  if (r < 0) { q -= 1; r += d; }
+  if (r >= d) { q += 1; r -= d; }
+#else
+  q = n / d;
+  r = n % d;
+#endif
+}
+
 // Decoded + partitioned candidate, per class (steps a0 + a1), without
 // per-stage arrays: layer counts are re-derived from the class's digit block.
 // Replica k of the class gets m_k = q + [k < seats] + add + [k < rm]
@@ -313,7 +329,8 @@ HD int partition_c(const Tables& T, const TplRec& tp, i64 local, ClassSplit (&cs
       if (l < 1) status = -1;
       worst = imax(worst, (i64)l * st[s].tcomp + st[s].wext);
     }
-    w[c] = ((i64)1 << 40) / worst;
+    i64 wr;
+    divmod_est((i64)1 << 40, worst, w[c], wr);
   }
   if (status) return status;
   i64 W = 0, R = 0, left = tp.M, rem[C];
@@ -321,8 +338,7 @@ HD int partition_c(const Tables& T, const TplRec& tp, i64 local, ClassSplit (&cs
   for (int c = 0; c < C; ++c) W += D[c] * w[c];
 #pragma unroll
   for (int c = 0; c < C; ++c) {
-    cs[c].q = (i64)tp.M * w[c] / W;
-    rem[c] = (i64)tp.M * w[c] % W;
+    divmod_est((i64)tp.M * w[c], W, cs[c].q, rem[c]);
     left -= D[c] * cs[c].q;
     cs[c].seats = 0;
     cs[c].rm = 0;

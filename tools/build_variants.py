@@ -7,6 +7,9 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2508_05370_b200 import build as B  # noqa: E402
 
 VARIANTS = {
+    "nb2": ["-DHSIM_NBATCH=2"],
+    "nb3": ["-DHSIM_NBATCH=3"],
+    "nb4": ["-DHSIM_NBATCH=4"],
     "rq1": ["-DHSIM_DEFER_MIN=1", "-DHSIM_REQ_MINP=2", "-DHSIM_REQ_MINJOBS=0"],
     "norq": ["-DHSIM_REQ_MAXP=1"],
     "rq64": ["-DHSIM_DEFER_MIN=64"],
