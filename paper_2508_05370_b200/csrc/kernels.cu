@@ -113,7 +113,7 @@ constexpr int CNT_DEEP = 17, CNT_NDEEP = 18, CNT_CELLS = 19, CNT_FULL = 20, CNT_
 #define HSIM_REQ_MAXP 8
 #endif
 #ifndef HSIM_REQ_MINP
-#define HSIM_REQ_MINP 5  // measured: re-queueing P <= 4 costs config 2 more than it saves
+#define HSIM_REQ_MINP 2  // every register depth with enough jobs in the space (HSIM_REQ_MINJOBS)
 #endif
 #ifndef HSIM_REQ_MINJOBS
 #define HSIM_REQ_MINJOBS (1LL << 20)  // ... and depths with few jobs in the space (extra launch, no gain)

@@ -7,6 +7,14 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2508_05370_b200 import build as B  # noqa: E402
 
 VARIANTS = {
+    "rq5": ["-DHSIM_REQ_MINP=5"],
+    "rq4": ["-DHSIM_REQ_MINP=4"],
+    "rq4d8": ["-DHSIM_REQ_MINP=4", "-DHSIM_DEFER_MIN=8"],
+    "rq4d32": ["-DHSIM_REQ_MINP=4", "-DHSIM_DEFER_MIN=32"],
+    "rq2": ["-DHSIM_REQ_MINP=2"],
+    "fm16": ["-DHSIM_FINAL_MULT=16"],
+    "fm12": ["-DHSIM_FINAL_MULT=12"],
+    "fm6": ["-DHSIM_FINAL_MULT=6"],
     "nb2": ["-DHSIM_NBATCH=2"],
     "nb3": ["-DHSIM_NBATCH=3"],
     "nb4": ["-DHSIM_NBATCH=4"],
