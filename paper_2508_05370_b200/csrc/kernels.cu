@@ -3,26 +3,30 @@
 // A call (hsim_eval_batch / hsim_topk / hsim_count_cells) maps its candidate
 // list onto 32-candidate chunks that never straddle a template (range and
 // block-cyclic lists; explicit lists use 32 consecutive entries) and runs in
-// batches of up to 2^17 chunks.  Per batch, each phase is a small kernel with
-// its own register budget; a chunk's 32 lanes occupy 32 scratch "slots":
+// batches of up to 2^17 chunks (one batch unless the scratch cap forces
+// more).  Each phase is a small kernel with its own register budget; a
+// chunk's 32 lanes occupy 32 scratch "slots":
 //
 //   K_split   warp per chunk, lane per candidate: decode (mixed-radix digits)
 //             + step (1) partition -> compact per-class split in HBM; appends
 //             one job segment per (depth P, class) of the chunk's template.
-//   K_pipe<P> P = 1..8, one launch per depth present: warp per segment, lane =
-//             (candidate, class of depth P) of one template and class, so the
-//             32 lanes have near-equal micro-batch counts; register-resident
-//             1F1B max-plus (step 4) over stage durations (step 2) and p2p
-//             costs (step 3) -> T_pipe per class.
-//   K_deep    depth > 8: warp per candidate; the warp sweeps the 1F1B
+//   K_pipe<P> P = 1..16, one launch per depth present: warp per segment, lane
+//             = (candidate, class of depth P) of one template and class;
+//             register-resident 1F1B max-plus (step 4) over stage durations
+//             (step 2) and p2p costs (step 3) with the exact steady-regime
+//             jumps -> T_pipe per class.  P >= 9 on high-priority streams.
+//   K_pipe_cont<P>  P = 2..8: the jobs K_pipe<P> re-queued (unsettled after
+//             the first block), 32 per warp (lane compaction).
+//   K_deep    depth > 16: warp per candidate; the warp sweeps the 1F1B
 //             anti-diagonal wavefront, lane = stage, __shfl max-plus.
 //   K_sync    thread per candidate: step (5) gradient sync incl. reshard as the
-//             T0-independent "extra" (runs concurrently with the 1F1B kernels).
+//             T0-independent "extra" (runs concurrently with the 1F1B kernels);
+//             K_sync_overlap instead (S.1 mode) after them.
 //   K_final   T = max over classes of T_pipe + extra, coalesced int64 store,
 //             per-warp top-k lists with a global pruning bound.
-//   K_merge   (top-k only, once per call) merges the per-warp sorted lists.
+//   K_merge   (top-k only, once per call) merges the per-block sorted lists.
 // The depth kernels, K_deep and K_sync of a batch run concurrently on fork /
-// join side streams.
+// join side streams.  HSIM_TRACE=1 prints a per-launch timeline.
 #include <cstdio>
 #include <cstdlib>
 #include <cuda_runtime.h>
