@@ -708,7 +708,9 @@ HD PipeOut class_pipes_inl(const Tables& T, int32_t off, const ClassSplit& cs, i
     i64 sk;
     const i64 tp = p.run(m, sk, dc, u);
     r.T0 = imax(r.T0, tp);
-    r.cells += 2 * P * (m - sk);  // cells executed
+    // cells executed; a re-queued job is counted once, by its complete run in
+    // K_pipe_cont (the cells of the abandoned first attempt are not counted)
+    r.cells += tp < 0 ? 0 : 2 * P * (m - sk);
     if (R) {  // offset coordinates -> real ends: end_s = X_s + c_0 + ... + c_{s-1}
       double o = 0;
 #pragma unroll
