@@ -360,7 +360,9 @@ HD int partition_c(const Tables& T, const TplRec& tp, i64 local, ClassSplit (&cs
     cs[c].seats = imax(0, imin(D[c], left - before));
   }
   const i64 Dl = D[C - 1];
-  const i64 fl = R >= 0 ? R / Dl : -((-R + Dl - 1) / Dl);
+  // |R| <= sum_c D_c r_batch and D_l are small: 32-bit floor division
+  const int32_t R32 = (int32_t)R, D32 = (int32_t)Dl;
+  const i64 fl = R32 >= 0 ? R32 / D32 : -((-R32 + D32 - 1) / D32);
   cs[C - 1].add = fl;
   cs[C - 1].rm = R - fl * Dl;
 #pragma unroll
