@@ -850,6 +850,51 @@ __global__ void __launch_bounds__(NT) k_final_small(const Tables* __restrict__ g
     i64 thT = __shfl_sync(FULL, (long long)r.t, k - 1), thI = __shfl_sync(FULL, (long long)r.i, k - 1);
     unsigned cand = __ballot_sync(FULL, t >= 0 && T >= 0 && T <= g && key_less(T, i, thT, thI));
     if (!cand) continue;
+    if (__popc(cand) > 6) {
+      // many candidates (early in the scan): sort them across the warp
+      // (bitonic, 15 compare-exchange steps) and merge with the list by rank
+      // instead of one insert per candidate
+      const bool mine = cand >> lane & 1;
+      i64 bt_ = mine ? T : KEY_INF, bi_ = mine ? i : KEY_INF;
+#pragma unroll
+      for (int size = 2; size <= 32; size <<= 1)
+#pragma unroll
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+          const i64 ot = __shfl_xor_sync(FULL, (long long)bt_, stride), oi = __shfl_xor_sync(FULL, (long long)bi_, stride);
+          const bool up = (lane & size) == 0, lower = (lane & stride) == 0;
+          const bool olt = key_less(ot, oi, bt_, bi_);
+          if (lower == up ? olt : !olt && !(ot == bt_ && oi == bi_)) { bt_ = ot; bi_ = oi; }
+        }
+      // rank merge of the sorted lists A = r (lane j = j-th) and B = (bt_, bi_)
+      int lo = 0, hi = 32;  // #B < A[lane]
+#pragma unroll
+      for (int it = 0; it < 6; ++it) {
+        const int mid = (lo + hi) >> 1;
+        const int src = mid < 32 ? mid : 31;
+        const i64 mt = __shfl_sync(FULL, (long long)bt_, src), mi = __shfl_sync(FULL, (long long)bi_, src);
+        if (lo < hi) { if (key_less(mt, mi, r.t, r.i)) lo = mid + 1; else hi = mid; }
+      }
+      const int pa = lane + lo;
+      int lo2 = 0, hi2 = 32;  // #A < B[lane]
+#pragma unroll
+      for (int it = 0; it < 6; ++it) {
+        const int mid = (lo2 + hi2) >> 1;
+        const int src = mid < 32 ? mid : 31;
+        const i64 mt = __shfl_sync(FULL, (long long)r.t, src), mi = __shfl_sync(FULL, (long long)r.i, src);
+        if (lo2 < hi2) { if (key_less(mt, mi, bt_, bi_)) lo2 = mid + 1; else hi2 = mid; }
+      }
+      const int pb = lane + lo2;
+      __syncwarp();
+      if (pa < 32) { bt[w][pa] = r.t; bi[w][pa] = r.i; }
+      if (pb < 32) { bt[w][pb] = bt_; bi[w][pb] = bi_; }
+      __syncwarp();
+      r.t = bt[w][lane];
+      r.i = bi[w][lane];
+      __syncwarp();
+      thT = __shfl_sync(FULL, (long long)r.t, k - 1);
+      if (lane == 0 && thT != KEY_INF) atomicMin(gthr, (unsigned long long)thT);
+      continue;
+    }
     while (cand) {
       const int src = __ffs(cand) - 1;
       cand &= cand - 1;
