@@ -209,7 +209,10 @@ __device__ __forceinline__ int split_store(const Tables& T, const TplRec& tp, i6
 }
 
 // ---- K_split -------------------------------------------------------------------
-__global__ void __launch_bounds__(NT, 6) k_split(const Tables* __restrict__ gT, Cands c, i64 ca, i64 cb, Scratch S,
+#ifndef HSIM_SPLIT_MINB
+#define HSIM_SPLIT_MINB 8  // measured: 8 >= 6 > 5 > 4 (occupancy over the spills it costs)
+#endif
+__global__ void __launch_bounds__(NT, HSIM_SPLIT_MINB) k_split(const Tables* __restrict__ gT, Cands c, i64 ca, i64 cb, Scratch S,
                                               uint32_t pm_all) {
   __shared__ Tables sT;
   load_tables(sT, gT);

@@ -7,6 +7,9 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2508_05370_b200 import build as B  # noqa: E402
 
 VARIANTS = {
+    "sp8": ["-DHSIM_SPLIT_MINB=8"],
+    "sp4": ["-DHSIM_SPLIT_MINB=4"],
+    "sp5": ["-DHSIM_SPLIT_MINB=5"],
     "rq5": ["-DHSIM_REQ_MINP=5"],
     "rq4": ["-DHSIM_REQ_MINP=4"],
     "rq4d8": ["-DHSIM_REQ_MINP=4", "-DHSIM_DEFER_MIN=8"],
