@@ -210,7 +210,7 @@ __device__ __forceinline__ int split_store(const Tables& T, const TplRec& tp, i6
 
 // ---- K_split -------------------------------------------------------------------
 #ifndef HSIM_SPLIT_MINB
-#define HSIM_SPLIT_MINB 8  // measured: 8 >= 6 > 5 > 4 (occupancy over the spills it costs)
+#define HSIM_SPLIT_MINB 6  // measured: 8 is ~1 % faster on range sweeps but ~8 % slower on explicit lists (e2e)
 #endif
 __global__ void __launch_bounds__(NT, HSIM_SPLIT_MINB) k_split(const Tables* __restrict__ gT, Cands c, i64 ca, i64 cb, Scratch S,
                                               uint32_t pm_all) {

@@ -7,6 +7,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2508_05370_b200 import build as B  # noqa: E402
 
 VARIANTS = {
+    "sp6": ["-DHSIM_SPLIT_MINB=6"],
     "sp8": ["-DHSIM_SPLIT_MINB=8"],
     "sp4": ["-DHSIM_SPLIT_MINB=4"],
     "sp5": ["-DHSIM_SPLIT_MINB=5"],
