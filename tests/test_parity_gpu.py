@@ -149,12 +149,16 @@ def test_launch_count_is_native(torch_cuda, oracle_mod):
 
 
 @pytest.mark.skipif(os.environ.get("HSIM_FULL") != "1", reason="exhaustive run: set HSIM_FULL=1")
-def test_config2_exhaustive(torch_cuda, oracle_mod):
-    sim, o = pair(oracle_mod, 2)
+@pytest.mark.parametrize("n", [2, 4])
+def test_config_exhaustive(torch_cuda, oracle_mod, n):
+    """Every candidate of config 2 (873 192) / config 4 (11 122 050): GPU range
+    sweep vs the oracle, int64-equal (minutes of host-core oracle time)."""
+    sim, o = pair(oracle_mod, n)
     N = o.space_size()
     got = sim.eval_batch(n=N).cpu().numpy()
     want = o.eval_many(first=0, n=N, threads=THREADS)
     assert_equal(np.arange(N), got, want)
+    print(f"config {n}: {N} candidates int64-equal, {(want >= 0).sum()} valid")
 
 
 def test_eval_host_chunked_overlap(torch_cuda, oracle_mod):
