@@ -149,11 +149,12 @@ def test_launch_count_is_native(torch_cuda, oracle_mod):
 
 
 @pytest.mark.skipif(os.environ.get("HSIM_FULL") != "1", reason="exhaustive run: set HSIM_FULL=1")
-@pytest.mark.parametrize("n", [2, 4, 3])
+@pytest.mark.parametrize("n", [2, 4])
 def test_config_exhaustive(torch_cuda, oracle_mod, n):
-    """Every candidate of config 2 (873 192) / config 4 (11 122 050) / config 3
-    (62 232 390): GPU range sweep vs the oracle, int64-equal (minutes to a
-    quarter hour of host-core oracle time)."""
+    """Every candidate of config 2 (873 192) / config 4 (11 122 050): GPU range
+    sweep vs the oracle, int64-equal (about 6 min of 16 host cores; config 3's
+    6.2e7 candidates take the oracle more than 40 min and are covered by
+    samples and full-sweep properties instead)."""
     sim, o = pair(oracle_mod, n)
     N = o.space_size()
     got = sim.eval_batch(n=N).cpu().numpy()
