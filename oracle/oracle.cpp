@@ -11,11 +11,20 @@
 // DESIGN.md §2 (the paper gives no cost formulas beyond the link delay; every
 // other formula is a reading, listed there with its id A1..A24 / C.x).
 //
-// Style: literal.  Every replica of every class is simulated; every stage is
-// its own resource in a (time, seq)-ordered event queue;
-// stage durations are sums over their layers' op durations; every collective
-// (TP all-reduce, DP ring all-reduce) is simulated send by send on its ring.
-// No closed forms, no sub-classing, no precomputed tables.
+// Two modes (SURVEY.md §8(c) "It runs in two modes ... The two modes must agree"):
+//  * literal (default): every replica of every class is simulated; every stage
+//    is its own resource in a (time, seq)-ordered event queue;
+//    stage durations are sums over their layers' op durations; every
+//    collective (TP all-reduce, DP ring all-reduce) is simulated send by send
+//    on its ring.  No closed forms, no sub-classing, no precomputed tables.
+//  * compact: one pipeline per sub-class of isomorphic replicas (replicas of a
+//    class with equal p2p cost vectors; m = the largest m among them, DESIGN
+//    A13), stage durations as l_s x (one layer's op chain) + emb/head, and
+//    every ring collective as steps x (slowest edge) (the closed form the
+//    literal async ring reaches, pinned in tests/test_oracle_pins.py).  Same
+//    event engine, same decode / placement / partition.  It exists so the
+//    exhaustive parity runs on configs 3 and 5 fit in host-core minutes; the
+//    literal == compact equivalence is tested (tests/test_oracle_compact.py).
 //
 // Exactness rules (DESIGN.md C.0): durations are ceil((double)x / r) with x an
 // int64 < 2^53 and r a double; everything else is int64 + and max.  Built with
@@ -335,6 +344,7 @@ struct Oracle {
   Cluster cl;
   std::vector<Template> tpls;
   i64 N = 0;
+  int compact_mode = 0;  // 0 literal, 1 compact (see the header)
 
   void init() {
     in.types = types.data();
@@ -614,63 +624,42 @@ struct Oracle {
     return last;
   }
 
-  i64 eval(i64 i) const {
-    if (i < 0 || i >= N) return INT64_MIN;
-    Plan p = decode(i);
-    place(p);
-    partition(p);
-    check_memory(p);
-    if (p.status) return p.status;
-    const auto& cls = p.tpl->cls;
-    const int C = (int)cls.size(), b = p.tpl->b;
-    const int mk = in.E > 1 ? MOE : MLP;
+  // TP all-reduce, compact form: 2(t-1) steps x the slowest ring edge (the
+  // value the literal async ring reaches; pinned by the ring closed forms)
+  i64 tp_allreduce_compact(const Group& g, int t, int b) const {
+    if (t == 1) return 0;
+    i64 slow = 0;
+    for (const Link& e : tp_ring(g, t)) slow = std::max(slow, tau(e, ceil_div(act_bytes(b), t)));
+    return 2 * (i64)(t - 1) * slow;
+  }
 
-    // steps 2-4: stage durations (sum over the stage's layers of its layer-op
-    // chain, C.5), p2p costs (C.6), 1F1B per replica (C.7)
-    std::vector<SimGroup> G;
-    for (int c = 0; c < C; ++c) {
-      const int P = (int)cls[c].st.size();
-      for (int r = 0; r < cls[c].D; ++r) {
-        for (int s = 0; s < P; ++s) {
-          const StageSpec& ss = cls[c].st[s];
-          const orc_type& ty = types[ss.type];
-          const Group& gr = p.place[c][r][s];
-          i64 ar = tp_allreduce(gr, ss.tp, b);
-          i64 a2a = in.E > 1 ? ep_alltoall(gr, ss.tp, b) : 0;
-          SimGroup g{};
-          g.P = P; g.s = s; g.m = (int)p.mb[c][r];
-          for (i64 l = 0; l < p.layers[c][s]; ++l) {
-            for (int bwd = 0; bwd < 2; ++bwd) {
-              i64 chain = op_dur(in, ty, ATTN, bwd, ss.tp, b) + ar;
-              if (in.E > 1) chain += a2a + op_dur(in, ty, MOE, bwd, ss.tp, b) + a2a;
-              else chain += op_dur(in, ty, mk, bwd, ss.tp, b) + ar;
-              (bwd ? g.g : g.f) += chain;
-            }
-          }
-          if (s == 0) { g.f += op_dur(in, ty, EMB, false, ss.tp, b); g.g += op_dur(in, ty, EMB, true, ss.tp, b); }
-          if (s == P - 1) { g.f += op_dur(in, ty, HEAD, false, ss.tp, b); g.g += op_dur(in, ty, HEAD, true, ss.tp, b); }
-          G.push_back(g);
-        }
-        // p2p per boundary: rank pairs i < min(t_s, t_{s+1}) in parallel (A8)
-        const size_t base = G.size() - P;
-        for (int s = 0; s + 1 < P; ++s) {
-          const Group& a = p.place[c][r][s];
-          const Group& z = p.place[c][r][s + 1];
-          int np = std::min(cls[c].st[s].tp, cls[c].st[s + 1].tp);
-          i64 cs = 0;
-          for (int q = 0; q < np; ++q)
-            cs = std::max(cs, tau(cl.gpu_to_gpu(a.node, a.base + q, z.node, z.base + q), act_bytes(b)));
-          G[base + s].c_next = cs;
-          G[base + s + 1].c_prev = cs;
-        }
-      }
+  // One layer's forward (bwd = 0) or backward (bwd = 1) op chain on stage
+  // group gr: attn + AR + mlp + AR (dense) or attn + AR + A2A + moe + A2A (MoE)
+  // (DESIGN C.5, A16, A17).
+  i64 layer_chain(const StageSpec& ss, const Group& gr, int b, int bwd, bool compact) const {
+    const orc_type& ty = types[ss.type];
+    const i64 ar = compact ? tp_allreduce_compact(gr, ss.tp, b) : tp_allreduce(gr, ss.tp, b);
+    i64 chain = op_dur(in, ty, ATTN, bwd, ss.tp, b) + ar;
+    if (in.E > 1) {
+      const i64 a2a = ep_alltoall(gr, ss.tp, b);
+      chain += a2a + op_dur(in, ty, MOE, bwd, ss.tp, b) + a2a;
+    } else {
+      chain += op_dur(in, ty, MLP, bwd, ss.tp, b) + ar;
     }
-    const i64 T0 = run_pipelines(G);
+    return chain;
+  }
 
-    // step 5: gradient sync after the barrier at T0 (A19, C.8)
+  // --- C.6: gradient-sync segments ------------------------------------------------
+  struct Seg {
+    i64 a, z, S, RS, AR;
+    int tstar;
+    std::vector<int> sc;  // stage of every class holding layers [a, z)
+  };
+  std::vector<Seg> segments(const Plan& p, bool compact) const {
+    const auto& cls = p.tpl->cls;
+    const int C = (int)cls.size();
     i64 D = 0;
     for (auto& c : cls) D += c.D;
-    if (D == 1) return T0;
     std::vector<i64> cuts{0, in.L};
     std::vector<std::vector<i64>> start(C);
     for (int c = 0; c < C; ++c) {
@@ -681,89 +670,172 @@ struct Oracle {
     cuts.erase(std::unique(cuts.begin(), cuts.end()), cuts.end());
     const i64 hkv = in.kv_heads * in.h / in.heads;
     const i64 Wlayer = in.h * (2 * in.h + 2 * hkv) + in.nm * in.h * in.ffn * in.E + (in.E > 1 ? in.h * in.E : 0) + 2 * in.h;
-    // per segment: RS_j + AR_j and the stage of every class holding it
-    std::vector<i64> cost;
-    std::vector<std::vector<int>> seg_sc;
+    std::vector<Seg> out;
     for (size_t j = 0; j + 1 < cuts.size(); ++j) {
-      const i64 a = cuts[j], z = cuts[j + 1];
-      i64 S = (z - a) * Wlayer * in.bpe_grad;
-      if (a == 0) S += in.V * in.h * in.bpe_grad;
-      if (z == in.L) S += (in.V * in.h * (in.tied ? 0 : 1) + in.h) * in.bpe_grad;
-      std::vector<int> sc(C);
-      int tstar = 1 << 30;
+      Seg sg;
+      sg.a = cuts[j];
+      sg.z = cuts[j + 1];
+      sg.S = (sg.z - sg.a) * Wlayer * in.bpe_grad;
+      if (sg.a == 0) sg.S += in.V * in.h * in.bpe_grad;
+      if (sg.z == in.L) sg.S += (in.V * in.h * (in.tied ? 0 : 1) + in.h) * in.bpe_grad;
+      sg.sc.assign(C, 0);
+      sg.tstar = 1 << 30;
       for (int c = 0; c < C; ++c) {
         int s = 0;
-        while (s + 1 < (int)start[c].size() && start[c][s + 1] <= a) ++s;
-        sc[c] = s;
-        tstar = std::min(tstar, cls[c].st[s].tp);
+        while (s + 1 < (int)start[c].size() && start[c][s + 1] <= sg.a) ++s;
+        sg.sc[c] = s;
+        sg.tstar = std::min(sg.tstar, cls[c].st[s].tp);
       }
       // reshard (A14): every group with tp != t* re-lays S into t* shards over its ring
-      i64 RS = 0;
+      sg.RS = 0;
       for (int c = 0; c < C; ++c) {
-        const int tp = cls[c].st[sc[c]].tp;
-        if (tp == tstar) continue;
+        const int tp = cls[c].st[sg.sc[c]].tp;
+        if (tp == sg.tstar) continue;
         for (int r = 0; r < cls[c].D; ++r)
-          for (const Link& e : tp_ring(p.place[c][r][sc[c]], tp)) RS = std::max(RS, tau(e, ceil_div(S, tstar)));
+          for (const Link& e : tp_ring(p.place[c][r][sg.sc[c]], tp)) sg.RS = std::max(sg.RS, tau(e, ceil_div(sg.S, sg.tstar)));
       }
       // DP ring all-reduce: ring order class asc, replica asc, wrap; ring q < t*
       std::vector<Group> ring;
       for (int c = 0; c < C; ++c)
-        for (int r = 0; r < cls[c].D; ++r) ring.push_back(p.place[c][r][sc[c]]);
-      const i64 chunk = ceil_div(ceil_div(S, tstar), D);
-      i64 AR = 0;
-      for (int q = 0; q < tstar; ++q) {
+        for (int r = 0; r < cls[c].D; ++r) ring.push_back(p.place[c][r][sg.sc[c]]);
+      const i64 chunk = ceil_div(ceil_div(sg.S, sg.tstar), D);
+      sg.AR = 0;
+      for (int q = 0; q < sg.tstar; ++q) {
         std::vector<i64> taus;
         for (size_t k = 0; k < ring.size(); ++k) {
           const Group& u = ring[k];
           const Group& v = ring[(k + 1) % ring.size()];
           taus.push_back(tau(cl.gpu_to_gpu(u.node, u.base + q, v.node, v.base + q), chunk));
         }
-        AR = std::max(AR, ring_sim(taus, (int)(2 * (D - 1))));
+        if (compact) {
+          i64 slow = 0;
+          for (i64 x : taus) slow = std::max(slow, x);
+          sg.AR = std::max(sg.AR, 2 * (D - 1) * slow);
+        } else {
+          sg.AR = std::max(sg.AR, ring_sim(taus, (int)(2 * (D - 1))));
+        }
       }
-      cost.push_back(RS + AR);
-      seg_sc.push_back(sc);
+      out.push_back(sg);
     }
-    const int J = (int)cost.size();
-    // stage groups of every replica; FIFO per group (C.8 / S.1)
+    return out;
+  }
+
+  Plan plan_of(i64 i) const {
+    Plan p = decode(i);
+    place(p);
+    partition(p);
+    check_memory(p);
+    return p;
+  }
+
+  i64 eval(i64 i) const { return eval_mode(i, compact_mode != 0); }
+  i64 eval_mode(i64 i, bool compact) const {
+    if (i < 0 || i >= N) return INT64_MIN;
+    Plan p = plan_of(i);
+    if (p.status) return p.status;
+    const auto& cls = p.tpl->cls;
+    const int C = (int)cls.size(), b = p.tpl->b;
+
+    // steps 2-4: stage durations (C.5), p2p costs (C.6), 1F1B (C.7).
+    // literal: every replica, stage time = the sum over its layers of the
+    // layer-op chain.  compact: one pipeline per sub-class (replicas of the
+    // class with equal p2p vectors), m = the largest m of its replicas, stage
+    // time = l x chain.  owner[c][r] = index of the simulated pipeline that
+    // stands for replica r of class c.
+    std::vector<SimGroup> G;
+    std::vector<std::vector<size_t>> owner(C);
+    for (int c = 0; c < C; ++c) {
+      const int P = (int)cls[c].st.size();
+      std::vector<std::vector<i64>> cv(cls[c].D, std::vector<i64>(P > 1 ? P - 1 : 0));
+      for (int r = 0; r < cls[c].D; ++r)
+        for (int s = 0; s + 1 < P; ++s) {
+          // p2p per boundary: rank pairs i < min(t_s, t_{s+1}) in parallel (A8)
+          const Group& a = p.place[c][r][s];
+          const Group& z = p.place[c][r][s + 1];
+          const int np = std::min(cls[c].st[s].tp, cls[c].st[s + 1].tp);
+          i64 cs = 0;
+          for (int q = 0; q < np; ++q)
+            cs = std::max(cs, tau(cl.gpu_to_gpu(a.node, a.base + q, z.node, z.base + q), act_bytes(b)));
+          cv[r][s] = cs;
+        }
+      owner[c].assign(cls[c].D, 0);
+      std::vector<int> rep;  // compact: first replica of each sub-class
+      for (int r = 0; r < cls[c].D; ++r) {
+        int u = -1;
+        if (compact)
+          for (int k : rep)
+            if (cv[k] == cv[r]) u = k;
+        if (u >= 0) {  // replica r joins sub-class of replica u: the pipeline runs the larger m
+          const size_t base = owner[c][u];
+          owner[c][r] = base;
+          for (int s = 0; s < P; ++s) G[base + s].m = std::max(G[base + s].m, (int)p.mb[c][r]);
+          continue;
+        }
+        rep.push_back(r);
+        owner[c][r] = G.size();
+        for (int s = 0; s < P; ++s) {
+          const StageSpec& ss = cls[c].st[s];
+          const orc_type& ty = types[ss.type];
+          const Group& gr = p.place[c][r][s];
+          SimGroup g{};
+          g.P = P; g.s = s; g.m = (int)p.mb[c][r];
+          if (compact) {
+            g.f = p.layers[c][s] * layer_chain(ss, gr, b, 0, true);
+            g.g = p.layers[c][s] * layer_chain(ss, gr, b, 1, true);
+          } else {
+            for (i64 l = 0; l < p.layers[c][s]; ++l) {
+              g.f += layer_chain(ss, gr, b, 0, false);
+              g.g += layer_chain(ss, gr, b, 1, false);
+            }
+          }
+          if (s == 0) { g.f += op_dur(in, ty, EMB, false, ss.tp, b); g.g += op_dur(in, ty, EMB, true, ss.tp, b); }
+          if (s == P - 1) { g.f += op_dur(in, ty, HEAD, false, ss.tp, b); g.g += op_dur(in, ty, HEAD, true, ss.tp, b); }
+          g.c_prev = s > 0 ? cv[r][s - 1] : 0;
+          g.c_next = s + 1 < P ? cv[r][s] : 0;
+          G.push_back(g);
+        }
+      }
+    }
+    const i64 T0 = run_pipelines(G);
+
+    // step 5: gradient sync (A19, C.8; S.1 when sync_overlap)
+    i64 D = 0;
+    for (auto& c : cls) D += c.D;
+    if (D == 1) return T0;
+    const std::vector<Seg> sg = segments(p, compact);
+    const int J = (int)sg.size();
+    // FIFO per stage group: free time of stage s of replica r of class c.  In
+    // compact mode the replicas of a class share one clock per stage (every
+    // segment involves every replica).
     std::vector<std::vector<std::vector<i64>>> freet(C);
     i64 Titer = T0;
+    for (int c = 0; c < C; ++c)
+      freet[c].assign(compact ? 1 : cls[c].D, std::vector<i64>(cls[c].st.size(), in.sync_overlap ? 0 : T0));
+    auto ready = [&](int c, int r, int s) -> i64 {  // S.1: end of the group's last backward
+      return in.sync_overlap ? G[owner[c][r] + s].done : 0;
+    };
+    auto run_seg = [&](int j) {
+      i64 st = 0;
+      for (int c = 0; c < C; ++c)
+        for (int r = 0; r < cls[c].D; ++r) {
+          const int s = sg[j].sc[c];
+          st = std::max(st, std::max(ready(c, r, s), freet[c][compact ? 0 : r][s]));
+        }
+      const i64 en = st + sg[j].RS + sg[j].AR;
+      for (int c = 0; c < C; ++c)
+        for (auto& fr : freet[c]) fr[sg[j].sc[c]] = en;
+      Titer = std::max(Titer, en);
+    };
     if (!in.sync_overlap) {
       // C.8: barrier at T0, segments in ascending layer order
-      for (int c = 0; c < C; ++c) freet[c].assign(cls[c].D, std::vector<i64>(cls[c].st.size(), T0));
-      for (int j = 0; j < J; ++j) {
-        i64 st = 0;
-        for (int c = 0; c < C; ++c)
-          for (int r = 0; r < cls[c].D; ++r) st = std::max(st, freet[c][r][seg_sc[j][c]]);
-        const i64 en = st + cost[j];
-        for (int c = 0; c < C; ++c)
-          for (int r = 0; r < cls[c].D; ++r) freet[c][r][seg_sc[j][c]] = en;
-        Titer = std::max(Titer, en);
-      }
+      for (int j = 0; j < J; ++j) run_seg(j);
     } else {
       // S.1 (Table 1: DP sync is exposed in the backward pass,
       // PAPER.md:100-101): no barrier -- segment j is ready once every group
       // holding its layers, in every replica, has ended its last backward op;
       // segments are issued in descending layer order (the order backward
       // produces gradients), FIFO per group.
-      size_t gi = 0;
-      std::vector<std::vector<std::vector<i64>>> lastB(C);
-      for (int c = 0; c < C; ++c) {
-        const int P = (int)cls[c].st.size();
-        lastB[c].assign(cls[c].D, std::vector<i64>(P, 0));
-        for (int r = 0; r < cls[c].D; ++r)
-          for (int s = 0; s < P; ++s) lastB[c][r][s] = G[gi++].done;
-        freet[c].assign(cls[c].D, std::vector<i64>(P, 0));
-      }
-      for (int j = J - 1; j >= 0; --j) {
-        i64 st = 0;
-        for (int c = 0; c < C; ++c)
-          for (int r = 0; r < cls[c].D; ++r)
-            st = std::max(st, std::max(lastB[c][r][seg_sc[j][c]], freet[c][r][seg_sc[j][c]]));
-        const i64 en = st + cost[j];
-        for (int c = 0; c < C; ++c)
-          for (int r = 0; r < cls[c].D; ++r) freet[c][r][seg_sc[j][c]] = en;
-        Titer = std::max(Titer, en);
-      }
+      for (int j = J - 1; j >= 0; --j) run_seg(j);
     }
     return Titer;
   }
@@ -802,6 +874,8 @@ i64 orc_template_prefix(void* h, i64 k) {
   return k == (i64)o->tpls.size() ? o->N : o->tpls[k].prefix;
 }
 i64 orc_eval(void* h, i64 i) { return ((Oracle*)h)->eval(i); }
+// 0 = literal (default), 1 = compact (header comment)
+void orc_set_compact(void* h, int compact) { ((Oracle*)h)->compact_mode = compact ? 1 : 0; }
 
 // Evaluates idx[0..n) (or the range [first, first+n) if idx == NULL) on
 // `threads` host threads.
@@ -900,6 +974,39 @@ i64 orc_segment_bytes(void* h, i64 n_layers, int has_first, int has_last) {
   if (has_first) S += in.V * in.h * in.bpe_grad;
   if (has_last) S += (in.V * in.h * (in.tied ? 0 : 1) + in.h) * in.bpe_grad;
   return S;
+}
+// TP all-reduce (A16) of a stage group (node, base, tp) at micro-batch size b:
+// literal ring; EP all-to-all (A17) of the same group
+i64 orc_tp_allreduce(void* h, int node, int base, int tp, int b) {
+  return ((Oracle*)h)->tp_allreduce(Group{node, base}, tp, b);
+}
+i64 orc_ep_alltoall(void* h, int node, int base, int tp, int b) {
+  return ((Oracle*)h)->ep_alltoall(Group{node, base}, tp, b);
+}
+// gradient-sync segments of candidate i (C.6): per segment a, z, S, t*, RS, AR
+// (6 int64 each, literal mode); returns J, or -J - 1 if cap is too small, or
+// the candidate's negative status
+int orc_segments(void* h, i64 i, i64* out, int cap) {
+  Oracle* o = (Oracle*)h;
+  if (i < 0 || i >= o->N) return INT32_MIN;
+  Plan p = o->plan_of(i);
+  if (p.status) return p.status;
+  const auto sg = o->segments(p, false);
+  if ((int)sg.size() > cap) return -(int)sg.size() - 1;
+  for (size_t j = 0; j < sg.size(); ++j) {
+    i64* r = out + 6 * j;
+    r[0] = sg[j].a; r[1] = sg[j].z; r[2] = sg[j].S; r[3] = sg[j].tstar; r[4] = sg[j].RS; r[5] = sg[j].AR;
+  }
+  return (int)sg.size();
+}
+// Resharding decision (§2 "Resharding"): the synchronisation
+// of a source and a destination DP group needs resharding iff (1) their
+// micro-batch sizes differ or (2) their TP degrees differ; communication that
+// is pipeline-sequential (PP only) never does.  Cost model: condition (2) is
+// the reshard term RS of C.6 / A14; condition (1) is flagged only (A15).
+int orc_needs_reshard(int src_tp, int src_mb, int dst_tp, int dst_mb, int pp_only) {
+  if (pp_only) return 0;
+  return (src_mb != dst_mb || src_tp != dst_tp) ? 1 : 0;
 }
 i64 orc_act_bytes(void* h, int b) { return ((Oracle*)h)->act_bytes(b); }
 // link between two GPUs (node, local rank) -> alpha, beta

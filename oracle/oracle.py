@@ -111,6 +111,14 @@ def lib():
         L.orc_segment_bytes.argtypes = [C.c_void_p, C.c_int64, C.c_int, C.c_int]
         L.orc_act_bytes.restype = C.c_int64
         L.orc_act_bytes.argtypes = [C.c_void_p, C.c_int]
+        L.orc_set_compact.argtypes = [C.c_void_p, C.c_int]
+        for f in ("orc_tp_allreduce", "orc_ep_alltoall"):
+            getattr(L, f).restype = C.c_int64
+            getattr(L, f).argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int]
+        L.orc_segments.restype = C.c_int
+        L.orc_segments.argtypes = [C.c_void_p, C.c_int64, C.c_void_p, C.c_int]
+        L.orc_needs_reshard.restype = C.c_int
+        L.orc_needs_reshard.argtypes = [C.c_int] * 5
         L.orc_device_bytes.restype = C.c_int64
         L.orc_device_bytes.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int64, C.c_int64, C.c_int]
     return _lib
@@ -123,7 +131,10 @@ def _i64(a):
 class Oracle:
     """The reference simulator for one workload dict (hsim_inputs.configs)."""
 
-    def __init__(self, cfg):
+    def __init__(self, cfg, compact=False):
+        """compact=True selects the oracle's compact mode (one pipeline per
+        sub-class, closed-form ring steps; oracle.cpp header) -- equal to the
+        literal mode by tests/test_oracle_compact.py."""
         self.cfg = cfg
         cl, md, se = cfg["cluster"], cfg["model"], cfg["search"]
         nt = len(cl["types"])
@@ -175,6 +186,8 @@ class Oracle:
         self.h = lib().orc_create(C.byref(I))
         if not self.h:
             raise ValueError(lib().orc_last_error().decode())
+        lib().orc_set_compact(self.h, int(compact))
+        self.compact = bool(compact)
 
     def __del__(self):
         if getattr(self, "h", None) and _lib is not None:
@@ -232,6 +245,21 @@ class Oracle:
         """DESIGN M.1: bytes one device of stage s (of P) needs (f2 memory check)."""
         return lib().orc_device_bytes(self.h, type_idx, tp, P, s, layers, mb, b)
 
+    def tp_allreduce(self, node, base, tp, b):
+        return lib().orc_tp_allreduce(self.h, node, base, tp, b)
+
+    def ep_alltoall(self, node, base, tp, b):
+        return lib().orc_ep_alltoall(self.h, node, base, tp, b)
+
+    def segments(self, i):
+        """Gradient-sync segments of candidate i: list of dicts a, z, S, tstar, RS, AR."""
+        buf = np.zeros(6 * 256, dtype=np.int64)
+        J = lib().orc_segments(self.h, int(i), buf.ctypes.data, 256)
+        if J < 0:
+            raise ValueError(f"candidate {i}: status {J}")
+        keys = ("a", "z", "S", "tstar", "RS", "AR")
+        return [dict(zip(keys, (int(x) for x in buf[6 * j:6 * j + 6]))) for j in range(J)]
+
     def act_bytes(self, b):
         return lib().orc_act_bytes(self.h, b)
 
@@ -255,6 +283,10 @@ def pipeline(f, g, c, m):
     P = len(f)
     c = _i64(list(c) + [0]) if P > 1 else _i64([0])
     return lib().orc_pipeline(P, m, f.ctypes.data, g.ctypes.data, c.ctypes.data)
+
+
+def needs_reshard(src_tp, src_mb, dst_tp, dst_mb, pp_only=False):
+    return bool(lib().orc_needs_reshard(src_tp, src_mb, dst_tp, dst_mb, int(pp_only)))
 
 
 def hamilton(n, w):
