@@ -143,6 +143,31 @@ def tiny_random(seed):
     return {"name": f"tiny-{seed}", "cluster": cl, "model": md, "search": se}
 
 
+def deep_tiny(variant=0):
+    """Deep pipelines for the lane-per-stage kernels (16 < P <= 32 and
+    32 < P <= 64): 4 A100 + 4 H100 nodes of 8 GPUs, a small 64-layer model,
+    pipeline depths 17..32 per type (MIXED pipelines reach 34..64 stages),
+    long steady regimes (M = 256 with b = 1).  variant 1: a100-pcie (bridge
+    pairs) instead of A100 SXM, so p2p costs differ between boundaries."""
+    first = presets.a100_pcie() if variant else presets.a100_sxm()
+    cl = _cluster([first, presets.h100_sxm()], [4, 4], 200)
+    md = _model(64, 256, 4, 4, 1024, 2, 128, 2000, True, 256)
+    se = _search([1, 4], [[1, 2], [1]], [17, 20, 24, 31, 32], homo=1, mixed=1,
+                 use_all=0, r_layer=1, pmax=2, r_batch=1)
+    return {"name": f"deep-tiny-{variant}", "cluster": cl, "model": md, "search": se}
+
+
+def four_types_tiny():
+    """Four device types (A100, H100, B200, A100-PCIe), one 4-GPU node each:
+    HOMO templates with up to four classes (the 4-class partition path)."""
+    cl = _cluster([presets.a100_sxm(4), presets.h100_sxm(4), presets.b200(4), presets.a100_pcie(4)],
+                  [1, 1, 1, 1], 200)
+    md = _model(8, 256, 4, 4, 1024, 2, 128, 2000, False, 16)
+    se = _search([2], [[1]] * 4, [1, 2], homo=1, mixed=0,
+                 use_all=0, r_layer=0, pmax=0, r_batch=1)
+    return {"name": "four-types-tiny", "cluster": cl, "model": md, "search": se}
+
+
 def with_changes(cfg, **paths):
     """Copy of cfg with dotted-path overrides, e.g. ``model__global_batch=64``."""
     out = copy.deepcopy(cfg)

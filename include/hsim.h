@@ -20,10 +20,20 @@
  *     them.  No pointer passed to hsim_create is retained.
  *   - Device buffers (out_ns, out_t_ns, out_idx, cands.idx) are caller-owned
  *     CUDA device memory; `stream` is a cudaStream_t passed as void* (0 = the
- *     legacy default stream).  hsim_eval_batch / hsim_topk only enqueue work;
- *     launch errors return HSIM_ECUDA, asynchronous faults surface at the
- *     caller's next synchronisation.
- *   - A handle may be used by one host thread at a time (it owns scratch).
+ *     legacy default stream).  hsim_eval_batch / hsim_topk enqueue their
+ *     kernels and return; they do not wait for the GPU, with one bounded
+ *     exception: a block-cyclic list (cands.block > 0) stages its chunk plan
+ *     (16 B per block) through a ring of 4 pinned host buffers, so the host
+ *     waits if the copy issued 4 such calls earlier has not run yet.  Launch
+ *     errors return HSIM_ECUDA; asynchronous faults surface at the caller's
+ *     next synchronisation.
+ *   - Streams: the handle owns scratch and side streams.  Consecutive calls on
+ *     one handle are ordered on the device even when the caller passes
+ *     different streams (each call waits for the previous call's completion
+ *     event); the caller's outputs are complete when its `stream` reaches the
+ *     point after the call.
+ *   - A handle may be used by one host thread at a time.  Different handles
+ *     are independent (any thread, any device current at hsim_create).
  *   - Errors: a non-zero hsim_status; hsim_last_error() (thread-local) holds a
  *     one-line message naming the SPEC.md error kind where one applies
  *     (MissingField / InvalidValue / DivisibilityViolation, SPEC.md:63;
@@ -187,9 +197,13 @@ int hsim_merge_topk(const int64_t* lists, int32_t nlists, int32_t k, int64_t* ou
 /* Number of device kernels the last hsim_eval_batch / hsim_topk call launched. */
 int32_t hsim_last_launch_count(const hsim_handle* h);
 
-/* Algorithmic work counters of candidate list (host, exact): sum over the
- * candidates of 1F1B cells (2 * P_u * m_u per simulated pipeline) — used for
- * the ALU-roofline fraction.  Returns -1 on error. */
+/* Executed 1F1B max-plus cells of the candidates [first, first + n): runs the
+ * same device kernels as hsim_eval_batch in a counting mode on the legacy
+ * default stream and blocks until they finish.  A pipeline of P stages and m
+ * micro-batches has 2 P m cells; the exact steady-regime jumps of DESIGN.md §5
+ * skip some of them, and only the cells actually executed are counted (this is
+ * the numerator of the ALU-roofline fraction in bench.py).  A re-queued job
+ * (lane compaction) is counted once, by its complete run.  Returns -1 on error. */
 int64_t hsim_count_cells(const hsim_handle* h, int64_t first, int64_t n);
 
 /* Message of the last failing call on this thread ("" if none). */

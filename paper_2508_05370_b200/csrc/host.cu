@@ -98,8 +98,14 @@ struct hsim_handle {
   int32_t* d_bucket = nullptr;
   i64* d_cprefix = nullptr;
   int32_t* d_cbucket = nullptr;
-  i64* h_plan = nullptr;        // pinned host staging of the per-call chunk plan
-  size_t h_plan_cap = 0;
+  static constexpr int NPLAN = 4;   // ring of pinned chunk-plan staging buffers (block-cyclic lists)
+  i64* h_plan[NPLAN] = {};
+  size_t h_plan_cap[NPLAN] = {};
+  int plan_slot = 0;
+  cudaEvent_t ev_plan[NPLAN] = {};
+  cudaEvent_t ev_done = nullptr;  // end of the last call's work (orders calls made on different streams)
+  bool done_recorded = false;
+  int grid_cache[64] = {};        // resident blocks per SM per kernel (kernels.cu), per handle
   u64* d_xmask = nullptr;
   std::vector<u64> xmask_cross, xmask_same;
   i64* d_work = nullptr;      // work counter + per-range plan (kernels.cu)
@@ -114,7 +120,7 @@ struct hsim_handle {
   i64* d_cells = nullptr;
   static constexpr int NSIDE = 20, NEV = 48;
   cudaStream_t side[NSIDE] = {};     // one stream per phase-kernel type + the final stream
-  cudaEvent_t ev_fork = nullptr, ev_join[NSIDE] = {}, ev_plan = nullptr, ev_pool[NEV] = {};
+  cudaEvent_t ev_fork = nullptr, ev_join[NSIDE] = {}, ev_pool[NEV] = {};
   int32_t last_launches = 0;
   int sm_count = 148;
 
@@ -209,6 +215,7 @@ void hsim_handle::validate() {
   for (int t = 0; t < c.n_device_types; ++t)
     if (m.tpset_mask[t] & ~0xF) fail(HSIM_EINVAL, "InvalidValue: tpset_mask allows TP 1, 2, 4, 8 only");
   if (m.r_layer < 0 || m.r_batch < 0 || m.r_layer > 8 || m.r_batch > 8) fail(HSIM_EINVAL, "InvalidValue: radii");
+  if (m.pmax_perturb < 0 || m.pmax_perturb > MAXP) fail(HSIM_EINVAL, "InvalidValue: pmax_perturb must be 0..64");
   if (m.homo && c.n_device_types > MAXC) fail(HSIM_EINVAL, "InvalidValue: too many classes");
 }
 
@@ -475,12 +482,15 @@ void hsim_handle::enumerate() {
            md.kv_heads % tp == 0;
   };
   const i64 rl = 2 * md.r_layer + 1, rb = 2 * md.r_batch + 1;
+  // mixed radix of a template; saturates at 2^31 (rejected below) so no
+  // product can overflow whatever pmax_perturb / P are
   auto radix_of = [&](const std::vector<int>& Ps) {
+    const i64 cap = (i64)1 << 31;
     i64 r = 1;
     for (int P : Ps)
       if (P <= md.pmax_perturb)
-        for (int k = 0; k + 1 < P; ++k) r *= rl;
-    for (size_t k = 0; k + 1 < Ps.size(); ++k) r *= rb;
+        for (int k = 0; k + 1 < P; ++k) r = std::min(cap, r * rl);
+    for (size_t k = 0; k + 1 < Ps.size(); ++k) r = std::min(cap, r * rb);
     return r;
   };
   i64 acc = 0;
@@ -493,6 +503,8 @@ void hsim_handle::enumerate() {
       std::vector<int> Ps;
       for (auto& c : classes) { Dt += c.first; Ps.push_back((int)c.second.size()); }
       if (M < Dt) return;
+      const i64 R = radix_of(Ps);  // before crec(): its u32 digit radix must not wrap
+      if (R >= ((i64)1 << 31)) fail(HSIM_ERANGE, "template radix exceeds 2^31");
       TplRec r{};
       r.prefix = acc;
       r.rD = 1.0 / (double)Dt;
@@ -504,16 +516,13 @@ void hsim_handle::enumerate() {
       int cnt[33] = {0};
       for (auto& cl : classes) cnt[std::min<int>((int)cl.second.size(), 32)]++;
       for (int q = 0; q <= FASTP; ++q) pcnt_max[q] = std::max(pcnt_max[q], cnt[q]);
-      const i64 Rt = radix_of(Ps);
-      for (int q = 0; q <= FASTP; ++q) depth_jobs_space[q] += Rt * cnt[q];
+      for (int q = 0; q <= FASTP; ++q) depth_jobs_space[q] += R * cnt[q];
       pmask_all |= r.pmask;
       {
         int sp = 0;
         for (int P : Ps) sp += P;
         stages_max = std::max(stages_max, sp);
       }
-      const i64 R = radix_of(Ps);
-      if (R >= ((i64)1 << 31)) fail(HSIM_ERANGE, "template radix exceeds 2^31");
       tpl.push_back(r);
       prefix.push_back(acc);
       acc += R;
@@ -751,7 +760,8 @@ void hsim_handle::upload() {
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, dev);
   ck(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming), "cudaEventCreate");
-  ck(cudaEventCreateWithFlags(&ev_plan, cudaEventDisableTiming), "cudaEventCreate");
+  for (int q = 0; q < NPLAN; ++q) ck(cudaEventCreateWithFlags(&ev_plan[q], cudaEventDisableTiming), "cudaEventCreate");
+  ck(cudaEventCreateWithFlags(&ev_done, cudaEventDisableTiming), "cudaEventCreate");
   for (int q = 0; q < NEV; ++q) ck(cudaEventCreateWithFlags(&ev_pool[q], cudaEventDisableTiming), "cudaEventCreate");
   // latency-bound phase kernels (deep 1F1B chains: K_pipe<P >= 9> on streams
   // 9..16, K_deep on 17) get the highest stream priority so their few
@@ -844,7 +854,8 @@ void hsim_destroy(hsim_handle* h) {
   cudaFree(h->d_bucket);
   cudaFree(h->d_cprefix);
   cudaFree(h->d_cbucket);
-  if (h->h_plan) cudaFreeHost(h->h_plan);
+  for (int q = 0; q < hsim_handle::NPLAN; ++q)
+    if (h->h_plan[q]) cudaFreeHost(h->h_plan[q]);
   cudaFree(h->d_xmask);
   cudaFree(h->d_work);
   cudaFree(h->d_tpl);
@@ -858,7 +869,9 @@ void hsim_destroy(hsim_handle* h) {
     if (h->ev_join[q]) cudaEventDestroy(h->ev_join[q]);
   }
   if (h->ev_fork) cudaEventDestroy(h->ev_fork);
-  if (h->ev_plan) cudaEventDestroy(h->ev_plan);
+  for (int q = 0; q < hsim_handle::NPLAN; ++q)
+    if (h->ev_plan[q]) cudaEventDestroy(h->ev_plan[q]);
+  if (h->ev_done) cudaEventDestroy(h->ev_done);
   for (int q = 0; q < hsim_handle::NEV; ++q)
     if (h->ev_pool[q]) cudaEventDestroy(h->ev_pool[q]);
   delete h;
@@ -998,18 +1011,23 @@ static i64 host_chunk_of(const hsim_handle* h, i64 i) {
 }
 // Per-call chunk plan of a range / block-cyclic candidate list: for range r,
 // c0[r] = chunk of its first candidate and pre[r] = #chunks of ranges < r.
-// Written to a pinned host buffer [c0 (nr) | pre (nr + 1)]; returns the total.
-i64 host_plan(hsim_handle* h, i64 first, i64 block, i64 stride, i64 n, i64 nr, i64** buf) {
+// Written to one of NPLAN pinned host buffers [c0 (nr) | pre (nr + 1)] (a
+// ring: the host waits only if the buffer's copy from NPLAN calls ago has not
+// run yet); *ev = the event to record after the copy.  Returns the total.
+i64 host_plan(hsim_handle* h, i64 first, i64 block, i64 stride, i64 n, i64 nr, i64** buf, cudaEvent_t* ev) {
+  const int q = h->plan_slot;
+  h->plan_slot = (q + 1) % hsim_handle::NPLAN;
+  cudaEventSynchronize(h->ev_plan[q]);  // that buffer's previous H2D copy has been consumed
   const size_t need = (size_t)(2 * nr + 1);
-  if (need > h->h_plan_cap) {
-    if (h->h_plan) cudaFreeHost(h->h_plan);
-    h->h_plan = nullptr;
-    h->h_plan_cap = 0;
-    if (cudaMallocHost(&h->h_plan, need * 8) != cudaSuccess) return -1;
-    h->h_plan_cap = need;
+  if (need > h->h_plan_cap[q]) {
+    if (h->h_plan[q]) cudaFreeHost(h->h_plan[q]);
+    h->h_plan[q] = nullptr;
+    h->h_plan_cap[q] = 0;
+    if (cudaMallocHost(&h->h_plan[q], need * 8) != cudaSuccess) return -1;
+    h->h_plan_cap[q] = need;
   }
-  i64* c0 = h->h_plan;
-  i64* pre = h->h_plan + nr;
+  i64* c0 = h->h_plan[q];
+  i64* pre = h->h_plan[q] + nr;
   i64 acc = 0;
   for (i64 r = 0; r < nr; ++r) {
     const i64 start = block ? first + r * stride : first;
@@ -1019,13 +1037,28 @@ i64 host_plan(hsim_handle* h, i64 first, i64 block, i64 stride, i64 n, i64 nr, i
     acc += host_chunk_of(h, start + len - 1) - c0[r] + 1;
   }
   pre[nr] = acc;
-  *buf = h->h_plan;
+  *buf = h->h_plan[q];
+  *ev = h->ev_plan[q];
   return acc;
 }
+// chunk range [c0, c0 + count) of one contiguous candidate range (no staging)
+i64 range_chunks(const hsim_handle* h, i64 first, i64 n, i64* c0) {
+  *c0 = host_chunk_of(h, first);
+  return host_chunk_of(h, first + n - 1) - *c0 + 1;
+}
+// per-handle cross-call ordering: a call waits for the previous call's work
+// (whatever stream it ran on) and records its own end
+void call_begin(hsim_handle* h, cudaStream_t st) {
+  if (h->done_recorded) cudaStreamWaitEvent(st, h->ev_done, 0);
+}
+void call_end(hsim_handle* h, cudaStream_t st) {
+  cudaEventRecord(h->ev_done, st);
+  h->done_recorded = true;
+}
+int* grid_cache(hsim_handle* h) { return h->grid_cache; }
 uint32_t depth_mask(const hsim_handle* h) { return h->pmask_all; }
 cudaStream_t side_stream(const hsim_handle* h, int q) { return h->side[q % hsim_handle::NSIDE]; }
 cudaEvent_t fork_event(const hsim_handle* h) { return h->ev_fork; }
-cudaEvent_t plan_event(const hsim_handle* h) { return h->ev_plan; }
 cudaEvent_t pool_event(const hsim_handle* h, int q) { return h->ev_pool[q % hsim_handle::NEV]; }
 cudaEvent_t join_event(const hsim_handle* h, int q) { return h->ev_join[q % hsim_handle::NSIDE]; }
 int depth_jobs_max(const hsim_handle* h, int P) { return P >= 0 && P <= FASTP ? h->pcnt_max[P] : 0; }

@@ -47,10 +47,13 @@ int sync_overlap(const hsim_handle* h);
 cudaStream_t side_stream(const hsim_handle* h, int q);
 cudaEvent_t fork_event(const hsim_handle* h);
 cudaEvent_t join_event(const hsim_handle* h, int q);
-cudaEvent_t plan_event(const hsim_handle* h);
 cudaEvent_t pool_event(const hsim_handle* h, int q);
 constexpr int NSTREAM_FINAL = 19;
-i64 host_plan(hsim_handle* h, i64 first, i64 block, i64 stride, i64 n, i64 nr, i64** buf);
+i64 host_plan(hsim_handle* h, i64 first, i64 block, i64 stride, i64 n, i64 nr, i64** buf, cudaEvent_t* ev);
+i64 range_chunks(const hsim_handle* h, i64 first, i64 n, i64* c0);
+void call_begin(hsim_handle* h, cudaStream_t st);
+void call_end(hsim_handle* h, cudaStream_t st);
+int* grid_cache(hsim_handle* h);
 void set_launches(hsim_handle* h, int n);
 void set_error(const char* m);
 
@@ -100,7 +103,7 @@ struct Trace {
     n = 0;
   }
 };
-static Trace g_trace;
+static thread_local Trace g_trace;  // diagnostics only (HSIM_TRACE=1)
 
 constexpr int NT = 128;              // threads per block (phase kernels)
 constexpr int MT = 256;              // threads of K_merge
@@ -128,8 +131,9 @@ static_assert(FASTP <= 16, "counter layout");
 struct Cands {
   const i64* idx;
   i64 first, block, stride, n;
-  const i64* plan;   // device [c0 (nr) | pre (nr + 1)] (range / block-cyclic)
+  const i64* plan;   // device [c0 (nr) | pre (nr + 1)] (block-cyclic lists)
   i64 nr;
+  i64 c0;            // contiguous range (block == 0): chunk of its first candidate (no staged plan)
 };
 
 __device__ __forceinline__ i64 cand_index(const Cands& c, i64 t) {
@@ -230,10 +234,13 @@ __global__ void __launch_bounds__(NT, HSIM_SPLIT_MINB) k_split(const Tables* __r
         t = -1;
       }
     } else {
-      const i64* c0 = c.plan;
-      const i64* pre = c.plan + c.nr;
-      const i64 r = bsearch_le(pre, c.nr, item);
-      const i64 g = c0[r] + (item - pre[r]);
+      i64 r = 0, g = c.c0 + item;
+      if (c.block) {
+        const i64* c0 = c.plan;
+        const i64* pre = c.plan + c.nr;
+        r = bsearch_le(pre, c.nr, item);
+        g = c0[r] + (item - pre[r]);
+      }
       const i64 tg = find_template_of_chunk(sT, g);
       const i64 lo = sT.tpl_prefix[tg] + (g - sT.tpl_cprefix[tg]) * CHUNK;
       const i64 start = c.block ? c.first + r * c.stride : c.first;
@@ -1184,10 +1191,14 @@ static int grid_of(const hsim_handle* h, K kern, int& cache) {
 }
 
 static void merge_attr() {
-  static bool attr = false;
-  if (!attr) {
+  // per device (the attribute is per device); idempotent, so a race between
+  // host threads only repeats the call
+  static int attr_dev[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 64 && !attr_dev[dev]) {
     cudaFuncSetAttribute(k_merge, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(TopK));
-    attr = true;
+    attr_dev[dev] = 1;
   }
 }
 
@@ -1210,17 +1221,23 @@ static int final_grid(const hsim_handle* h, int k) { return sm_count(h) * (k && 
 // count optional.
 static int run_phases(hsim_handle* h, const Tables* dT, Cands c, int64_t n, int64_t* out_ns, int32_t k, i64* lists,
                       int count, i64* cells_out, cudaStream_t st, int& launches) {
-  static int g_split = 0, g_pipe[FASTP + 1] = {0}, g_cont[FASTP + 1] = {0}, g_deep = 0, g_sync = 0;
+  // resident blocks per SM of each kernel, cached per handle
+  int* gc = grid_cache(h);
+  int &g_split = gc[0], &g_deep = gc[1], &g_sync = gc[2], *g_pipe = gc + 3, *g_cont = gc + 3 + FASTP + 1;
+  static_assert(3 + 2 * (FASTP + 1) <= 64, "grid cache");
   // chunk plan
   i64 nchunks;
   i64* hplan = nullptr;
+  cudaEvent_t plan_ev = nullptr;
   if (c.idx) {
     nchunks = (n + 31) / 32;
     c.nr = 0;
+  } else if (!c.block) {
+    c.nr = 1;
+    nchunks = range_chunks(h, c.first, n, &c.c0);
   } else {
-    c.nr = c.block ? (n + c.block - 1) / c.block : 1;
-    cudaEventSynchronize(plan_event(h));  // the pinned plan buffer is free again
-    nchunks = host_plan(h, c.first, c.block, c.stride, n, c.nr, &hplan);
+    c.nr = (n + c.block - 1) / c.block;
+    nchunks = host_plan(h, c.first, c.block, c.stride, n, c.nr, &hplan, &plan_ev);
     if (nchunks < 0) return HSIM_ENOMEM;
   }
   // batches of chunks, double-buffered: batch b+1's K_split overlaps batch b's
@@ -1243,7 +1260,7 @@ static int run_phases(hsim_handle* h, const Tables* dT, Cands c, int64_t n, int6
     jobcap[P] = (pm >> P & 1) ? (size_t)depth_jobs_max(h, P) * ns : 0;
     jobw += 2 * jobcap[P];
   }
-  const size_t planw = c.idx ? 0 : (size_t)(2 * c.nr + 1);
+  const size_t planw = hplan ? (size_t)(2 * c.nr + 1) : 0;
   const size_t n32 = (size_t)(4 + 4 * MAXC) * ns + jobw;
   const size_t bufw0 = (size_t)(MAXC + 2) * ns + NCNT + (n32 + 1) / 2 + 8;
   size_t reqw = 0, reqcap[HSIM_REQ_MAXP + 1] = {0};
@@ -1290,10 +1307,10 @@ static int run_phases(hsim_handle* h, const Tables* dT, Cands c, int64_t n, int6
       pj += 2 * jobcap[P];
     }
   }
-  if (!c.idx) {
+  if (hplan) {
     i64* pw = base + NBUF * bufw;
     cudaMemcpyAsync(pw, hplan, planw * 8, cudaMemcpyHostToDevice, st);
-    cudaEventRecord(plan_event(h), st);
+    cudaEventRecord(plan_ev, st);
     c.plan = pw;
   }
   const int gs = grid_of(h, k_split, g_split), gd = grid_of(h, k_deep, g_deep), gy = grid_of(h, k_sync, g_sync),
@@ -1449,9 +1466,10 @@ int launch_merge(const int64_t* lists, int32_t nlists, int32_t k, int64_t* out_t
 
 int launch_eval(hsim_handle* h, const Tables* dT, const hsim_cands* cc, int64_t n, int64_t* out_ns, int32_t k,
                 int64_t* out_t, int64_t* out_i, cudaStream_t st) {
-  Cands c{cc->idx, cc->first, cc->block, cc->stride, n, nullptr, 0};
+  Cands c{cc->idx, cc->first, cc->block, cc->stride, n, nullptr, 0, 0};
   int launches = 0;
   i64* lists = nullptr;
+  call_begin(h, st);
   const int nlists = final_grid(h, k) * (k <= 32 ? 1 : NT / 32);  // per block (k <= 32) or per warp
   if (k) {
     if (ensure_block_scratch(h, (size_t)nlists * 2 * k + 1, &lists)) return HSIM_ENOMEM;
@@ -1473,18 +1491,21 @@ int launch_eval(hsim_handle* h, const Tables* dT, const hsim_cands* cc, int64_t 
     g_trace.post(tq, st);
     ++launches;
   }
+  call_end(h, st);
   g_trace.dump();
   return finish(h, launches);
 }
 
 int launch_count(hsim_handle* h, const Tables* dT, int64_t first, int64_t n, int64_t* d_acc, cudaStream_t st) {
-  Cands c{nullptr, first, 0, 0, n, nullptr, 0};
+  Cands c{nullptr, first, 0, 0, n, nullptr, 0, 0};
   int launches = 0;
   i64 total = 0;
+  call_begin(h, st);
   if (n > 0) {
     const int rc = run_phases(h, dT, c, n, nullptr, 0, nullptr, 1, &total, st, launches);
     if (rc) return rc;
   }
+  call_end(h, st);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     set_error(cudaGetErrorString(e));

@@ -40,15 +40,25 @@ def _device_merge(gathered, k, out):
 
 def sweep(sim, k, group=None, block=DEFAULT_BLOCK, stream=None, out=None, merge=None, device=None):
     """Global top-k (times, indices) over the whole space of `sim`, identical
-    on every rank.  Single process when torch.distributed is not initialised."""
+    on every rank.  Single process when torch.distributed is not initialised.
+
+    Everything -- the local top-k, the all_gather and the merge -- is queued on
+    `stream` (default: the current stream): the NCCL collective is issued with
+    `stream` as the current stream, so it waits for the local top-k."""
+    import contextlib
     world = dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
     rank = dist.get_rank(group) if world > 1 else 0
     first, n, blk, stride = shard(sim.space_size(), rank, world, block)
-    if world == 1:
-        return sim.topk(k, n=n, first=first, stream=stream, out=out)
     device = device or "cuda"
-    local = torch.empty(2 * k, dtype=torch.int64, device=device)
-    sim.topk(k, n=n, first=first, block=blk, stride=stride, stream=stream, out=(local[:k], local[k:]))
-    gathered = torch.empty(world * 2 * k, dtype=torch.int64, device=device)
-    dist.all_gather_into_tensor(gathered, local, group=group)
-    return (merge or _device_merge)(gathered.view(world, 2 * k), k, out)
+    on_gpu = torch.device(device).type == "cuda"
+    if on_gpu and stream is None:
+        stream = torch.cuda.current_stream()
+    ctx = torch.cuda.stream(stream) if on_gpu else contextlib.nullcontext()
+    with ctx:
+        if world == 1:
+            return sim.topk(k, n=n, first=first, stream=stream, out=out)
+        local = torch.empty(2 * k, dtype=torch.int64, device=device)
+        sim.topk(k, n=n, first=first, block=blk, stride=stride, stream=stream, out=(local[:k], local[k:]))
+        gathered = torch.empty(world * 2 * k, dtype=torch.int64, device=device)
+        dist.all_gather_into_tensor(gathered, local, group=group)
+        return (merge or _device_merge)(gathered.view(world, 2 * k), k, out)
