@@ -20,7 +20,7 @@ import time
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 BIN = os.path.join(ROOT, "tools", "alu_peak")
 SRC = os.path.join(ROOT, "tools", "alu_peak.cu")
-OUT = os.path.join(ROOT, "profiles", "alu_peak_r02.json")
+OUT = os.path.join(ROOT, "profiles", "r02", "alu_peak.json")
 METRICS = ["smsp__inst_executed.sum", "smsp__thread_inst_executed.sum", "sm__inst_executed_pipe_alu.sum",
            "sm__inst_executed_pipe_fma.sum", "sm__inst_executed_pipe_fp64.sum", "gpu__time_duration.sum"]
 NAMES = {"k_iadd": "iadd", "k_mix": "mix", "k_imax64": "imax64", "k_dcell": "dcell", "k_dadd": "dadd"}
