@@ -37,6 +37,8 @@
 // times are "parity unpinned" (the paper prints none).
 
 #include <algorithm>
+#include <array>
+#include <map>
 #include <atomic>
 #include <cmath>
 #include <cstdint>
@@ -187,6 +189,51 @@ i64 ring_sim(const std::vector<i64>& edge_tau, int steps) {
   i64 t = 0;
   for (i64 e : end) t = std::max(t, e);
   return t;
+}
+
+// --- f3 progressive filling (DESIGN F.1): nf flows over links; flow f uses
+// links inc[f][0..nfl[f]) of capacity linkcap[e] and is capped at cap[f]
+// (its own path); rates out.  share_e = residual_e / unfrozen_e (one IEEE
+// division); s = min(share over links with unfrozen flows, unfrozen caps);
+// every unfrozen flow on an argmin link or with cap == s freezes at s; each
+// link's residual -= (flows frozen on it) x s.
+void maxmin_fill(int nf, const std::vector<std::vector<int>>& inc, const std::map<int, double>& linkcap,
+                 const std::vector<double>& cap, std::vector<double>& rate) {
+  std::map<int, double> res;
+  std::map<int, int> cnt;
+  for (int f = 0; f < nf; ++f)
+    for (int e : inc[f]) {
+      res[e] = linkcap.at(e);
+      cnt[e] += 1;
+    }
+  std::vector<char> frozen(nf, 0);
+  int left = nf;
+  rate.assign(nf, 0.0);
+  while (left) {
+    double s = 1e300;
+    for (auto& kv : cnt)
+      if (kv.second > 0) s = std::min(s, res[kv.first] / kv.second);
+    for (int f = 0; f < nf; ++f)
+      if (!frozen[f]) s = std::min(s, cap[f]);
+    std::vector<int> fz;
+    for (int f = 0; f < nf; ++f) {
+      if (frozen[f]) continue;
+      bool hit = cap[f] == s;
+      for (int e : inc[f]) hit = hit || (cnt[e] > 0 && res[e] / cnt[e] == s);
+      if (hit) fz.push_back(f);
+    }
+    std::map<int, int> took;
+    for (int f : fz) {
+      frozen[f] = 1;
+      rate[f] = s;
+      for (int e : inc[f]) took[e] += 1;
+      --left;
+    }
+    for (auto& kv : took) {
+      res[kv.first] = res[kv.first] - (double)kv.second * s;
+      cnt[kv.first] -= kv.second;
+    }
+  }
 }
 
 // --- Hamilton / largest remainder (DESIGN C.4): ties -> lower index ----------
@@ -729,7 +776,7 @@ struct Oracle {
   }
 
   i64 eval(i64 i) const { return eval_mode(i, compact_mode != 0); }
-  i64 eval_mode(i64 i, bool compact) const {
+  i64 eval_mode(i64 i, bool compact, i64* T0_out = nullptr) const {
     if (i < 0 || i >= N) return INT64_MIN;
     Plan p = plan_of(i);
     if (p.status) return p.status;
@@ -797,6 +844,7 @@ struct Oracle {
       }
     }
     const i64 T0 = run_pipelines(G);
+    if (T0_out) *T0_out = T0;
 
     // step 5: gradient sync (A19, C.8; S.1 when sync_overlap)
     i64 D = 0;
@@ -838,6 +886,296 @@ struct Oracle {
       for (int j = J - 1; j >= 0; --j) run_seg(j);
     }
     return Titer;
+  }
+
+  // =====================================================================
+  // f3 (DESIGN F.1): flow-level contention re-simulation of
+  // a candidate's gradient synchronisation.  Every collective step of C.6 /
+  // C.8 becomes a set of flows on the rail-only link graph (SPEC.md:340-373
+  // build_topology / route / simulate_flows; "bandwidth
+  // contention", :400 FCT per flow, :409-412 the slowest flow gates a
+  // blocking collective) sharing directed links by progressive-filling
+  // max-min fairness.
+  //
+  // Links (directed, B/ns): per GPU (n, r) an NVLink egress and ingress port
+  // (capacity = the fastest intra-node path out of / into it), the PCIe path
+  // to its rail NIC and back (the gpu_nic path's beta), and the NIC's wire to
+  // the rail switch and back (min(NIC, rail port)); the NVSwitch and the rail
+  // fabric are non-blocking.  A flow from (n1, r1) to (n2, r2) uses: same node
+  // -> egress(n1,r1), ingress(n1,r2); other node, same rank -> pcie_up, nic_tx
+  // at (n1,r1), nic_rx, pcie_dn at (n2,r1); other node and rank (Fig 2 (c))
+  // -> egress(n1,r1), ingress(n1,r2), then the rail path of rank r2.  Its own
+  // path caps it at the alpha-beta link's beta (a private link), and its fixed
+  // latency is the link's alpha.
+  //
+  // Rates: progressive filling over the active flows -- share_e = residual_e
+  // / (unfrozen flows on e) (one IEEE division); s = min over links with
+  // unfrozen flows and over unfrozen flows' private caps; every unfrozen flow
+  // on an argmin link, or whose cap equals s, is frozen at rate s; each link's
+  // residual -= (number of flows frozen on it) x s; repeat.
+  // Time (integer ns): each active flow's time to drain d_f = max(0,
+  // ceil(rem_f / rate_f)); the next drain event is t + min d_f; at an event
+  // every flow with d_f == the minimum finishes (drain end = that time),
+  // every other flow keeps rem_f - rate_f x delta.  A flow's completion =
+  // drain end + alpha; FCT = completion - arrival.  Without contention a flow
+  // drains in ceilq(bytes, beta), so its FCT is the alpha-beta tau exactly.
+  //
+  // Schedule: C.8 (barrier at T0, segments FIFO per stage group in ascending
+  // layer order).  A segment is a sequence of synchronous steps -- the
+  // reshard step (when some class has tp != t*: every group with tp != t*
+  // sends ceil(S/t*) bytes over each of its TP-ring edges) and the 2(D-1)
+  // ring steps (for each ring q < t*, every ring position sends the chunk to
+  // the next) -- and a step's flows all arrive when the previous step's last
+  // flow completes (the blocking collective).  A segment starts when
+  // the previous segment of each of its groups has completed.  Output, time
+  // relative to T0: sync_ab (the same schedule with every step lasting its
+  // slowest flow's tau: the C.8 extra T_iter - T0) and sync_flow (the flow
+  // level schedule), plus every flow's FCT.
+  // =====================================================================
+  struct FFlow {
+    i64 bytes, alpha, arrive;
+    double cap, rem, rate;
+    int link[6], nl;
+    int step;       // global step id
+  };
+  struct FStep {
+    int seg, k;     // segment, index within it
+    std::vector<std::array<int, 4>> pairs;  // (n1, r1, n2, r2)
+    i64 bytes;
+  };
+
+  int gpn0() const { return cl.gpn[0]; }
+  int lid(int kind, int n, int r) const { return ((n * gpn0() + r) * 6) + kind; }  // 0 eg 1 in 2 up 3 dn 4 tx 5 rx
+  std::vector<double> ext_linkcap;  // orc_flow_sim only: explicit link capacities
+  double link_cap(int id) const {
+    if (!ext_linkcap.empty()) return ext_linkcap[id];
+    const int kind = id % 6, g = id / 6, n = g / gpn0(), r = g % gpn0();
+    const orc_type& t = T(n);
+    const i64 fr = in.frame_bytes;
+    if (kind <= 1) {
+      double c = 0;
+      for (int j = 0; j < t.gpus_per_node; ++j)
+        if (j != r) c = std::max(c, path_link(t.link_kind[kind == 0 ? t.intra_kind[r][j] : t.intra_kind[j][r]], fr).beta);
+      return c;
+    }
+    if (kind <= 3) return path_link(t.gpu_nic, fr).beta;
+    return std::min(t.nic_gbps / 8.0, in.rail_gbps / 8.0);
+  }
+  const orc_type& T(int n) const { return types[node_type[n]]; }
+  FFlow make_flow(int n1, int r1, int n2, int r2, i64 bytes) const {
+    FFlow f{};
+    const Link l = cl.gpu_to_gpu(n1, r1, n2, r2);
+    f.bytes = bytes;
+    f.alpha = l.alpha;
+    f.cap = l.beta;
+    f.rem = (double)bytes;
+    f.nl = 0;
+    if (n1 == n2) {
+      f.link[f.nl++] = lid(0, n1, r1);
+      f.link[f.nl++] = lid(1, n1, r2);
+    } else {
+      if (r1 != r2) {
+        f.link[f.nl++] = lid(0, n1, r1);
+        f.link[f.nl++] = lid(1, n1, r2);
+      }
+      f.link[f.nl++] = lid(2, n1, r2);
+      f.link[f.nl++] = lid(4, n1, r2);
+      f.link[f.nl++] = lid(5, n2, r2);
+      f.link[f.nl++] = lid(3, n2, r2);
+    }
+    return f;
+  }
+
+  // progressive filling (maxmin_fill) over the flows in `act`
+  void maxmin(std::vector<FFlow>& fl, const std::vector<int>& act) const {
+    std::vector<std::vector<int>> inc(act.size());
+    std::map<int, double> cap_of;
+    std::vector<double> cap(act.size()), rate;
+    for (size_t k = 0; k < act.size(); ++k) {
+      const FFlow& f = fl[act[k]];
+      inc[k].assign(f.link, f.link + f.nl);
+      for (int e : inc[k])
+        if (!cap_of.count(e)) cap_of[e] = link_cap(e);
+      cap[k] = f.cap;
+    }
+    maxmin_fill((int)act.size(), inc, cap_of, cap, rate);
+    for (size_t k = 0; k < act.size(); ++k) fl[act[k]].rate = rate[k];
+  }
+
+  // The fluid event engine: active flows drain at their max-min rates; timers
+  // (time, seq, tag) fire callbacks that may add flows.  At each step the
+  // earlier of the next drain completion and the next timer is processed; on
+  // a tie drains go first.  on_done(flow, completion) with completion = drain
+  // end + alpha; on_timer(tag, now).
+  struct FlowEngine {
+    const Oracle* o;
+    std::vector<FFlow> fl;
+    std::vector<int> act;
+    std::priority_queue<std::tuple<i64, i64, int>, std::vector<std::tuple<i64, i64, int>>, std::greater<>> tm;
+    i64 t = 0, seq = 0;
+    bool dirty = true;
+    void add(FFlow f, i64 now) {
+      f.arrive = now;
+      f.rem = (double)f.bytes;
+      act.push_back((int)fl.size());
+      fl.push_back(f);
+      dirty = true;
+    }
+    void timer(i64 when, int tag) { tm.push({when, seq++, tag}); }
+    template <typename OnDone, typename OnTimer>
+    void run(OnDone on_done, OnTimer on_timer) {
+      while (!act.empty() || !tm.empty()) {
+        if (dirty && !act.empty()) o->maxmin(fl, act);
+        dirty = false;
+        i64 dmin = INT64_MAX;
+        std::vector<i64> d(act.size());
+        for (size_t k = 0; k < act.size(); ++k) {
+          const FFlow& f = fl[act[k]];
+          d[k] = f.rem <= 0 ? 0 : (i64)std::ceil(f.rem / f.rate);
+          dmin = std::min(dmin, d[k]);
+        }
+        const i64 t_drain = act.empty() ? INT64_MAX : t + dmin;
+        const i64 t_ev = tm.empty() ? INT64_MAX : std::get<0>(tm.top());
+        if (t_drain <= t_ev) {
+          const double delta = (double)dmin;
+          std::vector<int> keep, done;
+          for (size_t k = 0; k < act.size(); ++k) {
+            FFlow& f = fl[act[k]];
+            if (d[k] == dmin) {
+              done.push_back(act[k]);
+            } else {
+              f.rem = f.rem - f.rate * delta;
+              keep.push_back(act[k]);
+            }
+          }
+          act.swap(keep);
+          t = t_drain;
+          dirty = true;
+          for (int x : done) on_done(fl[x], t + fl[x].alpha);
+        } else {
+          const double delta = (double)(t_ev - t);
+          for (int x : act) fl[x].rem = fl[x].rem - fl[x].rate * delta;
+          t = t_ev;
+          dirty = true;
+          while (!tm.empty() && std::get<0>(tm.top()) == t) {
+            const int tag = std::get<2>(tm.top());
+            tm.pop();
+            on_timer(tag, t);
+          }
+        }
+      }
+    }
+  };
+
+  // f3 for candidate i: returns status (0 ok, < 0 invalid); sync_ab, sync_flow
+  // relative to T0; fcts appended in completion order
+  int flow_resim(i64 i, i64& sync_ab, i64& sync_flow, std::vector<i64>& fcts) const {
+    sync_ab = sync_flow = 0;
+    if (i < 0 || i >= N) return INT32_MIN;
+    Plan p = plan_of(i);
+    if (p.status) return p.status;
+    const auto& cls = p.tpl->cls;
+    const int C = (int)cls.size();
+    i64 D = 0;
+    for (auto& c : cls) D += c.D;
+    if (D == 1) return 0;
+    const std::vector<Seg> sg = segments(p, false);
+    const int J = (int)sg.size();
+    // the steps of every segment
+    std::vector<FStep> steps;
+    std::vector<int> seg_first(J), seg_n(J);
+    for (int j = 0; j < J; ++j) {
+      seg_first[j] = (int)steps.size();
+      const i64 xs = ceil_div(sg[j].S, sg[j].tstar);
+      FStep rs{j, 0, {}, xs};
+      for (int c = 0; c < C; ++c) {
+        const int s = sg[j].sc[c], tp = cls[c].st[s].tp;
+        if (tp == sg[j].tstar) continue;
+        for (int r = 0; r < cls[c].D; ++r) {
+          const Group& g = p.place[c][r][s];
+          for (int q = 0; q < tp; ++q) rs.pairs.push_back({g.node, g.base + q, g.node, g.base + (q + 1) % tp});
+        }
+      }
+      if (!rs.pairs.empty()) steps.push_back(rs);
+      std::vector<Group> ring;
+      for (int c = 0; c < C; ++c)
+        for (int r = 0; r < cls[c].D; ++r) ring.push_back(p.place[c][r][sg[j].sc[c]]);
+      FStep st{j, 0, {}, ceil_div(xs, D)};
+      for (int q = 0; q < sg[j].tstar; ++q)
+        for (size_t k = 0; k < ring.size(); ++k) {
+          const Group& u = ring[k];
+          const Group& v = ring[(k + 1) % ring.size()];
+          st.pairs.push_back({u.node, u.base + q, v.node, v.base + q});
+        }
+      for (i64 k = 0; k < 2 * (D - 1); ++k) steps.push_back(st);
+      seg_n[j] = (int)steps.size() - seg_first[j];
+      for (int k = 0; k < seg_n[j]; ++k) steps[seg_first[j] + k].k = k;
+    }
+    // FIFO predecessors: the previous segment on each of its groups (every
+    // segment involves every replica of every class, so a group is (c, stage))
+    std::vector<std::vector<int>> preds(J);
+    for (int j = 0; j < J; ++j)
+      for (int jj = j - 1; jj >= 0; --jj) {
+        bool share = false;
+        for (int c = 0; c < C; ++c) share |= sg[jj].sc[c] == sg[j].sc[c];
+        if (share) {
+          bool already = false;
+          for (int x : preds[j]) already |= x == jj;
+          if (!already) preds[j].push_back(jj);
+        }
+      }
+    // alpha-beta schedule: a step lasts its slowest flow's tau
+    {
+      std::vector<i64> end(J, 0);
+      for (int j = 0; j < J; ++j) {
+        i64 t = 0;
+        for (int x : preds[j]) t = std::max(t, end[x]);
+        for (int k = 0; k < seg_n[j]; ++k) {
+          const FStep& st = steps[seg_first[j] + k];
+          i64 m = 0;
+          for (auto& pr : st.pairs) m = std::max(m, tau(cl.gpu_to_gpu(pr[0], pr[1], pr[2], pr[3]), st.bytes));
+          t += m;
+        }
+        end[j] = t;
+        sync_ab = std::max(sync_ab, t);
+      }
+    }
+    // flow level
+    std::vector<int> pending(steps.size(), 0);
+    std::vector<i64> step_done(steps.size(), 0);
+    std::vector<int> waiting(J, 0);  // unfinished predecessors
+    for (int j = 0; j < J; ++j) waiting[j] = (int)preds[j].size();
+    FlowEngine E{this};
+    auto start_step = [&](int id, i64 now) {
+      for (auto& pr : steps[id].pairs) {
+        FFlow f = make_flow(pr[0], pr[1], pr[2], pr[3], steps[id].bytes);
+        f.step = id;
+        E.add(f, now);
+      }
+      pending[id] = (int)steps[id].pairs.size();
+    };
+    for (int j = 0; j < J; ++j)
+      if (!waiting[j]) start_step(seg_first[j], 0);
+    E.run(
+        [&](const FFlow& f, i64 done) {  // a flow completed: its step ends with its last flow
+          fcts.push_back(done - f.arrive);
+          step_done[f.step] = std::max(step_done[f.step], done);
+          if (--pending[f.step] == 0) E.timer(step_done[f.step], f.step);
+        },
+        [&](int id, i64 now) {  // a step completed at `now`
+          const int j = steps[id].seg;
+          if (steps[id].k + 1 < seg_n[j]) {
+            start_step(id + 1, now);
+            return;
+          }
+          sync_flow = std::max(sync_flow, now);
+          for (int jj = j + 1; jj < J; ++jj) {
+            bool dep = false;
+            for (int x : preds[jj]) dep |= x == j;
+            if (dep && --waiting[jj] == 0) start_step(seg_first[jj], now);
+          }
+        });
+    return 0;
   }
 };
 
@@ -1007,6 +1345,54 @@ int orc_segments(void* h, i64 i, i64* out, int cap) {
 int orc_needs_reshard(int src_tp, int src_mb, int dst_tp, int dst_mb, int pp_only) {
   if (pp_only) return 0;
   return (src_mb != dst_mb || src_tp != dst_tp) ? 1 : 0;
+}
+// f3 (DESIGN F.1): out = {status, sync_ab, sync_flow, n_flows, T0, T_iter}; fct (may be
+// NULL) receives up to cap FCTs in completion order
+void orc_flow_resim(void* h, i64 i, i64* out, i64* fct, i64 cap) {
+  i64 ab = 0, fw = 0, T0 = 0;
+  std::vector<i64> f;
+  const int st = ((Oracle*)h)->flow_resim(i, ab, fw, f);
+  const i64 T = st ? st : ((Oracle*)h)->eval_mode(i, true, &T0);
+  out[0] = st; out[1] = ab; out[2] = fw; out[3] = (i64)f.size(); out[4] = st ? 0 : T0; out[5] = T;
+  if (fct)
+    for (i64 k = 0; k < std::min<i64>(cap, (i64)f.size()); ++k) fct[k] = f[k];
+}
+// f3 building block: independent flows through the same fluid engine.  Flow f
+// arrives at arrive[f] with bytes[f], fixed latency alpha[f], private cap
+// cap[f] and links inc[f * maxl + q] (q < nfl[f]) of capacity linkcap[e];
+// completion times (drain end + alpha) out.
+void orc_flow_sim(void* h, int nf, const double* linkcap, const int* nfl, const int* inc, int maxl, const i64* arrive,
+                  const i64* bytes, const i64* alpha, const double* cap, i64* done) {
+  Oracle* o = (Oracle*)h;
+  o->ext_linkcap.assign(linkcap, linkcap + [&] { int m = 0; for (int f = 0; f < nf; ++f) for (int q = 0; q < nfl[f]; ++q) m = std::max(m, inc[f * maxl + q] + 1); return m; }());
+  Oracle::FlowEngine E{o};
+  std::vector<Oracle::FFlow> fs(nf);
+  for (int f = 0; f < nf; ++f) {
+    Oracle::FFlow x{};
+    x.bytes = bytes[f];
+    x.alpha = alpha[f];
+    x.cap = cap[f];
+    x.nl = nfl[f];
+    for (int q = 0; q < nfl[f]; ++q) x.link[q] = inc[f * maxl + q];
+    x.step = f;
+    fs[f] = x;
+    E.timer(arrive[f], f);
+  }
+  E.run([&](const Oracle::FFlow& x, i64 t) { done[x.step] = t; }, [&](int f, i64 now) { E.add(fs[f], now); });
+  o->ext_linkcap.clear();
+}
+// f3 building block for the max-min pins: nf flows over nl links; flow f
+// uses the links inc[f * maxl + q] (q < nfl[f], -1 padded); per-flow cap;
+// rates out (progressive filling as in Oracle::maxmin, capacities given)
+void orc_maxmin(int nf, int nl, const double* linkcap, const int* nfl, const int* inc, int maxl, const double* cap,
+                double* rate) {
+  std::vector<std::vector<int>> I(nf);
+  std::map<int, double> lc;
+  for (int e = 0; e < nl; ++e) lc[e] = linkcap[e];
+  for (int f = 0; f < nf; ++f) I[f].assign(inc + f * maxl, inc + f * maxl + nfl[f]);
+  std::vector<double> r;
+  maxmin_fill(nf, I, lc, std::vector<double>(cap, cap + nf), r);
+  for (int f = 0; f < nf; ++f) rate[f] = r[f];
 }
 i64 orc_act_bytes(void* h, int b) { return ((Oracle*)h)->act_bytes(b); }
 // link between two GPUs (node, local rank) -> alpha, beta

@@ -119,6 +119,9 @@ def lib():
         L.orc_segments.argtypes = [C.c_void_p, C.c_int64, C.c_void_p, C.c_int]
         L.orc_needs_reshard.restype = C.c_int
         L.orc_needs_reshard.argtypes = [C.c_int] * 5
+        L.orc_flow_resim.argtypes = [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_int64]
+        L.orc_flow_sim.argtypes = [C.c_void_p, C.c_int] + [C.c_void_p] * 3 + [C.c_int] + [C.c_void_p] * 5
+        L.orc_maxmin.argtypes = [C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]
         L.orc_device_bytes.restype = C.c_int64
         L.orc_device_bytes.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int64, C.c_int64, C.c_int]
     return _lib
@@ -260,6 +263,36 @@ class Oracle:
         keys = ("a", "z", "S", "tstar", "RS", "AR")
         return [dict(zip(keys, (int(x) for x in buf[6 * j:6 * j + 6]))) for j in range(J)]
 
+    def flow_resim(self, i, fct_cap=0):
+        """f3 (DESIGN F.1): dict(status, sync_ab, sync_flow, n_flows, T0, T_iter[, fct]);
+        T0 / T_iter from the compact mode's C.8 evaluation of the same candidate."""
+        out = np.zeros(6, dtype=np.int64)
+        fct = np.zeros(max(fct_cap, 1), dtype=np.int64)
+        lib().orc_flow_resim(self.h, int(i), out.ctypes.data, fct.ctypes.data if fct_cap else None, fct_cap)
+        r = dict(zip(("status", "sync_ab", "sync_flow", "n_flows", "T0", "T_iter"), (int(x) for x in out)))
+        if fct_cap:
+            r["fct"] = fct[:min(fct_cap, r["n_flows"])].copy()
+        return r
+
+    def flow_sim(self, linkcap, flows):
+        """The f3 fluid engine on independent flows: flows = list of dicts
+        (links, arrive, bytes, alpha, cap); returns completion times."""
+        nf = len(flows)
+        maxl = max([len(f["links"]) for f in flows] + [1])
+        inc = np.full(nf * maxl, -1, dtype=np.int32)
+        for k, f in enumerate(flows):
+            inc[k * maxl:k * maxl + len(f["links"])] = f["links"]
+        nfl = np.array([len(f["links"]) for f in flows], dtype=np.int32)
+        lc = np.asarray(linkcap, dtype=np.float64)
+        arr = _i64([f["arrive"] for f in flows])
+        by = _i64([f["bytes"] for f in flows])
+        al = _i64([f["alpha"] for f in flows])
+        cp = np.asarray([f["cap"] for f in flows], dtype=np.float64)
+        done = np.zeros(nf, dtype=np.int64)
+        lib().orc_flow_sim(self.h, nf, lc.ctypes.data, nfl.ctypes.data, inc.ctypes.data, maxl, arr.ctypes.data,
+                           by.ctypes.data, al.ctypes.data, cp.ctypes.data, done.ctypes.data)
+        return done
+
     def act_bytes(self, b):
         return lib().orc_act_bytes(self.h, b)
 
@@ -283,6 +316,22 @@ def pipeline(f, g, c, m):
     P = len(f)
     c = _i64(list(c) + [0]) if P > 1 else _i64([0])
     return lib().orc_pipeline(P, m, f.ctypes.data, g.ctypes.data, c.ctypes.data)
+
+
+def maxmin(linkcap, flows, caps):
+    """Progressive-filling max-min rates (the oracle's f3 building block):
+    flows = list of link-index lists, caps = per-flow private caps."""
+    nf, nl = len(flows), len(linkcap)
+    maxl = max([len(f) for f in flows] + [1])
+    inc = np.full(nf * maxl, -1, dtype=np.int32)
+    for k, f in enumerate(flows):
+        inc[k * maxl:k * maxl + len(f)] = f
+    nfl = np.array([len(f) for f in flows], dtype=np.int32)
+    lc = np.asarray(linkcap, dtype=np.float64)
+    cp = np.asarray(caps, dtype=np.float64)
+    rate = np.zeros(nf, dtype=np.float64)
+    lib().orc_maxmin(nf, nl, lc.ctypes.data, nfl.ctypes.data, inc.ctypes.data, maxl, cp.ctypes.data, rate.ctypes.data)
+    return rate
 
 
 def needs_reshard(src_tp, src_mb, dst_tp, dst_mb, pp_only=False):
