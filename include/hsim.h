@@ -194,6 +194,27 @@ int hsim_topk(hsim_handle* h, const hsim_cands* cands, int64_t n, int32_t k,
  * the NCCL all_gather.  1 <= k <= 1024, nlists >= 0. */
 int hsim_merge_topk(const int64_t* lists, int32_t nlists, int32_t k, int64_t* out_t_ns, int64_t* out_idx, void* stream);
 
+/* flow-level contention re-simulation of the gradient
+ * synchronisation of k candidates (DESIGN.md F.1; "bandwidth
+ * contention", :400 flow completion time per flow, :409-412 the slowest flow
+ * of a blocking collective gates it; SPEC.md:358-373 fluid max-min).  Every
+ * reshard / ring step of the candidate's C.8 sync becomes flows on the
+ * rail-only link graph (NVLink ports, GPU-NIC PCIe paths, NIC-rail wires) that
+ * share links max-min fairly; a step starts when the previous step's last
+ * flow completes.
+ *   idx   device, k candidate indices (e.g. hsim_topk's out_idx), 0 <= k <= 1024
+ *   out   device, k x 8 int64: status (0, or the candidate's -1 / -2 / -3, or
+ *         INT32_MIN for an index out of range), sync_ab (the alpha-beta C.8
+ *         sync time beyond T0, = T_iter - T0), sync_flow (the same schedule at
+ *         flow level, >= sync_ab), n_flows, then the nearest-rank FCT
+ *         percentiles p50, p99, p99.9 and the maximum FCT (ns).
+ *   fct   device, k x fct_cap int64 or NULL: each candidate's flow completion
+ *         times (unordered; the first min(n_flows, fct_cap)) for a CCDF.
+ * Blocking: sizes its scratch from a device-side flow count, so it returns
+ * after the work on `stream` has finished.  Models up to 256 layers. */
+int hsim_flow_resim(hsim_handle* h, const int64_t* idx, int32_t k, int64_t* out, int64_t* fct, int64_t fct_cap,
+                    void* stream);
+
 /* Number of device kernels the last hsim_eval_batch / hsim_topk call launched. */
 int32_t hsim_last_launch_count(const hsim_handle* h);
 

@@ -12,7 +12,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libhsim.so")
-SOURCES = [os.path.join(CSRC, f) for f in ("host.cu", "kernels.cu")]
+SOURCES = [os.path.join(CSRC, f) for f in ("host.cu", "kernels.cu", "flow.cu")]
 DEPS = SOURCES + [os.path.join(CSRC, "hsim_core.cuh"), os.path.join(ROOT, "include", "hsim.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 

@@ -114,10 +114,14 @@ struct hsim_handle {
   i64* d_pool = nullptr;
   int8_t* d_node_type = nullptr;
   std::vector<int8_t> node_type8;
+  std::vector<int32_t> type_nodes;   // f3: node ids grouped by type
+  int32_t* d_type_nodes = nullptr;
   // top-k scratch
   i64* d_blk = nullptr;
   size_t blk_cap = 0;
   i64* d_cells = nullptr;
+  void* d_flow = nullptr;     // f3 scratch (flow.cu)
+  size_t flow_cap = 0;
   static constexpr int NSIDE = 20, NEV = 48;
   cudaStream_t side[NSIDE] = {};     // one stream per phase-kernel type + the final stream
   cudaEvent_t ev_fork = nullptr, ev_join[NSIDE] = {}, ev_pool[NEV] = {};
@@ -716,6 +720,30 @@ void hsim_handle::prepare() {
     hT.cbucket_shift = cs;
     hT.tpl_cbucket = cbucket.data();
   }
+  // f3 link graph (DESIGN.md F.1): node lists per type, port / PCIe / NIC capacities
+  {
+    type_nodes.clear();
+    for (int t = 0; t < MAXT; ++t) {
+      hT.type_node_off[t] = (int32_t)type_nodes.size();
+      if (t < nt)
+        for (int n : nodes_of_type[t]) type_nodes.push_back(n);
+    }
+    hT.type_node_off[MAXT] = (int32_t)type_nodes.size();
+    hT.type_nodes = type_nodes.data();
+    hT.gpn = types[0].gpus_per_node;
+    std::memset(hT.port_cap, 0, sizeof(hT.port_cap));
+    for (int t = 0; t < nt; ++t) {
+      const int g = types[t].gpus_per_node;
+      for (int r = 0; r < g; ++r)
+        for (int j = 0; j < g; ++j)
+          if (j != r) {  // the port's line rate: its fastest intra-node path
+            hT.port_cap[t][r][0] = std::max(hT.port_cap[t][r][0], intra[t][r][j].beta);
+            hT.port_cap[t][r][1] = std::max(hT.port_cap[t][r][1], intra[t][j][r].beta);
+          }
+      hT.pcie_cap[t] = path_link(types[t].gpu_nic, cd.frame_bytes).beta;
+      hT.nic_cap[t] = std::min(types[t].nic_gbps / 8.0, cd.rail_gbps / 8.0);
+    }
+  }
   hT.tpl_prefix = prefix.data();
   hT.tpl = tpl.data();
   hT.pool = pool.data();
@@ -755,6 +783,9 @@ void hsim_handle::upload() {
   dt.tpl = d_tpl;
   dt.pool = d_pool;
   dt.node_type = d_node_type;
+  ck(cudaMalloc(&d_type_nodes, std::max<size_t>(1, type_nodes.size()) * 4), "cudaMalloc type nodes");
+  ck(cudaMemcpy(d_type_nodes, type_nodes.data(), type_nodes.size() * 4, cudaMemcpyHostToDevice), "H2D type nodes");
+  dt.type_nodes = d_type_nodes;
   ck(cudaMemcpy(dT, &dt, sizeof(Tables), cudaMemcpyHostToDevice), "H2D tables");
   int dev = 0;
   cudaGetDevice(&dev);
@@ -787,6 +818,8 @@ int launch_eval(hsim_handle* h, const Tables* dT, const hsim_cands* c, int64_t n
                 int64_t* out_t, int64_t* out_i, cudaStream_t st);
 int launch_count(hsim_handle* h, const Tables* dT, int64_t first, int64_t n, int64_t* d_acc, cudaStream_t st);
 int launch_merge(const int64_t* lists, int32_t nlists, int32_t k, int64_t* out_t, int64_t* out_i, cudaStream_t st);
+int launch_flow(hsim_handle* h, const Tables* dT, const Tables& hT, const int64_t* idx, int32_t k, int64_t* out,
+                int64_t* fct, int64_t fct_cap, cudaStream_t st);
 }
 
 extern "C" {
@@ -861,9 +894,11 @@ void hsim_destroy(hsim_handle* h) {
   cudaFree(h->d_tpl);
   cudaFree(h->d_pool);
   cudaFree(h->d_node_type);
+  cudaFree(h->d_type_nodes);
   cudaFree(h->dT);
   cudaFree(h->d_blk);
   cudaFree(h->d_cells);
+  cudaFree(h->d_flow);
   for (int q = 0; q < hsim_handle::NSIDE; ++q) {
     if (h->side[q]) cudaStreamDestroy(h->side[q]);
     if (h->ev_join[q]) cudaEventDestroy(h->ev_join[q]);
@@ -978,6 +1013,21 @@ int hsim_merge_topk(const int64_t* lists, int32_t nlists, int32_t k, int64_t* ou
   return launch_merge(lists, nlists, k, out_t_ns, out_idx, (cudaStream_t)stream);
 }
 
+int hsim_flow_resim(hsim_handle* h, const int64_t* idx, int32_t k, int64_t* out, int64_t* fct, int64_t fct_cap,
+                    void* stream) {
+  g_err.clear();
+  if (!h) { g_err = "NULL handle"; return HSIM_ESTATE; }
+  if (k < 0 || k > 1024 || (k > 0 && (!idx || !out)) || fct_cap < 0) {
+    g_err = "InvalidValue: k must be 0..1024 with idx and out";
+    return HSIM_EINVAL;
+  }
+  if ((i64)h->md.layers > 256) { g_err = "InvalidValue: flow re-simulation supports up to 256 layers"; return HSIM_EINVAL; }
+  if (k == 0) return HSIM_OK;
+  int rc = h->ensure_device();
+  if (rc) return rc;
+  return launch_flow(h, h->dT, h->hT, idx, k, out, fct, fct_cap, (cudaStream_t)stream);
+}
+
 int64_t hsim_count_cells(const hsim_handle* h, int64_t first, int64_t n) {
   g_err.clear();
   if (!h || first < 0 || n < 0 || first + n > h->N) { g_err = "index out of range"; return -1; }
@@ -1077,6 +1127,17 @@ int ensure_block_scratch(hsim_handle* h, size_t entries, int64_t** out) {
   return 0;
 }
 int sm_count(const hsim_handle* h) { return h->sm_count; }
+int ensure_flow_scratch(hsim_handle* h, size_t bytes, void** out) {
+  if (bytes > h->flow_cap) {
+    cudaFree(h->d_flow);
+    h->d_flow = nullptr;
+    h->flow_cap = 0;
+    if (cudaMalloc(&h->d_flow, bytes) != cudaSuccess) { g_err = "cudaMalloc flow scratch"; return HSIM_ENOMEM; }
+    h->flow_cap = bytes;
+  }
+  *out = h->d_flow;
+  return 0;
+}
 void set_launches(hsim_handle* h, int n) { h->last_launches = n; }
 void set_error(const char* m) { g_err = m; }
 }  // namespace hsim

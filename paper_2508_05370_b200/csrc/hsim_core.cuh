@@ -137,6 +137,13 @@ struct Tables {
   int32_t mem_check, sync_overlap;
   i64 mem_layer[4], mem_emb[4], mem_head[4], mem_K[4];
   i64 mem_cap[MAXT];
+  // f3 flow-level re-simulation (DESIGN.md F.1): rail-only link graph
+  const int32_t* type_nodes;       // node ids grouped by device type (placement order)
+  int32_t type_node_off[MAXT + 1]; // type t's nodes: type_nodes[off[t] .. off[t+1])
+  int32_t gpn, _pad6;              // GPUs per node (every node type)
+  double port_cap[MAXT][MAXG][2];  // NVLink egress / ingress port of local rank r, B/ns
+  double pcie_cap[MAXT];           // GPU <-> rail NIC path, B/ns
+  double nic_cap[MAXT];            // NIC <-> rail switch port, min(NIC, rail), B/ns
 };
 
 // --- C.0 --------------------------------------------------------------------

@@ -20,7 +20,7 @@ STATUS = {1: "HSIM_EINVAL", 2: "HSIM_ENOMEM", 3: "HSIM_ECUDA", 4: "HSIM_ERANGE",
 # symbols include/hsim.h declares (checked by tests/test_abi.py)
 EXPORTS = ("hsim_create", "hsim_destroy", "hsim_space_size", "hsim_n_templates", "hsim_template_first",
            "hsim_decode", "hsim_eval_batch", "hsim_topk", "hsim_last_launch_count", "hsim_count_cells",
-           "hsim_last_error", "hsim_merge_topk")
+           "hsim_last_error", "hsim_merge_topk", "hsim_flow_resim")
 
 
 class HsimError(RuntimeError):
@@ -103,6 +103,8 @@ def lib():
         L.hsim_count_cells.restype = C.c_int64
         L.hsim_count_cells.argtypes = [C.c_void_p, C.c_int64, C.c_int64]
         L.hsim_last_error.restype = C.c_char_p
+        L.hsim_flow_resim.restype = C.c_int
+        L.hsim_flow_resim.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]
         L.hsim_merge_topk.restype = C.c_int
         L.hsim_merge_topk.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p]
         _lib = L
@@ -286,6 +288,25 @@ class Sim:
         if rc:
             _err(rc)
         return t, i
+
+    FLOW_FIELDS = ("status", "sync_ab", "sync_flow", "n_flows", "fct_p50", "fct_p99", "fct_p999", "fct_max")
+
+    def flow_resim(self, idx, fct_cap=0, stream=None):
+        """SURVEY 8(f) f3 (hsim_flow_resim): flow-level re-simulation of the
+        gradient sync of the candidates in the device tensor idx.  Returns the
+        (k, 8) int64 device tensor (FLOW_FIELDS) and, if fct_cap > 0, the
+        (k, fct_cap) tensor of flow completion times (unordered, -1 padded)."""
+        import torch
+        assert idx.is_cuda and idx.dtype == torch.int64 and idx.is_contiguous()
+        k = idx.numel()
+        out = torch.empty((k, 8), dtype=torch.int64, device=idx.device)
+        fct = torch.full((k, fct_cap), -1, dtype=torch.int64, device=idx.device) if fct_cap else None
+        rc = lib().hsim_flow_resim(self.h, C.c_void_p(idx.data_ptr() if k else 0), k,
+                                   C.c_void_p(out.data_ptr() if k else 0),
+                                   C.c_void_p(fct.data_ptr() if fct is not None else 0), fct_cap, _stream(stream))
+        if rc:
+            _err(rc)
+        return (out, fct) if fct_cap else out
 
     def last_launch_count(self):
         return lib().hsim_last_launch_count(self.h)
