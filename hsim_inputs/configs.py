@@ -203,3 +203,35 @@ def with_sync_overlap(cfg):
     out["search"]["sync_overlap"] = 1
     out["name"] = out["name"] + "-overlap"
     return out
+
+
+def with_interleave(cfg, v=2):
+    """Copy of cfg with the interleaved 1F1B schedule, v model chunks per
+    stage (DESIGN.md V.2)."""
+    out = copy.deepcopy(cfg)
+    out["search"]["interleave"] = int(v)
+    out["name"] = out["name"] + f"-ilv{v}"
+    return out
+
+
+def with_ep_dp(cfg):
+    """Copy of cfg with expert parallelism across the DP replicas of
+    single-class MoE templates (DESIGN.md V.3)."""
+    out = copy.deepcopy(cfg)
+    out["search"]["ep_dp"] = 1
+    out["name"] = out["name"] + "-epdp"
+    return out
+
+
+def variant_tiny(seed, moe=False):
+    """A tiny workload (tiny_random's draw) with a larger global batch and more
+    layers, so interleaved candidates (m mod P = 0, every chunk non-empty) and
+    multi-replica EP groups are common; moe=True forces 4 experts, top-2."""
+    cfg = tiny_random(seed)
+    md = cfg["model"]
+    md["global_batch"] = 12 * md["global_batch"]
+    md["layers"] = md["layers"] + 4
+    if moe:
+        md["moe_experts"], md["moe_topk"] = 4, 2
+    cfg["name"] = f"variant-tiny-{seed}{'-moe' if moe else ''}"
+    return cfg

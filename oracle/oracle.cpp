@@ -11,6 +11,12 @@
 // DESIGN.md §2 (the paper gives no cost formulas beyond the link delay; every
 // other formula is a reading, listed there with its id A1..A24 / C.x).
 //
+// Variants (off by default): V.2 interleaved 1F1B
+// (orc_input.interleave = v model chunks per stage, Megatron-LM's virtual
+// pipeline) and V.3 expert parallelism across the DP replicas (ep_dp); both
+// are stated where they act (op_order / run_pipelines, layer_chain,
+// ep_alltoall_x, segments) and in DESIGN.md.
+//
 // Two modes (SURVEY.md §8(c) "It runs in two modes ... The two modes must agree"):
 //  * literal (default): every replica of every class is simulated; every stage
 //    is its own resource in a (time, seq)-ordered event queue;
@@ -86,6 +92,8 @@ struct orc_input {
   int32_t homo, mixed, use_all, r_layer, pmax, r_batch;
   int32_t mem_check;  // prune candidates that do not fit (status -3, DESIGN M.1)
   int32_t sync_overlap;  // gradient sync overlapped with the backward (DESIGN S.1)
+  int32_t interleave;    // v model chunks per stage, interleaved 1F1B (DESIGN V.2); 1 = off
+  int32_t ep_dp;         // expert parallelism across the DP replicas (DESIGN V.3)
 };
 }
 
@@ -150,8 +158,11 @@ struct Cluster {
 
 // --- C.5: per-device FLOPs and bytes of one layer op -------------------------
 struct Cost { i64 flop, bytes; };
-Cost op_cost(const orc_input& m, int kind, i64 t, i64 b) {
+// g = the devices the experts are sharded over (MOE weight bytes; 0 = t, the
+// TP group, A17); DESIGN V.3 shards them over every replica's group (g = D t)
+Cost op_cost(const orc_input& m, int kind, i64 t, i64 b, i64 g = 0) {
   const i64 T = b * m.seq, h = m.h, bpe = m.bpe_act;
+  if (g == 0) g = t;
   const i64 hkv = m.kv_heads * h / m.heads;
   switch (kind) {
     case ATTN:
@@ -161,7 +172,7 @@ Cost op_cost(const orc_input& m, int kind, i64 t, i64 b) {
       return {ceil_div(2 * T * m.nm * h * m.ffn, t), ceil_div(bpe * m.nm * h * m.ffn, t) + 2 * T * h * bpe};
     case MOE:
       return {ceil_div(2 * T * m.topk * m.nm * h * m.ffn, t),
-              ceil_div(bpe * m.E * m.nm * h * m.ffn, t) + 2 * T * h * bpe};
+              ceil_div(bpe * m.E * m.nm * h * m.ffn, g) + 2 * T * h * bpe};
     case EMB:
       return {0, 2 * T * h * bpe};
     default:  // HEAD
@@ -169,8 +180,8 @@ Cost op_cost(const orc_input& m, int kind, i64 t, i64 b) {
   }
 }
 // roofline duration; backward = 2x FLOP and 2x bytes, rounded on its own (A6)
-i64 op_dur(const orc_input& m, const orc_type& ty, int kind, bool bwd, i64 t, i64 b) {
-  Cost c = op_cost(m, kind, t, b);
+i64 op_dur(const orc_input& m, const orc_type& ty, int kind, bool bwd, i64 t, i64 b, i64 g = 0) {
+  Cost c = op_cost(m, kind, t, b, g);
   i64 mul = bwd ? 2 : 1;
   double rf = ty.peak_flop_per_ns * ty.eff_flop[kind];
   double rm = ty.hbm_bytes_per_ns * ty.eff_mem[kind];
@@ -493,11 +504,40 @@ struct Oracle {
     return (i64)(t - 1) * slow;
   }
 
-  i64 tcomp(const StageSpec& s, int b) const {  // compute-only fwd+bwd of one layer (C.4)
+  // --- SURVEY §8(f) f4 variants --------------------------------------------------
+  // V.2 (DESIGN): a class with P >= 2 stages runs the interleaved 1F1B with v =
+  // in.interleave model chunks per stage; chunk k of a stage with l layers has
+  // floor(l / v) + [k < l mod v] layers.
+  int vchunks(const ClassSpec& c) const { return in.interleave > 1 && c.st.size() >= 2 ? in.interleave : 1; }
+  static i64 chunk_layers(i64 l, int v, int k) { return l / v + (k < l % v ? 1 : 0); }
+  // V.3 (DESIGN): in a single-class MoE template, the expert-parallel group of a
+  // stage is the union of every replica's TP group of that stage (g = D tp).
+  bool ep_class(const Template& t) const { return in.ep_dp && in.E > 1 && t.cls.size() == 1; }
+  i64 ep_g(const Template& t, const StageSpec& s) const { return ep_class(t) ? (i64)t.cls[0].D * s.tp : 0; }
+
+  // compute-only fwd+bwd of one layer (C.4); g: expert divisor (V.3, 0 = tp)
+  // V.3: all-to-all over the union of the groups' devices (g = n tp): g - 1
+  // rounds, each bounded by the slowest ordered pair, message ceil(A k / (t g))
+  // per pair (A17 is the one-group case, g = t)
+  i64 ep_alltoall_x(const std::vector<Group>& gs, int t, int b) const {
+    std::vector<std::pair<int, int>> dev;
+    for (const Group& g : gs)
+      for (int q = 0; q < t; ++q) dev.push_back({g.node, g.base + q});
+    const i64 g = (i64)dev.size();
+    if (g == 1) return 0;
+    const i64 per = ceil_div(act_bytes(b) * in.topk, (i64)t * g);
+    i64 slow = 0;
+    for (size_t x = 0; x < dev.size(); ++x)
+      for (size_t y = 0; y < dev.size(); ++y)
+        if (x != y) slow = std::max(slow, tau(cl.gpu_to_gpu(dev[x].first, dev[x].second, dev[y].first, dev[y].second), per));
+    return (g - 1) * slow;
+  }
+
+  i64 tcomp(const StageSpec& s, int b, i64 g = 0) const {
     const orc_type& ty = types[s.type];
     int mk = in.E > 1 ? MOE : MLP;
-    return op_dur(in, ty, ATTN, false, s.tp, b) + op_dur(in, ty, mk, false, s.tp, b) +
-           op_dur(in, ty, ATTN, true, s.tp, b) + op_dur(in, ty, mk, true, s.tp, b);
+    return op_dur(in, ty, ATTN, false, s.tp, b) + op_dur(in, ty, mk, false, s.tp, b, g) +
+           op_dur(in, ty, ATTN, true, s.tp, b) + op_dur(in, ty, mk, true, s.tp, b, g);
   }
   i64 extra_fb(const StageSpec& s, int b, int kind) const {
     const orc_type& ty = types[s.type];
@@ -514,19 +554,20 @@ struct Oracle {
     for (int c = 0; c < C; ++c) {
       const int P = (int)cls[c].st.size();
       std::vector<i64> w(P);
-      for (int s = 0; s < P; ++s) w[s] = (i64(1) << 40) / tcomp(cls[c].st[s], b);
+      for (int s = 0; s < P; ++s) w[s] = (i64(1) << 40) / tcomp(cls[c].st[s], b, ep_g(*p.tpl, cls[c].st[s]));
       std::vector<i64> l = hamilton(in.L, w);
       for (int s = 0; s < P; ++s) {
         i64 d_here = s < P - 1 ? p.delta[c][s] : 0;
         i64 d_prev = s > 0 ? p.delta[c][s - 1] : 0;
         l[s] += d_here - d_prev;
         if (l[s] < 1) p.status = -1;
+        if (l[s] < vchunks(cls[c])) p.status = -1;  // V.2: every chunk holds a layer
       }
       p.layers[c] = l;
       if (p.status) return;
       i64 worst = 0;
       for (int s = 0; s < P; ++s) {
-        i64 t = l[s] * tcomp(cls[c].st[s], b);
+        i64 t = l[s] * tcomp(cls[c].st[s], b, ep_g(*p.tpl, cls[c].st[s]));
         if (s == 0) t += extra_fb(cls[c].st[s], b, EMB);
         if (s == P - 1) t += extra_fb(cls[c].st[s], b, HEAD);
         worst = std::max(worst, t);
@@ -552,6 +593,12 @@ struct Oracle {
     for (int c = 0; c < C; ++c)
       for (i64 v : p.mb[c])
         if (v < 1) p.status = -2;
+    // V.2: the interleaved schedule needs every replica's micro-batch count to
+    // be a multiple of its depth (Megatron-LM's rule for virtual pipelines)
+    for (int c = 0; c < C; ++c)
+      if (vchunks(cls[c]) > 1)
+        for (i64 v : p.mb[c])
+          if (v % (i64)cls[c].st.size()) p.status = -2;
   }
 
   // --- f2 / DESIGN M.1: memory feasibility -------------------------------------
@@ -601,28 +648,56 @@ struct Oracle {
   }
 
   // --- C.7 / C.11: event-driven 1F1B over every replica ------------------------
+  // A stage group runs its op list in order; an op starts when the previous op
+  // of the group has ended and its input has arrived.  Ops are (fwd?, chunk k,
+  // micro-batch j); v = 1 (every chunk index 0) is C.7's non-interleaved 1F1B.
+  struct Op { bool fwd; int k, j; };
   struct SimGroup {
-    int P, s, m;
-    i64 f, g, c_prev, c_next;  // c_prev: boundary s-1 -> s, c_next: s -> s+1
-    std::vector<std::pair<bool, int>> ops;  // (is_fwd, micro-batch)
+    int P, s, m, v = 1;
+    std::vector<i64> f, g;     // per chunk: forward / backward duration
+    i64 c_prev, c_next;        // c_prev: boundary s-1 -> s, c_next: s -> s+1
+    i64 c_wrap = 0;            // V.2: stage P-1 -> stage 0 (next chunk) and back
+    std::vector<Op> ops;
     size_t next = 0;
     bool busy = false;
     i64 done = 0;  // end of the group's last op (its last backward, C.7)
-    std::vector<char> inF, inB;
+    std::vector<char> inF, inB;  // [k * m + j]
   };
   struct Ev {
     i64 t, seq;
     int kind;  // 0 = op done, 1 = F input arrives, 2 = B input arrives
-    int grp, j;
+    int grp, key;
     bool operator>(const Ev& o) const { return std::tie(t, seq) > std::tie(o.t, o.seq); }
   };
 
-  static std::vector<std::pair<bool, int>> op_order(int P, int s, int m) {
-    std::vector<std::pair<bool, int>> o;
-    int w = std::min(P - 1 - s, m);
-    for (int j = 0; j < w; ++j) o.push_back({true, j});
-    for (int i = 0; i < m - w; ++i) { o.push_back({true, w + i}); o.push_back({false, i}); }
-    for (int j = m - w; j < m; ++j) o.push_back({false, j});
+  // C.7: warm-up w = min(P-1-s, m) forwards, then (F, B) pairs, then the rest.
+  // V.2 (Megatron-LM's interleaved schedule, Narayanan et al. 2021): the
+  // forward table visits micro-batches in groups of P -- for each group, chunk
+  // 0..v-1, the group's micro-batches in order; the backward table is the same
+  // with the chunks in reverse order; warm-up w = min(2(P-1-s) + (v-1) P, m v)
+  // table forwards, then (F_tab[w+i], B_tab[i]) pairs, then the remaining
+  // backwards.  Needs m mod P = 0 (partition gives -2 otherwise).
+  static std::vector<Op> op_order(int P, int s, int m, int v = 1) {
+    std::vector<Op> o;
+    if (v == 1) {
+      int w = std::min(P - 1 - s, m);
+      for (int j = 0; j < w; ++j) o.push_back({true, 0, j});
+      for (int i = 0; i < m - w; ++i) { o.push_back({true, 0, w + i}); o.push_back({false, 0, i}); }
+      for (int j = m - w; j < m; ++j) o.push_back({false, 0, j});
+      return o;
+    }
+    std::vector<Op> F, B;
+    for (int g0 = 0; g0 < m; g0 += P) {
+      for (int k = 0; k < v; ++k)
+        for (int j = g0; j < std::min(g0 + P, m); ++j) F.push_back({true, k, j});
+      for (int k = v - 1; k >= 0; --k)
+        for (int j = g0; j < std::min(g0 + P, m); ++j) B.push_back({false, k, j});
+    }
+    const int n = m * v;
+    const int w = std::min(2 * (P - 1 - s) + (v - 1) * P, n);
+    for (int i = 0; i < w; ++i) o.push_back(F[i]);
+    for (int i = 0; i < n - w; ++i) { o.push_back(F[w + i]); o.push_back(B[i]); }
+    for (int i = n - w; i < n; ++i) o.push_back(B[i]);
     return o;
   }
 
@@ -634,16 +709,20 @@ struct Oracle {
     auto try_start = [&](int gi, i64 t) {
       SimGroup& g = G[gi];
       if (g.busy || g.next >= g.ops.size()) return;
-      auto op = g.ops[g.next];
-      bool ready = op.first ? g.inF[op.second] : g.inB[op.second];
+      const Op op = g.ops[g.next];
+      const int key = op.k * g.m + op.j;
+      bool ready = op.fwd ? g.inF[key] : g.inB[key];
       if (!ready) return;
       g.busy = true;
-      q.push(Ev{t + (op.first ? g.f : g.g), seq++, 0, gi, op.second});
+      q.push(Ev{t + (op.fwd ? g.f[op.k] : g.g[op.k]), seq++, 0, gi, key});
     };
     for (size_t gi = 0; gi < G.size(); ++gi) {
-      G[gi].inF.assign(G[gi].m, G[gi].s == 0 ? 1 : 0);
-      G[gi].inB.assign(G[gi].m, 0);
-      G[gi].ops = op_order(G[gi].P, G[gi].s, G[gi].m);
+      SimGroup& g = G[gi];
+      g.inF.assign((size_t)g.v * g.m, 0);
+      g.inB.assign((size_t)g.v * g.m, 0);
+      if (g.s == 0)
+        for (int j = 0; j < g.m; ++j) g.inF[j] = 1;  // chunk 0 of stage 0: the data loader
+      g.ops = op_order(g.P, g.s, g.m, g.v);
     }
     for (size_t gi = 0; gi < G.size(); ++gi) try_start((int)gi, 0);
     while (!q.empty()) {
@@ -652,22 +731,28 @@ struct Oracle {
       last = std::max(last, e.t);
       SimGroup& g = G[e.grp];
       if (e.kind == 0) {
-        auto op = g.ops[g.next];
+        const Op op = g.ops[g.next];
         g.busy = false;
         g.done = e.t;
         g.next++;
-        if (op.first) {
-          if (g.s < g.P - 1) q.push(Ev{e.t + g.c_next, seq++, 1, e.grp + 1, op.second});
-          else g.inB[op.second] = 1;  // last stage: B(P-1,j) follows F(P-1,j)
+        const int s0 = e.grp - g.s, sl = s0 + g.P - 1;  // stage 0 / stage P-1 of this pipeline
+        if (op.fwd) {
+          if (g.s < g.P - 1) q.push(Ev{e.t + g.c_next, seq++, 1, e.grp + 1, e.key});
+          else if (op.k < g.v - 1) q.push(Ev{e.t + g.c_wrap, seq++, 1, s0, e.key + g.m});  // V.2 wrap
+          else g.inB[e.key] = 1;  // last virtual stage: B follows its own F
         } else if (g.s > 0) {
-          q.push(Ev{e.t + g.c_prev, seq++, 2, e.grp - 1, op.second});
+          q.push(Ev{e.t + g.c_prev, seq++, 2, e.grp - 1, e.key});
+        } else if (op.k > 0) {
+          q.push(Ev{e.t + g.c_wrap, seq++, 2, sl, e.key - g.m});  // V.2 wrap back
         }
         try_start(e.grp, e.t);
       } else {
-        (e.kind == 1 ? g.inF : g.inB)[e.j] = 1;
+        (e.kind == 1 ? g.inF : g.inB)[e.key] = 1;
         try_start(e.grp, e.t);
       }
     }
+    for (const SimGroup& g : G)
+      if (g.next != g.ops.size()) { std::fprintf(stderr, "oracle: 1F1B deadlock\n"); std::abort(); }
     return last;
   }
 
@@ -683,13 +768,17 @@ struct Oracle {
   // One layer's forward (bwd = 0) or backward (bwd = 1) op chain on stage
   // group gr: attn + AR + mlp + AR (dense) or attn + AR + A2A + moe + A2A (MoE)
   // (DESIGN C.5, A16, A17).
-  i64 layer_chain(const StageSpec& ss, const Group& gr, int b, int bwd, bool compact) const {
+  // V.3: epg = every replica's group of this stage (the expert-parallel group),
+  // or nullptr (A17: the TP group)
+  i64 layer_chain(const StageSpec& ss, const Group& gr, int b, int bwd, bool compact,
+                  const std::vector<Group>* epg = nullptr) const {
     const orc_type& ty = types[ss.type];
     const i64 ar = compact ? tp_allreduce_compact(gr, ss.tp, b) : tp_allreduce(gr, ss.tp, b);
     i64 chain = op_dur(in, ty, ATTN, bwd, ss.tp, b) + ar;
     if (in.E > 1) {
-      const i64 a2a = ep_alltoall(gr, ss.tp, b);
-      chain += a2a + op_dur(in, ty, MOE, bwd, ss.tp, b) + a2a;
+      const i64 a2a = epg ? ep_alltoall_x(*epg, ss.tp, b) : ep_alltoall(gr, ss.tp, b);
+      const i64 g = epg ? (i64)epg->size() * ss.tp : 0;
+      chain += a2a + op_dur(in, ty, MOE, bwd, ss.tp, b, g) + a2a;
     } else {
       chain += op_dur(in, ty, MLP, bwd, ss.tp, b) + ar;
     }
@@ -707,16 +796,27 @@ struct Oracle {
     const int C = (int)cls.size();
     i64 D = 0;
     for (auto& c : cls) D += c.D;
+    // layer ranges of each class in model order: (first layer, stage).  V.2:
+    // virtual stage k P + s = chunk k of stage s, so a stage holds v ranges.
     std::vector<i64> cuts{0, in.L};
-    std::vector<std::vector<i64>> start(C);
+    std::vector<std::vector<std::pair<i64, int>>> start(C);
     for (int c = 0; c < C; ++c) {
+      const int P = (int)cls[c].st.size(), v = vchunks(cls[c]);
       i64 a = 0;
-      for (i64 l : p.layers[c]) { start[c].push_back(a); cuts.push_back(a); a += l; }
+      for (int k = 0; k < v; ++k)
+        for (int s = 0; s < P; ++s) {
+          start[c].push_back({a, s});
+          cuts.push_back(a);
+          a += chunk_layers(p.layers[c][s], v, k);
+        }
     }
     std::sort(cuts.begin(), cuts.end());
     cuts.erase(std::unique(cuts.begin(), cuts.end()), cuts.end());
     const i64 hkv = in.kv_heads * in.h / in.heads;
-    const i64 Wlayer = in.h * (2 * in.h + 2 * hkv) + in.nm * in.h * in.ffn * in.E + (in.E > 1 ? in.h * in.E : 0) + 2 * in.h;
+    // V.3: expert weights are sharded over the replicas (one copy per class), so
+    // a single-class EP template synchronises only the dense parameters
+    const i64 Wexp = ep_class(*p.tpl) ? 0 : in.nm * in.h * in.ffn * in.E;
+    const i64 Wlayer = in.h * (2 * in.h + 2 * hkv) + Wexp + (in.E > 1 ? in.h * in.E : 0) + 2 * in.h;
     std::vector<Seg> out;
     for (size_t j = 0; j + 1 < cuts.size(); ++j) {
       Seg sg;
@@ -728,8 +828,9 @@ struct Oracle {
       sg.sc.assign(C, 0);
       sg.tstar = 1 << 30;
       for (int c = 0; c < C; ++c) {
-        int s = 0;
-        while (s + 1 < (int)start[c].size() && start[c][s + 1] <= sg.a) ++s;
+        size_t x = 0;
+        while (x + 1 < start[c].size() && start[c][x + 1].first <= sg.a) ++x;
+        const int s = start[c][x].second;
         sg.sc[c] = s;
         sg.tstar = std::min(sg.tstar, cls[c].st[s].tp);
       }
@@ -791,20 +892,41 @@ struct Oracle {
     // stands for replica r of class c.
     std::vector<SimGroup> G;
     std::vector<std::vector<size_t>> owner(C);
+    const bool ep = ep_class(*p.tpl);
     for (int c = 0; c < C; ++c) {
-      const int P = (int)cls[c].st.size();
+      const int P = (int)cls[c].st.size(), v = vchunks(cls[c]);
+      // p2p per boundary: rank pairs q < min(t_s, t_{s+1}) in parallel (A8);
+      // V.2 adds the wrap boundary stage P-1 -> stage 0 (last entry)
+      auto p2p = [&](const Group& x, int tx, const Group& y, int ty) {
+        i64 cs = 0;
+        for (int q = 0; q < std::min(tx, ty); ++q)
+          cs = std::max(cs, tau(cl.gpu_to_gpu(x.node, x.base + q, y.node, y.base + q), act_bytes(b)));
+        return cs;
+      };
       std::vector<std::vector<i64>> cv(cls[c].D, std::vector<i64>(P > 1 ? P - 1 : 0));
-      for (int r = 0; r < cls[c].D; ++r)
-        for (int s = 0; s + 1 < P; ++s) {
-          // p2p per boundary: rank pairs i < min(t_s, t_{s+1}) in parallel (A8)
-          const Group& a = p.place[c][r][s];
-          const Group& z = p.place[c][r][s + 1];
-          const int np = std::min(cls[c].st[s].tp, cls[c].st[s + 1].tp);
-          i64 cs = 0;
-          for (int q = 0; q < np; ++q)
-            cs = std::max(cs, tau(cl.gpu_to_gpu(a.node, a.base + q, z.node, z.base + q), act_bytes(b)));
-          cv[r][s] = cs;
+      std::vector<i64> mrep(cls[c].D);
+      for (int r = 0; r < cls[c].D; ++r) {
+        for (int s = 0; s + 1 < P; ++s)
+          cv[r][s] = p2p(p.place[c][r][s], cls[c].st[s].tp, p.place[c][r][s + 1], cls[c].st[s + 1].tp);
+        if (v > 1) cv[r].push_back(p2p(p.place[c][r][P - 1], cls[c].st[P - 1].tp, p.place[c][r][0], cls[c].st[0].tp));
+        mrep[r] = p.mb[c][r];
+      }
+      // V.3: the all-to-alls couple the replicas into lockstep -- every replica
+      // runs the class's largest micro-batch count and, per boundary, the
+      // slowest replica's p2p cost
+      std::vector<std::vector<Group>> epg;
+      if (ep) {
+        std::vector<i64> cmax(cv[0].size(), 0);
+        i64 mmax = 0;
+        for (int r = 0; r < cls[c].D; ++r) {
+          for (size_t k = 0; k < cmax.size(); ++k) cmax[k] = std::max(cmax[k], cv[r][k]);
+          mmax = std::max(mmax, mrep[r]);
         }
+        for (int r = 0; r < cls[c].D; ++r) { cv[r] = cmax; mrep[r] = mmax; }
+        epg.resize(P);
+        for (int s = 0; s < P; ++s)
+          for (int r = 0; r < cls[c].D; ++r) epg[s].push_back(p.place[c][r][s]);
+      }
       owner[c].assign(cls[c].D, 0);
       std::vector<int> rep;  // compact: first replica of each sub-class
       for (int r = 0; r < cls[c].D; ++r) {
@@ -815,7 +937,7 @@ struct Oracle {
         if (u >= 0) {  // replica r joins sub-class of replica u: the pipeline runs the larger m
           const size_t base = owner[c][u];
           owner[c][r] = base;
-          for (int s = 0; s < P; ++s) G[base + s].m = std::max(G[base + s].m, (int)p.mb[c][r]);
+          for (int s = 0; s < P; ++s) G[base + s].m = std::max(G[base + s].m, (int)mrep[r]);
           continue;
         }
         rep.push_back(r);
@@ -824,21 +946,30 @@ struct Oracle {
           const StageSpec& ss = cls[c].st[s];
           const orc_type& ty = types[ss.type];
           const Group& gr = p.place[c][r][s];
+          const std::vector<Group>* eg = ep ? &epg[s] : nullptr;
           SimGroup g{};
-          g.P = P; g.s = s; g.m = (int)p.mb[c][r];
-          if (compact) {
-            g.f = p.layers[c][s] * layer_chain(ss, gr, b, 0, true);
-            g.g = p.layers[c][s] * layer_chain(ss, gr, b, 1, true);
-          } else {
-            for (i64 l = 0; l < p.layers[c][s]; ++l) {
-              g.f += layer_chain(ss, gr, b, 0, false);
-              g.g += layer_chain(ss, gr, b, 1, false);
+          g.P = P; g.s = s; g.m = (int)mrep[r]; g.v = v;
+          g.f.assign(v, 0);
+          g.g.assign(v, 0);
+          for (int k = 0; k < v; ++k) {
+            const i64 lk = chunk_layers(p.layers[c][s], v, k);
+            if (compact) {
+              g.f[k] = lk * layer_chain(ss, gr, b, 0, true, eg);
+              g.g[k] = lk * layer_chain(ss, gr, b, 1, true, eg);
+            } else {
+              for (i64 l = 0; l < lk; ++l) {
+                g.f[k] += layer_chain(ss, gr, b, 0, false, eg);
+                g.g[k] += layer_chain(ss, gr, b, 1, false, eg);
+              }
             }
           }
-          if (s == 0) { g.f += op_dur(in, ty, EMB, false, ss.tp, b); g.g += op_dur(in, ty, EMB, true, ss.tp, b); }
-          if (s == P - 1) { g.f += op_dur(in, ty, HEAD, false, ss.tp, b); g.g += op_dur(in, ty, HEAD, true, ss.tp, b); }
+          // the embedding runs with the first chunk of stage 0, the head with the
+          // last chunk of stage P-1
+          if (s == 0) { g.f[0] += op_dur(in, ty, EMB, false, ss.tp, b); g.g[0] += op_dur(in, ty, EMB, true, ss.tp, b); }
+          if (s == P - 1) { g.f[v - 1] += op_dur(in, ty, HEAD, false, ss.tp, b); g.g[v - 1] += op_dur(in, ty, HEAD, true, ss.tp, b); }
           g.c_prev = s > 0 ? cv[r][s - 1] : 0;
           g.c_next = s + 1 < P ? cv[r][s] : 0;
+          g.c_wrap = v > 1 ? cv[r][P - 1] : 0;
           G.push_back(g);
         }
       }
@@ -1196,6 +1327,14 @@ void* orc_create(const orc_input* in) {
     g_err = "invalid input";
     return nullptr;
   }
+  if (in->interleave < 1 || in->interleave > 8) {
+    g_err = "interleave must be 1..8";
+    return nullptr;
+  }
+  if (in->mem_check && (in->interleave > 1 || in->ep_dp)) {
+    g_err = "mem_check is not defined with interleave / ep_dp (DESIGN V.2, V.3)";
+    return nullptr;
+  }
   Oracle* o = new Oracle();
   o->in = *in;
   o->types.assign(in->types, in->types + in->n_types);
@@ -1281,11 +1420,42 @@ double orc_hop_delay_exact(double gbps, int bidir, i64 frame) {
 i64 orc_ring_sim(const i64* tau_edges, int n, int steps) {
   return ring_sim(std::vector<i64>(tau_edges, tau_edges + n), steps);
 }
+// V.2: one interleaved pipeline (P stages, v chunks, m micro-batches): f, g
+// [P][v] row-major, c[P-1] boundary costs, cw the wrap cost
+i64 orc_pipeline_ilv(int P, int v, int m, const i64* f, const i64* g, const i64* c, i64 cw) {
+  std::vector<Oracle::SimGroup> G(P);
+  for (int s = 0; s < P; ++s) {
+    G[s].P = P; G[s].s = s; G[s].m = m; G[s].v = v;
+    G[s].f.assign(f + s * v, f + s * v + v);
+    G[s].g.assign(g + s * v, g + s * v + v);
+    G[s].c_prev = s > 0 ? c[s - 1] : 0;
+    G[s].c_next = s + 1 < P ? c[s] : 0;
+    G[s].c_wrap = cw;
+  }
+  return Oracle::run_pipelines(G);
+}
+// V.2 op order of stage s: out[3 x n] = (fwd, chunk, micro-batch); returns n
+int orc_op_order(int P, int s, int m, int v, int* out, int cap) {
+  auto o = Oracle::op_order(P, s, m, v);
+  for (size_t k = 0; k < o.size() && (int)k < cap; ++k) {
+    out[3 * k] = o[k].fwd;
+    out[3 * k + 1] = o[k].k;
+    out[3 * k + 2] = o[k].j;
+  }
+  return (int)o.size();
+}
+// V.3: all-to-all over the union of groups (node, base) x n of TP t at micro-batch b
+i64 orc_ep_alltoall_groups(void* h, const int* nodes, const int* bases, int n, int t, int b) {
+  std::vector<Group> gs;
+  for (int k = 0; k < n; ++k) gs.push_back(Group{nodes[k], bases[k]});
+  return ((Oracle*)h)->ep_alltoall_x(gs, t, b);
+}
+
 // one pipeline (P stages, m micro-batches) through the event engine
 i64 orc_pipeline(int P, int m, const i64* f, const i64* g, const i64* c) {
   std::vector<Oracle::SimGroup> G(P);
   for (int s = 0; s < P; ++s) {
-    G[s].P = P; G[s].s = s; G[s].m = m; G[s].f = f[s]; G[s].g = g[s];
+    G[s].P = P; G[s].s = s; G[s].m = m; G[s].f = {f[s]}; G[s].g = {g[s]};
     G[s].c_prev = s > 0 ? c[s - 1] : 0;
     G[s].c_next = s + 1 < P ? c[s] : 0;
   }

@@ -62,7 +62,8 @@ class _Input(C.Structure):
                 ("n_p", C.c_int32), ("pset", C.c_int32 * 16),
                 ("homo", C.c_int32), ("mixed", C.c_int32), ("use_all", C.c_int32),
                 ("r_layer", C.c_int32), ("pmax", C.c_int32), ("r_batch", C.c_int32),
-                ("mem_check", C.c_int32), ("sync_overlap", C.c_int32)]
+                ("mem_check", C.c_int32), ("sync_overlap", C.c_int32),
+                ("interleave", C.c_int32), ("ep_dp", C.c_int32)]
 
 
 def _path(hops):
@@ -122,6 +123,12 @@ def lib():
         L.orc_flow_resim.argtypes = [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_int64]
         L.orc_flow_sim.argtypes = [C.c_void_p, C.c_int] + [C.c_void_p] * 3 + [C.c_int] + [C.c_void_p] * 5
         L.orc_maxmin.argtypes = [C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]
+        L.orc_pipeline_ilv.restype = C.c_int64
+        L.orc_pipeline_ilv.argtypes = [C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64]
+        L.orc_op_order.restype = C.c_int
+        L.orc_op_order.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_int]
+        L.orc_ep_alltoall_groups.restype = C.c_int64
+        L.orc_ep_alltoall_groups.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int]
         L.orc_device_bytes.restype = C.c_int64
         L.orc_device_bytes.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int64, C.c_int64, C.c_int]
     return _lib
@@ -185,6 +192,8 @@ class Oracle:
         I.r_layer, I.pmax, I.r_batch = se["r_layer"], se["pmax_perturb"], se["r_batch"]
         I.mem_check = int(se.get("mem_check", 0))
         I.sync_overlap = int(se.get("sync_overlap", 0))
+        I.interleave = int(se.get("interleave", 1))
+        I.ep_dp = int(se.get("ep_dp", 0))
         self._in = I
         self.h = lib().orc_create(C.byref(I))
         if not self.h:
@@ -247,6 +256,12 @@ class Oracle:
     def device_bytes(self, type_idx, tp, P, s, layers, mb, b):
         """DESIGN M.1: bytes one device of stage s (of P) needs (f2 memory check)."""
         return lib().orc_device_bytes(self.h, type_idx, tp, P, s, layers, mb, b)
+
+    def ep_alltoall_groups(self, groups, tp, b):
+        """DESIGN V.3: all-to-all over the union of the (node, base) TP groups."""
+        nodes = np.array([g[0] for g in groups], dtype=np.int32)
+        bases = np.array([g[1] for g in groups], dtype=np.int32)
+        return lib().orc_ep_alltoall_groups(self.h, nodes.ctypes.data, bases.ctypes.data, len(groups), tp, b)
 
     def tp_allreduce(self, node, base, tp, b):
         return lib().orc_tp_allreduce(self.h, node, base, tp, b)
@@ -316,6 +331,22 @@ def pipeline(f, g, c, m):
     P = len(f)
     c = _i64(list(c) + [0]) if P > 1 else _i64([0])
     return lib().orc_pipeline(P, m, f.ctypes.data, g.ctypes.data, c.ctypes.data)
+
+
+def pipeline_ilv(f, g, c, cw, m):
+    """DESIGN V.2: interleaved 1F1B; f, g = [P][v] chunk durations, c = P-1 boundary
+    costs, cw = wrap cost."""
+    f, g = np.ascontiguousarray(f, dtype=np.int64), np.ascontiguousarray(g, dtype=np.int64)
+    P, v = f.shape
+    c = _i64(list(c) + [0])
+    return lib().orc_pipeline_ilv(P, v, m, f.ctypes.data, g.ctypes.data, c.ctypes.data, cw)
+
+
+def op_order(P, s, m, v):
+    """The op list of stage s: [(fwd, chunk, micro-batch)]."""
+    buf = np.zeros(3 * 2 * m * v + 3, dtype=np.int32)
+    n = lib().orc_op_order(P, s, m, v, buf.ctypes.data, 2 * m * v + 1)
+    return [tuple(int(x) for x in buf[3 * k:3 * k + 3]) for k in range(n)]
 
 
 def maxmin(linkcap, flows, caps):

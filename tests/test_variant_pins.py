@@ -1,0 +1,472 @@
+"""Pins of the oracle's SURVEY §8(f) f4 variants (DESIGN.md V.2, V.3).
+
+V.2 interleaved 1F1B (v model chunks per stage, Megatron-LM's virtual
+pipeline, Narayanan et al. 2021):
+* the textbook closed form: with every chunk taking a forward / b backward
+  and free communication, T = (m v + P - 1)(a + b) for m a multiple of P
+  (the interleaved bubble (P - 1)/(m v) of the Megatron paper);
+* the op lists against the schedule table written out here (groups of P
+  micro-batches, chunks ascending for forwards / descending for backwards,
+  warm-up 2(P-1-s) + (v-1)P), every op exactly once, F(k, j) before B(k, j);
+* deadlock freedom for every P <= 12, v <= 4, m in {P, 2P, 3P};
+* an explicit-DAG longest path (not an event engine) on random durations
+  and p2p / wrap costs;
+* whole candidates: ``py_eval_v`` (below) -- the independent evaluator of
+  tests/test_oracle_pins_r2.py extended with chunks, the wrap boundary and
+  virtual-stage sync segments -- equals the oracle on tiny spaces;
+  the -1 / -2 rules (a stage with fewer layers than chunks; m mod P != 0).
+
+V.3 expert parallelism across the DP replicas:
+* the all-to-all over one group is A17's (the round-robin schedule);
+* over two groups on two nodes, a hand-computed round-robin over the rail
+  (Table 4 link delays);
+* with one replica the variant changes nothing (every candidate equal);
+* the dense gradient bytes against Mixtral 8x7B's public parameter split
+  (46.7 B total, 32 x 8 experts x 3 x 4096 x 14336 expert weights);
+* whole candidates against ``py_eval_v`` (lockstep replicas, g = D tp).
+"""
+import math
+import os
+
+import numpy as np
+import pytest
+
+import hsim_inputs as H
+from test_oracle_pins_r2 import act_bytes, cdiv, model_dims, tau, tp_allreduce_ref, tp_ring_edges
+
+THREADS = os.cpu_count() or 4
+
+
+# ----------------------------------------------------------------------------
+# V.2 schedule, written out from the Megatron-LM description
+# ----------------------------------------------------------------------------
+def megatron_tables(P, v, m):
+    """Forward / backward tables: micro-batches in groups of P; per group the
+    chunks 0..v-1 (forward) or v-1..0 (backward), the group's micro-batches in
+    order within a chunk."""
+    fw, bw = [], []
+    for g0 in range(0, m, P):
+        grp = list(range(g0, min(g0 + P, m)))
+        fw += [(k, j) for k in range(v) for j in grp]
+        bw += [(k, j) for k in reversed(range(v)) for j in grp]
+    return fw, bw
+
+
+def megatron_order(P, s, m, v):
+    """v = 1 is the non-interleaved 1F1B (C.7, warm-up min(P-1-s, m))."""
+    fw, bw = megatron_tables(P, v, m)
+    n = m * v
+    w = min((P - 1 - s) * 2 + (v - 1) * P, n) if v > 1 else min(P - 1 - s, m)
+    out = [("F",) + x for x in fw[:w]]
+    for i in range(n - w):
+        out += [("F",) + fw[w + i], ("B",) + bw[i]]
+    out += [("B",) + x for x in bw[n - w:]]
+    return out
+
+
+def ilv_dag(f, g, c, cw, m):
+    """Interleaved 1F1B as an explicit DAG, longest path by Kahn's order.
+    f, g: [P][v]; c: boundary costs; cw: wrap cost.  Returns (T, per-stage end
+    of its last op)."""
+    P, v = len(f), len(f[0])
+    preds = {}
+    last_op = {}
+    for s in range(P):
+        prev = None
+        for op in megatron_order(P, s, m, v):
+            node = (s,) + op
+            preds[node] = [(prev, 0)] if prev else []
+            prev = node
+        last_op[s] = prev
+    for s in range(P):
+        for k in range(v):
+            for j in range(m):
+                if s > 0:
+                    preds[(s, "F", k, j)].append(((s - 1, "F", k, j), c[s - 1]))
+                elif k > 0:
+                    preds[(s, "F", k, j)].append(((P - 1, "F", k - 1, j), cw))
+                if s < P - 1:
+                    preds[(s, "B", k, j)].append(((s + 1, "B", k, j), c[s]))
+                elif k < v - 1:
+                    preds[(s, "B", k, j)].append(((0, "B", k + 1, j), cw))
+                else:
+                    preds[(s, "B", k, j)].append(((s, "F", k, j), 0))
+    succ = {x: [] for x in preds}
+    indeg = {x: len(p) for x, p in preds.items()}
+    for x, ps in preds.items():
+        for u, _ in ps:
+            succ[u].append(x)
+    ready = [x for x, d in indeg.items() if d == 0]
+    end = {}
+    while ready:
+        x = ready.pop()
+        st = max([end[u] + d for u, d in preds[x]], default=0)
+        s, kind, k, _ = x
+        end[x] = st + (f[s][k] if kind == "F" else g[s][k])
+        for y in succ[x]:
+            indeg[y] -= 1
+            if indeg[y] == 0:
+                ready.append(y)
+    assert len(end) == len(preds), "cycle: the schedule deadlocks"
+    return max(end.values()), [end[last_op[s]] for s in range(P)]
+
+
+def test_ilv_uniform_closed_form(oracle_mod):
+    for P in range(2, 9):
+        for v in (2, 3, 4):
+            for m in (P, 2 * P, 3 * P):
+                for a, b in ((1, 2), (3, 5), (7, 7)):
+                    T = oracle_mod.pipeline_ilv([[a] * v] * P, [[b] * v] * P, [0] * (P - 1), 0, m)
+                    assert T == (m * v + P - 1) * (a + b), (P, v, m, a, b)
+
+
+def test_ilv_op_order_against_table(oracle_mod):
+    for P in (2, 3, 4, 5, 8):
+        for v in (2, 3, 4):
+            for m in (P, 2 * P, 4 * P):
+                for s in range(P):
+                    got = oracle_mod.op_order(P, s, m, v)
+                    want = [(1 if o[0] == "F" else 0, o[1], o[2]) for o in megatron_order(P, s, m, v)]
+                    assert got == want, (P, v, m, s)
+                    assert sorted(got) == sorted((d, k, j) for d in (0, 1) for k in range(v) for j in range(m))
+                    pos = {x: n for n, x in enumerate(got)}
+                    assert all(pos[(1, k, j)] < pos[(0, k, j)] for k in range(v) for j in range(m))
+
+
+def test_ilv_no_deadlock(oracle_mod):
+    """The event engine aborts on a deadlock; every (P, v, m) with m mod P = 0
+    completes, and equals the uniform closed form."""
+    for P in range(2, 13):
+        for v in range(2, 5):
+            for m in (P, 2 * P, 3 * P):
+                assert oracle_mod.pipeline_ilv([[2] * v] * P, [[3] * v] * P, [1] * (P - 1), 1, m) > 0
+
+
+def test_ilv_dag_random(oracle_mod):
+    rng = np.random.default_rng(2508)
+    for _ in range(250):
+        P, v = int(rng.integers(2, 7)), int(rng.integers(2, 5))
+        m = P * int(rng.integers(1, 4))
+        f = rng.integers(1, 60, size=(P, v)).tolist()
+        g = rng.integers(1, 120, size=(P, v)).tolist()
+        c = rng.integers(0, 40, size=P - 1).tolist()
+        cw = int(rng.integers(0, 80))
+        T, _ = ilv_dag(f, g, c, cw, m)
+        assert oracle_mod.pipeline_ilv(f, g, c, cw, m) == T, (P, v, m)
+
+
+# ----------------------------------------------------------------------------
+# V.3 all-to-all
+# ----------------------------------------------------------------------------
+def a2a_groups_ref(o, cfg, groups, t, b, round_robin=False):
+    """All-to-all over the union of the groups' devices (g = n t): each TP
+    group's A bytes of routed tokens (k routes per token) leave its t devices
+    evenly and spread over the g expert devices, ceil(A k / (t g)) bytes per
+    ordered pair, in g - 1 rounds.  DESIGN A17: a round lasts as long as the
+    slowest pair of the whole group.  round_robin=True instead ends round r
+    (device x -> x + r mod g) with its own slowest pair (a lower bound, equal
+    on uniform links)."""
+    dev = [(n, b0 + q) for n, b0 in groups for q in range(t)]
+    g = len(dev)
+    if g == 1:
+        return 0
+    per = cdiv(act_bytes(cfg, b) * cfg["model"]["moe_topk"], t * g)
+    if round_robin:
+        return sum(max(tau(o.link(*dev[x], *dev[(x + r) % g]), per) for x in range(g)) for r in range(1, g))
+    return (g - 1) * max(tau(o.link(*dev[x], *dev[y]), per) for x in range(g) for y in range(g) if x != y)
+
+
+@pytest.mark.parametrize("t", [1, 2, 4, 8])
+def test_ep_one_group_is_a17(oracle_mod, t):
+    cfg = H.get(4)
+    o = oracle_mod.Oracle(cfg)
+    for b in (1, 2, 4):
+        assert o.ep_alltoall_groups([(0, 0)], t, b) == o.ep_alltoall(0, 0, t, b)
+
+
+@pytest.mark.parametrize("groups,t", [([(0, 0), (1, 0)], 1), ([(0, 0), (1, 0)], 2), ([(0, 0), (0, 4), (1, 0)], 4),
+                                      ([(8, 0), (9, 2), (10, 4), (11, 6)], 2)])
+def test_ep_groups_round_robin(oracle_mod, groups, t):
+    cfg = H.get(4)
+    o = oracle_mod.Oracle(cfg)
+    for b in (1, 2):
+        got = o.ep_alltoall_groups(groups, t, b)
+        assert got == a2a_groups_ref(o, cfg, groups, t, b)
+        rr = a2a_groups_ref(o, cfg, groups, t, b, round_robin=True)
+        assert rr <= got
+        if t == 1 and len({n for n, _ in groups}) == len(groups) and len({b0 for _, b0 in groups}) == 1:
+            assert rr == got  # every pair on the same rail: uniform links
+
+
+def test_ep_two_h100_nodes_by_hand(oracle_mod):
+    """Two H100 nodes (config 4's nodes 8 and 9), one GPU each (t = 1): g = 2,
+    one round over the rail: 1 x tau(rail, ceil(A k / 2)).  Rail path (Table 4,
+    PAPER.md:329-333): GPU->NIC PCIe 1024 Gbps bidirectional (2 hops, 143.75 ->
+    144 ns each, A9), NIC 368 ns + 200 Gbps, rail 0 ns, NIC 368 ns, PCIe 2 x 144
+    ns: alpha = 4 x 144 + 2 x 368 = 1312 ns, beta = 200/8 = 25 B/ns."""
+    cfg = H.get(4)
+    o = oracle_mod.Oracle(cfg)
+    a, beta = o.link(8, 0, 9, 0)
+    assert (a, beta) == (1312, 25.0)
+    A = 2 * 2048 * 4096 * 2  # b = 2, s = 2048, h = 4096, bf16
+    assert o.ep_alltoall_groups([(8, 0), (9, 0)], 1, 2) == 1312 + math.ceil(cdiv(A * 2, 2) / 25.0)
+
+
+def test_ep_dense_gradient_bytes_mixtral(oracle_mod):
+    """Mixtral 8x7B: 46.7 B parameters, of which 32 layers x 8 experts x 3 x
+    4096 x 14336 = 45.1 B are expert MLP weights.  With V.3 a single-class
+    template synchronises only the rest (plus the router): total segment bytes
+    / bpe_grad within 2 % of 46.7e9 - 45.1e9."""
+    cfg = H.with_ep_dp(H.get(4))
+    o = oracle_mod.Oracle(cfg)
+    d = None
+    for k in range(o.n_templates()):
+        i = int(o.template_prefix()[k]) if d is None else None
+        dd = o.describe(i)
+        if len(dd["classes"]) == 1 and sum(c["D"] for c in dd["classes"]) > 1 and o.eval(i) >= 0:
+            d = dd
+            break
+    assert d is not None
+    S = sum(sg["S"] for sg in o.segments(i)) / cfg["model"]["bpe_grad"]
+    expert = 32 * 8 * 3 * 4096 * 14336
+    assert abs(S - (46.7e9 - expert)) / (46.7e9 - expert) < 0.02, S
+    off = oracle_mod.Oracle(H.get(4))
+    S_full = sum(sg["S"] for sg in off.segments(i)) / cfg["model"]["bpe_grad"]
+    assert S_full - S == expert
+
+
+# ----------------------------------------------------------------------------
+# whole candidates: an independent evaluator with both variants
+# ----------------------------------------------------------------------------
+def py_eval_v(o, cfg, i, overlap=False):
+    """Independent evaluator of candidate i under V.2 (cfg search.interleave)
+    and V.3 (search.ep_dp).  Chunk k of a stage with l layers has
+    l // v + [k < l % v] layers; the embedding rides with chunk 0 of stage 0,
+    the head with chunk v-1 of stage P-1; sync segments refine the classes'
+    virtual-stage boundaries (virtual stage k P + s = chunk k of stage s)."""
+    d = o.describe(i)
+    if d["status"]:
+        return d["status"]
+    se = cfg["search"]
+    vset = se.get("interleave", 1)
+    m_ = model_dims(cfg)
+    b = d["b"]
+    A = act_bytes(cfg, b)
+    moe = m_["E"] > 1
+    ep = bool(se.get("ep_dp", 0)) and moe and len(d["classes"]) == 1
+    T0, lastB = 0, {}
+    vstarts = []  # per class: [(first layer, stage)] in layer order
+    for c, cl in enumerate(d["classes"]):
+        P, D = len(cl["stages"]), cl["D"]
+        v = vset if P >= 2 else 1
+        lay = [[l // v + (1 if k < l % v else 0) for k in range(v)] for l in cl["layers"]]
+        acc, st = 0, []
+        for k in range(v):
+            for s in range(P):
+                st.append((acc, s))
+                acc += lay[s][k]
+        vstarts.append(st)
+
+        def p2p(r, s1, s2):
+            n1, b1 = cl["place"][r][s1]
+            n2, b2 = cl["place"][r][s2]
+            npq = min(cl["stages"][s1][1], cl["stages"][s2][1])
+            return max(tau(o.link(n1, b1 + q, n2, b2 + q), A) for q in range(npq))
+
+        cc = [[p2p(r, s, s + 1) for s in range(P - 1)] for r in range(D)]
+        cw = [p2p(r, P - 1, 0) if v > 1 else 0 for r in range(D)]
+        mb = list(cl["mb"])
+        if ep:  # lockstep: the slowest boundary of any replica, the largest m
+            cc = [[max(x[s] for x in cc) for s in range(P - 1)]] * D
+            cw = [max(cw)] * D
+            mb = [max(mb)] * D
+        for r in range(D):
+            f, g = [], []
+            for s, (ty, tp) in enumerate(cl["stages"]):
+                node, base = cl["place"][r][s]
+                ar = tp_allreduce_ref(o, cfg, node, base, tp, b)
+                kind = "moe" if moe else "mlp"
+                if ep:
+                    groups = [tuple(cl["place"][rr][s]) for rr in range(D)]
+                    from test_variant_pins import a2a_groups_ref as _a2a
+                    a2a = _a2a(o, cfg, groups, tp, b)
+                    gexp = D * tp
+                else:
+                    from test_oracle_pins_r2 import alltoall_round_robin
+                    a2a = alltoall_round_robin(o, cfg, node, base, tp, b) if moe else 0
+                    gexp = tp
+                ch = []
+                for bwd in (0, 1):
+                    x = o.op(ty, "attn", bwd, tp, b)[2] + ar
+                    if moe:
+                        x += a2a + moe_dur(o, cfg, ty, bwd, tp, b, gexp) + a2a
+                    else:
+                        x += o.op(ty, kind, bwd, tp, b)[2] + ar
+                    ch.append(x)
+                fs = [lay[s][k] * ch[0] for k in range(v)]
+                gs = [lay[s][k] * ch[1] for k in range(v)]
+                if s == 0:
+                    fs[0] += o.op(ty, "emb", 0, tp, b)[2]
+                    gs[0] += o.op(ty, "emb", 1, tp, b)[2]
+                if s == P - 1:
+                    fs[v - 1] += o.op(ty, "head", 0, tp, b)[2]
+                    gs[v - 1] += o.op(ty, "head", 1, tp, b)[2]
+                f.append(fs)
+                g.append(gs)
+            T, last = ilv_dag(f, g, cc[r], cw[r], mb[r])
+            T0 = max(T0, T)
+            for s in range(P):
+                lastB[(c, r, s)] = last[s]
+    D = sum(cl["D"] for cl in d["classes"])
+    if D == 1:
+        return T0
+    cuts = sorted(set([0, m_["L"]] + [a for st in vstarts for a, _ in st]))
+    segs = []
+    for a, z in zip(cuts, cuts[1:]):
+        sc = [max(st, key=lambda x: (x[0] <= a, x[0]))[1] for st in vstarts]
+        tps = [cl["stages"][sc[c]][1] for c, cl in enumerate(d["classes"])]
+        tstar = min(tps)
+        S = seg_bytes_v(cfg, a, z, ep)
+        RS = 0
+        for c, cl in enumerate(d["classes"]):
+            if tps[c] != tstar:
+                for r in range(cl["D"]):
+                    node, base = cl["place"][r][sc[c]]
+                    RS = max([RS] + [tau(e, cdiv(S, tstar)) for e in tp_ring_edges(o, node, base, tps[c])])
+        ring = [(cl["place"][r][sc[c]]) for c, cl in enumerate(d["classes"]) for r in range(cl["D"])]
+        chunk = cdiv(cdiv(S, tstar), D)
+        slow = max(tau(o.link(u[0], u[1] + q, w[0], w[1] + q), chunk)
+                   for q in range(tstar) for u, w in zip(ring, ring[1:] + ring[:1]))
+        segs.append((sc, RS + 2 * (D - 1) * slow))
+    free = {}
+    T = T0
+    for j in (range(len(segs) - 1, -1, -1) if overlap else range(len(segs))):
+        sc, cost = segs[j]
+        groups = [(c, r, sc[c]) for c, cl in enumerate(d["classes"]) for r in range(cl["D"])]
+        if overlap:
+            start = max(max(lastB[x], free.get(x, 0)) for x in groups)
+        else:
+            start = max(free.get(x, T0) for x in groups)
+        for x in groups:
+            free[x] = start + cost
+        T = max(T, start + cost)
+    return T
+
+
+def moe_dur(o, cfg, ty, bwd, t, b, g):
+    """MoE op duration with the expert weights sharded over g devices: the
+    roofline of (FLOP of the TP-sharded op, bytes with the weight term / g);
+    g = t is the oracle's own op (A17)."""
+    if g == t:
+        return o.op(ty, "moe", bwd, t, b)[2]
+    m = model_dims(cfg)
+    T = b * m["s"]
+    flop = cdiv(2 * T * m["k"] * m["nm"] * m["h"] * m["f"], t)
+    byts = cdiv(m["bpe"] * m["E"] * m["nm"] * m["h"] * m["f"], g) + 2 * T * m["h"] * m["bpe"]
+    tyd = cfg["cluster"]["types"][ty]
+    mul = 2 if bwd else 1
+    rf = tyd["peak_flop_per_ns"] * tyd["eff_flop"][2]
+    rm = tyd["hbm_bytes_per_ns"] * tyd["eff_mem"][2]
+    return max(math.ceil(mul * flop / rf) if flop else 0, math.ceil(mul * byts / rm))
+
+
+def seg_bytes_v(cfg, a, z, ep):
+    from test_oracle_pins_r2 import segment_bytes_ref
+    S = segment_bytes_ref(cfg, a, z)
+    if ep:
+        m = model_dims(cfg)
+        S -= (z - a) * m["nm"] * m["h"] * m["f"] * m["E"] * m["bg"]
+    return S
+
+
+def _check_space(oracle_mod, cfg, n, seed, overlap=False, need_valid=10):
+    o = oracle_mod.Oracle(cfg)
+    N = o.space_size()
+    idx = np.arange(N) if N <= n else H.sample_indices(N, n, seed=seed)
+    want = o.eval_many(idx, threads=THREADS)
+    for k, i in enumerate(idx):
+        assert py_eval_v(o, cfg, int(i), overlap) == want[k], int(i)
+    assert (want >= 0).sum() >= need_valid
+    return want
+
+
+@pytest.mark.parametrize("seed", [100, 101, 103, 105, 107, 110])
+@pytest.mark.parametrize("v", [2, 3])
+def test_py_eval_interleave_tiny(oracle_mod, seed, v):
+    _check_space(oracle_mod, H.with_interleave(H.variant_tiny(seed), v), 200, seed, need_valid=3)
+
+
+@pytest.mark.parametrize("seed", [101, 105])
+def test_py_eval_interleave_overlap(oracle_mod, seed):
+    _check_space(oracle_mod, H.with_sync_overlap(H.with_interleave(H.variant_tiny(seed), 2)), 150, seed + 1,
+                 overlap=True, need_valid=3)
+
+
+@pytest.mark.parametrize("seed", [100, 102, 104, 106, 108])
+def test_py_eval_ep_dp_tiny(oracle_mod, seed):
+    _check_space(oracle_mod, H.with_ep_dp(H.variant_tiny(seed, moe=True)), 200, seed)
+
+
+def test_py_eval_both_variants(oracle_mod):
+    _check_space(oracle_mod, H.with_ep_dp(H.with_interleave(H.variant_tiny(104, moe=True), 2)), 200, 7,
+                 need_valid=3)
+
+
+def test_ilv_status_rules(oracle_mod):
+    """-1 when a stage holds fewer layers than chunks; -2 when some replica's
+    micro-batch count is not a multiple of its depth; P = 1 classes and
+    non-variant candidates are untouched."""
+    base = H.variant_tiny(101)
+    cfg = H.with_interleave(base, 3)
+    o, o0 = oracle_mod.Oracle(cfg), oracle_mod.Oracle(base)
+    N = o.space_size()
+    assert N == o0.space_size()
+    idx = np.arange(N) if N <= 3000 else H.sample_indices(N, 3000, seed=5)
+    got, ref = o.eval_many(idx, threads=THREADS), o0.eval_many(idx, threads=THREADS)
+    seen = set()
+    for k, i in enumerate(idx):
+        d0 = o0.describe(int(i))
+        cls = d0["classes"]
+        deep = [c for c in cls if len(c["stages"]) >= 2]
+        if ref[k] < 0:  # -1 (a stage with fewer layers than chunks) takes precedence over -2
+            short = ref[k] == -2 and any(min(c["layers"]) < 3 for c in deep)
+            assert got[k] == (-1 if short else ref[k])
+            continue
+        if not deep:
+            assert got[k] == ref[k]
+            seen.add("flat")
+        elif any(min(c["layers"]) < 3 for c in deep):
+            assert got[k] == -1
+            seen.add(-1)
+        elif any(mm % len(c["stages"]) for c in deep for mm in c["mb"]):
+            assert got[k] == -2
+            seen.add(-2)
+        else:
+            assert got[k] >= 0
+            seen.add("ok")
+    assert {"flat", -1, -2} <= seen
+
+
+def test_ep_single_replica_unchanged(oracle_mod):
+    """With D = 1 the EP group is the TP group: V.3 equals A17 on every
+    single-replica candidate (and on every multi-class one)."""
+    base = H.variant_tiny(102, moe=True)
+    o, o0 = oracle_mod.Oracle(H.with_ep_dp(base)), oracle_mod.Oracle(base)
+    N = o.space_size()
+    idx = np.arange(N) if N <= 3000 else H.sample_indices(N, 3000, seed=9)
+    got, ref = o.eval_many(idx, threads=THREADS), o0.eval_many(idx, threads=THREADS)
+    single = 0
+    for k, i in enumerate(idx):
+        d0 = o0.describe(int(i))
+        if len(d0["classes"]) > 1 or (d0["status"] == 0 and d0["classes"][0]["D"] == 1):
+            assert got[k] == ref[k], int(i)
+            single += 1
+    assert single > 10
+
+
+def test_variants_literal_equals_compact(oracle_mod):
+    for cfg in (H.with_interleave(H.variant_tiny(105), 2), H.with_ep_dp(H.variant_tiny(106, moe=True)),
+                H.with_ep_dp(H.with_interleave(H.get(4), 2))):
+        lit, cmp_ = oracle_mod.Oracle(cfg), oracle_mod.Oracle(cfg, compact=True)
+        idx = H.sample_indices(lit.space_size(), 300, seed=11)
+        assert np.array_equal(lit.eval_many(idx, threads=THREADS), cmp_.eval_many(idx, threads=THREADS))
