@@ -136,6 +136,22 @@ typedef struct {
    * FIFO per group (DESIGN.md S.1; Table 1: DP sync is
    * exposed in the backward pass). */
   int32_t sync_overlap;
+  /* SURVEY.md §8(f) f4 variants, off when 0 (a zero-initialised descriptor
+   * keeps the default path):
+   * interleave: 0 or 1 = the non-interleaved 1F1B (DESIGN.md C.7); v = 2..8 =
+   *   every pipeline of >= 2 stages runs Megatron-LM's interleaved 1F1B with v
+   *   model chunks per stage (DESIGN.md V.2): chunk k of a stage with l layers
+   *   holds floor(l/v) + [k < l mod v] layers, virtual stage k P + s = chunk k
+   *   of stage s; a stage with fewer than v layers -> status -1, a replica
+   *   whose micro-batch count is not a multiple of its depth -> -2.
+   * ep_dp: 1 = in single-class MoE templates the experts of a stage are
+   *   sharded over every replica's TP group of that stage, g = D tp devices
+   *   (DESIGN.md V.3): the all-to-all spans them and couples the replicas
+   *   into lockstep, and expert gradients are not all-reduced.
+   * Neither combines with mem_check (HSIM_EINVAL at create) nor with
+   * hsim_flow_resim (HSIM_EINVAL). */
+  int32_t interleave;
+  int32_t ep_dp;
 } hsim_model_desc;
 
 /* Which candidates the t-th work item (t = 0..n-1) evaluates. */

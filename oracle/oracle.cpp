@@ -45,6 +45,7 @@
 #include <algorithm>
 #include <array>
 #include <map>
+#include <mutex>
 #include <atomic>
 #include <cmath>
 #include <cstdint>
@@ -519,7 +520,23 @@ struct Oracle {
   // V.3: all-to-all over the union of the groups' devices (g = n tp): g - 1
   // rounds, each bounded by the slowest ordered pair, message ceil(A k / (t g))
   // per pair (A17 is the one-group case, g = t)
+  // (memoised per (groups, t, b): the group-wide pair scan is O(g^2))
+  mutable std::mutex a2a_mu;
+  mutable std::map<std::tuple<std::vector<std::pair<int, int>>, int, int>, i64> a2a_memo;
   i64 ep_alltoall_x(const std::vector<Group>& gs, int t, int b) const {
+    std::vector<std::pair<int, int>> key;
+    for (const Group& g : gs) key.push_back({g.node, g.base});
+    {
+      std::lock_guard<std::mutex> lk(a2a_mu);
+      auto it = a2a_memo.find(std::make_tuple(key, t, b));
+      if (it != a2a_memo.end()) return it->second;
+    }
+    const i64 v = ep_alltoall_x_scan(gs, t, b);
+    std::lock_guard<std::mutex> lk(a2a_mu);
+    a2a_memo[std::make_tuple(key, t, b)] = v;
+    return v;
+  }
+  i64 ep_alltoall_x_scan(const std::vector<Group>& gs, int t, int b) const {
     std::vector<std::pair<int, int>> dev;
     for (const Group& g : gs)
       for (int q = 0; q < t; ++q) dev.push_back({g.node, g.base + q});

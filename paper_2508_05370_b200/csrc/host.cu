@@ -89,6 +89,9 @@ struct hsim_handle {
   int depth_max = 0;
   int stages_max = 0;       // max over templates of the stages of all classes (S.1 scratch rows)
   int pcnt_max[FASTP + 1] = {0};  // max #classes of depth P in one template (job-list capacity)
+  int ilv = 1;              // V.2: model chunks per stage (1 = non-interleaved)
+  int ilv_jobs_max = 0;     // V.2: max #classes with P >= 2 in one template (K_ilv job-list capacity)
+  int ilv_depth_max = 0;    // V.2: deepest interleaved pipeline
   i64 depth_jobs_space[FASTP + 1] = {0};  // class-jobs of depth P over the whole space
   i64 N = 0;
   Tables hT{};  // host pointers (for hsim_decode)
@@ -151,7 +154,9 @@ struct hsim_handle {
   void derive_links();
   void derive_durations();
   void enumerate();
-  int32_t crec(int b_idx, int M, int D, const std::vector<std::pair<int, int>>& stages);
+  int32_t crec(int b_idx, int M, int D, const std::vector<std::pair<int, int>>& stages, bool ep);
+  i64 moe_dur(int t, int tp, i64 b, i64 g, bool bwd) const;
+  i64 a2a_groups(const std::vector<std::pair<int, int>>& groups, int tp, i64 b) const;
   std::vector<std::vector<std::pair<int, int>>> place(int D, const std::vector<std::pair<int, int>>& stages) const;
   void prepare();
   void upload();
@@ -221,6 +226,10 @@ void hsim_handle::validate() {
   if (m.r_layer < 0 || m.r_batch < 0 || m.r_layer > 8 || m.r_batch > 8) fail(HSIM_EINVAL, "InvalidValue: radii");
   if (m.pmax_perturb < 0 || m.pmax_perturb > MAXP) fail(HSIM_EINVAL, "InvalidValue: pmax_perturb must be 0..64");
   if (m.homo && c.n_device_types > MAXC) fail(HSIM_EINVAL, "InvalidValue: too many classes");
+  if (m.interleave < 0 || m.interleave > 8) fail(HSIM_EINVAL, "InvalidValue: interleave must be 0..8");
+  if (m.ep_dp != 0 && m.ep_dp != 1) fail(HSIM_EINVAL, "InvalidValue: ep_dp must be 0 or 1");
+  if (m.mem_check && (m.interleave > 1 || m.ep_dp))
+    fail(HSIM_EINVAL, "InvalidValue: mem_check is not defined with interleave / ep_dp (DESIGN.md V.2, V.3)");
 }
 
 void hsim_handle::derive_links() {
@@ -381,15 +390,67 @@ std::vector<std::vector<std::pair<int, int>>> hsim_handle::place(int D, const st
   return out;
 }
 
-// class record: (b, D, stages) -> offset of the record in the pool
-int32_t hsim_handle::crec(int bi, int M, int D, const std::vector<std::pair<int, int>>& stages) {
-  std::vector<int> key{bi, D};
+// V.3: MoE op duration on type t with TP tp and the expert weights sharded
+// over g devices (DESIGN.md C.5 with the weight-byte divisor g; g = tp is C.5)
+i64 hsim_handle::moe_dur(int t, int tp, i64 b, i64 g, bool bwd) const {
+  const i64 h = md.hidden, T = b * md.seq, f = md.ffn, nm = md.mlp_mats, bpe = md.bpe_act;
+  const i64 fl = ceil_div(2 * T * md.moe_topk * nm * h * f, tp);
+  const i64 by = ceil_div(bpe * md.moe_experts * nm * h * f, g) + 2 * T * h * bpe;
+  const hsim_device_type& ty = types[t];
+  const i64 mul = bwd ? 2 : 1;
+  return std::max(ceilq(mul * fl, ty.peak_flop_per_ns * ty.eff_flop[HSIM_KIND_MOE]),
+                  ceilq(mul * by, ty.hbm_bytes_per_ns * ty.eff_mem[HSIM_KIND_MOE]));
+}
+
+// V.3: all-to-all over the union of the TP groups (node, base) of size tp:
+// (g - 1) x the slowest ordered pair at ceil(A k / (tp g)) bytes (A17 with g =
+// #groups x tp).  Pairs are visited per distinct (node type, rank set) node
+// signature -- a link depends only on (same node?, types, ranks) -- so the
+// cost stays O(signatures^2 x 64) for any number of replicas.
+i64 hsim_handle::a2a_groups(const std::vector<std::pair<int, int>>& groups, int tp, i64 b) const {
+  const i64 g = (i64)groups.size() * tp;
+  if (g == 1) return 0;
+  std::map<int, uint32_t> ranks;  // node -> local ranks used
+  for (auto& gr : groups)
+    for (int q = 0; q < tp; ++q) ranks[gr.first] |= 1u << (gr.second + q);
+  // (type, ranks) -> up to two nodes with that signature
+  std::map<std::pair<int, uint32_t>, std::vector<int>> sig;
+  for (auto& kv : ranks) {
+    auto& v = sig[std::make_pair(node_type[kv.first], kv.second)];
+    if (v.size() < 2) v.push_back(kv.first);
+  }
+  const i64 per = ceil_div(b * md.seq * md.hidden * md.bpe_act * md.moe_topk, (i64)tp * g);
+  i64 slow = 0;
+  for (auto& x : sig)
+    for (auto& y : sig) {
+      const int n1 = x.second[0];
+      // a node of y other than n1 (cross-node links depend on types and ranks only)
+      const int n2 = &x == &y ? (x.second.size() > 1 ? x.second[1] : -1) : y.second[0];
+      for (int r1 = 0; r1 < MAXG; ++r1) {
+        if (!(x.first.second >> r1 & 1)) continue;
+        for (int r2 = 0; r2 < MAXG; ++r2) {
+          if (!(y.first.second >> r2 & 1)) continue;
+          if (&x == &y && r1 != r2) slow = std::max(slow, tau(link(n1, r1, n1, r2), per));  // same node
+          if (n2 >= 0) slow = std::max(slow, tau(link(n1, r1, n2, r2), per));
+        }
+      }
+    }
+  return (g - 1) * slow;
+}
+
+// class record: (b, D, stages, ep) -> offset of the record in the pool.
+// ep (V.3): the class is a single-class MoE template whose experts span its
+// replicas -- per-stage all-to-all over every replica's group, lockstep
+// replicas (one sub-class: the slowest boundary of any replica, replica 0's m).
+int32_t hsim_handle::crec(int bi, int M, int D, const std::vector<std::pair<int, int>>& stages, bool ep) {
+  std::vector<int> key{bi, D, ep ? 1 : 0};
   for (auto& s : stages) { key.push_back(s.first); key.push_back(s.second); }
   auto it = crec_of.find(key);
   if (it != crec_of.end()) return it->second;
   (void)M;
   const int P = (int)stages.size();
   const i64 b = bs[bi];
+  const auto pl = place(D, stages);
   std::vector<StageRec> sr(P);
   std::vector<i64> w(P);
   for (int s = 0; s < P; ++s) {
@@ -398,14 +459,22 @@ int32_t hsim_handle::crec(int bi, int M, int D, const std::vector<std::pair<int,
     StageRec& r = sr[s];
     std::memset(&r, 0, sizeof r);
     r.type = t; r.tp = tp; r.lg_tp = lg;
+    i64 mlp_f = d.mlp_f, mlp_b = d.mlp_b, a2a = d.a2a;
+    if (ep) {
+      std::vector<std::pair<int, int>> grp(D);
+      for (int q = 0; q < D; ++q) grp[q] = pl[q][s];
+      a2a = a2a_groups(grp, tp, b);
+      mlp_f = moe_dur(t, tp, b, (i64)D * tp, false);
+      mlp_b = moe_dur(t, tp, b, (i64)D * tp, true);
+    }
     if (md.moe_experts > 1) {
-      r.layer_f = d.attn_f + d.ar + d.a2a + d.mlp_f + d.a2a;
-      r.layer_b = d.attn_b + d.ar + d.a2a + d.mlp_b + d.a2a;
+      r.layer_f = d.attn_f + d.ar + a2a + mlp_f + a2a;
+      r.layer_b = d.attn_b + d.ar + a2a + mlp_b + a2a;
     } else {
       r.layer_f = d.attn_f + d.ar + d.mlp_f + d.ar;
       r.layer_b = d.attn_b + d.ar + d.mlp_b + d.ar;
     }
-    r.tcomp = d.attn_f + d.mlp_f + d.attn_b + d.mlp_b;
+    r.tcomp = d.attn_f + mlp_f + d.attn_b + mlp_b;
     if (s == 0) { r.fext += d.emb_f; r.gext += d.emb_b; r.wext += d.emb_f + d.emb_b; }
     if (s == P - 1) { r.fext += d.head_f; r.gext += d.head_b; r.wext += d.head_f + d.head_b; }
     r.tp_mask = tp_mask[t][lg];
@@ -424,7 +493,6 @@ int32_t hsim_handle::crec(int bi, int M, int D, const std::vector<std::pair<int,
     std::stable_sort(ord.begin(), ord.end(), [&](int x, int y) { return rem[x] > rem[y]; });
     for (i64 k = 0; k < md.layers - given; ++k) sr[ord[k]].l0 += 1;
   }
-  const auto pl = place(D, stages);
   for (int s = 0; s < P; ++s) {
     sr[s].first_node = pl[0][s].first; sr[s].first_base = pl[0][s].second;
     sr[s].last_node = pl[D - 1][s].first; sr[s].last_base = pl[D - 1][s].second;
@@ -433,26 +501,34 @@ int32_t hsim_handle::crec(int bi, int M, int D, const std::vector<std::pair<int,
         for (int q = 0; q < (1 << lg); ++q)
           sr[s].dp_mask[lg] |= (u64)1 << lc(link(pl[r][s].first, pl[r][s].second + q, pl[r + 1][s].first, pl[r + 1][s].second + q));
   }
-  // p2p cost per replica per boundary (A8): rank pairs q < min(tp_s, tp_s+1), max of tau(A)
+  // p2p cost per replica per boundary (A8): rank pairs q < min(tp_s, tp_s+1),
+  // max of tau(A); V.2 appends the wrap boundary stage P-1 -> stage 0
   const i64 A = b * md.seq * md.hidden * md.bpe_act;
-  std::vector<std::vector<i64>> cv(D, std::vector<i64>(P > 1 ? P - 1 : 0));
-  for (int r = 0; r < D; ++r)
-    for (int s = 0; s + 1 < P; ++s) {
-      const int np = std::min(stages[s].second, stages[s + 1].second);
-      i64 c = 0;
-      for (int q = 0; q < np; ++q)
-        c = std::max(c, tau(link(pl[r][s].first, pl[r][s].second + q, pl[r][s + 1].first, pl[r][s + 1].second + q), A));
-      cv[r][s] = c;
-      c_max = std::max(c_max, c);
-    }
+  const bool wrap = ilv > 1 && P >= 2;
+  auto p2p = [&](int r, int s1, int s2) {
+    const int np = std::min(stages[s1].second, stages[s2].second);
+    i64 c = 0;
+    for (int q = 0; q < np; ++q)
+      c = std::max(c, tau(link(pl[r][s1].first, pl[r][s1].second + q, pl[r][s2].first, pl[r][s2].second + q), A));
+    return c;
+  };
+  std::vector<std::vector<i64>> cv(D, std::vector<i64>(P, 0));  // [0, P-1) boundaries, [P-1] wrap
+  for (int r = 0; r < D; ++r) {
+    for (int s = 0; s + 1 < P; ++s) cv[r][s] = p2p(r, s, s + 1);
+    if (wrap) cv[r][P - 1] = p2p(r, P - 1, 0);
+    for (i64 c : cv[r]) c_max = std::max(c_max, c);
+  }
+  if (ep)  // lockstep: every replica runs the slowest boundary of any replica
+    for (int r = 1; r < D; ++r)
+      for (int s = 0; s < P; ++s) cv[0][s] = std::max(cv[0][s], cv[r][s]);
   depth_max = std::max(depth_max, P);
   // sub-classes (A13): replicas with identical p2p vectors, ordered by lowest replica
   std::vector<int> rep;
   std::map<std::vector<i64>, int> seen;
-  for (int r = 0; r < D; ++r)
+  for (int r = 0; r < (ep ? 1 : D); ++r)
     if (seen.emplace(cv[r], r).second) rep.push_back(r);
   const int32_t off = (int32_t)pool.size();
-  if ((size_t)off + HDR_WORDS + 16 * P + rep.size() * P > (size_t)INT32_MAX)
+  if ((size_t)off + HDR_WORDS + 16 * P + rep.size() * (P + 1) > (size_t)INT32_MAX)
     fail(HSIM_ERANGE, "class-record pool exceeds 2^31 entries");
   CrecHdr hd{};
   hd.P = P;
@@ -462,13 +538,13 @@ int32_t hsim_handle::crec(int bi, int M, int D, const std::vector<std::pair<int,
   hd.pw = 1;
   for (int q = 0; q < hd.nd; ++q) hd.pw *= (u32)(2 * md.r_layer + 1);
   hd.pwdiv = make_fastdiv(hd.pw);
-  pool.resize(off + HDR_WORDS + 16 * P + rep.size() * P);
+  pool.resize(off + HDR_WORDS + 16 * P + rep.size() * (P + 1));
   std::memcpy(&pool[off], &hd, sizeof hd);
   std::memcpy(&pool[off + HDR_WORDS], sr.data(), sizeof(StageRec) * P);
   for (size_t u = 0; u < rep.size(); ++u) {
-    i64* sub = &pool[off + HDR_WORDS + 16 * P + u * P];
+    i64* sub = &pool[off + HDR_WORDS + 16 * P + u * (P + 1)];
     sub[0] = rep[u];
-    for (int s = 0; s + 1 < P; ++s) sub[1 + s] = cv[rep[u]][s];
+    for (int s = 0; s < P; ++s) sub[1 + s] = cv[rep[u]][s];
   }
   crec_of[key] = off;
   return off;
@@ -513,12 +589,22 @@ void hsim_handle::enumerate() {
       r.prefix = acc;
       r.rD = 1.0 / (double)Dt;
       r.b = b; r.M = (int32_t)M; r.C = (int32_t)classes.size(); r.D = (int32_t)Dt;
+      const bool ep = md.ep_dp && md.moe_experts > 1 && classes.size() == 1;  // V.3
+      r.flags = ep ? 1 : 0;
+      int cnt[33] = {0}, nilv = 0;
       for (size_t c = 0; c < classes.size(); ++c) {
-        r.crec[c] = crec((int)bi, (int)M, classes[c].first, classes[c].second);
-        r.pmask |= 1u << std::min<int>((int)classes[c].second.size(), 31);
+        const int P = (int)classes[c].second.size();
+        r.crec[c] = crec((int)bi, (int)M, classes[c].first, classes[c].second, ep);
+        if (ilv > 1 && P >= 2) {  // V.2: every interleaved pipeline runs in K_ilv (pmask bit 0)
+          r.pmask |= 1u;
+          ++nilv;
+          ilv_depth_max = std::max(ilv_depth_max, P);
+        } else {
+          r.pmask |= 1u << std::min<int>(P, 31);
+          cnt[std::min<int>(P, 32)]++;
+        }
       }
-      int cnt[33] = {0};
-      for (auto& cl : classes) cnt[std::min<int>((int)cl.second.size(), 32)]++;
+      ilv_jobs_max = std::max(ilv_jobs_max, nilv);
       for (int q = 0; q <= FASTP; ++q) pcnt_max[q] = std::max(pcnt_max[q], cnt[q]);
       for (int q = 0; q <= FASTP; ++q) depth_jobs_space[q] += R * cnt[q];
       pmask_all |= r.pmask;
@@ -615,6 +701,9 @@ void hsim_handle::prepare() {
   // memory feasibility (DESIGN.md M.1); overlapped sync (DESIGN.md S.1)
   hT.mem_check = md.mem_check ? 1 : 0;
   hT.sync_overlap = md.sync_overlap ? 1 : 0;
+  hT.interleave = ilv;
+  hT.ep_dp = md.ep_dp;
+  hT.seg_layer_dense = (h * (2 * h + 2 * hkv) + (E > 1 ? h * E : 0) + 2 * h) * md.bpe_grad;  // V.3
   if (md.sync_overlap && md.layers > 32767) fail(HSIM_ERANGE, "sync_overlap needs layers < 2^15");
   {
     const i64 bst = (i64)md.bpe_act + md.bpe_grad + 12;  // weights + gradients + Adam fp32 master / m / v
@@ -856,12 +945,15 @@ int hsim_create(const hsim_cluster_desc* cluster, const hsim_model_desc* model, 
     for (const auto& d : h->dur)
       if (d.ok && (i64)model->layers * (d.attn_f + d.mlp_f + d.attn_b + d.mlp_b) + d.emb_f + d.emb_b + d.head_f + d.head_b >= ((i64)1 << 40))
         fail(HSIM_ERANGE, "a stage's compute time reaches 2^40 ns");
+    h->ilv = model->interleave > 1 ? model->interleave : 1;
     h->enumerate();
     if (h->N <= 0) fail(HSIM_EINVAL, "InsufficientDevices: the candidate space is empty");
     {  // every 1F1B time <= sum of all op and message weights <= m (L max layer f+g + 2 max emb/head f+g
        // + 2 P max p2p), m <= global batch
+      // (V.2: every micro-batch crosses v P boundaries each way, the wraps included)
       const double bound = (double)model->global_batch *
-                           ((double)model->layers * h->layer_fb_max + 2.0 * h->ext_max + 2.0 * h->depth_max * (double)h->c_max);
+                           ((double)model->layers * h->layer_fb_max + 2.0 * h->ext_max +
+                            2.0 * h->ilv * (h->depth_max + 1) * (double)h->c_max);
       if (bound >= 4503599627370496.0) fail(HSIM_ERANGE, "1F1B times may reach 2^52 ns");
     }
     h->prepare();
@@ -1022,6 +1114,7 @@ int hsim_flow_resim(hsim_handle* h, const int64_t* idx, int32_t k, int64_t* out,
     return HSIM_EINVAL;
   }
   if ((i64)h->md.layers > 256) { g_err = "InvalidValue: flow re-simulation supports up to 256 layers"; return HSIM_EINVAL; }
+  if (h->ilv > 1 || h->md.ep_dp) { g_err = "InvalidValue: flow re-simulation is defined for the default schedule only (no interleave / ep_dp)"; return HSIM_EINVAL; }
   if (k == 0) return HSIM_OK;
   int rc = h->ensure_device();
   if (rc) return rc;
@@ -1115,6 +1208,9 @@ int depth_jobs_max(const hsim_handle* h, int P) { return P >= 0 && P <= FASTP ? 
 int64_t depth_jobs_space(const hsim_handle* h, int P) { return P >= 0 && P <= FASTP ? h->depth_jobs_space[P] : 0; }
 int stages_max(const hsim_handle* h) { return h->stages_max; }
 int sync_overlap(const hsim_handle* h) { return h->md.sync_overlap; }
+int interleave_v(const hsim_handle* h) { return h->ilv; }
+int ilv_jobs_max(const hsim_handle* h) { return h->ilv_jobs_max; }
+int ilv_depth_max(const hsim_handle* h) { return h->ilv_depth_max; }
 int ensure_block_scratch(hsim_handle* h, size_t entries, int64_t** out) {
   if (entries > h->blk_cap) {
     cudaFree(h->d_blk);

@@ -83,15 +83,17 @@ struct CrecHdr {
   int32_t _pad;
 };
 static_assert(sizeof(CrecHdr) == 32, "CrecHdr layout");
-// crec layout in the int64 pool: CrecHdr (4 x i64) | StageRec[P] (16 x i64 each) | U x (i64 k_u, i64 c[P-1])
+// crec layout in the int64 pool: CrecHdr (4 x i64) | StageRec[P] (16 x i64 each) |
+// U x (i64 k_u, i64 c[P-1], i64 c_wrap): sub-class records of P + 1 words; c_wrap
+// = the stage P-1 -> stage 0 p2p cost of the interleaved schedule (V.2; else 0)
 constexpr int HDR_WORDS = 4;
 
 struct TplRec {
   i64 prefix;             // first candidate index
   int32_t b, M, C, D;     // micro-batch size, #micro-batches, classes, total replicas
   int32_t crec[MAXC];     // int64-offsets of the class records in the pool
-  uint32_t pmask;         // bit min(P, 31) set for every class depth P
-  int32_t _pad;
+  uint32_t pmask;         // bit min(P, 31) set for every class depth P (V.2: P >= 2 -> bit 0)
+  int32_t flags;          // bit 0: V.3 expert parallelism across the replicas (dense-only gradient sync)
   double rD;              // 1.0 / D (ring chunk: ceil division by D with exact fix-up)
 };
 
@@ -135,6 +137,8 @@ struct Tables {
   // layer / for the embedding / for the head on one device, and
   // K[lg] = s h (10 t + 24) (activation bytes per layer = ceil(b K / t))
   int32_t mem_check, sync_overlap;
+  int32_t interleave, ep_dp;  // DESIGN.md V.2 (v chunks per stage; 1 = off), V.3
+  i64 seg_layer_dense;        // V.3: W_layer without the expert matrices, x bpe_grad
   i64 mem_layer[4], mem_emb[4], mem_head[4], mem_K[4];
   i64 mem_cap[MAXT];
   // f3 flow-level re-simulation (DESIGN.md F.1): rail-only link graph
@@ -221,7 +225,7 @@ HD i64 eval_mask(const Tables& T, u64 mask, i64 x) {
 HD const CrecHdr* crec_hdr(const Tables& T, int32_t off) { return (const CrecHdr*)(T.pool + off); }
 HD const StageRec* crec_stages(const Tables& T, int32_t off) { return (const StageRec*)(T.pool + off + HDR_WORDS); }
 HD const i64* crec_sub(const Tables& T, int32_t off, int P, int u) {
-  return T.pool + off + HDR_WORDS + 16 * P + (i64)u * P;  // (k_u, c[0..P-2]) = P int64
+  return T.pool + off + HDR_WORDS + 16 * P + (i64)u * (P + 1);  // (k_u, c[0..P-2], c_wrap)
 }
 
 // upper_bound(x) - 1 over a sorted int64 array of n+1 entries (first entry 0)
@@ -331,9 +335,10 @@ HD int partition_c(const Tables& T, const TplRec& tp, i64 local, ClassSplit (&cs
     loc = lq;
     LayerWalk lw = walk(T, h, cs[c].dig);
     i64 worst = 0;
+    const int lmin = T.interleave > 1 && h->P >= 2 ? T.interleave : 1;  // V.2: every chunk holds a layer
     for (int s = 0; s < h->P; ++s) {
       const int l = lw.next(st);
-      if (l < 1) status = -1;
+      if (l < lmin) status = -1;
       worst = imax(worst, (i64)l * st[s].tcomp + st[s].wext);
     }
     i64 wr;
@@ -375,6 +380,18 @@ HD int partition_c(const Tables& T, const TplRec& tp, i64 local, ClassSplit (&cs
 #pragma unroll
   for (int c = 0; c < C; ++c)
     if (mb_of(cs[c], D[c] - 1) < 1) return -2;  // m non-increasing in k
+  if (T.interleave > 1) {
+    // V.2: every replica's m must be a multiple of its depth; the distinct m
+    // of a class occur at k = 0, D-1 and next to the seats / rm thresholds
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      const i64 P = crec_hdr(T, tp.crec[c])->P;
+      if (P < 2) continue;
+      const i64 ks[6] = {0, D[c] - 1, cs[c].seats - 1, cs[c].seats, cs[c].rm - 1, cs[c].rm};
+      for (int q = 0; q < 6; ++q)
+        if (ks[q] >= 0 && ks[q] < D[c] && mb_of(cs[c], ks[q]) % P) return -2;
+    }
+  }
   if (T.mem_check) {
     // DESIGN.md M.1: every device of every stage fits; replica 0 has the most
     // micro-batches (m non-increasing in k) and need is non-decreasing in m
@@ -753,7 +770,10 @@ HD PipeOut class_pipes_inl(const Tables& T, int32_t off, const ClassSplit& cs, i
 // through device base + q, q < t*.
 template <int C>
 HD i64 seg_cost_c(const Tables& T, const TplRec& tp, const StageRec* const (&st)[C], const int (&sc)[C], i64 a, i64 z) {
-  const i64 S = (z - a) * T.seg_layer_bytes + (a == 0 ? T.seg_first_bytes : 0) + (z == T.L ? T.seg_last_bytes : 0);
+  // V.3 (tp.flags bit 0): the expert weights are sharded over the replicas, so
+  // only the dense parameters are all-reduced
+  const i64 lb = (tp.flags & 1) ? T.seg_layer_dense : T.seg_layer_bytes;
+  const i64 S = (z - a) * lb + (a == 0 ? T.seg_first_bytes : 0) + (z == T.L ? T.seg_last_bytes : 0);
   int tstar = 1 << 30, lg = 0;
 #pragma unroll
   for (int c = 0; c < C; ++c) {
@@ -875,6 +895,73 @@ HD i64 grad_sync_overlap_c(const Tables& T, const TplRec& tp, const ClassSplit (
       }
     }
     z = a;
+  }
+  return Titer;
+}
+
+// V.2 (interleaved 1F1B): stage s of a class holds v layer ranges (virtual
+// stage k P + s = chunk k of stage s, chunk k of l layers = l / v + [k < l mod
+// v]), so a (class, stage) group is revisited by later segments: the group
+// clocks are explicit.  C.8 (R == nullptr): segments in ascending layer order
+// from T0; S.1: descending, each ready when its groups' last backward ended
+// (R[(coff_c + s) * rs]).  FIFO per group either way.
+template <int C>
+HD i64 grad_sync_ilv_c(const Tables& T, const TplRec& tp, const ClassSplit (&cs)[C], const i64* R, i64 rs, i64 T0) {
+  const StageRec* st[C];
+  int P[C], v[C], coff[C], x[C], sc[C];
+  int16_t lay[C][MAXP];
+  i64 fr[C][MAXP], lo[C], hi[C];
+  const bool desc = R != nullptr;
+  int off = 0;
+  for (int c = 0; c < C; ++c) {
+    const CrecHdr* h = crec_hdr(T, tp.crec[c]);
+    st[c] = crec_stages(T, tp.crec[c]);
+    P[c] = h->P;
+    v[c] = h->P >= 2 ? T.interleave : 1;
+    coff[c] = off;
+    off += h->P;
+    LayerWalk lw = walk(T, h, cs[c].dig);
+    for (int q = 0; q < h->P; ++q) {
+      lay[c][q] = (int16_t)lw.next(st[c]);
+      fr[c][q] = desc ? 0 : T0;
+    }
+    x[c] = desc ? v[c] * P[c] - 1 : 0;
+  }
+  auto chunk = [&](int c, int xx) {  // layers of virtual stage xx of class c
+    const int s = xx % P[c], k = xx / P[c], l = lay[c][s];
+    return (i64)(l / v[c] + (k < l % v[c] ? 1 : 0));
+  };
+  for (int c = 0; c < C; ++c) {
+    sc[c] = x[c] % P[c];
+    if (desc) { hi[c] = T.L; lo[c] = T.L - chunk(c, x[c]); }
+    else { lo[c] = 0; hi[c] = chunk(c, 0); }
+  }
+  // segment = [max lo, min hi): the common refinement at the cursors
+  i64 Titer = T0;
+  for (;;) {
+    i64 sa = 0, sz = T.L, ready = 0, begin = 0;
+    for (int c = 0; c < C; ++c) {
+      sa = imax(sa, lo[c]);
+      sz = imin(sz, hi[c]);
+      begin = imax(begin, fr[c][sc[c]]);
+      if (desc) ready = imax(ready, R[(i64)(coff[c] + sc[c]) * rs]);
+    }
+    const i64 end = imax(begin, ready) + seg_cost_c<C>(T, tp, st, sc, sa, sz);
+    Titer = imax(Titer, end);
+    for (int c = 0; c < C; ++c) fr[c][sc[c]] = end;
+    if (desc ? sa == 0 : sz == T.L) break;
+    for (int c = 0; c < C; ++c) {
+      if (desc && lo[c] == sa) {
+        --x[c];
+        hi[c] = lo[c];
+        lo[c] = hi[c] - chunk(c, x[c]);
+      } else if (!desc && hi[c] == sz) {
+        ++x[c];
+        lo[c] = hi[c];
+        hi[c] = lo[c] + chunk(c, x[c]);
+      }
+      sc[c] = x[c] % P[c];
+    }
   }
   return Titer;
 }

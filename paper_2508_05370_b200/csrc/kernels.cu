@@ -44,6 +44,9 @@ int depth_jobs_max(const hsim_handle* h, int P);
 int64_t depth_jobs_space(const hsim_handle* h, int P);
 int stages_max(const hsim_handle* h);
 int sync_overlap(const hsim_handle* h);
+int interleave_v(const hsim_handle* h);
+int ilv_jobs_max(const hsim_handle* h);
+int ilv_depth_max(const hsim_handle* h);
 cudaStream_t side_stream(const hsim_handle* h, int q);
 cudaEvent_t fork_event(const hsim_handle* h);
 cudaEvent_t join_event(const hsim_handle* h, int q);
@@ -115,6 +118,8 @@ constexpr unsigned FULL = 0xffffffffu;
 // counter slots: P (1..FASTP) = work counter of K_pipe<P>; CNT_FULL + P = #jobs of
 // depth P in full (32-aligned) chunks, CNT_PART + P = #jobs from partial chunks
 constexpr int CNT_DEEP = 17, CNT_NDEEP = 18, CNT_CELLS = 19, CNT_FULL = 20, CNT_PART = 40, CNT_REQ = 55, NCNT = 64;
+// V.2 (interleaved 1F1B): #jobs in the K_ilv list, K_ilv's work counter
+constexpr int CNT_ILV = 37, CNT_ILVW = 38;
 // re-queued jobs of depth P (lane compaction), P in [2, HSIM_REQ_MAXP]: count at CNT_REQ + P
 #ifndef HSIM_REQ_MAXP
 #define HSIM_REQ_MAXP 8
@@ -158,6 +163,7 @@ struct Scratch {
   i64* req[HSIM_REQ_MAXP + 1];  // per depth: re-queued jobs (slot << 16 | u << 4 | class)
   i64 req_cap[HSIM_REQ_MAXP + 1];
   int32_t* deep;      // [ns] slots with a class deeper than FASTP (compacted)
+  int32_t* ilv;       // V.2: jobs (slot << 2 | class) of interleaved pipelines (P >= 2), or nullptr
   int32_t* full[FASTP + 1];  // per depth: jobs (slot << 2 | class) of full chunks, 32-aligned groups
   int32_t* part[FASTP + 1];  // per depth: jobs of partial chunks, packed
   unsigned long long* counters;  // [NCNT]
@@ -282,10 +288,22 @@ __global__ void __launch_bounds__(NT, HSIM_SPLIT_MINB) k_split(const Tables* __r
     // lanes have near-equal micro-batch counts; partial chunks (small-radix
     // templates) are packed densely
     u64 combos = 0;
+    uint32_t ilvc = 0;  // V.2: classes of this lane's candidate that run interleaved (K_ilv)
     if (mypm)
       for (int k = 0; k < sT.tpl[tau].C; ++k) {
         const int P = crec_hdr(sT, sT.tpl[tau].crec[k])->P;
-        if (P <= FASTP) combos |= (u64)1 << ((P - 1) * 4 + k);
+        if (sT.interleave > 1 && P >= 2) ilvc |= 1u << k;
+        else if (P <= FASTP) combos |= (u64)1 << ((P - 1) * 4 + k);
+      }
+    if (__any_sync(FULL, ilvc != 0))
+      for (int k = 0; k < MAXC; ++k) {
+        const bool has = ilvc >> k & 1;
+        const unsigned bal = __ballot_sync(FULL, has);
+        if (!bal) continue;
+        unsigned long long o = 0;
+        if (lane == 0) o = atomicAdd(&S.counters[CNT_ILV], (unsigned long long)__popc(bal));
+        o = __shfl_sync(FULL, o, 0) + __popc(bal & ((1u << lane) - 1));
+        if (has) S.ilv[o] = (int32_t)(slot << 2 | k);
       }
     u64 all = (u64)__reduce_or_sync(FULL, (unsigned)combos) | (u64)__reduce_or_sync(FULL, (unsigned)(combos >> 32)) << 32;
     while (all) {
@@ -662,6 +680,199 @@ __global__ void __launch_bounds__(NT) k_deep(const Tables* __restrict__ gT, Scra
   if (count) {
     cells = warp_sum(cells);
     if (lane == 0 && cells) atomicAdd(&S.counters[CNT_CELLS], (unsigned long long)cells);
+  }
+}
+
+// ---- K_ilv: interleaved 1F1B (DESIGN.md V.2), warp per (candidate, class) -----
+// Megatron-LM's virtual pipeline: stage s runs the table forwards F_tab[0..w),
+// w = min(2(P-1-s) + (v-1)P, m v), then pairs (F_tab[w+i], B_tab[i]), then the
+// remaining backwards; the tables visit micro-batches in groups of P, chunks
+// 0..v-1 (forward) / v-1..0 (backward) within a group (m mod P = 0 is
+// checked by the partition).  Lane l owns stages l and l + 32.  The warp
+// advances all stages in rounds: a stage runs its next op once the op's input
+// exists (produced in an earlier round) -- an as-soon-as-possible order of
+// the same max-plus recurrence, so the values do not depend on the rounds.
+// A stage keeps the end times of its last Q forward and backward ops in
+// shared-memory rings indexed by table position; a consumer reads position x
+// of its producer's table, and the producer is then at most P/2 + 1 positions
+// ahead (tests/test_ilv_host.py checks every P <= 64, v <= 8 on the host), so
+// Q >= P/2 + 2 (a power of two chosen by the host) never overwrites an unread
+// slot; a violation would set status -5 (never expected).
+__device__ __forceinline__ double ilv_dur(double lf, double ext, int l, int v, int k, bool with_ext) {
+  return (double)(l / v + (k < l % v ? 1 : 0)) * lf + (with_ext ? ext : 0.0);
+}
+
+// dynamic shared memory per warp: ILV_WORDS(PM, Q) doubles (PM = deepest
+// interleaved pipeline, Q = ring length, both from the host)
+#define ILV_WORDS(PM, Q) (2 * (PM) * (Q) + (PM))
+__global__ void __launch_bounds__(NT) k_ilv(const Tables* __restrict__ gT, Scratch S, int count, int PM, int Q) {
+  __shared__ Tables sT;
+  extern __shared__ double ilv_smem[];
+  load_tables(sT, gT);
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  double* rf = ilv_smem + (size_t)wib * ILV_WORDS(PM, Q);  // [PM][Q] forward ends
+  double* rb = rf + PM * Q;                                // [PM][Q] backward ends
+  int* cf = (int*)(rb + PM * Q);                           // [PM] forwards done per stage
+  int* cb = cf + PM;                                       // [PM] backwards done per stage
+  const i64 njobs = (i64)S.counters[CNT_ILV];
+  const int v = sT.interleave;
+  i64 cells = 0;
+  for (;;) {
+    i64 item = 0;
+    if (lane == 0) item = (i64)atomicAdd(&S.counters[CNT_ILVW], 1ull);
+    item = __shfl_sync(FULL, item, 0);
+    if (item >= njobs) break;
+    const int job = S.ilv[item];
+    const int c = job & 3;
+    const i64 slot = job >> 2;
+    if (S.status[slot] != 0) continue;
+    const TplRec& tp = sT.tpl[S.tau[slot]];
+    const int32_t off = tp.crec[c];
+    const CrecHdr* h = crec_hdr(sT, off);
+    const StageRec* st = crec_stages(sT, off);
+    const int P = h->P, U = h->U;
+    const ClassSplit cs = load_split(S, c, tp.C, slot);
+    i64* R = S.Rs ? S.Rs + (i64)class_stage_off(sT, tp, c) * S.ns + slot : nullptr;
+    // this lane's stages: layers and per-layer durations
+    int ls[2] = {0, 0};
+    {
+      LayerWalk lw = walk(sT, h, cs.dig);
+      for (int q = 0; q < P; ++q) {
+        const int l = lw.next(st);
+        if (q == lane) ls[0] = l;
+        if (q == lane + 32) ls[1] = l;
+      }
+    }
+    double best = 0;
+    bool bad = false;
+    for (int u = 0; u < U; ++u) {
+      const i64* sub = crec_sub(sT, off, P, u);
+      const i64 m = mb_of(cs, sub[0]);
+      const i64 n = m * v, pv = (i64)P * v;
+      const double cw = (double)sub[P];
+      int p[2] = {0, 0}, nf[2] = {0, 0}, nb[2] = {0, 0};
+      double X[2] = {0, 0};
+      for (int q = lane; q < P; q += 32) { cf[q] = 0; cb[q] = 0; }
+      __syncwarp();
+      for (;;) {
+        bool act = false, run[2] = {false, false};
+        double ne[2] = {0, 0};
+        bool isF[2] = {false, false};
+        i64 ix[2] = {0, 0};
+#pragma unroll
+        for (int o = 0; o < 2; ++o) {
+          const int s = lane + 32 * o;
+          if (s >= P || p[o] >= 2 * n) continue;
+          act = true;
+          const i64 w = imin(2 * (P - 1 - s) + (i64)(v - 1) * P, n);
+          const bool f = p[o] < w || (p[o] < 2 * n - w && !((p[o] - w) & 1));
+          const i64 idx = f ? nf[o] : nb[o];
+          const i64 rem = idx % pv, gi = idx / pv;
+          const int k = f ? (int)(rem / P) : v - 1 - (int)(rem / P);
+          int ps = -1;
+          i64 x = 0;
+          double cost = 0;
+          bool fring = f;
+          if (f) {
+            if (s > 0) { ps = s - 1; x = idx; cost = (double)sub[s]; }
+            else if (k > 0) { ps = P - 1; x = idx - P; cost = cw; }
+          } else {
+            if (s < P - 1) { ps = s + 1; x = idx; cost = (double)sub[1 + s]; }
+            else if (k < v - 1) { ps = 0; x = idx - P; cost = cw; }
+            else { ps = s; fring = true; x = gi * pv + (i64)(v - 1) * P + rem % P; cost = 0; }
+          }
+          double tin = 0;
+          if (ps >= 0) {
+            const int have = fring ? cf[ps] : cb[ps];
+            if (have <= x) continue;  // input not produced yet
+            if (have - x > Q) bad = true;
+            tin = (fring ? rf : rb)[ps * Q + (int)(x & (Q - 1))] + cost;
+          }
+          const bool ext = f ? ((s == 0 && k == 0) || (s == P - 1 && k == v - 1))
+                             : ((s == 0 && k == 0) || (s == P - 1 && k == v - 1));
+          const double dur = f ? ilv_dur((double)st[s].layer_f, (double)st[s].fext, ls[o], v, k, ext)
+                               : ilv_dur((double)st[s].layer_b, (double)st[s].gext, ls[o], v, k, ext);
+          ne[o] = fmax(X[o], tin) + dur;
+          run[o] = true;
+          isF[o] = f;
+          ix[o] = idx;
+        }
+        if (!__any_sync(FULL, act)) break;
+        if (!__any_sync(FULL, run[0] || run[1])) {  // no op could run: a deadlock (never expected)
+          bad = true;
+          break;
+        }
+        __syncwarp();
+#pragma unroll
+        for (int o = 0; o < 2; ++o) {
+          if (!run[o]) continue;
+          const int s = lane + 32 * o;
+          (isF[o] ? rf : rb)[s * Q + (int)(ix[o] & (Q - 1))] = ne[o];
+          if (isF[o]) { cf[s] = ++nf[o]; } else { cb[s] = ++nb[o]; }
+          X[o] = ne[o];
+          ++p[o];
+        }
+        __syncwarp();
+      }
+      // T_pipe = the latest stage end; S.1: every stage's last op (its last backward)
+      double mx = fmax(X[0], X[1]);
+      for (int o2 = 16; o2 > 0; o2 >>= 1) mx = fmax(mx, __shfl_xor_sync(FULL, mx, o2));
+      best = fmax(best, mx);
+      if (R)
+        for (int o = 0; o < 2; ++o) {
+          const int s = lane + 32 * o;
+          if (s < P) R[s * S.ns] = u == 0 ? (i64)X[o] : imax(R[s * S.ns], (i64)X[o]);
+        }
+      cells += lane == 0 ? 2 * (i64)P * n : 0;
+      __syncwarp();
+    }
+    if (__any_sync(FULL, bad)) {
+      if (lane == 0) S.status[slot] = -5;
+    } else if (lane == 0) {
+      S.Tc[c * S.ns + slot] = (i64)best;
+    }
+  }
+  if (count) {
+    cells = warp_sum(cells);
+    if (lane == 0 && cells) atomicAdd(&S.counters[CNT_CELLS], (unsigned long long)cells);
+  }
+}
+
+// K_sync for the interleaved schedule (C.8: concurrent with K_ilv, T0 = 0;
+// S.1: after it, from the stage ends)
+__device__ i64 sync_ilv_any(const Tables& T, const TplRec& tp, const Scratch& S, i64 t, const i64* R, i64 T0) {
+  switch (tp.C) {
+    case 1: { ClassSplit cs[1] = {load_split(S, 0, 1, t)}; return grad_sync_ilv_c<1>(T, tp, cs, R, S.ns, T0); }
+    case 2: {
+      ClassSplit cs[2] = {load_split(S, 0, 2, t), load_split(S, 1, 2, t)};
+      return grad_sync_ilv_c<2>(T, tp, cs, R, S.ns, T0);
+    }
+    case 3: {
+      ClassSplit cs[3] = {load_split(S, 0, 3, t), load_split(S, 1, 3, t), load_split(S, 2, 3, t)};
+      return grad_sync_ilv_c<3>(T, tp, cs, R, S.ns, T0);
+    }
+    default: {
+      ClassSplit cs[4] = {load_split(S, 0, 4, t), load_split(S, 1, 4, t), load_split(S, 2, 4, t), load_split(S, 3, 4, t)};
+      return grad_sync_ilv_c<4>(T, tp, cs, R, S.ns, T0);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(NT) k_sync_ilv(const Tables* __restrict__ gT, Scratch S, i64 ns, int overlap) {
+  __shared__ Tables sT;
+  load_tables(sT, gT);
+  for (i64 t = (i64)blockIdx.x * NT + threadIdx.x; t < ns; t += (i64)gridDim.x * NT) {
+    const int tau = S.tau[t];
+    if (tau < 0 || S.status[t] != 0) continue;
+    const TplRec& tp = sT.tpl[tau];
+    if (tp.D == 1) { S.extra[t] = 0; continue; }
+    if (!overlap) {
+      S.extra[t] = sync_ilv_any(sT, tp, S, t, nullptr, 0);
+      continue;
+    }
+    i64 T0 = 0;
+    for (int q = 0; q < tp.C; ++q) T0 = imax(T0, S.Tc[q * S.ns + t]);
+    S.extra[t] = sync_ilv_any(sT, tp, S, t, S.Rs + t, T0) - T0;
   }
 }
 
@@ -1260,6 +1471,10 @@ static int run_phases(hsim_handle* h, const Tables* dT, Cands c, int64_t n, int6
     jobcap[P] = (pm >> P & 1) ? (size_t)depth_jobs_max(h, P) * ns : 0;
     jobw += 2 * jobcap[P];
   }
+  // V.2: the K_ilv job list
+  const bool ilv = interleave_v(h) > 1;
+  const size_t ilvcap = ilv ? (size_t)ilv_jobs_max(h) * ns : 0;
+  jobw += ilvcap;
   const size_t planw = hplan ? (size_t)(2 * c.nr + 1) : 0;
   const size_t n32 = (size_t)(4 + 4 * MAXC) * ns + jobw;
   const size_t bufw0 = (size_t)(MAXC + 2) * ns + NCNT + (n32 + 1) / 2 + 8;
@@ -1306,6 +1521,7 @@ static int run_phases(hsim_handle* h, const Tables* dT, Cands c, int64_t n, int6
       S.part[P] = pj + jobcap[P];
       pj += 2 * jobcap[P];
     }
+    S.ilv = ilvcap ? pj : nullptr;
   }
   if (hplan) {
     i64* pw = base + NBUF * bufw;
@@ -1397,6 +1613,30 @@ static int run_phases(hsim_handle* h, const Tables* dT, Cands c, int64_t n, int6
 #ifndef HSIM_DEEPFIRST
     launch_deep();
 #endif
+    if (ilv && ilvcap) {  // V.2: every interleaved pipeline (warp per job, rings in shared memory)
+      const int PM = ilv_depth_max(h);
+      int Q = 4;
+      while (Q < PM / 2 + 2) Q *= 2;
+      const size_t per_warp = (size_t)ILV_WORDS(PM, Q) * 8;
+      int W = 4;
+      while (W > 1 && W * per_warp > (size_t)200 * 1024) --W;
+      const size_t smem = W * per_warp;
+      static int attr_set[64] = {0};
+      int dev = 0;
+      cudaGetDevice(&dev);
+      if (smem > 48 * 1024 && dev < 64 && attr_set[dev] < (int)smem) {
+        cudaFuncSetAttribute(k_ilv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr_set[dev] = (int)smem;
+      }
+      int per = 0;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_ilv, 32 * W, smem) != cudaSuccess || per < 1) per = 1;
+      cudaStream_t ss = side(17);
+      tq = g_trace.pre("k_ilv", 17, ss);
+      k_ilv<<<sm_count(h) * per, 32 * W, smem, ss>>>(dT, S, count, PM, Q);
+      g_trace.post(tq, ss);
+      ++launches;
+      join(ss);
+    }
     if (count) {
       unsigned long long v = 0;
       cudaMemcpyAsync(&v, S.counters + CNT_CELLS, 8, cudaMemcpyDeviceToHost, st);
@@ -1404,7 +1644,14 @@ static int run_phases(hsim_handle* h, const Tables* dT, Cands c, int64_t n, int6
       cells += (i64)v;
       continue;
     }
-    if (overlap) {  // S.1: needs the stages' last-backward ends -> after the 1F1B kernels
+    if (ilv) {  // V.2: revisited stage groups (C.8 concurrently with K_ilv; S.1 after it)
+      cudaStream_t ss = overlap ? fin : side(18);
+      tq = g_trace.pre("k_sync_ilv", 18, ss);
+      k_sync_ilv<<<gy, NT, 0, ss>>>(dT, S, nsb, overlap ? 1 : 0);
+      g_trace.post(tq, ss);
+      ++launches;
+      if (!overlap) join(ss);
+    } else if (overlap) {  // S.1: needs the stages' last-backward ends -> after the 1F1B kernels
       tq = g_trace.pre("k_sync_overlap", NSTREAM_FINAL, fin);
       k_sync_overlap<<<gy, NT, 0, fin>>>(dT, S, nsb);
       g_trace.post(tq, fin);

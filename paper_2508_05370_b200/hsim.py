@@ -66,7 +66,8 @@ class hsim_model_desc(C.Structure):
                 ("n_pset", C.c_int32), ("pset", C.c_int32 * 16),
                 ("homo", C.c_int32), ("mixed", C.c_int32), ("use_all", C.c_int32),
                 ("r_layer", C.c_int32), ("pmax_perturb", C.c_int32), ("r_batch", C.c_int32),
-                ("mem_check", C.c_int32), ("sync_overlap", C.c_int32)]
+                ("mem_check", C.c_int32), ("sync_overlap", C.c_int32),
+                ("interleave", C.c_int32), ("ep_dp", C.c_int32)]
 
 
 class hsim_cands(C.Structure):
@@ -166,6 +167,8 @@ def descriptors(cfg):
         setattr(m, k, se[k])
     m.mem_check = int(se.get("mem_check", 0))
     m.sync_overlap = int(se.get("sync_overlap", 0))
+    m.interleave = int(se.get("interleave", 1))
+    m.ep_dp = int(se.get("ep_dp", 0))
     return cd, m, (types, nodes)
 
 

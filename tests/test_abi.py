@@ -125,3 +125,41 @@ def test_host_decode_memcheck_status_matches_oracle(oracle_mod, L, n):
     got = [s.decode(int(i))["status"] for i in idx]
     want = [o.describe(int(i))["status"] for i in idx]
     assert got == want and -3 in got
+
+
+@pytest.mark.parametrize("cfg_name", ["ilv2-c2", "ilv3-c4", "ilv2-c5", "ep-c4", "ep-ilv-tiny"])
+def test_host_decode_variants_match_oracle(oracle_mod, L, cfg_name):
+    """SURVEY §8(f) f4 (DESIGN.md V.2, V.3): the product's host-side split (the
+    HD partition the kernels run: -1 for a stage with fewer layers than chunks,
+    -2 for a micro-batch count that is not a multiple of the depth; V.3's
+    expert-sharded partition weights) agrees with the oracle's plan."""
+    cfg = {"ilv2-c2": lambda: H.with_interleave(H.get(2), 2),
+           "ilv3-c4": lambda: H.with_interleave(H.get(4), 3),
+           "ilv2-c5": lambda: H.with_interleave(H.get(5), 2),
+           "ep-c4": lambda: H.with_ep_dp(H.get(4)),
+           "ep-ilv-tiny": lambda: H.with_ep_dp(H.with_interleave(H.variant_tiny(104, moe=True), 2))}[cfg_name]()
+    s = hsim.Sim(cfg, host_only=True)
+    o = oracle_mod.Oracle(cfg)
+    assert s.space_size() == o.space_size()
+    idx = H.sample_indices(o.space_size(), 400, seed=17)
+    seen = set()
+    for i in idx:
+        a, b = s.decode(int(i)), o.describe(int(i))
+        assert a["status"] == b["status"], (i, a, b)
+        seen.add(b["status"])
+        for ca, cb in zip(a["classes"], b["classes"]):
+            if b["status"] != -1:
+                assert ca["layers"] == cb["layers"], (i, ca, cb)
+            if b["status"] == 0:
+                assert ca["mb"] == cb["mb"], (i, ca, cb)
+    assert 0 in seen
+
+
+def test_variant_validation(L):
+    """interleave outside 0..8, ep_dp outside {0, 1}, and mem_check with either
+    variant are HSIM_EINVAL (include/hsim.h)."""
+    for cfg in (H.with_interleave(H.get(2), 9), H.with_mem_check(H.with_interleave(H.get(2), 2)),
+                H.with_mem_check(H.with_ep_dp(H.get(4))), H.with_changes(H.with_ep_dp(H.get(4)), search__ep_dp=2)):
+        with pytest.raises(hsim.HsimError) as e:
+            hsim.Sim(cfg, host_only=True)
+        assert e.value.code == hsim.HSIM_EINVAL
