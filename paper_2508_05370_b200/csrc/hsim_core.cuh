@@ -319,7 +319,8 @@ HD LayerWalk walk(const Tables& T, const CrecHdr* h, u32 dig) {
 // then the batch digits of classes 0..C-2.  Layer split = template base split
 // + deltas; batch split = Hamilton over all replicas with weights
 // floor(2^40 / slowest stage) (C.4).  Returns 0, -1 (layer) or -2 (batch).
-template <int C>
+// ILV: the V.2 rules (T.interleave > 1) are compiled in (K_split<true>).
+template <int C, bool ILV = false>
 HD int partition_c(const Tables& T, const TplRec& tp, i64 local, ClassSplit (&cs)[C]) {
   const u32 bb = (u32)(2 * T.r_batch + 1);
   u32 loc = (u32)local;  // radix < 2^31 (validated at create)
@@ -335,7 +336,7 @@ HD int partition_c(const Tables& T, const TplRec& tp, i64 local, ClassSplit (&cs
     loc = lq;
     LayerWalk lw = walk(T, h, cs[c].dig);
     i64 worst = 0;
-    const int lmin = T.interleave > 1 && h->P >= 2 ? T.interleave : 1;  // V.2: every chunk holds a layer
+    const int lmin = ILV && h->P >= 2 ? T.interleave : 1;  // V.2: every chunk holds a layer
     for (int s = 0; s < h->P; ++s) {
       const int l = lw.next(st);
       if (l < lmin) status = -1;
@@ -380,7 +381,7 @@ HD int partition_c(const Tables& T, const TplRec& tp, i64 local, ClassSplit (&cs
 #pragma unroll
   for (int c = 0; c < C; ++c)
     if (mb_of(cs[c], D[c] - 1) < 1) return -2;  // m non-increasing in k
-  if (T.interleave > 1) {
+  if (ILV) {
     // V.2: every replica's m must be a multiple of its depth; the distinct m
     // of a class occur at k = 0, D-1 and next to the seats / rm thresholds
 #pragma unroll
@@ -967,15 +968,19 @@ HD i64 grad_sync_ilv_c(const Tables& T, const TplRec& tp, const ClassSplit (&cs)
 }
 
 // host-side rendering of a candidate's split (hsim_decode)
-HD int partition_any(const Tables& T, const TplRec& tp, i64 local, ClassSplit* out) {
+template <bool ILV>
+HD int partition_any_t(const Tables& T, const TplRec& tp, i64 local, ClassSplit* out) {
   int st = 0;
   switch (tp.C) {
-    case 1: { ClassSplit cs[1]; st = partition_c<1>(T, tp, local, cs); for (int c = 0; c < 1; ++c) out[c] = cs[c]; break; }
-    case 2: { ClassSplit cs[2]; st = partition_c<2>(T, tp, local, cs); for (int c = 0; c < 2; ++c) out[c] = cs[c]; break; }
-    case 3: { ClassSplit cs[3]; st = partition_c<3>(T, tp, local, cs); for (int c = 0; c < 3; ++c) out[c] = cs[c]; break; }
-    default: { ClassSplit cs[4]; st = partition_c<4>(T, tp, local, cs); for (int c = 0; c < 4; ++c) out[c] = cs[c]; break; }
+    case 1: { ClassSplit cs[1]; st = partition_c<1, ILV>(T, tp, local, cs); for (int c = 0; c < 1; ++c) out[c] = cs[c]; break; }
+    case 2: { ClassSplit cs[2]; st = partition_c<2, ILV>(T, tp, local, cs); for (int c = 0; c < 2; ++c) out[c] = cs[c]; break; }
+    case 3: { ClassSplit cs[3]; st = partition_c<3, ILV>(T, tp, local, cs); for (int c = 0; c < 3; ++c) out[c] = cs[c]; break; }
+    default: { ClassSplit cs[4]; st = partition_c<4, ILV>(T, tp, local, cs); for (int c = 0; c < 4; ++c) out[c] = cs[c]; break; }
   }
   return st;
+}
+HD int partition_any(const Tables& T, const TplRec& tp, i64 local, ClassSplit* out) {
+  return T.interleave > 1 ? partition_any_t<true>(T, tp, local, out) : partition_any_t<false>(T, tp, local, out);
 }
 
 #ifdef __CUDACC__

@@ -201,10 +201,10 @@ __device__ __forceinline__ i64 warp_sum(i64 v) {
 }
 
 // steps a0 + a1 for a C-class template; stores the compact split of each class
-template <int C>
+template <int C, bool ILV>
 __device__ __forceinline__ int split_store(const Tables& T, const TplRec& tp, i64 local, const Scratch& S, i64 slot) {
   ClassSplit cs[C];
-  const int st = partition_c<C>(T, tp, local, cs);
+  const int st = partition_c<C, ILV>(T, tp, local, cs);
   if (st == 0) {
 #pragma unroll
     for (int k = 0; k < C; ++k) {
@@ -222,6 +222,9 @@ __device__ __forceinline__ int split_store(const Tables& T, const TplRec& tp, i6
 #ifndef HSIM_SPLIT_MINB
 #define HSIM_SPLIT_MINB 6  // measured: 8 is ~1 % faster on range sweeps but ~8 % slower on explicit lists (e2e)
 #endif
+// ILV: V.2 (interleaved schedule) compiled in -- its partition rules and the
+// K_ilv job list; the default path carries none of it
+template <bool ILV>
 __global__ void __launch_bounds__(NT, HSIM_SPLIT_MINB) k_split(const Tables* __restrict__ gT, Cands c, i64 ca, i64 cb, Scratch S,
                                               uint32_t pm_all) {
   __shared__ Tables sT;
@@ -266,10 +269,10 @@ __global__ void __launch_bounds__(NT, HSIM_SPLIT_MINB) k_split(const Tables* __r
       const TplRec& tp = sT.tpl[tau];
       // class count specialised: the per-class split stays in registers
       switch (tp.C) {
-        case 1: st = split_store<1>(sT, tp, i - tp.prefix, S, slot); break;
-        case 2: st = split_store<2>(sT, tp, i - tp.prefix, S, slot); break;
-        case 3: st = split_store<3>(sT, tp, i - tp.prefix, S, slot); break;
-        default: st = split_store<4>(sT, tp, i - tp.prefix, S, slot); break;
+        case 1: st = split_store<1, ILV>(sT, tp, i - tp.prefix, S, slot); break;
+        case 2: st = split_store<2, ILV>(sT, tp, i - tp.prefix, S, slot); break;
+        case 3: st = split_store<3, ILV>(sT, tp, i - tp.prefix, S, slot); break;
+        default: st = split_store<4, ILV>(sT, tp, i - tp.prefix, S, slot); break;
       }
       S.status[slot] = st;
       if (st == 0) mypm = tp.pmask;
@@ -292,10 +295,10 @@ __global__ void __launch_bounds__(NT, HSIM_SPLIT_MINB) k_split(const Tables* __r
     if (mypm)
       for (int k = 0; k < sT.tpl[tau].C; ++k) {
         const int P = crec_hdr(sT, sT.tpl[tau].crec[k])->P;
-        if (sT.interleave > 1 && P >= 2) ilvc |= 1u << k;
+        if (ILV && P >= 2) ilvc |= 1u << k;
         else if (P <= FASTP) combos |= (u64)1 << ((P - 1) * 4 + k);
       }
-    if (__any_sync(FULL, ilvc != 0))
+    if (ILV && __any_sync(FULL, ilvc != 0))
       for (int k = 0; k < MAXC; ++k) {
         const bool has = ilvc >> k & 1;
         const unsigned bal = __ballot_sync(FULL, has);
@@ -305,18 +308,30 @@ __global__ void __launch_bounds__(NT, HSIM_SPLIT_MINB) k_split(const Tables* __r
         o = __shfl_sync(FULL, o, 0) + __popc(bal & ((1u << lane) - 1));
         if (has) S.ilv[o] = (int32_t)(slot << 2 | k);
       }
+    // one list reservation per combo, all of a warp's reservations in flight at
+    // once (lane j reserves for the warp's j-th combo), then the appends: the
+    // atomics' round trips overlap instead of forming a chain
     u64 all = (u64)__reduce_or_sync(FULL, (unsigned)combos) | (u64)__reduce_or_sync(FULL, (unsigned)(combos >> 32)) << 32;
     while (all) {
-      const int bit = __ffsll((long long)all) - 1;
-      all &= all - 1;
-      const int P = bit / 4 + 1, k = bit & 3;
-      const bool has = combos >> bit & 1;
-      const unsigned bal = __ballot_sync(FULL, has);
-      const int cnt = __popc(bal);
-      unsigned long long o = 0;
-      if (lane == 0) o = atomicAdd(&S.counters[(cnt == 32 ? CNT_FULL : CNT_PART) + P], (unsigned long long)cnt);
-      o = __shfl_sync(FULL, o, 0) + __popc(bal & ((1u << lane) - 1));
-      if (has) (cnt == 32 ? S.full[P] : S.part[P])[o] = (int32_t)(slot << 2 | k);
+      u64 grp = 0, rest = all;
+      unsigned long long mine = 0;
+      for (int j = 0; j < 32 && rest; ++j) {
+        const int bit = __ffsll((long long)rest) - 1;
+        rest &= rest - 1;
+        grp |= (u64)1 << bit;
+        const int cnt = __popc(__ballot_sync(FULL, combos >> bit & 1));
+        if (lane == j) mine = atomicAdd(&S.counters[(cnt == 32 ? CNT_FULL : CNT_PART) + bit / 4 + 1], (unsigned long long)cnt);
+      }
+      all = rest;
+      for (int j = 0; grp; ++j) {
+        const int bit = __ffsll((long long)grp) - 1;
+        grp &= grp - 1;
+        const int P = bit / 4 + 1, k = bit & 3;
+        const bool has = combos >> bit & 1;
+        const unsigned bal = __ballot_sync(FULL, has);
+        const unsigned long long o = __shfl_sync(FULL, mine, j) + __popc(bal & ((1u << lane) - 1));
+        if (has) (__popc(bal) == 32 ? S.full[P] : S.part[P])[o] = (int32_t)(slot << 2 | k);
+      }
     }
   }
 }
@@ -1014,35 +1029,44 @@ struct RegTopK {
   }
 };
 
-// T of one slot (K_final)
-__device__ __forceinline__ i64 final_T(const Tables& sT, const Cands& c, const Scratch& S, i64 slot, i64* t_out, i64* i_out) {
-  // every scratch word of the slot is loaded up front (independent loads, one
-  // memory latency instead of a chain); rows / words that do not apply to the
-  // slot (empty slot, invalid split, classes >= C) are read but ignored
-  const i64 t = __ldcs(&S.tpos[slot]);
-  const int tau = __ldcs(&S.tau[slot]);
-  const int st = __ldcs(&S.status[slot]);
-  const i64 ex = __ldcs(&S.extra[slot]);
-  i64 tc[MAXC];
+// T of one slot (K_final), in two parts so the loop can issue the next
+// chunk's loads before it works on this one (software pipelining: K_final is
+// bound by memory latency, not bandwidth).  Every scratch word of the slot is
+// loaded up front (independent loads, one memory latency instead of a chain);
+// rows / words that do not apply to the slot (empty slot, invalid split,
+// classes >= C) are read but ignored.
+struct SlotW {
+  i64 t, ex, tc[MAXC];
+  int tau, st;
+};
+__device__ __forceinline__ SlotW slot_load(const Scratch& S, i64 slot) {
+  SlotW w;
+  w.t = __ldcs(&S.tpos[slot]);
+  w.tau = __ldcs(&S.tau[slot]);
+  w.st = __ldcs(&S.status[slot]);
+  w.ex = __ldcs(&S.extra[slot]);
 #pragma unroll
-  for (int q = 0; q < MAXC; ++q) tc[q] = __ldcs(&S.Tc[q * S.ns + slot]);
+  for (int q = 0; q < MAXC; ++q) w.tc[q] = __ldcs(&S.Tc[q * S.ns + slot]);
+  return w;
+}
+__device__ __forceinline__ i64 slot_T(const Tables& sT, const Cands& c, const SlotW& w, i64* t_out, i64* i_out) {
   i64 T = INT64_MIN, i = -1;
-  if (t >= 0) {
-    i = cand_index(c, t);
-    if (tau >= 0) {
-      if (st) {
-        T = st;
+  if (w.t >= 0) {
+    i = cand_index(c, w.t);
+    if (w.tau >= 0) {
+      if (w.st) {
+        T = w.st;
       } else {
-        const int C = sT.tpl[tau].C;
+        const int C = sT.tpl[w.tau].C;
         i64 T0 = 0;
 #pragma unroll
         for (int q = 0; q < MAXC; ++q)
-          if (q < C) T0 = imax(T0, tc[q]);
-        T = T0 + ex;
+          if (q < C) T0 = imax(T0, w.tc[q]);
+        T = T0 + w.ex;
       }
     }
   }
-  *t_out = t;
+  *t_out = w.t;
   *i_out = i;
   return T;
 }
@@ -1063,9 +1087,13 @@ __global__ void __launch_bounds__(NT) k_final_small(const Tables* __restrict__ g
   RegTopK r;
   r.init();
   if (w == 0 && lane < k && blist[lane] != LIST_PAD && blist[lane] != KEY_INF) { r.t = blist[lane]; r.i = blist[k + lane]; }
+  SlotW nxt;
+  if (wid * 32 < ns) nxt = slot_load(S, wid * 32 + lane);
   for (i64 base = wid * 32; base < ns; base += nw * 32) {
+    const SlotW cur = nxt;
+    if (base + nw * 32 < ns) nxt = slot_load(S, base + nw * 32 + lane);  // next chunk's loads in flight
     i64 t, i;
-    const i64 T = final_T(sT, c, S, base + lane, &t, &i);
+    const i64 T = slot_T(sT, c, cur, &t, &i);
     if (out && t >= 0) out[t] = T;
     const i64 g = (i64)*(volatile unsigned long long*)gthr;
     i64 thT = __shfl_sync(FULL, (long long)r.t, k - 1), thI = __shfl_sync(FULL, (long long)r.i, k - 1);
@@ -1156,26 +1184,14 @@ __global__ void __launch_bounds__(NT) k_final(const Tables* __restrict__ gT, Can
   WarpTopK tk{k ? lists + wid * 2 * k : nullptr, k, 0, KEY_INF, KEY_INF,
               k ? (unsigned long long*)(lists + nw * 2 * k) : nullptr};
   if (k) warp_topk_load(tk);
+  SlotW nxt;
+  if (wid * 32 < ns) nxt = slot_load(S, wid * 32 + lane);
   for (i64 base = wid * 32; base < ns; base += nw * 32) {
-    const i64 slot = base + lane;
-    i64 T = INT64_MIN, i = -1;
-    const i64 t = S.tpos[slot];
-    if (t >= 0) {
-      i = cand_index(c, t);
-      const int tau = S.tau[slot];
-      if (tau >= 0) {
-        const int st = S.status[slot];
-        if (st) {
-          T = st;
-        } else {
-          const int C = sT.tpl[tau].C;
-          i64 T0 = 0;
-          for (int q = 0; q < C; ++q) T0 = imax(T0, S.Tc[q * S.ns + slot]);
-          T = T0 + S.extra[slot];
-        }
-      }
-      if (out) out[t] = T;
-    }
+    const SlotW cur = nxt;
+    if (base + nw * 32 < ns) nxt = slot_load(S, base + nw * 32 + lane);  // next chunk's loads in flight
+    i64 t, i;
+    const i64 T = slot_T(sT, c, cur, &t, &i);
+    if (out && t >= 0) out[t] = T;
     if (k) warp_offer(tk, T, i, t >= 0 && T >= 0);
   }
 }
@@ -1529,7 +1545,7 @@ static int run_phases(hsim_handle* h, const Tables* dT, Cands c, int64_t n, int6
     cudaEventRecord(plan_ev, st);
     c.plan = pw;
   }
-  const int gs = grid_of(h, k_split, g_split), gd = grid_of(h, k_deep, g_deep), gy = grid_of(h, k_sync, g_sync),
+  const int gs = grid_of(h, k_split<false>, g_split), gd = grid_of(h, k_deep, g_deep), gy = grid_of(h, k_sync, g_sync),
             gf = final_grid(h, k);
   // launch order: longest total work first; the latency-bound deep depths run
   // on high-priority streams (host.cu), which matters more than the order
@@ -1551,7 +1567,8 @@ static int run_phases(hsim_handle* h, const Tables* dT, Cands c, int64_t n, int6
     if (b >= NBUF && !count) cudaStreamWaitEvent(st, pool_event(h, 2 + q), 0);  // buffer free: final(b-2) done
     cudaMemsetAsync(S.counters, 0, NCNT * sizeof(unsigned long long), st);
     int tq = g_trace.pre("k_split", 0, st);
-    k_split<<<gs, NT, 0, st>>>(dT, c, ca, cb, S, pm);
+    if (ilv) k_split<true><<<gs, NT, 0, st>>>(dT, c, ca, cb, S, pm);
+    else k_split<false><<<gs, NT, 0, st>>>(dT, c, ca, cb, S, pm);
     g_trace.post(tq, st);
     ++launches;
     cudaEventRecord(pool_event(h, q), st);

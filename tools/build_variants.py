@@ -33,20 +33,15 @@ VARIANTS = {
     "w16": ["-DHSIM_WHOLE_MAXP=16"],
     "pm6": ["-DHSIM_PIPE_MINB=6"],
     "pm7": ["-DHSIM_PIPE_MINB=7"],
-    "nb3": ["-DHSIM_NBATCH=3"],
     "nb1": ["-DHSIM_NBATCH=1"],
     "s7": ["-DHSIM_SYNC_MINB=7"],
-    "s4": ["-DHSIM_SYNC_MINB=4"],
-    "s5": ["-DHSIM_SYNC_MINB=5"],
     "noprio": ["-DHSIM_NOPRIO"],
     "deepfirst": ["-DHSIM_DEEPFIRST"],
     "w8": ["-DHSIM_WHOLE_MAXP=8"],
-    "w16": ["-DHSIM_WHOLE_MAXP=16"],
     "fm4": ["-DHSIM_FINAL_MULT=4"],
     "fm2": ["-DHSIM_FINAL_MULT=2"],
     "aff11": ["-DHSIM_AFFINE_MAXP=11"],
     "aff16": ["-DHSIM_AFFINE_MAXP=16"],
-    "pm6": ["-DHSIM_PIPE_MINB=6"],
     "pm5": ["-DHSIM_PIPE_MINB=5"],
     "pm4": ["-DHSIM_PIPE_MINB=4"],
     "noaff": ["-DHSIM_AFFINE_MAXP=0"],
@@ -55,15 +50,11 @@ VARIANTS = {
     "u4": ["-DHSIM_UNROLL_MAXP=4"],
     "u6": ["-DHSIM_UNROLL_MAXP=6"],
     "u16": ["-DHSIM_UNROLL_MAXP=16"],
-    "nb1": ["-DHSIM_NBATCH=1"],
     "p8s6": ["-DHSIM_PIPE_MINB=8", "-DHSIM_SYNC_MINB=6"],
-    "nb1": ["-DHSIM_NBATCH=1"],
     "wcells": ["-DHSIM_WARPCELLS"],
     "diag": ["-DHSIM_DIAG"],
     "noskip": ["-DHSIM_NOSKIP"],
     "noskip_wc": ["-DHSIM_NOSKIP", "-DHSIM_WARPCELLS"],
-    "nb2": ["-DHSIM_NBATCH=2"],
-    "nb3": ["-DHSIM_NBATCH=3"],
     "nb6": ["-DHSIM_NBATCH=6"],
     "nb8": ["-DHSIM_NBATCH=8"],
     "p6s5": ["-DHSIM_PIPE_MINB=6", "-DHSIM_SYNC_MINB=5"],
