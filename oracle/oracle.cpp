@@ -95,6 +95,7 @@ struct orc_input {
   int32_t sync_overlap;  // gradient sync overlapped with the backward (DESIGN S.1)
   int32_t interleave;    // v model chunks per stage, interleaved 1F1B (DESIGN V.2); 1 = off
   int32_t ep_dp;         // expert parallelism across the DP replicas (DESIGN V.3)
+  int32_t mixtp;         // mixed-type TP groups, the MIXTP family (DESIGN V.1)
 };
 }
 
@@ -268,7 +269,9 @@ std::vector<i64> hamilton(i64 n, const std::vector<i64>& w) {
 }
 
 // --- candidate space (DESIGN C.2) --------------------------------------------
-struct StageSpec { int type; int tp; };
+// type2 >= 0: a mixed-type TP group (DESIGN V.1): tp/2 devices of `type` and
+// tp/2 of `type2`
+struct StageSpec { int type; int tp; int type2 = -1; };
 struct ClassSpec { std::vector<StageSpec> st; int D; };
 struct Template { int b; std::vector<ClassSpec> cls; i64 radix; i64 prefix; };
 
@@ -377,6 +380,36 @@ std::vector<Template> enumerate(const orc_input& in, const Cluster& cl) {
         }
       }
     }
+    if (in.mixtp && nt >= 2) {
+      // V.1 (DESIGN): one class whose every stage is a mixed TP group of tp
+      // devices, tp/2 of type a and tp/2 of type a2 (a < a2); tp >= 2 in both
+      // types' TP sets, tp | heads and kv heads, tp/2 | GPUs per node (each
+      // half fits a node); D replicas of P stages need
+      // D P tp/2 GPUs of each type (use_all: exactly all of both)
+      for (int a = 0; a < nt; ++a)
+        for (int a2 = a + 1; a2 < nt; ++a2) {
+          std::vector<int> tps;
+          for (int q = 0; q < in.n_tp[a]; ++q) tps.push_back(in.tpset[a][q]);
+          std::sort(tps.begin(), tps.end());
+          for (int tp : tps) {
+            bool in2 = false;
+            for (int q = 0; q < in.n_tp[a2]; ++q) in2 |= in.tpset[a2][q] == tp;
+            if (tp < 2 || !in2 || in.heads % tp || in.kv_heads % tp || in.types[a].gpus_per_node % (tp / 2) ||
+                in.types[a2].gpus_per_node % (tp / 2))
+              continue;
+            for (int P : ps) {
+              if (P > in.L) continue;
+              for (i64 D = 1; D * P * (tp / 2) <= std::min(cl.n_of_type[a], cl.n_of_type[a2]); ++D) {
+                if (in.use_all && (D * P * (tp / 2) != cl.n_of_type[a] || D * P * (tp / 2) != cl.n_of_type[a2])) continue;
+                ClassSpec c;
+                c.D = (int)D;
+                for (int st = 0; st < P; ++st) c.st.push_back(StageSpec{a, tp, a2});
+                emit({c});
+              }
+            }
+          }
+        }
+    }
   }
   i64 acc = 0;
   for (auto& t : out) { t.prefix = acc; acc += t.radix; }
@@ -384,7 +417,9 @@ std::vector<Template> enumerate(const orc_input& in, const Cluster& cl) {
 }
 
 // --- one decoded, placed and partitioned candidate ---------------------------
-struct Group { int node, base; };  // a stage group: tp GPUs [base, base+tp) on node
+// a stage group: tp GPUs [base, base+tp) on node; V.1 mixed group: tp/2 GPUs
+// [base, base+tp/2) on node and tp/2 at the same base on node2
+struct Group { int node, base, node2 = -1; };
 
 struct Plan {
   const Template* tpl;
@@ -462,27 +497,50 @@ struct Oracle {
       p.place[c].resize(cls[c].D);
       for (int r = 0; r < cls[c].D; ++r) {
         for (const StageSpec& s : cls[c].st) {
+          // V.1: a mixed group takes tp/2-blocks; the a2 half sits at the same
+          // base on the lowest node of type a2 where that block is free
+          const int w = s.type2 >= 0 ? s.tp / 2 : s.tp;
           Group g{-1, -1};
           for (int n : cl.nodes_of_type[s.type]) {
-            for (int k = 0; k * s.tp < cl.gpn[n] && g.node < 0; ++k) {
+            for (int k = 0; k * w < cl.gpn[n] && g.node < 0; ++k) {
               bool fr = true;
-              for (int q = 0; q < s.tp; ++q) fr &= !used[n][k * s.tp + q];
-              if (fr) g = Group{n, k * s.tp};
+              for (int q = 0; q < w; ++q) fr &= !used[n][k * w + q];
+              if (fr) g = Group{n, k * w};
             }
             if (g.node >= 0) break;
           }
+          if (g.node >= 0 && s.type2 >= 0) {
+            for (int n : cl.nodes_of_type[s.type2]) {
+              bool fr = true;
+              for (int q = 0; q < w; ++q) fr &= !used[n][g.base + q];
+              if (fr) { g.node2 = n; break; }
+            }
+            if (g.node2 < 0) g.node = -1;
+          }
           if (g.node < 0) { std::fprintf(stderr, "oracle: placement failed\n"); std::abort(); }
-          for (int q = 0; q < s.tp; ++q) used[g.node][g.base + q] = 1;
+          for (int q = 0; q < w; ++q) used[g.node][g.base + q] = 1;
+          if (g.node2 >= 0)
+            for (int q = 0; q < w; ++q) used[g.node2][g.base + q] = 1;
           p.place[c][r].push_back(g);
         }
       }
     }
   }
 
-  // TP ring of a stage group: base -> base+1 -> ... -> base+t-1 -> base
+  // device q of a group of t GPUs as (node, local rank); V.1: devices
+  // [0, t/2) on node, [t/2, t) on node2, both from base
+  static std::pair<int, int> dev(const Group& g, int t, int q) {
+    if (g.node2 < 0) return {g.node, g.base + q};
+    return q < t / 2 ? std::make_pair(g.node, g.base + q) : std::make_pair(g.node2, g.base + q - t / 2);
+  }
+  Link link_dd(const Group& g1, int t1, int q1, const Group& g2, int t2, int q2) const {
+    const auto a = dev(g1, t1, q1), z = dev(g2, t2, q2);
+    return cl.gpu_to_gpu(a.first, a.second, z.first, z.second);
+  }
+  // TP ring of a stage group: device 0 -> 1 -> ... -> t-1 -> 0
   std::vector<Link> tp_ring(const Group& g, int t) const {
     std::vector<Link> e;
-    for (int q = 0; q < t; ++q) e.push_back(cl.gpu_to_gpu(g.node, g.base + q, g.node, g.base + (q + 1) % t));
+    for (int q = 0; q < t; ++q) e.push_back(link_dd(g, t, q, g, t, (q + 1) % t));
     return e;
   }
   i64 act_bytes(int b) const { return (i64)b * in.seq * in.h * in.bpe_act; }  // A5
@@ -501,7 +559,7 @@ struct Oracle {
     i64 slow = 0;
     for (int x = 0; x < t; ++x)
       for (int y = 0; y < t; ++y)
-        if (x != y) slow = std::max(slow, tau(cl.gpu_to_gpu(g.node, g.base + x, g.node, g.base + y), per));
+        if (x != y) slow = std::max(slow, tau(link_dd(g, t, x, g, t, y), per));
     return (i64)(t - 1) * slow;
   }
 
@@ -550,16 +608,21 @@ struct Oracle {
     return (g - 1) * slow;
   }
 
+  // duration of one op on one device of stage group ss; V.1: a mixed group's
+  // devices hold equal shards and every op ends with a TP collective, so the
+  // op lasts as long as on its slower device type -- "the bottleneck device"
+  // (PAPER.md:280 C4)
+  i64 sdur(const StageSpec& ss, int kind, bool bwd, int b, i64 g = 0) const {
+    i64 d = op_dur(in, types[ss.type], kind, bwd, ss.tp, b, g);
+    if (ss.type2 >= 0) d = std::max(d, op_dur(in, types[ss.type2], kind, bwd, ss.tp, b, g));
+    return d;
+  }
+  // compute-only fwd+bwd of one layer (C.4); g: expert divisor (V.3, 0 = tp)
   i64 tcomp(const StageSpec& s, int b, i64 g = 0) const {
-    const orc_type& ty = types[s.type];
     int mk = in.E > 1 ? MOE : MLP;
-    return op_dur(in, ty, ATTN, false, s.tp, b) + op_dur(in, ty, mk, false, s.tp, b, g) +
-           op_dur(in, ty, ATTN, true, s.tp, b) + op_dur(in, ty, mk, true, s.tp, b, g);
+    return sdur(s, ATTN, false, b) + sdur(s, mk, false, b, g) + sdur(s, ATTN, true, b) + sdur(s, mk, true, b, g);
   }
-  i64 extra_fb(const StageSpec& s, int b, int kind) const {
-    const orc_type& ty = types[s.type];
-    return op_dur(in, ty, kind, false, s.tp, b) + op_dur(in, ty, kind, true, s.tp, b);
-  }
+  i64 extra_fb(const StageSpec& s, int b, int kind) const { return sdur(s, kind, false, b) + sdur(s, kind, true, b); }
 
   // C.4 step 1: non-uniform partition
   void partition(Plan& p) const {
@@ -789,15 +852,14 @@ struct Oracle {
   // or nullptr (A17: the TP group)
   i64 layer_chain(const StageSpec& ss, const Group& gr, int b, int bwd, bool compact,
                   const std::vector<Group>* epg = nullptr) const {
-    const orc_type& ty = types[ss.type];
     const i64 ar = compact ? tp_allreduce_compact(gr, ss.tp, b) : tp_allreduce(gr, ss.tp, b);
-    i64 chain = op_dur(in, ty, ATTN, bwd, ss.tp, b) + ar;
+    i64 chain = sdur(ss, ATTN, bwd, b) + ar;
     if (in.E > 1) {
       const i64 a2a = epg ? ep_alltoall_x(*epg, ss.tp, b) : ep_alltoall(gr, ss.tp, b);
       const i64 g = epg ? (i64)epg->size() * ss.tp : 0;
-      chain += a2a + op_dur(in, ty, MOE, bwd, ss.tp, b, g) + a2a;
+      chain += a2a + sdur(ss, MOE, bwd, b, g) + a2a;
     } else {
-      chain += op_dur(in, ty, MLP, bwd, ss.tp, b) + ar;
+      chain += sdur(ss, MLP, bwd, b) + ar;
     }
     return chain;
   }
@@ -861,8 +923,12 @@ struct Oracle {
       }
       // DP ring all-reduce: ring order class asc, replica asc, wrap; ring q < t*
       std::vector<Group> ring;
+      std::vector<int> ring_c;  // class of each ring position
       for (int c = 0; c < C; ++c)
-        for (int r = 0; r < cls[c].D; ++r) ring.push_back(p.place[c][r][sg.sc[c]]);
+        for (int r = 0; r < cls[c].D; ++r) {
+          ring.push_back(p.place[c][r][sg.sc[c]]);
+          ring_c.push_back(c);
+        }
       const i64 chunk = ceil_div(ceil_div(sg.S, sg.tstar), D);
       sg.AR = 0;
       for (int q = 0; q < sg.tstar; ++q) {
@@ -870,7 +936,7 @@ struct Oracle {
         for (size_t k = 0; k < ring.size(); ++k) {
           const Group& u = ring[k];
           const Group& v = ring[(k + 1) % ring.size()];
-          taus.push_back(tau(cl.gpu_to_gpu(u.node, u.base + q, v.node, v.base + q), chunk));
+          taus.push_back(tau(link_dd(u, cls[ring_c[k]].st[sg.sc[ring_c[k]]].tp, q, v, cls[ring_c[(k + 1) % ring.size()]].st[sg.sc[ring_c[(k + 1) % ring.size()]]].tp, q), chunk));
         }
         if (compact) {
           i64 slow = 0;
@@ -916,8 +982,7 @@ struct Oracle {
       // V.2 adds the wrap boundary stage P-1 -> stage 0 (last entry)
       auto p2p = [&](const Group& x, int tx, const Group& y, int ty) {
         i64 cs = 0;
-        for (int q = 0; q < std::min(tx, ty); ++q)
-          cs = std::max(cs, tau(cl.gpu_to_gpu(x.node, x.base + q, y.node, y.base + q), act_bytes(b)));
+        for (int q = 0; q < std::min(tx, ty); ++q) cs = std::max(cs, tau(link_dd(x, tx, q, y, ty, q), act_bytes(b)));
         return cs;
       };
       std::vector<std::vector<i64>> cv(cls[c].D, std::vector<i64>(P > 1 ? P - 1 : 0));
@@ -961,7 +1026,6 @@ struct Oracle {
         owner[c][r] = G.size();
         for (int s = 0; s < P; ++s) {
           const StageSpec& ss = cls[c].st[s];
-          const orc_type& ty = types[ss.type];
           const Group& gr = p.place[c][r][s];
           const std::vector<Group>* eg = ep ? &epg[s] : nullptr;
           SimGroup g{};
@@ -982,8 +1046,8 @@ struct Oracle {
           }
           // the embedding runs with the first chunk of stage 0, the head with the
           // last chunk of stage P-1
-          if (s == 0) { g.f[0] += op_dur(in, ty, EMB, false, ss.tp, b); g.g[0] += op_dur(in, ty, EMB, true, ss.tp, b); }
-          if (s == P - 1) { g.f[v - 1] += op_dur(in, ty, HEAD, false, ss.tp, b); g.g[v - 1] += op_dur(in, ty, HEAD, true, ss.tp, b); }
+          if (s == 0) { g.f[0] += sdur(ss, EMB, false, b); g.g[0] += sdur(ss, EMB, true, b); }
+          if (s == P - 1) { g.f[v - 1] += sdur(ss, HEAD, false, b); g.g[v - 1] += sdur(ss, HEAD, true, b); }
           g.c_prev = s > 0 ? cv[r][s - 1] : 0;
           g.c_next = s + 1 < P ? cv[r][s] : 0;
           g.c_wrap = v > 1 ? cv[r][P - 1] : 0;
@@ -1241,19 +1305,28 @@ struct Oracle {
         if (tp == sg[j].tstar) continue;
         for (int r = 0; r < cls[c].D; ++r) {
           const Group& g = p.place[c][r][s];
-          for (int q = 0; q < tp; ++q) rs.pairs.push_back({g.node, g.base + q, g.node, g.base + (q + 1) % tp});
+          for (int q = 0; q < tp; ++q) {
+            const auto x = dev(g, tp, q), y = dev(g, tp, (q + 1) % tp);
+            rs.pairs.push_back({x.first, x.second, y.first, y.second});
+          }
         }
       }
       if (!rs.pairs.empty()) steps.push_back(rs);
       std::vector<Group> ring;
+      std::vector<int> rtp;
       for (int c = 0; c < C; ++c)
-        for (int r = 0; r < cls[c].D; ++r) ring.push_back(p.place[c][r][sg[j].sc[c]]);
+        for (int r = 0; r < cls[c].D; ++r) {
+          ring.push_back(p.place[c][r][sg[j].sc[c]]);
+          rtp.push_back(cls[c].st[sg[j].sc[c]].tp);
+        }
       FStep st{j, 0, {}, ceil_div(xs, D)};
       for (int q = 0; q < sg[j].tstar; ++q)
         for (size_t k = 0; k < ring.size(); ++k) {
           const Group& u = ring[k];
           const Group& v = ring[(k + 1) % ring.size()];
-          st.pairs.push_back({u.node, u.base + q, v.node, v.base + q});
+          const size_t k2 = (k + 1) % ring.size();
+          const auto x = dev(u, rtp[k], q), y = dev(v, rtp[k2], q);
+          st.pairs.push_back({x.first, x.second, y.first, y.second});
         }
       for (i64 k = 0; k < 2 * (D - 1); ++k) steps.push_back(st);
       seg_n[j] = (int)steps.size() - seg_first[j];
@@ -1348,8 +1421,12 @@ void* orc_create(const orc_input* in) {
     g_err = "interleave must be 1..8";
     return nullptr;
   }
-  if (in->mem_check && (in->interleave > 1 || in->ep_dp)) {
-    g_err = "mem_check is not defined with interleave / ep_dp (DESIGN V.2, V.3)";
+  if (in->mem_check && (in->interleave > 1 || in->ep_dp || in->mixtp)) {
+    g_err = "mem_check is not defined with interleave / ep_dp / mixtp (DESIGN V.1-V.3)";
+    return nullptr;
+  }
+  if (in->ep_dp && in->mixtp) {
+    g_err = "ep_dp is not defined with mixtp (DESIGN V.1)";
     return nullptr;
   }
   Oracle* o = new Oracle();
@@ -1403,7 +1480,8 @@ int orc_describe(void* h, i64 i, char* buf, int cap) {
     s += c ? ",{" : "{";
     s += "\"D\":" + std::to_string(cs.D) + ",\"stages\":[";
     for (size_t k = 0; k < cs.st.size(); ++k)
-      s += (k ? ",[" : "[") + std::to_string(cs.st[k].type) + "," + std::to_string(cs.st[k].tp) + "]";
+      s += (k ? ",[" : "[") + std::to_string(cs.st[k].type) + "," + std::to_string(cs.st[k].tp) +
+           (cs.st[k].type2 >= 0 ? "," + std::to_string(cs.st[k].type2) : std::string()) + "]";
     s += "],\"layers\":[";
     for (size_t k = 0; k < p.layers[c].size(); ++k) s += (k ? "," : "") + std::to_string(p.layers[c][k]);
     s += "],\"mb\":[";
@@ -1413,7 +1491,8 @@ int orc_describe(void* h, i64 i, char* buf, int cap) {
     for (size_t r = 0; r < p.place[c].size(); ++r) {
       s += r ? ",[" : "[";
       for (size_t k = 0; k < p.place[c][r].size(); ++k)
-        s += (k ? ",[" : "[") + std::to_string(p.place[c][r][k].node) + "," + std::to_string(p.place[c][r][k].base) + "]";
+        s += (k ? ",[" : "[") + std::to_string(p.place[c][r][k].node) + "," + std::to_string(p.place[c][r][k].base) +
+             (p.place[c][r][k].node2 >= 0 ? "," + std::to_string(p.place[c][r][k].node2) : std::string()) + "]";
       s += "]";
     }
     s += "]}";

@@ -63,7 +63,7 @@ class _Input(C.Structure):
                 ("homo", C.c_int32), ("mixed", C.c_int32), ("use_all", C.c_int32),
                 ("r_layer", C.c_int32), ("pmax", C.c_int32), ("r_batch", C.c_int32),
                 ("mem_check", C.c_int32), ("sync_overlap", C.c_int32),
-                ("interleave", C.c_int32), ("ep_dp", C.c_int32)]
+                ("interleave", C.c_int32), ("ep_dp", C.c_int32), ("mixtp", C.c_int32)]
 
 
 def _path(hops):
@@ -194,6 +194,7 @@ class Oracle:
         I.sync_overlap = int(se.get("sync_overlap", 0))
         I.interleave = int(se.get("interleave", 1))
         I.ep_dp = int(se.get("ep_dp", 0))
+        I.mixtp = int(se.get("mixtp", 0))
         self._in = I
         self.h = lib().orc_create(C.byref(I))
         if not self.h:

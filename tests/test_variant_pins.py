@@ -238,6 +238,45 @@ def test_ep_dense_gradient_bytes_mixtral(oracle_mod):
 # ----------------------------------------------------------------------------
 # whole candidates: an independent evaluator with both variants
 # ----------------------------------------------------------------------------
+def gdev(place, t, q):
+    """Device q of a stage group: [node, base] holds GPUs base..base+t-1; a V.1
+    mixed group [node, base, node2] holds q < t/2 on node, the rest at the
+    same base on node2."""
+    if len(place) == 2:
+        return place[0], place[1] + q
+    h = t // 2
+    return (place[0], place[1] + q) if q < h else (place[2], place[1] + q - h)
+
+
+def glink(o, p1, t1, q1, p2, t2, q2):
+    return o.link(*gdev(p1, t1, q1), *gdev(p2, t2, q2))
+
+
+def op_max(o, stage, kind, bwd, b):
+    """V.1 (PAPER.md:280 C4): a mixed group's op lasts as long as on its slower
+    device type; stage = [type, tp] or [type, tp, type2]."""
+    d = o.op(stage[0], kind, bwd, stage[1], b)[2]
+    if len(stage) == 3:
+        d = max(d, o.op(stage[2], kind, bwd, stage[1], b)[2])
+    return d
+
+
+def ring_ar(o, cfg, place, t, b):
+    """TP ring all-reduce over devices 0..t-1 of the group (ring law)."""
+    if t == 1:
+        return 0
+    A = cdiv(act_bytes(cfg, b), t)
+    return 2 * (t - 1) * max(tau(glink(o, place, t, q, place, t, (q + 1) % t), A) for q in range(t))
+
+
+def pair_a2a(o, cfg, place, t, b):
+    """A17 all-to-all inside one group: t - 1 rounds at its slowest ordered pair."""
+    if t == 1:
+        return 0
+    per = cdiv(act_bytes(cfg, b) * cfg["model"]["moe_topk"], t * t)
+    return (t - 1) * max(tau(glink(o, place, t, x, place, t, y), per) for x in range(t) for y in range(t) if x != y)
+
+
 def py_eval_v(o, cfg, i, overlap=False):
     """Independent evaluator of candidate i under V.2 (cfg search.interleave)
     and V.3 (search.ep_dp).  Chunk k of a stage with l layers has
@@ -268,10 +307,8 @@ def py_eval_v(o, cfg, i, overlap=False):
         vstarts.append(st)
 
         def p2p(r, s1, s2):
-            n1, b1 = cl["place"][r][s1]
-            n2, b2 = cl["place"][r][s2]
-            npq = min(cl["stages"][s1][1], cl["stages"][s2][1])
-            return max(tau(o.link(n1, b1 + q, n2, b2 + q), A) for q in range(npq))
+            t1, t2 = cl["stages"][s1][1], cl["stages"][s2][1]
+            return max(tau(glink(o, cl["place"][r][s1], t1, q, cl["place"][r][s2], t2, q), A) for q in range(min(t1, t2)))
 
         cc = [[p2p(r, s, s + 1) for s in range(P - 1)] for r in range(D)]
         cw = [p2p(r, P - 1, 0) if v > 1 else 0 for r in range(D)]
@@ -282,35 +319,37 @@ def py_eval_v(o, cfg, i, overlap=False):
             mb = [max(mb)] * D
         for r in range(D):
             f, g = [], []
-            for s, (ty, tp) in enumerate(cl["stages"]):
-                node, base = cl["place"][r][s]
-                ar = tp_allreduce_ref(o, cfg, node, base, tp, b)
+            for s, stage in enumerate(cl["stages"]):
+                ty, tp = stage[0], stage[1]
+                pl = cl["place"][r][s]
+                ar = ring_ar(o, cfg, pl, tp, b)
                 kind = "moe" if moe else "mlp"
                 if ep:
                     groups = [tuple(cl["place"][rr][s]) for rr in range(D)]
-                    from test_variant_pins import a2a_groups_ref as _a2a
-                    a2a = _a2a(o, cfg, groups, tp, b)
+                    a2a = a2a_groups_ref(o, cfg, groups, tp, b)
                     gexp = D * tp
                 else:
-                    from test_oracle_pins_r2 import alltoall_round_robin
-                    a2a = alltoall_round_robin(o, cfg, node, base, tp, b) if moe else 0
+                    a2a = pair_a2a(o, cfg, pl, tp, b) if moe else 0
                     gexp = tp
                 ch = []
                 for bwd in (0, 1):
-                    x = o.op(ty, "attn", bwd, tp, b)[2] + ar
+                    x = op_max(o, stage, "attn", bwd, b) + ar
                     if moe:
-                        x += a2a + moe_dur(o, cfg, ty, bwd, tp, b, gexp) + a2a
+                        mo = moe_dur(o, cfg, ty, bwd, tp, b, gexp)
+                        if len(stage) == 3:
+                            mo = max(mo, moe_dur(o, cfg, stage[2], bwd, tp, b, gexp))
+                        x += a2a + mo + a2a
                     else:
-                        x += o.op(ty, kind, bwd, tp, b)[2] + ar
+                        x += op_max(o, stage, kind, bwd, b) + ar
                     ch.append(x)
                 fs = [lay[s][k] * ch[0] for k in range(v)]
                 gs = [lay[s][k] * ch[1] for k in range(v)]
                 if s == 0:
-                    fs[0] += o.op(ty, "emb", 0, tp, b)[2]
-                    gs[0] += o.op(ty, "emb", 1, tp, b)[2]
+                    fs[0] += op_max(o, stage, "emb", 0, b)
+                    gs[0] += op_max(o, stage, "emb", 1, b)
                 if s == P - 1:
-                    fs[v - 1] += o.op(ty, "head", 0, tp, b)[2]
-                    gs[v - 1] += o.op(ty, "head", 1, tp, b)[2]
+                    fs[v - 1] += op_max(o, stage, "head", 0, b)
+                    gs[v - 1] += op_max(o, stage, "head", 1, b)
                 f.append(fs)
                 g.append(gs)
             T, last = ilv_dag(f, g, cc[r], cw[r], mb[r])
@@ -331,11 +370,11 @@ def py_eval_v(o, cfg, i, overlap=False):
         for c, cl in enumerate(d["classes"]):
             if tps[c] != tstar:
                 for r in range(cl["D"]):
-                    node, base = cl["place"][r][sc[c]]
-                    RS = max([RS] + [tau(e, cdiv(S, tstar)) for e in tp_ring_edges(o, node, base, tps[c])])
-        ring = [(cl["place"][r][sc[c]]) for c, cl in enumerate(d["classes"]) for r in range(cl["D"])]
+                    pl, t = cl["place"][r][sc[c]], tps[c]
+                    RS = max([RS] + [tau(glink(o, pl, t, q, pl, t, (q + 1) % t), cdiv(S, tstar)) for q in range(t)])
+        ring = [(cl["place"][r][sc[c]], tps[c]) for c, cl in enumerate(d["classes"]) for r in range(cl["D"])]
         chunk = cdiv(cdiv(S, tstar), D)
-        slow = max(tau(o.link(u[0], u[1] + q, w[0], w[1] + q), chunk)
+        slow = max(tau(glink(o, u[0], u[1], q, w[0], w[1], q), chunk)
                    for q in range(tstar) for u, w in zip(ring, ring[1:] + ring[:1]))
         segs.append((sc, RS + 2 * (D - 1) * slow))
     free = {}
@@ -470,3 +509,118 @@ def test_variants_literal_equals_compact(oracle_mod):
         lit, cmp_ = oracle_mod.Oracle(cfg), oracle_mod.Oracle(cfg, compact=True)
         idx = H.sample_indices(lit.space_size(), 300, seed=11)
         assert np.array_equal(lit.eval_many(idx, threads=THREADS), cmp_.eval_many(idx, threads=THREADS))
+
+
+# ----------------------------------------------------------------------------
+# V.1 mixed-type TP groups
+# ----------------------------------------------------------------------------
+def with_mixtp(cfg):
+    return H.with_changes(cfg, search__mixtp=1)
+
+
+def count_mixtp(cfg):
+    """Candidates of the MIXTP family, counted from DESIGN V.1's grammar
+    (written out independently of the oracle's enumeration)."""
+    cl, md, se = cfg["cluster"], cfg["model"], cfg["search"]
+    nt = len(cl["types"])
+    n_of = [sum(t["gpus_per_node"] for n, t in ((n, cl["types"][n]) for n in cl["nodes"]) if n == k) for k in range(nt)]
+    n_of = [cl["nodes"].count(k) * cl["types"][k]["gpus_per_node"] for k in range(nt)]
+    rl, rb = 2 * se["r_layer"] + 1, 2 * se["r_batch"] + 1
+    total = 0
+    for b in sorted(se["bset"]):
+        if md["global_batch"] % b:
+            continue
+        M = md["global_batch"] // b
+        for a in range(nt):
+            for a2 in range(a + 1, nt):
+                for tp in sorted(set(se["tpset"][a]) & set(se["tpset"][a2])):
+                    if tp < 2 or md["heads"] % tp or md["kv_heads"] % tp:
+                        continue
+                    if any(cl["types"][x]["gpus_per_node"] % (tp // 2) for x in (a, a2)):
+                        continue
+                    for P in sorted(set(se["pset"])):
+                        if P > md["layers"]:
+                            continue
+                        D = 1
+                        while D * P * (tp // 2) <= min(n_of[a], n_of[a2]):
+                            full = D * P * (tp // 2) == n_of[a] == n_of[a2]
+                            if (not se["use_all"] or full) and M >= D:
+                                total += rl ** (P - 1) if P <= se["pmax_perturb"] else 1
+                            D += 1
+    return total
+
+
+@pytest.mark.parametrize("n", [2, 3, 4, 5])
+def test_mixtp_space_size(oracle_mod, n):
+    base = oracle_mod.Oracle(H.get(n)).space_size()
+    assert oracle_mod.Oracle(with_mixtp(H.get(n))).space_size() == base + count_mixtp(H.get(n))
+
+
+def test_mixtp_placement_by_hand(oracle_mod):
+    """Config 2 (nodes 0-1 A100, 2-3 H100, 8 GPUs each), tp = 4 mixed groups
+    (2 A100 + 2 H100), P = 2, D = 2: groups fill the 2-GPU blocks of node 0
+    and node 2 in order -- (0, 0 | 2), (0, 2 | 2), then replica 1 (0, 4 | 2),
+    (0, 6 | 2)."""
+    o = oracle_mod.Oracle(with_mixtp(H.get(2)))
+    pre = o.template_prefix()
+    for k in range(o.n_templates()):
+        d = o.describe(int(pre[k]))
+        cl = d["classes"][0]
+        if len(cl["stages"][0]) == 3 and cl["stages"] == [[0, 4, 1]] * 2 and cl["D"] == 2:
+            assert cl["place"] == [[[0, 0, 2], [0, 2, 2]], [[0, 4, 2], [0, 6, 2]]]
+            return
+    raise AssertionError("template not found")
+
+
+def test_mixtp_single_group_closed_form(oracle_mod):
+    """One mixed A100/H100 group of tp = 2 (one GPU on node 0, one on node 2),
+    P = 1, D = 1, b = 4: T = M (f + g), each op the slower type's (the
+    bottleneck device), each layer with two TP all-reduces over the group's
+    two rail edges: 2 (t-1) x tau(rail, ceil(A / 2)).  Rail (Table 4): A100
+    PCIe 512 Gbps bidirectional = 2 x ceil(73600 / 256) = 2 x 288 ns, NIC 368 +
+    200 Gbps, H100 PCIe 1024 -> 2 x 144 ns, NIC 368: alpha = 576 + 368 + 368 +
+    288 = 1600 ns, beta = 25 B/ns."""
+    cfg = with_mixtp(H.get(2))
+    o = oracle_mod.Oracle(cfg)
+    a, beta = o.link(0, 0, 2, 0)
+    assert (a, beta) == (1600, 25.0)
+    pre = o.template_prefix()
+    for k in range(o.n_templates()):
+        d = o.describe(int(pre[k]))
+        if d["b"] == 4 and d["classes"][0]["stages"] == [[0, 2, 1]] and d["classes"][0]["D"] == 1:
+            break
+    else:
+        raise AssertionError("template not found")
+    b, L, M = 4, cfg["model"]["layers"], cfg["model"]["global_batch"] // 4
+    A = b * 4096 * 4096 * 2
+    ar = 2 * 1 * (1600 + math.ceil(cdiv(A, 2) / 25.0))
+    mx = lambda kind, bwd: max(o.op(0, kind, bwd, 2, b)[2], o.op(1, kind, bwd, 2, b)[2])
+    fg = [L * (mx("attn", bwd) + ar + mx("mlp", bwd) + ar) + mx("emb", bwd) + mx("head", bwd) for bwd in (0, 1)]
+    assert o.eval(int(pre[k])) == M * sum(fg)
+    assert mx("mlp", 0) == o.op(0, "mlp", 0, 2, b)[2] > o.op(1, "mlp", 0, 2, b)[2]  # the A100 half bounds it
+
+
+@pytest.mark.parametrize("cfgf", ["c2", "c4", "tiny101", "tiny105", "c2-ilv", "c4-overlap"])
+def test_py_eval_mixtp(oracle_mod, cfgf):
+    cfg = {"c2": lambda: with_mixtp(H.get(2)), "c4": lambda: with_mixtp(H.get(4)),
+           "tiny101": lambda: with_mixtp(H.variant_tiny(101)), "tiny105": lambda: with_mixtp(H.variant_tiny(105)),
+           "c2-ilv": lambda: H.with_interleave(with_mixtp(H.get(2)), 2),
+           "c4-overlap": lambda: H.with_sync_overlap(with_mixtp(H.get(4)))}[cfgf]()
+    o = oracle_mod.Oracle(cfg)
+    base = oracle_mod.Oracle(H.with_changes(cfg, search__mixtp=0)).space_size()
+    N = o.space_size()
+    assert N > base
+    idx = np.arange(base, N) if N - base <= 300 else np.unique(np.concatenate(
+        [H.sample_indices(N - base, 250, seed=3) + base, [base, N - 1]]))
+    want = o.eval_many(idx, threads=THREADS)
+    for k, i in enumerate(idx):
+        assert py_eval_v(o, cfg, int(i), overlap=bool(cfg["search"].get("sync_overlap", 0))) == want[k], int(i)
+    assert (want >= 0).sum() >= 3
+
+
+def test_mixtp_literal_equals_compact(oracle_mod):
+    cfg = with_mixtp(H.get(2))
+    lit, cmp_ = oracle_mod.Oracle(cfg), oracle_mod.Oracle(cfg, compact=True)
+    base = oracle_mod.Oracle(H.get(2)).space_size()
+    idx = np.arange(base, lit.space_size())
+    assert np.array_equal(lit.eval_many(idx, threads=THREADS), cmp_.eval_many(idx, threads=THREADS))
