@@ -148,10 +148,18 @@ typedef struct {
    *   sharded over every replica's TP group of that stage, g = D tp devices
    *   (DESIGN.md V.3): the all-to-all spans them and couples the replicas
    *   into lockstep, and expert gradients are not all-reduced.
-   * Neither combines with mem_check (HSIM_EINVAL at create) nor with
-   * hsim_flow_resim (HSIM_EINVAL). */
+   * mixtp: 1 = add the MIXTP template family (DESIGN.md V.1): one class
+   *   whose every stage is a mixed TP group of tp devices, tp/2 of type a and
+   *   tp/2 of type a2 > a at the same local base on two nodes (tp >= 2 in both
+   *   TP sets, tp/2 | GPUs per node); each op lasts as long as on the slower
+   *   type (the bottleneck device, PAPER.md:280 C4); its collectives and p2p
+   *   run over the group's two nodes.  Enumerated after the MIXED family of
+   *   each micro-batch size.
+   * None of them combines with mem_check (HSIM_EINVAL at create) nor with
+   * hsim_flow_resim (HSIM_EINVAL); ep_dp does not combine with mixtp. */
   int32_t interleave;
   int32_t ep_dp;
+  int32_t mixtp;
 } hsim_model_desc;
 
 /* Which candidates the t-th work item (t = 0..n-1) evaluates. */

@@ -49,6 +49,19 @@ Link path_link(const hsim_path& p, i64 frame) {
 Link cat(const Link& a, const Link& b) { return Link{a.alpha + b.alpha, std::min(a.beta, b.beta)}; }
 i64 tau(const Link& e, i64 x) { return e.alpha + ceilq(x, e.beta); }
 
+// A stage of a class is (type code, tp); the code carries a V.1 mixed group's
+// second type: code = type | (type2 + 1) << 8 (type2 = -1: homogeneous)
+int st_t(int code) { return code & 255; }
+int st_t2(int code) { return (code >> 8) - 1; }
+int st_code(int t, int t2) { return t | (t2 + 1) << 8; }
+// a placed stage group: tp GPUs from base on node; V.1: tp/2 from base on node
+// and tp/2 from base on node2
+struct GPl { int node, base, node2; };
+std::pair<int, int> gdev(const GPl& g, int tp, int q) {
+  if (g.node2 < 0) return {g.node, g.base + q};
+  return q < tp / 2 ? std::make_pair(g.node, g.base + q) : std::make_pair(g.node2, g.base + q - tp / 2);
+}
+
 i64 hamilton_floor_rem(i64 n, i64 w, i64 W, i64* rem) {
   *rem = n * w % W;
   return n * w / W;
@@ -157,7 +170,11 @@ struct hsim_handle {
   int32_t crec(int b_idx, int M, int D, const std::vector<std::pair<int, int>>& stages, bool ep);
   i64 moe_dur(int t, int tp, i64 b, i64 g, bool bwd) const;
   i64 a2a_groups(const std::vector<std::pair<int, int>>& groups, int tp, i64 b) const;
-  std::vector<std::vector<std::pair<int, int>>> place(int D, const std::vector<std::pair<int, int>>& stages) const;
+  std::vector<std::vector<GPl>> place(int D, const std::vector<std::pair<int, int>>& stages) const;
+  Link dlink(const GPl& a, int ta, int qa, const GPl& z, int tz, int qz) const {
+    const auto x = gdev(a, ta, qa), y = gdev(z, tz, qz);
+    return link(x.first, x.second, y.first, y.second);
+  }
   void prepare();
   void upload();
   int ensure_device() {
@@ -228,8 +245,10 @@ void hsim_handle::validate() {
   if (m.homo && c.n_device_types > MAXC) fail(HSIM_EINVAL, "InvalidValue: too many classes");
   if (m.interleave < 0 || m.interleave > 8) fail(HSIM_EINVAL, "InvalidValue: interleave must be 0..8");
   if (m.ep_dp != 0 && m.ep_dp != 1) fail(HSIM_EINVAL, "InvalidValue: ep_dp must be 0 or 1");
-  if (m.mem_check && (m.interleave > 1 || m.ep_dp))
-    fail(HSIM_EINVAL, "InvalidValue: mem_check is not defined with interleave / ep_dp (DESIGN.md V.2, V.3)");
+  if (m.mixtp != 0 && m.mixtp != 1) fail(HSIM_EINVAL, "InvalidValue: mixtp must be 0 or 1");
+  if (m.mem_check && (m.interleave > 1 || m.ep_dp || m.mixtp))
+    fail(HSIM_EINVAL, "InvalidValue: mem_check is not defined with interleave / ep_dp / mixtp (DESIGN.md V.1-V.3)");
+  if (m.ep_dp && m.mixtp) fail(HSIM_EINVAL, "InvalidValue: ep_dp is not defined with mixtp (DESIGN.md V.1)");
 }
 
 void hsim_handle::derive_links() {
@@ -311,7 +330,9 @@ void hsim_handle::derive_durations() {
     for (int lg = 0; lg < 4; ++lg) {
       const i64 tp = 1 << lg;
       if (!(md.tpset_mask[t] >> lg & 1)) continue;
-      if (types[t].gpus_per_node % tp || md.heads % tp || md.kv_heads % tp) continue;
+      // (tp > GPUs per node only in V.1 mixed groups, whose collectives crec() derives)
+      if (md.heads % tp || md.kv_heads % tp) continue;
+      const bool in_node = types[t].gpus_per_node % tp == 0;
       for (size_t bi = 0; bi < bs.size(); ++bi) {
         const i64 b = bs[bi], T = b * s;
         const hsim_device_type& ty = types[t];
@@ -345,7 +366,7 @@ void hsim_handle::derive_durations() {
         // TP all-reduce 2(t-1) * max over ring edges; EP all-to-all (t-1) * max over pairs (A16, A17)
         const i64 A = b * s * h * bpe;
         d.ar = 0; d.a2a = 0;
-        if (tp > 1) {
+        if (tp > 1 && in_node) {
           i64 mx = 0;
           for (int q = 0; q < tp; ++q) mx = std::max(mx, tau(intra[t][q][(q + 1) % tp], ceil_div(A, tp)));
           d.ar = 2 * (tp - 1) * mx;
@@ -364,28 +385,41 @@ void hsim_handle::derive_durations() {
 // C.3: class alone on a fresh cluster (classes of one template use disjoint
 // device types, so their placements do not interact): replica-major,
 // stage-major; lowest-id node of the stage's type with a free tp-aligned block.
-std::vector<std::vector<std::pair<int, int>>> hsim_handle::place(int D, const std::vector<std::pair<int, int>>& stages) const {
+// V.1 mixed group (type a, type a2): a tp/2-aligned block on the lowest node of
+// type a with one free, then the same block on the lowest node of type a2
+// where it is free.
+std::vector<std::vector<GPl>> hsim_handle::place(int D, const std::vector<std::pair<int, int>>& stages) const {
   std::vector<std::vector<char>> used(cd.n_nodes);
   for (int n = 0; n < cd.n_nodes; ++n) used[n].assign(types[node_type[n]].gpus_per_node, 0);
-  std::vector<std::vector<std::pair<int, int>>> out(D);
+  std::vector<std::vector<GPl>> out(D);
   for (int r = 0; r < D; ++r)
     for (const auto& st : stages) {
-      const int t = st.first, tp = st.second;
-      bool ok = false;
-      for (size_t ni = 0; ni < nodes_of_type[t].size() && !ok; ++ni) {
+      const int t = st_t(st.first), t2 = st_t2(st.first), tp = st.second;
+      const int w = t2 >= 0 ? tp / 2 : tp;
+      GPl g{-1, -1, -1};
+      for (size_t ni = 0; ni < nodes_of_type[t].size() && g.node < 0; ++ni) {
         const int n = nodes_of_type[t][ni];
-        const int g = types[t].gpus_per_node;
-        for (int base = 0; base + tp <= g && !ok; base += tp) {
+        const int gp = types[t].gpus_per_node;
+        for (int base = 0; base + w <= gp && g.node < 0; base += w) {
           bool fr = true;
-          for (int q = 0; q < tp; ++q) fr = fr && !used[n][base + q];
-          if (fr) {
-            for (int q = 0; q < tp; ++q) used[n][base + q] = 1;
-            out[r].push_back({n, base});
-            ok = true;
-          }
+          for (int q = 0; q < w; ++q) fr = fr && !used[n][base + q];
+          if (fr) g = GPl{n, base, -1};
         }
       }
-      if (!ok) fail(HSIM_EINVAL, "InsufficientDevices: placement failed");
+      if (g.node >= 0 && t2 >= 0) {
+        for (size_t ni = 0; ni < nodes_of_type[t2].size() && g.node2 < 0; ++ni) {
+          const int n = nodes_of_type[t2][ni];
+          bool fr = g.base + w <= types[t2].gpus_per_node;
+          for (int q = 0; q < w && fr; ++q) fr = !used[n][g.base + q];
+          if (fr) g.node2 = n;
+        }
+        if (g.node2 < 0) g.node = -1;
+      }
+      if (g.node < 0) fail(HSIM_EINVAL, "InsufficientDevices: placement failed");
+      for (int q = 0; q < w; ++q) used[g.node][g.base + q] = 1;
+      if (g.node2 >= 0)
+        for (int q = 0; q < w; ++q) used[g.node2][g.base + q] = 1;
+      out[r].push_back(g);
     }
   return out;
 }
@@ -450,19 +484,45 @@ int32_t hsim_handle::crec(int bi, int M, int D, const std::vector<std::pair<int,
   (void)M;
   const int P = (int)stages.size();
   const i64 b = bs[bi];
+  const i64 A = b * md.seq * md.hidden * md.bpe_act;
   const auto pl = place(D, stages);
+  bool mixed = false;
   std::vector<StageRec> sr(P);
   std::vector<i64> w(P);
   for (int s = 0; s < P; ++s) {
-    const int t = stages[s].first, tp = stages[s].second, lg = __builtin_ctz(tp);
-    const Dur& d = dur_at(t, lg, bi);
+    const int t = st_t(stages[s].first), t2 = st_t2(stages[s].first), tp = stages[s].second, lg = __builtin_ctz(tp);
+    Dur d = dur_at(t, lg, bi);
+    if (t2 >= 0) {
+      // V.1: equal shards on both types, every op ends with a TP collective, so
+      // each op lasts as long as on the slower type (PAPER.md:280 C4); the TP
+      // all-reduce ring and the all-to-all run over the group's device map
+      mixed = true;
+      const Dur& e = dur_at(t2, lg, bi);
+      d.attn_f = std::max(d.attn_f, e.attn_f); d.attn_b = std::max(d.attn_b, e.attn_b);
+      d.mlp_f = std::max(d.mlp_f, e.mlp_f);    d.mlp_b = std::max(d.mlp_b, e.mlp_b);
+      d.emb_f = std::max(d.emb_f, e.emb_f);    d.emb_b = std::max(d.emb_b, e.emb_b);
+      d.head_f = std::max(d.head_f, e.head_f); d.head_b = std::max(d.head_b, e.head_b);
+      for (int r = 0; r < D; ++r) {
+        i64 ar = 0, a2a = 0;
+        for (int q = 0; q < tp; ++q) ar = std::max(ar, tau(dlink(pl[r][s], tp, q, pl[r][s], tp, (q + 1) % tp), ceil_div(A, tp)));
+        ar *= 2 * (tp - 1);
+        if (md.moe_experts > 1)
+          for (int x = 0; x < tp; ++x)
+            for (int y = 0; y < tp; ++y)
+              if (x != y) a2a = std::max(a2a, (i64)(tp - 1) * tau(dlink(pl[r][s], tp, x, pl[r][s], tp, y), ceil_div(A * md.moe_topk, (i64)tp * tp)));
+        if (r > 0 && (ar != d.ar || a2a != d.a2a))
+          fail(HSIM_EINVAL, "InvalidValue: mixed TP groups' links differ between replicas");
+        d.ar = ar;
+        d.a2a = a2a;
+      }
+    }
     StageRec& r = sr[s];
     std::memset(&r, 0, sizeof r);
-    r.type = t; r.tp = tp; r.lg_tp = lg;
+    r.type = t; r.type2 = t2; r.tp = tp; r.lg_tp = lg;
     i64 mlp_f = d.mlp_f, mlp_b = d.mlp_b, a2a = d.a2a;
     if (ep) {
       std::vector<std::pair<int, int>> grp(D);
-      for (int q = 0; q < D; ++q) grp[q] = pl[q][s];
+      for (int q = 0; q < D; ++q) grp[q] = {pl[q][s].node, pl[q][s].base};
       a2a = a2a_groups(grp, tp, b);
       mlp_f = moe_dur(t, tp, b, (i64)D * tp, false);
       mlp_b = moe_dur(t, tp, b, (i64)D * tp, true);
@@ -477,7 +537,11 @@ int32_t hsim_handle::crec(int bi, int M, int D, const std::vector<std::pair<int,
     r.tcomp = d.attn_f + mlp_f + d.attn_b + mlp_b;
     if (s == 0) { r.fext += d.emb_f; r.gext += d.emb_b; r.wext += d.emb_f + d.emb_b; }
     if (s == P - 1) { r.fext += d.head_f; r.gext += d.head_b; r.wext += d.head_f + d.head_b; }
-    r.tp_mask = tp_mask[t][lg];
+    if (t2 >= 0) {
+      for (int q = 0; q < tp; ++q) r.tp_mask |= (u64)1 << lc(dlink(pl[0][s], tp, q, pl[0][s], tp, (q + 1) % tp));
+    } else {
+      r.tp_mask = tp_mask[t][lg];
+    }
     w[s] = ((i64)1 << 40) / r.tcomp;
     layer_fb_max = std::max(layer_fb_max, r.layer_f + r.layer_b);
     ext_max = std::max(ext_max, r.fext + r.gext);
@@ -494,22 +558,24 @@ int32_t hsim_handle::crec(int bi, int M, int D, const std::vector<std::pair<int,
     for (i64 k = 0; k < md.layers - given; ++k) sr[ord[k]].l0 += 1;
   }
   for (int s = 0; s < P; ++s) {
-    sr[s].first_node = pl[0][s].first; sr[s].first_base = pl[0][s].second;
-    sr[s].last_node = pl[D - 1][s].first; sr[s].last_base = pl[D - 1][s].second;
+    sr[s].first_node = pl[0][s].node; sr[s].first_base = pl[0][s].base;
+    sr[s].last_node = pl[D - 1][s].node; sr[s].last_base = pl[D - 1][s].base;
+    const int tp = sr[s].tp;
+    // V.1 (single-class MIXTP templates, TplRec flag 2): the ring's wrap edge
+    // D-1 -> 0 is folded in here too (the kernels' cross-class term assumes
+    // homogeneous groups)
     for (int lg = 0; lg <= sr[s].lg_tp; ++lg)
-      for (int r = 0; r + 1 < D; ++r)
+      for (int r = 0; r + 1 < D + (mixed && D > 1 ? 1 : 0); ++r)
         for (int q = 0; q < (1 << lg); ++q)
-          sr[s].dp_mask[lg] |= (u64)1 << lc(link(pl[r][s].first, pl[r][s].second + q, pl[r + 1][s].first, pl[r + 1][s].second + q));
+          sr[s].dp_mask[lg] |= (u64)1 << lc(dlink(pl[r][s], tp, q, pl[(r + 1) % D][s], tp, q));
   }
   // p2p cost per replica per boundary (A8): rank pairs q < min(tp_s, tp_s+1),
   // max of tau(A); V.2 appends the wrap boundary stage P-1 -> stage 0
-  const i64 A = b * md.seq * md.hidden * md.bpe_act;
   const bool wrap = ilv > 1 && P >= 2;
   auto p2p = [&](int r, int s1, int s2) {
-    const int np = std::min(stages[s1].second, stages[s2].second);
+    const int t1 = stages[s1].second, t2 = stages[s2].second;
     i64 c = 0;
-    for (int q = 0; q < np; ++q)
-      c = std::max(c, tau(link(pl[r][s1].first, pl[r][s1].second + q, pl[r][s2].first, pl[r][s2].second + q), A));
+    for (int q = 0; q < std::min(t1, t2); ++q) c = std::max(c, tau(dlink(pl[r][s1], t1, q, pl[r][s2], t2, q), A));
     return c;
   };
   std::vector<std::vector<i64>> cv(D, std::vector<i64>(P, 0));  // [0, P-1) boundaries, [P-1] wrap
@@ -591,6 +657,9 @@ void hsim_handle::enumerate() {
       r.b = b; r.M = (int32_t)M; r.C = (int32_t)classes.size(); r.D = (int32_t)Dt;
       const bool ep = md.ep_dp && md.moe_experts > 1 && classes.size() == 1;  // V.3
       r.flags = ep ? 1 : 0;
+      for (auto& c : classes)
+        for (auto& st : c.second)
+          if (st_t2(st.first) >= 0) r.flags |= 2;  // V.1 mixed TP groups
       int cnt[33] = {0}, nilv = 0;
       for (size_t c = 0; c < classes.size(); ++c) {
         const int P = (int)classes[c].second.size();
@@ -682,6 +751,27 @@ void hsim_handle::enumerate() {
           if (t < 0) break;
         }
       }
+    }
+    if (md.mixtp && nt >= 2) {
+      // V.1 MIXTP family: one class, every stage a mixed TP group of tp devices,
+      // tp/2 of type a and tp/2 of type a2 (a < a2): tp >= 2 in both TP sets,
+      // tp | heads and kv heads, tp/2 | GPUs per node; D replicas of P stages
+      // need D P tp/2 GPUs of each type (use_all: exactly all of both)
+      for (int a = 0; a < nt; ++a)
+        for (int a2 = a + 1; a2 < nt; ++a2)
+          for (int tp = 2; tp <= 8; tp *= 2) {
+            const int lg = __builtin_ctz(tp);
+            if (!(md.tpset_mask[a] >> lg & 1) || !(md.tpset_mask[a2] >> lg & 1) || md.heads % tp || md.kv_heads % tp ||
+                types[a].gpus_per_node % (tp / 2) || types[a2].gpus_per_node % (tp / 2))
+              continue;
+            for (int P : ps) {
+              if (P > md.layers) continue;
+              for (i64 D = 1; D * P * (tp / 2) <= std::min(n_of_type[a], n_of_type[a2]); ++D) {
+                if (md.use_all && (D * P * (tp / 2) != n_of_type[a] || D * P * (tp / 2) != n_of_type[a2])) continue;
+                push({{(int)D, std::vector<std::pair<int, int>>(P, {st_code(a, a2), tp})}});
+              }
+            }
+          }
     }
   }
   N = acc;
@@ -1025,10 +1115,12 @@ int hsim_decode(const hsim_handle* h, int64_t i, char* json, size_t cap) {
     const CrecHdr* hd = crec_hdr(h->hT, tp.crec[c]);
     const StageRec* sr = crec_stages(h->hT, tp.crec[c]);
     std::vector<std::pair<int, int>> stages;
-    for (int q = 0; q < hd->P; ++q) stages.push_back({sr[q].type, sr[q].tp});
+    for (int q = 0; q < hd->P; ++q) stages.push_back({st_code(sr[q].type, sr[q].type2), sr[q].tp});
     s += c ? ",{" : "{";
     s += "\"D\":" + std::to_string(hd->D) + ",\"subclasses\":" + std::to_string(hd->U) + ",\"stages\":[";
-    for (int q = 0; q < hd->P; ++q) s += (q ? ",[" : "[") + std::to_string(sr[q].type) + "," + std::to_string(sr[q].tp) + "]";
+    for (int q = 0; q < hd->P; ++q)
+      s += (q ? ",[" : "[") + std::to_string(sr[q].type) + "," + std::to_string(sr[q].tp) +
+           (sr[q].type2 >= 0 ? "," + std::to_string(sr[q].type2) : std::string()) + "]";
     s += "],\"layers\":[";
     {
       u32 dig = (u32)(i - tp.prefix);
@@ -1044,7 +1136,9 @@ int hsim_decode(const hsim_handle* h, int64_t i, char* json, size_t cap) {
       const auto pl = h->place(hd->D, stages);
       for (int r = 0; r < hd->D; ++r) {
         s += r ? ",[" : "[";
-        for (int q = 0; q < hd->P; ++q) s += (q ? ",[" : "[") + std::to_string(pl[r][q].first) + "," + std::to_string(pl[r][q].second) + "]";
+        for (int q = 0; q < hd->P; ++q)
+          s += (q ? ",[" : "[") + std::to_string(pl[r][q].node) + "," + std::to_string(pl[r][q].base) +
+               (pl[r][q].node2 >= 0 ? "," + std::to_string(pl[r][q].node2) : std::string()) + "]";
         s += "]";
       }
     } catch (const Fail& f) {
@@ -1114,7 +1208,7 @@ int hsim_flow_resim(hsim_handle* h, const int64_t* idx, int32_t k, int64_t* out,
     return HSIM_EINVAL;
   }
   if ((i64)h->md.layers > 256) { g_err = "InvalidValue: flow re-simulation supports up to 256 layers"; return HSIM_EINVAL; }
-  if (h->ilv > 1 || h->md.ep_dp) { g_err = "InvalidValue: flow re-simulation is defined for the default schedule only (no interleave / ep_dp)"; return HSIM_EINVAL; }
+  if (h->ilv > 1 || h->md.ep_dp || h->md.mixtp) { g_err = "InvalidValue: flow re-simulation is defined for the default schedule only (no interleave / ep_dp / mixtp)"; return HSIM_EINVAL; }
   if (k == 0) return HSIM_OK;
   int rc = h->ensure_device();
   if (rc) return rc;

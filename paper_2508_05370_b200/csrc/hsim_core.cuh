@@ -60,7 +60,8 @@ struct StageRec {
   u64 dp_mask[4];         // link classes of intra-class DP ring edges, rings q < 2^k (C.6)
   int32_t type, tp, l0, lg_tp;          // device type, TP, base layer split, log2(tp)
   int32_t first_node, first_base, last_node, last_base;  // replica 0 / replica D-1 group
-  int32_t _pad[2];
+  int32_t type2;          // V.1 mixed TP group: its second device type (-1: homogeneous)
+  int32_t _pad;
 };
 static_assert(sizeof(StageRec) == 128, "StageRec layout");
 
@@ -93,7 +94,8 @@ struct TplRec {
   int32_t b, M, C, D;     // micro-batch size, #micro-batches, classes, total replicas
   int32_t crec[MAXC];     // int64-offsets of the class records in the pool
   uint32_t pmask;         // bit min(P, 31) set for every class depth P (V.2: P >= 2 -> bit 0)
-  int32_t flags;          // bit 0: V.3 expert parallelism across the replicas (dense-only gradient sync)
+  int32_t flags;          // bit 0: V.3 expert parallelism across the replicas (dense-only gradient sync);
+                          // bit 1: V.1 mixed TP groups (the DP ring's wrap edge is in dp_mask)
   double rD;              // 1.0 / D (ring chunk: ceil division by D with exact fix-up)
 };
 
@@ -788,6 +790,7 @@ HD i64 seg_cost_c(const Tables& T, const TplRec& tp, const StageRec* const (&st)
     const StageRec& s = st[c][sc[c]];
     if (s.tp != tstar) rsmask |= s.tp_mask;  // reshard over this group's TP ring (A14)
     mask |= s.dp_mask[lg];
+    if (tp.flags & 2) continue;  // V.1: single class, the wrap edge is in dp_mask
     // edge from the last replica of class c to the first replica of the next
     // class (wrap: class C-1 -> class 0), ring q through device base + q
     const StageRec& t = st[c + 1 < C ? c + 1 : 0][sc[c + 1 < C ? c + 1 : 0]];

@@ -163,3 +163,37 @@ def test_variant_validation(L):
         with pytest.raises(hsim.HsimError) as e:
             hsim.Sim(cfg, host_only=True)
         assert e.value.code == hsim.HSIM_EINVAL
+
+
+@pytest.mark.parametrize("n", [2, 4, 5])
+def test_host_decode_mixtp_matches_oracle(oracle_mod, L, n):
+    """V.1: the MIXTP family's size, order, placement (two nodes
+    per group), layer and micro-batch splits agree with the oracle."""
+    cfg = H.with_changes(H.get(n), search__mixtp=1)
+    s = hsim.Sim(cfg, host_only=True)
+    o = oracle_mod.Oracle(cfg)
+    base = oracle_mod.Oracle(H.get(n)).space_size()
+    assert s.space_size() == o.space_size() > base
+    idx = np.unique(np.concatenate([H.sample_indices(s.space_size(), 100, seed=3),
+                                    [s.template_first(k) for k in range(s.n_templates() - 40, s.n_templates())]]))
+    mixed = 0
+    for i in idx:
+        a, b = s.decode(int(i)), o.describe(int(i))
+        assert a["status"] == b["status"], (i, a, b)
+        for ca, cb in zip(a["classes"], b["classes"]):
+            assert ca["stages"] == cb["stages"] and ca["place"] == cb["place"], (i, ca, cb)
+            mixed += len(ca["stages"][0]) == 3
+            if b["status"] != -1:
+                assert ca["layers"] == cb["layers"], (i, ca, cb)
+            if b["status"] == 0:
+                assert ca["mb"] == cb["mb"], (i, ca, cb)
+    assert mixed > 0
+
+
+def test_mixtp_validation(L):
+    for cfg in (H.with_mem_check(H.with_changes(H.get(2), search__mixtp=1)),
+                H.with_ep_dp(H.with_changes(H.get(4), search__mixtp=1)),
+                H.with_changes(H.get(2), search__mixtp=2)):
+        with pytest.raises(hsim.HsimError) as e:
+            hsim.Sim(cfg, host_only=True)
+        assert e.value.code == hsim.HSIM_EINVAL

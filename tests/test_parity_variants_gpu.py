@@ -129,3 +129,47 @@ def test_variant_rejections(torch_cuda):
     sim = Sim(H.with_interleave(H.get(2), 2))
     with pytest.raises(Exception):
         sim.flow_resim(torch.tensor([0], device="cuda"))
+
+
+# ----------------------------------------------------------------------------
+# V.1 mixed-type TP groups (the MIXTP family)
+# ----------------------------------------------------------------------------
+def mixtp_range(cfg, oracle_mod):
+    """Every candidate of the MIXTP family (appended after each micro-batch
+    size's MIXED templates: compared over the whole space's MIXTP templates)."""
+    from paper_2508_05370_b200 import Sim
+    sim, o = Sim(cfg), oracle_mod.Oracle(cfg, compact=True)
+    pre = o.template_prefix()
+    idx = []
+    for k in range(o.n_templates()):
+        st = o.describe(int(pre[k]))["classes"][0]["stages"][0]
+        if len(st) == 3:
+            idx.append(np.arange(pre[k], pre[k + 1]))
+    idx = np.concatenate(idx)
+    import torch
+    got = sim.eval_batch(idx=torch.as_tensor(idx, device="cuda")).cpu().numpy()
+    want = o.eval_many(idx, threads=THREADS)
+    assert_equal(idx, got, want)
+    return want
+
+
+@pytest.mark.parametrize("n", [2, 3, 4, 5])
+def test_mixtp_family_full(torch_cuda, oracle_mod, n):
+    want = mixtp_range(H.with_changes(H.get(n), search__mixtp=1), oracle_mod)
+    assert (want >= 0).sum() > 10
+
+
+@pytest.mark.parametrize("mode", ["interleave", "overlap"])
+def test_mixtp_with_schedule_variants(torch_cuda, oracle_mod, mode):
+    cfg = H.with_changes(H.get(2), search__mixtp=1)
+    cfg = H.with_interleave(cfg, 2) if mode == "interleave" else H.with_sync_overlap(cfg)
+    mixtp_range(cfg, oracle_mod)
+
+
+@pytest.mark.parametrize("seed", [101, 105, 110])
+def test_mixtp_tiny_full(torch_cuda, oracle_mod, seed):
+    full_space(H.with_changes(H.variant_tiny(seed), search__mixtp=1), oracle_mod)
+
+
+def test_mixtp_config2_topk(torch_cuda, oracle_mod):
+    full_space(H.with_changes(H.get(2), search__mixtp=1), oracle_mod, compact=True, topk=16)
