@@ -96,6 +96,7 @@ struct orc_input {
   int32_t interleave;    // v model chunks per stage, interleaved 1F1B (DESIGN V.2); 1 = off
   int32_t ep_dp;         // expert parallelism across the DP replicas (DESIGN V.3)
   int32_t mixtp;         // mixed-type TP groups, the MIXTP family (DESIGN V.1)
+  int32_t sync_buckets;  // 2 = two gradient buckets per stage group (DESIGN B.1); 0/1 = one
 };
 }
 
@@ -737,6 +738,7 @@ struct Oracle {
     std::vector<i64> f, g;     // per chunk: forward / backward duration
     i64 c_prev, c_next;        // c_prev: boundary s-1 -> s, c_next: s -> s+1
     i64 c_wrap = 0;            // V.2: stage P-1 -> stage 0 (next chunk) and back
+    i64 lowb = 0;              // B.1: backward work of the lower bucket (its last ceil(l/2) layers + embedding)
     std::vector<Op> ops;
     size_t next = 0;
     bool busy = false;
@@ -869,7 +871,12 @@ struct Oracle {
     i64 a, z, S, RS, AR;
     int tstar;
     std::vector<int> sc;  // stage of every class holding layers [a, z)
+    std::vector<int> bk;  // B.1: bucket of that stage holding them (0 lower, 1 upper)
   };
+  // B.1 (DESIGN): with two buckets a stage's l layers split into the lower
+  // ceil(l/2) (+ the embedding on stage 0) and the upper rest (+ the head)
+  bool two_buckets() const { return in.sync_buckets == 2; }
+  static i64 lower_half(i64 l) { return (l + 1) / 2; }
   std::vector<Seg> segments(const Plan& p, bool compact) const {
     const auto& cls = p.tpl->cls;
     const int C = (int)cls.size();
@@ -886,7 +893,9 @@ struct Oracle {
         for (int s = 0; s < P; ++s) {
           start[c].push_back({a, s});
           cuts.push_back(a);
-          a += chunk_layers(p.layers[c][s], v, k);
+          const i64 l = chunk_layers(p.layers[c][s], v, k);
+          if (two_buckets() && lower_half(l) < l) cuts.push_back(a + lower_half(l));  // B.1
+          a += l;
         }
     }
     std::sort(cuts.begin(), cuts.end());
@@ -906,11 +915,13 @@ struct Oracle {
       if (sg.z == in.L) sg.S += (in.V * in.h * (in.tied ? 0 : 1) + in.h) * in.bpe_grad;
       sg.sc.assign(C, 0);
       sg.tstar = 1 << 30;
+      sg.bk.assign(C, 0);
       for (int c = 0; c < C; ++c) {
         size_t x = 0;
         while (x + 1 < start[c].size() && start[c][x + 1].first <= sg.a) ++x;
         const int s = start[c][x].second;
         sg.sc[c] = s;
+        sg.bk[c] = two_buckets() && sg.a >= start[c][x].first + lower_half(p.layers[c][s]) ? 1 : 0;
         sg.tstar = std::min(sg.tstar, cls[c].st[s].tp);
       }
       // reshard (A14): every group with tp != t* re-lays S into t* shards over its ring
@@ -1037,13 +1048,17 @@ struct Oracle {
             if (compact) {
               g.f[k] = lk * layer_chain(ss, gr, b, 0, true, eg);
               g.g[k] = lk * layer_chain(ss, gr, b, 1, true, eg);
+              g.lowb = lower_half(lk) * layer_chain(ss, gr, b, 1, true, eg);
             } else {
               for (i64 l = 0; l < lk; ++l) {
                 g.f[k] += layer_chain(ss, gr, b, 0, false, eg);
-                g.g[k] += layer_chain(ss, gr, b, 1, false, eg);
+                const i64 gb = layer_chain(ss, gr, b, 1, false, eg);
+                g.g[k] += gb;
+                if (l < lower_half(lk)) g.lowb += gb;
               }
             }
           }
+          if (s == 0) g.lowb += sdur(ss, EMB, true, b);
           // the embedding runs with the first chunk of stage 0, the head with the
           // last chunk of stage P-1
           if (s == 0) { g.f[0] += sdur(ss, EMB, false, b); g.g[0] += sdur(ss, EMB, true, b); }
@@ -1071,15 +1086,21 @@ struct Oracle {
     i64 Titer = T0;
     for (int c = 0; c < C; ++c)
       freet[c].assign(compact ? 1 : cls[c].D, std::vector<i64>(cls[c].st.size(), in.sync_overlap ? 0 : T0));
-    auto ready = [&](int c, int r, int s) -> i64 {  // S.1: end of the group's last backward
-      return in.sync_overlap ? G[owner[c][r] + s].done : 0;
+    // S.1: a bucket is ready when its gradients are: the lower one at the end
+    // of the group's last backward, the upper one (B.1) that much earlier than
+    // the lower bucket's share of that backward (the backward runs head, layers
+    // top-down, embedding)
+    auto ready = [&](int c, int r, int s, int bk) -> i64 {
+      if (!in.sync_overlap) return 0;
+      const SimGroup& g = G[owner[c][r] + s];
+      return bk ? g.done - g.lowb : g.done;
     };
     auto run_seg = [&](int j) {
       i64 st = 0;
       for (int c = 0; c < C; ++c)
         for (int r = 0; r < cls[c].D; ++r) {
           const int s = sg[j].sc[c];
-          st = std::max(st, std::max(ready(c, r, s), freet[c][compact ? 0 : r][s]));
+          st = std::max(st, std::max(ready(c, r, s, sg[j].bk[c]), freet[c][compact ? 0 : r][s]));
         }
       const i64 en = st + sg[j].RS + sg[j].AR;
       for (int c = 0; c < C; ++c)
@@ -1423,6 +1444,10 @@ void* orc_create(const orc_input* in) {
   }
   if (in->mem_check && (in->interleave > 1 || in->ep_dp || in->mixtp)) {
     g_err = "mem_check is not defined with interleave / ep_dp / mixtp (DESIGN V.1-V.3)";
+    return nullptr;
+  }
+  if (in->sync_buckets < 0 || in->sync_buckets > 2 || (in->sync_buckets == 2 && in->interleave > 1)) {
+    g_err = "sync_buckets must be 0..2 and is not defined with interleave (DESIGN B.1)";
     return nullptr;
   }
   if (in->ep_dp && in->mixtp) {

@@ -63,7 +63,8 @@ class _Input(C.Structure):
                 ("homo", C.c_int32), ("mixed", C.c_int32), ("use_all", C.c_int32),
                 ("r_layer", C.c_int32), ("pmax", C.c_int32), ("r_batch", C.c_int32),
                 ("mem_check", C.c_int32), ("sync_overlap", C.c_int32),
-                ("interleave", C.c_int32), ("ep_dp", C.c_int32), ("mixtp", C.c_int32)]
+                ("interleave", C.c_int32), ("ep_dp", C.c_int32), ("mixtp", C.c_int32),
+                ("sync_buckets", C.c_int32)]
 
 
 def _path(hops):
@@ -195,6 +196,7 @@ class Oracle:
         I.interleave = int(se.get("interleave", 1))
         I.ep_dp = int(se.get("ep_dp", 0))
         I.mixtp = int(se.get("mixtp", 0))
+        I.sync_buckets = int(se.get("sync_buckets", 1))
         self._in = I
         self.h = lib().orc_create(C.byref(I))
         if not self.h:

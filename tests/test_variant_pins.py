@@ -293,8 +293,10 @@ def py_eval_v(o, cfg, i, overlap=False):
     A = act_bytes(cfg, b)
     moe = m_["E"] > 1
     ep = bool(se.get("ep_dp", 0)) and moe and len(d["classes"]) == 1
-    T0, lastB = 0, {}
+    T0, lastB, lowb = 0, {}, {}
+    two = se.get("sync_buckets", 1) == 2  # B.1: lower ceil(l/2) layers (+ embedding) and the rest
     vstarts = []  # per class: [(first layer, stage)] in layer order
+    bcut = []     # per class: {stage: first layer of its upper bucket}
     for c, cl in enumerate(d["classes"]):
         P, D = len(cl["stages"]), cl["D"]
         v = vset if P >= 2 else 1
@@ -305,6 +307,7 @@ def py_eval_v(o, cfg, i, overlap=False):
                 st.append((acc, s))
                 acc += lay[s][k]
         vstarts.append(st)
+        bcut.append({s0: a0 + (cl["layers"][s0] + 1) // 2 for a0, s0 in st} if two else {})
 
         def p2p(r, s1, s2):
             t1, t2 = cl["stages"][s1][1], cl["stages"][s2][1]
@@ -352,6 +355,9 @@ def py_eval_v(o, cfg, i, overlap=False):
                     gs[v - 1] += op_max(o, stage, "head", 1, b)
                 f.append(fs)
                 g.append(gs)
+                # the last backward runs head, layers top-down, embedding: the
+                # lower bucket's gradients take its last ceil(l/2) layers + emb
+                lowb[(c, r, s)] = (cl["layers"][s] + 1) // 2 * ch[1] + (op_max(o, stage, "emb", 1, b) if s == 0 else 0)
             T, last = ilv_dag(f, g, cc[r], cw[r], mb[r])
             T0 = max(T0, T)
             for s in range(P):
@@ -359,10 +365,12 @@ def py_eval_v(o, cfg, i, overlap=False):
     D = sum(cl["D"] for cl in d["classes"])
     if D == 1:
         return T0
-    cuts = sorted(set([0, m_["L"]] + [a for st in vstarts for a, _ in st]))
+    cuts = sorted(set([0, m_["L"]] + [a for st in vstarts for a, _ in st] +
+                      [x for bc in bcut for x in bc.values() if 0 < x < m_["L"]]))
     segs = []
     for a, z in zip(cuts, cuts[1:]):
         sc = [max(st, key=lambda x: (x[0] <= a, x[0]))[1] for st in vstarts]
+        bk = [1 if two and a >= bcut[c][sc[c]] else 0 for c in range(len(sc))]
         tps = [cl["stages"][sc[c]][1] for c, cl in enumerate(d["classes"])]
         tstar = min(tps)
         S = seg_bytes_v(cfg, a, z, ep)
@@ -376,14 +384,14 @@ def py_eval_v(o, cfg, i, overlap=False):
         chunk = cdiv(cdiv(S, tstar), D)
         slow = max(tau(glink(o, u[0], u[1], q, w[0], w[1], q), chunk)
                    for q in range(tstar) for u, w in zip(ring, ring[1:] + ring[:1]))
-        segs.append((sc, RS + 2 * (D - 1) * slow))
+        segs.append((sc, RS + 2 * (D - 1) * slow, bk))
     free = {}
     T = T0
     for j in (range(len(segs) - 1, -1, -1) if overlap else range(len(segs))):
-        sc, cost = segs[j]
+        sc, cost, bk = segs[j]
         groups = [(c, r, sc[c]) for c, cl in enumerate(d["classes"]) for r in range(cl["D"])]
         if overlap:
-            start = max(max(lastB[x], free.get(x, 0)) for x in groups)
+            start = max(max(lastB[x] - (lowb[x] if bk[x[0]] else 0), free.get(x, 0)) for x in groups)
         else:
             start = max(free.get(x, T0) for x in groups)
         for x in groups:
@@ -624,3 +632,63 @@ def test_mixtp_literal_equals_compact(oracle_mod):
     base = oracle_mod.Oracle(H.get(2)).space_size()
     idx = np.arange(base, lit.space_size())
     assert np.array_equal(lit.eval_many(idx, threads=THREADS), cmp_.eval_many(idx, threads=THREADS))
+
+
+# ----------------------------------------------------------------------------
+# B.1 two gradient buckets per stage group (Table 1 "DP frequency 2")
+# ----------------------------------------------------------------------------
+def with_buckets(cfg):
+    return H.with_changes(cfg, search__sync_buckets=2)
+
+
+@pytest.mark.parametrize("cfgf,overlap", [("c2", False), ("c2", True), ("c4", True), ("tiny105", True),
+                                          ("tiny110", False), ("c2-mixtp", True), ("c4-ep", True)])
+def test_py_eval_buckets(oracle_mod, cfgf, overlap):
+    cfg = {"c2": lambda: H.get(2), "c4": lambda: H.get(4), "tiny105": lambda: H.variant_tiny(105),
+           "tiny110": lambda: H.variant_tiny(110), "c2-mixtp": lambda: with_mixtp(H.get(2)),
+           "c4-ep": lambda: H.with_ep_dp(H.get(4))}[cfgf]()
+    cfg = with_buckets(H.with_sync_overlap(cfg) if overlap else cfg)
+    o = oracle_mod.Oracle(cfg)
+    N = o.space_size()
+    idx = np.arange(N) if N <= 300 else H.sample_indices(N, 250, seed=29)
+    want = o.eval_many(idx, threads=THREADS)
+    for k, i in enumerate(idx):
+        assert py_eval_v(o, cfg, int(i), overlap=overlap) == want[k], int(i)
+    assert (want >= 0).sum() >= 10
+
+
+def test_buckets_table1_frequency_two(oracle_mod):
+    """Table 1: DP frequency 2 per iteration.  A single-class
+    candidate whose stages hold >= 2 layers each all-reduces every stage
+    group's gradient in exactly 2 collectives (segments), and the segment
+    bytes of a stage add up to its one-bucket segment."""
+    cfg = H.get(2)
+    o1, o2 = oracle_mod.Oracle(cfg), oracle_mod.Oracle(with_buckets(cfg))
+    pre = o1.template_prefix()
+    seen = 0
+    for k in range(0, o1.n_templates(), 37):
+        i = int(pre[k])
+        d = o1.describe(i)
+        if d["status"] or len(d["classes"]) != 1 or d["classes"][0]["D"] < 2 or min(d["classes"][0]["layers"]) < 2:
+            continue
+        s1, s2 = o1.segments(i), o2.segments(i)
+        assert len(s2) == 2 * len(s1)
+        for j, sg in enumerate(s1):
+            lo, hi = s2[2 * j], s2[2 * j + 1]
+            assert (lo["a"], hi["z"]) == (sg["a"], sg["z"]) and lo["z"] == hi["a"] == sg["a"] + (sg["z"] - sg["a"] + 1) // 2
+            assert lo["S"] + hi["S"] == sg["S"]
+        seen += 1
+    assert seen > 5
+
+
+def test_buckets_d1_and_p1_invariants(oracle_mod):
+    """One replica: no sync, buckets change nothing.  C.8 with one stage of one
+    layer: a single bucket, unchanged."""
+    cfg = H.variant_tiny(105)
+    o1, o2 = oracle_mod.Oracle(cfg), oracle_mod.Oracle(with_buckets(cfg))
+    idx = np.arange(o1.space_size())
+    a, b = o1.eval_many(idx, threads=THREADS), o2.eval_many(idx, threads=THREADS)
+    for k, i in enumerate(idx):
+        d = o1.describe(int(i))
+        if d["status"] == 0 and sum(c["D"] for c in d["classes"]) == 1:
+            assert a[k] == b[k]
