@@ -160,6 +160,13 @@ typedef struct {
   int32_t interleave;
   int32_t ep_dp;
   int32_t mixtp;
+  /* gradient buckets per stage group (DESIGN.md B.1;
+   * Table 1's "DP frequency 2"): 0 or 1 = one (the segments of
+   * C.6), 2 = a stage's l layers sync as two buckets, the lower ceil(l/2) (+ the
+   * embedding) and the upper rest (+ the head); with sync_overlap the upper
+   * bucket is ready once the last backward has passed it (the backward runs
+   * head, layers top-down, embedding).  Not with interleave (HSIM_EINVAL). */
+  int32_t sync_buckets;
 } hsim_model_desc;
 
 /* Which candidates the t-th work item (t = 0..n-1) evaluates. */

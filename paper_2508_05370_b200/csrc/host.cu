@@ -249,6 +249,8 @@ void hsim_handle::validate() {
   if (m.mem_check && (m.interleave > 1 || m.ep_dp || m.mixtp))
     fail(HSIM_EINVAL, "InvalidValue: mem_check is not defined with interleave / ep_dp / mixtp (DESIGN.md V.1-V.3)");
   if (m.ep_dp && m.mixtp) fail(HSIM_EINVAL, "InvalidValue: ep_dp is not defined with mixtp (DESIGN.md V.1)");
+  if (m.sync_buckets < 0 || m.sync_buckets > 2 || (m.sync_buckets == 2 && m.interleave > 1))
+    fail(HSIM_EINVAL, "InvalidValue: sync_buckets must be 0..2 and 2 is not defined with interleave (DESIGN.md B.1)");
 }
 
 void hsim_handle::derive_links() {
@@ -535,7 +537,7 @@ int32_t hsim_handle::crec(int bi, int M, int D, const std::vector<std::pair<int,
       r.layer_b = d.attn_b + d.ar + d.mlp_b + d.ar;
     }
     r.tcomp = d.attn_f + mlp_f + d.attn_b + mlp_b;
-    if (s == 0) { r.fext += d.emb_f; r.gext += d.emb_b; r.wext += d.emb_f + d.emb_b; }
+    if (s == 0) { r.fext += d.emb_f; r.gext += d.emb_b; r.wext += d.emb_f + d.emb_b; r.emb_b = d.emb_b; }
     if (s == P - 1) { r.fext += d.head_f; r.gext += d.head_b; r.wext += d.head_f + d.head_b; }
     if (t2 >= 0) {
       for (int q = 0; q < tp; ++q) r.tp_mask |= (u64)1 << lc(dlink(pl[0][s], tp, q, pl[0][s], tp, (q + 1) % tp));
@@ -558,8 +560,8 @@ int32_t hsim_handle::crec(int bi, int M, int D, const std::vector<std::pair<int,
     for (i64 k = 0; k < md.layers - given; ++k) sr[ord[k]].l0 += 1;
   }
   for (int s = 0; s < P; ++s) {
-    sr[s].first_node = pl[0][s].node; sr[s].first_base = pl[0][s].base;
-    sr[s].last_node = pl[D - 1][s].node; sr[s].last_base = pl[D - 1][s].base;
+    sr[s].first_node = (int16_t)pl[0][s].node; sr[s].first_base = (int16_t)pl[0][s].base;
+    sr[s].last_node = (int16_t)pl[D - 1][s].node; sr[s].last_base = (int16_t)pl[D - 1][s].base;
     const int tp = sr[s].tp;
     // V.1 (single-class MIXTP templates, TplRec flag 2): the ring's wrap edge
     // D-1 -> 0 is folded in here too (the kernels' cross-class term assumes
@@ -792,6 +794,7 @@ void hsim_handle::prepare() {
   hT.mem_check = md.mem_check ? 1 : 0;
   hT.sync_overlap = md.sync_overlap ? 1 : 0;
   hT.interleave = ilv;
+  hT.buckets = md.sync_buckets == 2 ? 2 : 1;
   hT.ep_dp = md.ep_dp;
   hT.seg_layer_dense = (h * (2 * h + 2 * hkv) + (E > 1 ? h * E : 0) + 2 * h) * md.bpe_grad;  // V.3
   if (md.sync_overlap && md.layers > 32767) fail(HSIM_ERANGE, "sync_overlap needs layers < 2^15");
@@ -1208,7 +1211,7 @@ int hsim_flow_resim(hsim_handle* h, const int64_t* idx, int32_t k, int64_t* out,
     return HSIM_EINVAL;
   }
   if ((i64)h->md.layers > 256) { g_err = "InvalidValue: flow re-simulation supports up to 256 layers"; return HSIM_EINVAL; }
-  if (h->ilv > 1 || h->md.ep_dp || h->md.mixtp) { g_err = "InvalidValue: flow re-simulation is defined for the default schedule only (no interleave / ep_dp / mixtp)"; return HSIM_EINVAL; }
+  if (h->ilv > 1 || h->md.ep_dp || h->md.mixtp || h->md.sync_buckets == 2) { g_err = "InvalidValue: flow re-simulation is defined for the default schedule only (no interleave / ep_dp / mixtp)"; return HSIM_EINVAL; }
   if (k == 0) return HSIM_OK;
   int rc = h->ensure_device();
   if (rc) return rc;
@@ -1305,6 +1308,7 @@ int sync_overlap(const hsim_handle* h) { return h->md.sync_overlap; }
 int interleave_v(const hsim_handle* h) { return h->ilv; }
 int ilv_jobs_max(const hsim_handle* h) { return h->ilv_jobs_max; }
 int ilv_depth_max(const hsim_handle* h) { return h->ilv_depth_max; }
+int sync_buckets(const hsim_handle* h) { return h->md.sync_buckets == 2 ? 2 : 1; }
 int ensure_block_scratch(hsim_handle* h, size_t entries, int64_t** out) {
   if (entries > h->blk_cap) {
     cudaFree(h->d_blk);

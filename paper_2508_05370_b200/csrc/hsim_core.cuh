@@ -59,9 +59,10 @@ struct StageRec {
   u64 tp_mask;            // link classes of this stage group's TP ring (reshard, A14)
   u64 dp_mask[4];         // link classes of intra-class DP ring edges, rings q < 2^k (C.6)
   int32_t type, tp, l0, lg_tp;          // device type, TP, base layer split, log2(tp)
-  int32_t first_node, first_base, last_node, last_base;  // replica 0 / replica D-1 group
+  int16_t first_node, first_base, last_node, last_base;  // replica 0 / replica D-1 group
   int32_t type2;          // V.1 mixed TP group: its second device type (-1: homogeneous)
   int32_t _pad;
+  i64 emb_b;              // B.1: embedding backward of stage 0 (0 elsewhere)
 };
 static_assert(sizeof(StageRec) == 128, "StageRec layout");
 
@@ -140,6 +141,7 @@ struct Tables {
   // K[lg] = s h (10 t + 24) (activation bytes per layer = ceil(b K / t))
   int32_t mem_check, sync_overlap;
   int32_t interleave, ep_dp;  // DESIGN.md V.2 (v chunks per stage; 1 = off), V.3
+  int32_t buckets, _pad7;     // DESIGN.md B.1: 2 = two gradient buckets per stage group
   i64 seg_layer_dense;        // V.3: W_layer without the expert matrices, x bpe_grad
   i64 mem_layer[4], mem_emb[4], mem_head[4], mem_K[4];
   i64 mem_cap[MAXT];
@@ -807,10 +809,15 @@ HD i64 seg_cost_c(const Tables& T, const TplRec& tp, const StageRec* const (&st)
 // C.8: segments = common refinement of the classes' layer boundaries, in
 // ascending layer order, list-scheduled FIFO per (class, stage) group from T0:
 // a segment starts when every group it uses is free (all classes take part).
-template <int C>
+// BK (DESIGN.md B.1, Tables.buckets = 2): each stage's l layers are also cut
+// after its lower ceil(l/2) -- two buckets on the same group.
+HD i64 lower_half(i64 l) { return (l + 1) >> 1; }
+template <int C, bool BK = false>
 HD i64 grad_sync_c(const Tables& T, const TplRec& tp, const ClassSplit (&cs)[C], i64 T0) {
   int sc[C], P[C];
   i64 nextcut[C], cur_free[C];
+  i64 sa[C], ls[C];  // BK: start and layers of the current stage
+  int bk[C];         // BK: 0 lower bucket, 1 upper
   LayerWalk lw[C];
   const StageRec* st[C];
 #pragma unroll
@@ -822,6 +829,12 @@ HD i64 grad_sync_c(const Tables& T, const TplRec& tp, const ClassSplit (&cs)[C],
     sc[c] = 0;
     const i64 l0 = lw[c].next(st[c]);
     nextcut[c] = P[c] > 1 ? l0 : T.L;
+    if constexpr (BK) {
+      sa[c] = 0;
+      ls[c] = P[c] > 1 ? l0 : T.L;
+      bk[c] = 0;
+      if (lower_half(ls[c]) < ls[c]) nextcut[c] = lower_half(ls[c]);
+    }
     cur_free[c] = T0;
   }
   i64 a = 0, Titer = T0;
@@ -836,12 +849,25 @@ HD i64 grad_sync_c(const Tables& T, const TplRec& tp, const ClassSplit (&cs)[C],
     const i64 end = start + cost;
     Titer = imax(Titer, end);
 #pragma unroll
-    for (int c = 0; c < C; ++c) {  // advance classes whose stage ends at z
+    for (int c = 0; c < C; ++c) {  // advance classes whose stage (or lower bucket) ends at z
       cur_free[c] = end;
       if (nextcut[c] == z && z < T.L) {
+        if constexpr (BK) {
+          if (bk[c] == 0 && lower_half(ls[c]) < ls[c]) {  // into the upper bucket: same group
+            bk[c] = 1;
+            nextcut[c] = sa[c] + ls[c];
+            continue;
+          }
+        }
         sc[c]++;
         const i64 l = lw[c].next(st[c]);
         nextcut[c] = sc[c] + 1 < P[c] ? nextcut[c] + l : T.L;
+        if constexpr (BK) {
+          sa[c] = z;
+          ls[c] = nextcut[c] - z;
+          bk[c] = 0;
+          if (lower_half(ls[c]) < ls[c]) nextcut[c] = z + lower_half(ls[c]);
+        }
         cur_free[c] = T0;
       }
     }
@@ -855,12 +881,15 @@ HD i64 grad_sync_c(const Tables& T, const TplRec& tp, const ClassSplit (&cs)[C],
 // the class's replicas of that stage's end (written by the 1F1B kernels,
 // row stride rs) -- and segments are issued in descending layer order (the
 // order backward produces gradients), FIFO per group: a class entering a new
-// stage meets a group that has not synchronised yet.
-template <int C>
+// stage meets a group that has not synchronised yet.  BK (B.1): a stage's
+// upper bucket (its top l - ceil(l/2) layers, + the head) is ready earlier by
+// the lower bucket's share of the last backward, ceil(l/2) x layer_b (+ the
+// embedding on stage 0).
+template <int C, bool BK = false>
 HD i64 grad_sync_overlap_c(const Tables& T, const TplRec& tp, const ClassSplit (&cs)[C], const i64* R, i64 rs,
                            i64 T0) {
-  int sc[C], coff[C];
-  int16_t start[C][MAXP];
+  int sc[C], coff[C], bk[C];
+  int16_t start[C][MAXP + 1];
   i64 cur_free[C];
   const StageRec* st[C];
   int off = 0;
@@ -874,18 +903,33 @@ HD i64 grad_sync_overlap_c(const Tables& T, const TplRec& tp, const ClassSplit (
       start[c][s] = (int16_t)a;
       a += lw.next(st[c]);
     }
+    start[c][h->P] = (int16_t)T.L;
     sc[c] = h->P - 1;
     coff[c] = off;
     off += h->P;
     cur_free[c] = 0;
+    bk[c] = 0;
+    if constexpr (BK) {
+      const i64 l = start[c][sc[c] + 1] - start[c][sc[c]];
+      bk[c] = lower_half(l) < l ? 1 : 0;
+    }
   }
   i64 z = T.L, Titer = T0;
   while (z > 0) {
     i64 a = 0, ready = 0, begin = 0;
 #pragma unroll
     for (int c = 0; c < C; ++c) {
-      a = imax(a, (i64)start[c][sc[c]]);
-      ready = imax(ready, R[(i64)(coff[c] + sc[c]) * rs]);
+      const int s = sc[c];
+      i64 lo = start[c][s], rd = R[(i64)(coff[c] + s) * rs];
+      if constexpr (BK) {
+        if (bk[c]) {
+          const i64 l = start[c][s + 1] - start[c][s];
+          lo += lower_half(l);
+          rd -= lower_half(l) * st[c][s].layer_b + (s == 0 ? st[c][s].emb_b : 0);
+        }
+      }
+      a = imax(a, lo);
+      ready = imax(ready, rd);
       begin = imax(begin, cur_free[c]);
     }
     const i64 end = imax(begin, ready) + seg_cost_c<C>(T, tp, st, sc, a, z);
@@ -893,9 +937,20 @@ HD i64 grad_sync_overlap_c(const Tables& T, const TplRec& tp, const ClassSplit (
 #pragma unroll
     for (int c = 0; c < C; ++c) {
       cur_free[c] = end;
+      if constexpr (BK) {
+        if (bk[c]) {
+          const i64 l = start[c][sc[c] + 1] - start[c][sc[c]];
+          if (start[c][sc[c]] + lower_half(l) == a) bk[c] = 0;  // down into the lower bucket: same group
+          continue;
+        }
+      }
       if (a > 0 && start[c][sc[c]] == a) {
         sc[c]--;
         cur_free[c] = 0;
+        if constexpr (BK) {
+          const i64 l = start[c][sc[c] + 1] - start[c][sc[c]];
+          bk[c] = lower_half(l) < l ? 1 : 0;
+        }
       }
     }
     z = a;

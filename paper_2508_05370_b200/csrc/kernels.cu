@@ -47,6 +47,7 @@ int sync_overlap(const hsim_handle* h);
 int interleave_v(const hsim_handle* h);
 int ilv_jobs_max(const hsim_handle* h);
 int ilv_depth_max(const hsim_handle* h);
+int sync_buckets(const hsim_handle* h);
 cudaStream_t side_stream(const hsim_handle* h, int q);
 cudaEvent_t fork_event(const hsim_handle* h);
 cudaEvent_t join_event(const hsim_handle* h, int q);
@@ -951,17 +952,18 @@ __device__ void warp_offer(WarpTopK& w, i64 t, i64 i, bool valid) {
 }
 
 // ---- K_sync / K_final -----------------------------------------------------------------
+template <bool BK>
 __device__ i64 sync_any(const Tables& T, const TplRec& tp, const Scratch& S, i64 t, i64 T0) {
   switch (tp.C) {
-    case 1: { ClassSplit cs[1] = {load_split(S, 0, 1, t)}; return grad_sync_c<1>(T, tp, cs, T0); }
-    case 2: { ClassSplit cs[2] = {load_split(S, 0, 2, t), load_split(S, 1, 2, t)}; return grad_sync_c<2>(T, tp, cs, T0); }
+    case 1: { ClassSplit cs[1] = {load_split(S, 0, 1, t)}; return grad_sync_c<1, BK>(T, tp, cs, T0); }
+    case 2: { ClassSplit cs[2] = {load_split(S, 0, 2, t), load_split(S, 1, 2, t)}; return grad_sync_c<2, BK>(T, tp, cs, T0); }
     case 3: {
       ClassSplit cs[3] = {load_split(S, 0, 3, t), load_split(S, 1, 3, t), load_split(S, 2, 3, t)};
-      return grad_sync_c<3>(T, tp, cs, T0);
+      return grad_sync_c<3, BK>(T, tp, cs, T0);
     }
     default: {
       ClassSplit cs[4] = {load_split(S, 0, 4, t), load_split(S, 1, 4, t), load_split(S, 2, 4, t), load_split(S, 3, 4, t)};
-      return grad_sync_c<4>(T, tp, cs, T0);
+      return grad_sync_c<4, BK>(T, tp, cs, T0);
     }
   }
 }
@@ -970,6 +972,8 @@ __device__ i64 sync_any(const Tables& T, const TplRec& tp, const Scratch& S, i64
 // sharing a group of sum(RS + AR): every segment starts at T0 or when the
 // previous one ends (C.8) -- so the sync runs concurrently with the 1F1B
 // kernels (grad_sync_c with T0 = 0).
+// BK: two gradient buckets per stage group (DESIGN.md B.1)
+template <bool BK>
 __global__ void __launch_bounds__(NT, HSIM_SYNC_MINB) k_sync(const Tables* __restrict__ gT, Scratch S, i64 ns) {
   __shared__ Tables sT;
   load_tables(sT, gT);
@@ -977,31 +981,33 @@ __global__ void __launch_bounds__(NT, HSIM_SYNC_MINB) k_sync(const Tables* __res
     const int tau = S.tau[t];
     if (tau < 0 || S.status[t] != 0) continue;
     const TplRec& tp = sT.tpl[tau];
-    S.extra[t] = tp.D == 1 ? 0 : sync_any(sT, tp, S, t, 0);
+    S.extra[t] = tp.D == 1 ? 0 : sync_any<BK>(sT, tp, S, t, 0);
   }
 }
 
 // S.1 (overlap mode): after the 1F1B kernels; extra = T_iter - T0 with T_iter
 // from the overlapped schedule over the stages' last-backward ends (S.Rs)
+template <bool BK>
 __device__ i64 sync_overlap_any(const Tables& T, const TplRec& tp, const Scratch& S, i64 t, i64 T0) {
   const i64* R = S.Rs + t;
   switch (tp.C) {
-    case 1: { ClassSplit cs[1] = {load_split(S, 0, 1, t)}; return grad_sync_overlap_c<1>(T, tp, cs, R, S.ns, T0); }
+    case 1: { ClassSplit cs[1] = {load_split(S, 0, 1, t)}; return grad_sync_overlap_c<1, BK>(T, tp, cs, R, S.ns, T0); }
     case 2: {
       ClassSplit cs[2] = {load_split(S, 0, 2, t), load_split(S, 1, 2, t)};
-      return grad_sync_overlap_c<2>(T, tp, cs, R, S.ns, T0);
+      return grad_sync_overlap_c<2, BK>(T, tp, cs, R, S.ns, T0);
     }
     case 3: {
       ClassSplit cs[3] = {load_split(S, 0, 3, t), load_split(S, 1, 3, t), load_split(S, 2, 3, t)};
-      return grad_sync_overlap_c<3>(T, tp, cs, R, S.ns, T0);
+      return grad_sync_overlap_c<3, BK>(T, tp, cs, R, S.ns, T0);
     }
     default: {
       ClassSplit cs[4] = {load_split(S, 0, 4, t), load_split(S, 1, 4, t), load_split(S, 2, 4, t), load_split(S, 3, 4, t)};
-      return grad_sync_overlap_c<4>(T, tp, cs, R, S.ns, T0);
+      return grad_sync_overlap_c<4, BK>(T, tp, cs, R, S.ns, T0);
     }
   }
 }
 
+template <bool BK>
 __global__ void __launch_bounds__(NT) k_sync_overlap(const Tables* __restrict__ gT, Scratch S, i64 ns) {
   __shared__ Tables sT;
   load_tables(sT, gT);
@@ -1012,7 +1018,7 @@ __global__ void __launch_bounds__(NT) k_sync_overlap(const Tables* __restrict__ 
     if (tp.D == 1) { S.extra[t] = 0; continue; }
     i64 T0 = 0;
     for (int q = 0; q < tp.C; ++q) T0 = imax(T0, S.Tc[q * S.ns + t]);
-    S.extra[t] = sync_overlap_any(sT, tp, S, t, T0) - T0;
+    S.extra[t] = sync_overlap_any<BK>(sT, tp, S, t, T0) - T0;
   }
 }
 
@@ -1489,6 +1495,7 @@ static int run_phases(hsim_handle* h, const Tables* dT, Cands c, int64_t n, int6
   }
   // V.2: the K_ilv job list
   const bool ilv = interleave_v(h) > 1;
+  const bool bkt = sync_buckets(h) == 2;  // B.1
   const size_t ilvcap = ilv ? (size_t)ilv_jobs_max(h) * ns : 0;
   jobw += ilvcap;
   const size_t planw = hplan ? (size_t)(2 * c.nr + 1) : 0;
@@ -1545,7 +1552,7 @@ static int run_phases(hsim_handle* h, const Tables* dT, Cands c, int64_t n, int6
     cudaEventRecord(plan_ev, st);
     c.plan = pw;
   }
-  const int gs = grid_of(h, k_split<false>, g_split), gd = grid_of(h, k_deep, g_deep), gy = grid_of(h, k_sync, g_sync),
+  const int gs = grid_of(h, k_split<false>, g_split), gd = grid_of(h, k_deep, g_deep), gy = grid_of(h, k_sync<false>, g_sync),
             gf = final_grid(h, k);
   // launch order: longest total work first; the latency-bound deep depths run
   // on high-priority streams (host.cu), which matters more than the order
@@ -1670,13 +1677,15 @@ static int run_phases(hsim_handle* h, const Tables* dT, Cands c, int64_t n, int6
       if (!overlap) join(ss);
     } else if (overlap) {  // S.1: needs the stages' last-backward ends -> after the 1F1B kernels
       tq = g_trace.pre("k_sync_overlap", NSTREAM_FINAL, fin);
-      k_sync_overlap<<<gy, NT, 0, fin>>>(dT, S, nsb);
+      if (bkt) k_sync_overlap<true><<<gy, NT, 0, fin>>>(dT, S, nsb);
+      else k_sync_overlap<false><<<gy, NT, 0, fin>>>(dT, S, nsb);
       g_trace.post(tq, fin);
       ++launches;
     } else {
       cudaStream_t ss = side(18);
       tq = g_trace.pre("k_sync", 18, ss);
-      k_sync<<<gy, NT, 0, ss>>>(dT, S, nsb);
+      if (bkt) k_sync<true><<<gy, NT, 0, ss>>>(dT, S, nsb);
+      else k_sync<false><<<gy, NT, 0, ss>>>(dT, S, nsb);
       g_trace.post(tq, ss);
       ++launches;
       join(ss);

@@ -67,7 +67,8 @@ class hsim_model_desc(C.Structure):
                 ("homo", C.c_int32), ("mixed", C.c_int32), ("use_all", C.c_int32),
                 ("r_layer", C.c_int32), ("pmax_perturb", C.c_int32), ("r_batch", C.c_int32),
                 ("mem_check", C.c_int32), ("sync_overlap", C.c_int32),
-                ("interleave", C.c_int32), ("ep_dp", C.c_int32), ("mixtp", C.c_int32)]
+                ("interleave", C.c_int32), ("ep_dp", C.c_int32), ("mixtp", C.c_int32),
+                ("sync_buckets", C.c_int32)]
 
 
 class hsim_cands(C.Structure):
@@ -170,6 +171,7 @@ def descriptors(cfg):
     m.interleave = int(se.get("interleave", 1))
     m.ep_dp = int(se.get("ep_dp", 0))
     m.mixtp = int(se.get("mixtp", 0))
+    m.sync_buckets = int(se.get("sync_buckets", 1))
     return cd, m, (types, nodes)
 
 

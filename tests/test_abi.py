@@ -197,3 +197,15 @@ def test_mixtp_validation(L):
         with pytest.raises(hsim.HsimError) as e:
             hsim.Sim(cfg, host_only=True)
         assert e.value.code == hsim.HSIM_EINVAL
+
+
+def test_buckets_validation_and_decode(oracle_mod, L):
+    """B.1: sync_buckets outside 0..2 or 2 with interleave are HSIM_EINVAL; the
+    knob leaves the candidate space and the splits unchanged."""
+    for cfg in (H.with_changes(H.get(2), search__sync_buckets=3),
+                H.with_interleave(H.with_changes(H.get(2), search__sync_buckets=2), 2)):
+        with pytest.raises(hsim.HsimError) as e:
+            hsim.Sim(cfg, host_only=True)
+        assert e.value.code == hsim.HSIM_EINVAL
+    s = hsim.Sim(H.with_changes(H.get(4), search__sync_buckets=2), host_only=True)
+    assert s.space_size() == oracle_mod.Oracle(H.get(4)).space_size()

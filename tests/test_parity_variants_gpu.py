@@ -173,3 +173,34 @@ def test_mixtp_tiny_full(torch_cuda, oracle_mod, seed):
 
 def test_mixtp_config2_topk(torch_cuda, oracle_mod):
     full_space(H.with_changes(H.get(2), search__mixtp=1), oracle_mod, compact=True, topk=16)
+
+
+# ----------------------------------------------------------------------------
+# B.1 two gradient buckets per stage group (f1, Table 1 "DP frequency 2")
+# ----------------------------------------------------------------------------
+def with_buckets(cfg):
+    return H.with_changes(cfg, search__sync_buckets=2)
+
+
+@pytest.mark.parametrize("overlap", [False, True])
+def test_buckets_config2_full(torch_cuda, oracle_mod, overlap):
+    cfg = with_buckets(H.with_sync_overlap(H.get(2)) if overlap else H.get(2))
+    want = full_space(cfg, oracle_mod, compact=True, topk=16)
+    assert (want >= 0).sum() > 1000
+
+
+@pytest.mark.parametrize("n,overlap", [(3, True), (4, False), (4, True), (5, True)])
+def test_buckets_configs_sampled(torch_cuda, oracle_mod, n, overlap):
+    cfg = with_buckets(H.with_sync_overlap(H.get(n)) if overlap else H.get(n))
+    sampled(cfg, oracle_mod, 4000, seed=H.PARITY_SEED + 7 * n)
+
+
+@pytest.mark.parametrize("seed", [101, 105, 110])
+def test_buckets_tiny_full(torch_cuda, oracle_mod, seed):
+    full_space(with_buckets(H.with_sync_overlap(H.variant_tiny(seed))), oracle_mod)
+    full_space(with_buckets(H.variant_tiny(seed)), oracle_mod)
+
+
+def test_buckets_with_mixtp_and_ep(torch_cuda, oracle_mod):
+    mixtp_range(with_buckets(H.with_sync_overlap(H.with_changes(H.get(2), search__mixtp=1))), oracle_mod)
+    sampled(with_buckets(H.with_sync_overlap(H.with_ep_dp(H.get(4)))), oracle_mod, 4000, seed=13)
