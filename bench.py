@@ -109,12 +109,14 @@ class Clocks:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def overhead_ops(sim, first, n, blk, stride, world):
+def overhead_ops(sim, first, n, blk, stride, world, sync_units=-1):
     """SURVEY §8(d) per-candidate non-cell work: 50 ops per stage (partition +
     stage sums), 26 per gradient-sync segment (J = sum P_c - C + 1, the most the
     common refinement can have), 100 for the decode -- summed over this rank's
     candidates template by template (host decode of each template's first
-    candidate; outside the timed region)."""
+    candidate; outside the timed region).  sync_units >= 0: the sweep pruned the
+    sync (hsim_last_sync_units: sum of J over the candidates whose sync ran),
+    so only those segments are counted."""
     tot = 0
     nt = sim.n_templates()
     bounds = [sim.template_first(k) for k in range(nt + 1)]
@@ -128,9 +130,9 @@ def overhead_ops(sim, first, n, blk, stride, world):
             d = sim.decode(bounds[k])
             sp = sum(len(c["stages"]) for c in d["classes"])
             J = sp - len(d["classes"]) + 1
-            tot += cnt * (50 * sp + 26 * J + 100)
+            tot += cnt * (50 * sp + (26 * J if sync_units < 0 else 0) + 100)
             k += 1
-    return tot
+    return tot + (26 * sync_units if sync_units >= 0 else 0)
 
 
 def cpu_baseline(cfg, seconds=15.0):
@@ -270,7 +272,8 @@ def run_ours(a):
     sm_max = float(pk.get("sm_max_mhz", 1965.0))
     peak_gops = SMS * LANES_PER_SM * sm_max * 1e6 / 1e9
     my_ms = sum(ms) / a.steps
-    over = overhead_ops(sim, first, n, blk, stride, world)
+    sweep(sim, a.k, out=out)  # (untimed) the sync work the pruned sweep executes
+    over = overhead_ops(sim, first, n, blk, stride, world, sim.last_sync_units())
     ops = OPS_PER_CELL * cells + over
     achieved = ops / (my_ms / 1e3) / 1e9
     traffic, issue = None, None
@@ -318,6 +321,47 @@ def run_ours(a):
                "what": "Sim.eval_host: explicit index list in pinned host memory -> hsim_eval_batch in 2 chunks "
                        "-> int64 results in pinned host memory, H2D / compute / D2H overlapped on streams, every step"}
 
+    # e2e of the sweep call itself: hsim_topk over the range (its inputs are the
+    # descriptors, resident since create, and the range bounds) + the top-k read
+    # back to pinned host memory every step
+    e2e_sweep = None
+    if not a.no_e2e:
+        th = torch.empty(2 * a.k, dtype=torch.int64).pin_memory()
+        for _ in range(3):
+            t_, i_ = sweep(sim, a.k, out=out)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e_steps = max(3, min(a.steps, 50))
+        e0.record(stream)
+        for _ in range(e_steps):
+            t_, i_ = sweep(sim, a.k, out=out)
+            th[:a.k].copy_(t_, non_blocking=True)
+            th[a.k:].copy_(i_, non_blocking=True)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        et = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(et, op=dist.ReduceOp.MAX)
+        e2e_sweep = {"value": round(N * e_steps / (float(et.item()) / 1e3), 1), "unit": "configs/s",
+                     "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 16 * a.k,
+                     "what": "Sim.topk over the whole range (the call `value` times) with the global top-k copied to "
+                             "pinned host memory every step, back to back, no L2 flush"}
+
+    # measured issue peaks (tools/alu_peak.cu microbenchmarks, profiles/r02/alu_peak.json)
+    measured = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "r02", "alu_peak.json")) as f:
+            ap = json.load(f)["kernels"]
+        measured = {"iadd3_imad_mix_Gops": round(ap["mix"]["units_per_s"] / 1e9, 1),
+                    "fp64_maxplus_cell_Gcells": round(ap["dcell"]["units_per_s"] / 1e9, 1),
+                    "frac_of_mix": round(achieved / (ap["mix"]["units_per_s"] / 1e9), 4),
+                    "cells_frac_of_fp64_cell_peak": round(cells / (my_ms / 1e3) / ap["dcell"]["units_per_s"], 4),
+                    "from": "profiles/r02/alu_peak.json (B200, 1965 MHz)"}
+    except (OSError, KeyError, ValueError):
+        measured = None
+
     if rank == 0:
         line = {"metric": METRIC, "value": round(value, 1), "unit": "configs/s", "n_gpus": world, "steps": a.steps,
                 "warmup": a.warmup, "ms_per_step": round(tot_ms / a.steps, 4), "higher_is_better": True,
@@ -329,14 +373,18 @@ def run_ours(a):
                 "roofline": {"bound": "alu", "achieved": round(achieved, 1), "peak": round(peak_gops, 1),
                              "unit": "Gop/s", "frac": round(achieved / peak_gops, 4), "traffic": traffic,
                              "issue_slots": issue, "ops_cells": OPS_PER_CELL * cells, "ops_overhead": over,
-                             "kernel": "one hsim_topk sweep = K_split, K_pipe<P>, K_deep, K_sync (concurrent "
-                                       "fork/join streams), K_final, K_merge; per-kernel shares in profiles/",
+                             "kernel": "one hsim_topk sweep = K_split, K_pipe<P>, K_deep (concurrent fork/join "
+                                       "streams), K_final with the pruned gradient sync, K_merge; per-kernel shares "
+                                       "in profiles/",
                              "ops_per_launch": ops, "cells_per_launch": cells,
-                             "peak_from": f"{SMS} SMs x {LANES_PER_SM} lanes x {sm_max:.0f} MHz (issue slots)"},
+                             "peak_from": f"{SMS} SMs x {LANES_PER_SM} lanes x {sm_max:.0f} MHz (issue slots)",
+                             "measured_peaks": measured},
                 "gpu_launches": launches_per_step * a.steps,
                 "clocks": clk}
         if e2e:
             line["e2e"] = e2e
+        if e2e_sweep:
+            line["e2e_sweep"] = e2e_sweep
         if world == 1 and not a.no_cpu:
             line["cpu_baseline"] = cpu_baseline(cfg)
         print(json.dumps(line), flush=True)

@@ -258,6 +258,15 @@ int32_t hsim_last_launch_count(const hsim_handle* h);
  * (lane compaction) is counted once, by its complete run.  Returns -1 on error. */
 int64_t hsim_count_cells(const hsim_handle* h, int64_t first, int64_t n);
 
+/* Gradient-sync work of the last hsim_topk call on this handle: with k <= 32
+ * and out_ns == NULL the sync runs inside the final kernel, only for candidates
+ * whose pipeline time T0 can still enter the top-k (T >= T0; DESIGN.md §5
+ * "pruned sync"), and this returns the sum over the synced candidates of
+ * their segment bound J = sum_c P_c - C + 1 (the roofline numerator's sync
+ * term in bench.py).  -1 when the last call did not prune (out_ns given, k >
+ * 32, interleave) or on error.  Blocks until the device is idle. */
+int64_t hsim_last_sync_units(const hsim_handle* h);
+
 /* Message of the last failing call on this thread ("" if none). */
 const char* hsim_last_error(void);
 

@@ -136,6 +136,7 @@ struct hsim_handle {
   i64* d_blk = nullptr;
   size_t blk_cap = 0;
   i64* d_cells = nullptr;
+  i64* d_sync_units = nullptr;  // the last top-k call's synced-segment counter (pruned K_final), or nullptr
   void* d_flow = nullptr;     // f3 scratch (flow.cu)
   size_t flow_cap = 0;
   static constexpr int NSIDE = 20, NEV = 48;
@@ -1218,6 +1219,18 @@ int hsim_flow_resim(hsim_handle* h, const int64_t* idx, int32_t k, int64_t* out,
   return launch_flow(h, h->dT, h->hT, idx, k, out, fct, fct_cap, (cudaStream_t)stream);
 }
 
+int64_t hsim_last_sync_units(const hsim_handle* h) {
+  g_err.clear();
+  if (!h) { g_err = "NULL handle"; return -1; }
+  if (!h->d_sync_units || h->ilv > 1) return -1;
+  int64_t v = 0;
+  if (cudaDeviceSynchronize() != cudaSuccess || cudaMemcpy(&v, h->d_sync_units, 8, cudaMemcpyDeviceToHost) != cudaSuccess) {
+    g_err = "cudaMemcpy";
+    return -1;
+  }
+  return v;
+}
+
 int64_t hsim_count_cells(const hsim_handle* h, int64_t first, int64_t n) {
   g_err.clear();
   if (!h || first < 0 || n < 0 || first + n > h->N) { g_err = "index out of range"; return -1; }
@@ -1309,6 +1322,7 @@ int interleave_v(const hsim_handle* h) { return h->ilv; }
 int ilv_jobs_max(const hsim_handle* h) { return h->ilv_jobs_max; }
 int ilv_depth_max(const hsim_handle* h) { return h->ilv_depth_max; }
 int sync_buckets(const hsim_handle* h) { return h->md.sync_buckets == 2 ? 2 : 1; }
+void set_sync_counter(hsim_handle* h, i64* p) { h->d_sync_units = p; }
 int ensure_block_scratch(hsim_handle* h, size_t entries, int64_t** out) {
   if (entries > h->blk_cap) {
     cudaFree(h->d_blk);

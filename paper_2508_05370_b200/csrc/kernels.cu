@@ -48,6 +48,7 @@ int interleave_v(const hsim_handle* h);
 int ilv_jobs_max(const hsim_handle* h);
 int ilv_depth_max(const hsim_handle* h);
 int sync_buckets(const hsim_handle* h);
+void set_sync_counter(hsim_handle* h, i64* p);
 cudaStream_t side_stream(const hsim_handle* h, int q);
 cudaEvent_t fork_event(const hsim_handle* h);
 cudaEvent_t join_event(const hsim_handle* h, int q);
@@ -718,20 +719,34 @@ __device__ __forceinline__ double ilv_dur(double lf, double ext, int l, int v, i
   return (double)(l / v + (k < l % v ? 1 : 0)) * lf + (with_ext ? ext : 0.0);
 }
 
-// dynamic shared memory per warp: ILV_WORDS(PM, Q) doubles (PM = deepest
-// interleaved pipeline, Q = ring length, both from the host)
-#define ILV_WORDS(PM, Q) (2 * (PM) * (Q) + (PM))
-__global__ void __launch_bounds__(NT) k_ilv(const Tables* __restrict__ gT, Scratch S, int count, int PM, int Q) {
+// dynamic shared memory per warp: ILV_WORDS(PM, Q, PJ, v) doubles (PM =
+// deepest interleaved pipeline, Q = ring length, PJ = deepest pipeline with
+// the steady-regime jump and its period history, all from the host)
+#define ILV_WORDS(PM, Q, PJ, V) (2 * (PM) * (Q) + (PM) + (PJ) * 2 * (PJ) * (V))
+// Exact steady-regime jump (the uniform-shift test of DESIGN.md §5 applied to
+// the interleaved schedule): in its steady range [w_s, 2mv - w_s) stage s
+// alternates F / B over the table, which repeats every P v positions (m mod P
+// = 0), so its ops repeat with period L2 = 2 P v.  Each stage compares every
+// steady op with the same op one period earlier (a history of L2 ends); once
+// the last L2 ops of EVERY stage are the previous period's shifted by one
+// common d, every later period is too (the max-plus recurrence is homogeneous
+// and an op's inputs lie within its producer's last period -- the ring lead
+// bound), so the warp skips q whole periods at once: ends, rings and history
+// += q d, positions += q L2 (q keeps the ring slots aligned; every stage stays
+// inside its steady range).
+__global__ void __launch_bounds__(NT) k_ilv(const Tables* __restrict__ gT, Scratch S, int count, int PM, int Q, int PJ) {
   __shared__ Tables sT;
   extern __shared__ double ilv_smem[];
   load_tables(sT, gT);
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  double* rf = ilv_smem + (size_t)wib * ILV_WORDS(PM, Q);  // [PM][Q] forward ends
-  double* rb = rf + PM * Q;                                // [PM][Q] backward ends
-  int* cf = (int*)(rb + PM * Q);                           // [PM] forwards done per stage
-  int* cb = cf + PM;                                       // [PM] backwards done per stage
-  const i64 njobs = (i64)S.counters[CNT_ILV];
   const int v = sT.interleave;
+  double* rf = ilv_smem + (size_t)wib * ILV_WORDS(PM, Q, PJ, v);  // [PM][Q] forward ends
+  double* rb = rf + PM * Q;                                        // [PM][Q] backward ends
+  int* cf = (int*)(rb + PM * Q);                                   // [PM] forwards done per stage
+  int* cb = cf + PM;                                               // [PM] backwards done per stage
+  double* hist = rb + PM * Q + PM;                                 // [PJ][2 PJ v] last period's ends
+  const int HL = 2 * PJ * v;                                       // history row length
+  const i64 njobs = (i64)S.counters[CNT_ILV];
   i64 cells = 0;
   for (;;) {
     i64 item = 0;
@@ -749,7 +764,7 @@ __global__ void __launch_bounds__(NT) k_ilv(const Tables* __restrict__ gT, Scrat
     const int P = h->P, U = h->U;
     const ClassSplit cs = load_split(S, c, tp.C, slot);
     i64* R = S.Rs ? S.Rs + (i64)class_stage_off(sT, tp, c) * S.ns + slot : nullptr;
-    // this lane's stages: layers and per-layer durations
+    // this lane's stages: layers and per-op constants
     int ls[2] = {0, 0};
     {
       LayerWalk lw = walk(sT, h, cs.dig);
@@ -759,15 +774,27 @@ __global__ void __launch_bounds__(NT) k_ilv(const Tables* __restrict__ gT, Scrat
         if (q == lane + 32) ls[1] = l;
       }
     }
+    const int pv = P * v, L2 = 2 * pv;
+    const bool jump = P <= PJ;
+    // ring slots stay aligned when q P v = 0 mod Q: q a multiple of qstep
+    const int qstep = Q >> min(__ffs(pv) - 1, __ffs(Q) - 1);
     double best = 0;
     bool bad = false;
     for (int u = 0; u < U; ++u) {
       const i64* sub = crec_sub(sT, off, P, u);
       const i64 m = mb_of(cs, sub[0]);
-      const i64 n = m * v, pv = (i64)P * v;
+      const i64 n = m * v;
       const double cw = (double)sub[P];
-      int p[2] = {0, 0}, nf[2] = {0, 0}, nb[2] = {0, 0};
-      double X[2] = {0, 0};
+      // per owned stage: op position, table positions done (and their (micro-
+      // batch within group, chunk) digits), clock, warm-up, period bookkeeping
+      i64 p[2] = {0, 0}, nf[2] = {0, 0}, nb[2] = {0, 0}, w[2] = {0, 0};
+      int fj[2] = {0, 0}, fk[2] = {0, 0}, bj[2] = {0, 0}, bk[2] = {0, 0}, hp[2] = {0, 0}, runS[2] = {0, 0};
+      double X[2] = {0, 0}, dS[2] = {-1.0, -1.0};
+#pragma unroll
+      for (int o = 0; o < 2; ++o) {
+        const int s = lane + 32 * o;
+        w[o] = s < P ? imin(2 * (P - 1 - s) + (i64)(v - 1) * P, n) : 0;
+      }
       for (int q = lane; q < P; q += 32) { cf[q] = 0; cb[q] = 0; }
       __syncwarp();
       for (;;) {
@@ -780,11 +807,9 @@ __global__ void __launch_bounds__(NT) k_ilv(const Tables* __restrict__ gT, Scrat
           const int s = lane + 32 * o;
           if (s >= P || p[o] >= 2 * n) continue;
           act = true;
-          const i64 w = imin(2 * (P - 1 - s) + (i64)(v - 1) * P, n);
-          const bool f = p[o] < w || (p[o] < 2 * n - w && !((p[o] - w) & 1));
+          const bool f = p[o] < w[o] || (p[o] < 2 * n - w[o] && !((p[o] - w[o]) & 1));
           const i64 idx = f ? nf[o] : nb[o];
-          const i64 rem = idx % pv, gi = idx / pv;
-          const int k = f ? (int)(rem / P) : v - 1 - (int)(rem / P);
+          const int k = f ? fk[o] : v - 1 - bk[o];
           int ps = -1;
           i64 x = 0;
           double cost = 0;
@@ -795,7 +820,7 @@ __global__ void __launch_bounds__(NT) k_ilv(const Tables* __restrict__ gT, Scrat
           } else {
             if (s < P - 1) { ps = s + 1; x = idx; cost = (double)sub[1 + s]; }
             else if (k < v - 1) { ps = 0; x = idx - P; cost = cw; }
-            else { ps = s; fring = true; x = gi * pv + (i64)(v - 1) * P + rem % P; cost = 0; }
+            else { ps = s; fring = true; x = idx + (i64)(v - 1) * P; cost = 0; }  // its own F(v-1, j)
           }
           double tin = 0;
           if (ps >= 0) {
@@ -804,8 +829,7 @@ __global__ void __launch_bounds__(NT) k_ilv(const Tables* __restrict__ gT, Scrat
             if (have - x > Q) bad = true;
             tin = (fring ? rf : rb)[ps * Q + (int)(x & (Q - 1))] + cost;
           }
-          const bool ext = f ? ((s == 0 && k == 0) || (s == P - 1 && k == v - 1))
-                             : ((s == 0 && k == 0) || (s == P - 1 && k == v - 1));
+          const bool ext = (s == 0 && k == 0) || (s == P - 1 && k == v - 1);
           const double dur = f ? ilv_dur((double)st[s].layer_f, (double)st[s].fext, ls[o], v, k, ext)
                                : ilv_dur((double)st[s].layer_b, (double)st[s].gext, ls[o], v, k, ext);
           ne[o] = fmax(X[o], tin) + dur;
@@ -824,11 +848,65 @@ __global__ void __launch_bounds__(NT) k_ilv(const Tables* __restrict__ gT, Scrat
           if (!run[o]) continue;
           const int s = lane + 32 * o;
           (isF[o] ? rf : rb)[s * Q + (int)(ix[o] & (Q - 1))] = ne[o];
-          if (isF[o]) { cf[s] = ++nf[o]; } else { cb[s] = ++nb[o]; }
+          if (isF[o]) {
+            cf[s] = (int)++nf[o];
+            if (++fj[o] == P) { fj[o] = 0; if (++fk[o] == v) fk[o] = 0; }
+          } else {
+            cb[s] = (int)++nb[o];
+            if (++bj[o] == P) { bj[o] = 0; if (++bk[o] == v) bk[o] = 0; }
+          }
+          if (jump) {  // period history of the steady range
+            const i64 pp = p[o];
+            if (pp >= w[o] && pp < 2 * n - w[o]) {
+              double* hrow = hist + s * HL;
+              if (pp - L2 >= w[o]) {
+                const double d = ne[o] - hrow[hp[o]];
+                if (d == dS[o]) ++runS[o];
+                else { dS[o] = d; runS[o] = 1; }
+              }
+              hrow[hp[o]] = ne[o];
+              if (++hp[o] == L2) hp[o] = 0;
+            } else {
+              runS[o] = 0;
+            }
+          }
           X[o] = ne[o];
           ++p[o];
+          ++cells;
         }
         __syncwarp();
+        if (jump) {
+          const double d0 = __shfl_sync(FULL, dS[0], 0);
+          bool ok = true;
+#pragma unroll
+          for (int o = 0; o < 2; ++o)
+            if (lane + 32 * o < P) ok = ok && runS[o] >= L2 && dS[o] == d0;
+          if (__all_sync(FULL, ok)) {
+            i64 q = INT64_MAX;
+#pragma unroll
+            for (int o = 0; o < 2; ++o)
+              if (lane + 32 * o < P) q = imin(q, (2 * n - w[o] - p[o]) / L2);
+            for (int o2 = 16; o2 > 0; o2 >>= 1) q = imin(q, (i64)__shfl_xor_sync(FULL, (long long)q, o2));
+            q -= q % qstep;
+            if (q > 0) {
+              const double add = (double)q * d0;
+#pragma unroll
+              for (int o = 0; o < 2; ++o) {
+                const int s = lane + 32 * o;
+                if (s >= P) continue;
+                X[o] += add;
+                p[o] += q * L2;
+                nf[o] += q * pv;
+                nb[o] += q * pv;
+                cf[s] = (int)nf[o];
+                cb[s] = (int)nb[o];
+                for (int i = 0; i < Q; ++i) { rf[s * Q + i] += add; rb[s * Q + i] += add; }
+                for (int i = 0; i < L2; ++i) hist[s * HL + i] += add;
+              }
+              __syncwarp();
+            }
+          }
+        }
       }
       // T_pipe = the latest stage end; S.1: every stage's last op (its last backward)
       double mx = fmax(X[0], X[1]);
@@ -839,7 +917,6 @@ __global__ void __launch_bounds__(NT) k_ilv(const Tables* __restrict__ gT, Scrat
           const int s = lane + 32 * o;
           if (s < P) R[s * S.ns] = u == 0 ? (i64)X[o] : imax(R[s * S.ns], (i64)X[o]);
         }
-      cells += lane == 0 ? 2 * (i64)P * n : 0;
       __syncwarp();
     }
     if (__any_sync(FULL, bad)) {
@@ -1080,6 +1157,13 @@ __device__ __forceinline__ i64 slot_T(const Tables& sT, const Cands& c, const Sl
 // k <= 32: each warp keeps its top-k in registers (lane j = j-th entry), warps
 // share a global pruning bound, and each block merges its warps into one list
 // (lists[block], kept across batches) at the end.
+// MODE 0: T = T0 + extra (K_sync / K_sync_overlap ran).  MODE 1 (C.8) / 2
+// (S.1), top-k without out_ns: the gradient sync is computed here, and only
+// for candidates that can still enter the top-k -- T >= T0, so a candidate
+// whose T0 already exceeds the global bound (the k-th best T found so far, an
+// upper bound of the final k-th) or its warp list's k-th key is skipped.  Exact:
+// the skipped never belong to the top-k; the others get their exact T.
+template <int MODE, bool BK>
 __global__ void __launch_bounds__(NT) k_final_small(const Tables* __restrict__ gT, Cands c, Scratch S, i64 ns,
                                                     i64* __restrict__ out, int k, i64* __restrict__ lists) {
   __shared__ Tables sT;
@@ -1090,6 +1174,7 @@ __global__ void __launch_bounds__(NT) k_final_small(const Tables* __restrict__ g
   const i64 nw = (i64)gridDim.x * (NT / 32);
   i64* blist = lists + (i64)blockIdx.x * 2 * k;
   unsigned long long* gthr = (unsigned long long*)(lists + (i64)gridDim.x * 2 * k);
+  unsigned long long nsync = 0;  // MODE >= 1: sum over the synced candidates of J = sum P - C + 1
   RegTopK r;
   r.init();
   if (w == 0 && lane < k && blist[lane] != LIST_PAD && blist[lane] != KEY_INF) { r.t = blist[lane]; r.i = blist[k + lane]; }
@@ -1099,11 +1184,31 @@ __global__ void __launch_bounds__(NT) k_final_small(const Tables* __restrict__ g
     const SlotW cur = nxt;
     if (base + nw * 32 < ns) nxt = slot_load(S, base + nw * 32 + lane);  // next chunk's loads in flight
     i64 t, i;
-    const i64 T = slot_T(sT, c, cur, &t, &i);
-    if (out && t >= 0) out[t] = T;
     const i64 g = (i64)*(volatile unsigned long long*)gthr;
     i64 thT = __shfl_sync(FULL, (long long)r.t, k - 1), thI = __shfl_sync(FULL, (long long)r.i, k - 1);
-    unsigned cand = __ballot_sync(FULL, t >= 0 && T >= 0 && T <= g && key_less(T, i, thT, thI));
+    i64 T;
+    if constexpr (MODE == 0) {
+      T = slot_T(sT, c, cur, &t, &i);
+      if (out && t >= 0) out[t] = T;
+    } else {
+      SlotW z = cur;
+      z.ex = 0;
+      T = slot_T(sT, c, z, &t, &i);  // T0 (or the status)
+      const i64 slot = base + lane;
+      if (t >= 0 && T >= 0 && T <= g && T <= thT) {
+        const TplRec& tp = sT.tpl[cur.tau];
+        if (tp.D > 1) {
+          if constexpr (MODE == 1) T += sync_any<BK>(sT, tp, S, slot, 0);
+          else T = sync_overlap_any<BK>(sT, tp, S, slot, T);
+          int sp = 0;
+          for (int q = 0; q < tp.C; ++q) sp += crec_hdr(sT, tp.crec[q])->P;
+          nsync += (unsigned long long)(sp - tp.C + 1);
+        }
+      } else if (T >= 0) {
+        T = KEY_INF;  // pruned: cannot enter the top-k
+      }
+    }
+    unsigned cand = __ballot_sync(FULL, t >= 0 && T >= 0 && T != KEY_INF && T <= g && key_less(T, i, thT, thI));
     if (!cand) continue;
     if (__popc(cand) > 6) {
       // many candidates (early in the scan): sort them across the warp
@@ -1177,6 +1282,10 @@ __global__ void __launch_bounds__(NT) k_final_small(const Tables* __restrict__ g
       blist[lane] = r.t;
       blist[k + lane] = r.t == KEY_INF ? -1 : r.i;
     }
+  }
+  if constexpr (MODE != 0) {  // the call's synced segment units (hsim_last_sync_units)
+    nsync = warp_sum((i64)nsync);
+    if (lane == 0 && nsync) atomicAdd(gthr + 1, nsync);
   }
 }
 
@@ -1496,6 +1605,14 @@ static int run_phases(hsim_handle* h, const Tables* dT, Cands c, int64_t n, int6
   // V.2: the K_ilv job list
   const bool ilv = interleave_v(h) > 1;
   const bool bkt = sync_buckets(h) == 2;  // B.1
+  // top-k only (no out_ns, k <= 32): the sync is computed in K_final for the
+  // candidates that can still enter the top-k (HSIM_PRUNE=0 disables)
+  static int prune_env = -1;
+  if (prune_env < 0) {
+    const char* e = getenv("HSIM_PRUNE");
+    prune_env = e && e[0] == '0' ? 0 : 1;
+  }
+  const bool prune = prune_env && !ilv && !out_ns && k >= 1 && k <= 32 && !count;
   const size_t ilvcap = ilv ? (size_t)ilv_jobs_max(h) * ns : 0;
   jobw += ilvcap;
   const size_t planw = hplan ? (size_t)(2 * c.nr + 1) : 0;
@@ -1638,10 +1755,13 @@ static int run_phases(hsim_handle* h, const Tables* dT, Cands c, int64_t n, int6
     launch_deep();
 #endif
     if (ilv && ilvcap) {  // V.2: every interleaved pipeline (warp per job, rings in shared memory)
-      const int PM = ilv_depth_max(h);
+      const int PM = ilv_depth_max(h), v = interleave_v(h);
       int Q = 4;
       while (Q < PM / 2 + 2) Q *= 2;
-      const size_t per_warp = (size_t)ILV_WORDS(PM, Q) * 8;
+      // steady-regime jumps for pipelines of up to PJ stages (history 2 PJ^2 v doubles per warp)
+      int PJ = PM < 16 ? PM : 16;
+      while (PJ > 1 && (size_t)2 * PJ * PJ * v * 8 > 32 * 1024) --PJ;
+      const size_t per_warp = (size_t)ILV_WORDS(PM, Q, PJ, v) * 8;
       int W = 4;
       while (W > 1 && W * per_warp > (size_t)200 * 1024) --W;
       const size_t smem = W * per_warp;
@@ -1656,7 +1776,7 @@ static int run_phases(hsim_handle* h, const Tables* dT, Cands c, int64_t n, int6
       if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_ilv, 32 * W, smem) != cudaSuccess || per < 1) per = 1;
       cudaStream_t ss = side(17);
       tq = g_trace.pre("k_ilv", 17, ss);
-      k_ilv<<<sm_count(h) * per, 32 * W, smem, ss>>>(dT, S, count, PM, Q);
+      k_ilv<<<sm_count(h) * per, 32 * W, smem, ss>>>(dT, S, count, PM, Q, PJ);
       g_trace.post(tq, ss);
       ++launches;
       join(ss);
@@ -1668,7 +1788,9 @@ static int run_phases(hsim_handle* h, const Tables* dT, Cands c, int64_t n, int6
       cells += (i64)v;
       continue;
     }
-    if (ilv) {  // V.2: revisited stage groups (C.8 concurrently with K_ilv; S.1 after it)
+    if (prune) {
+      // the sync runs inside K_final, pruned by the top-k bound
+    } else if (ilv) {  // V.2: revisited stage groups (C.8 concurrently with K_ilv; S.1 after it)
       cudaStream_t ss = overlap ? fin : side(18);
       tq = g_trace.pre("k_sync_ilv", 18, ss);
       k_sync_ilv<<<gy, NT, 0, ss>>>(dT, S, nsb, overlap ? 1 : 0);
@@ -1691,7 +1813,15 @@ static int run_phases(hsim_handle* h, const Tables* dT, Cands c, int64_t n, int6
       join(ss);
     }
     tq = g_trace.pre("k_final", NSTREAM_FINAL, fin);
-    if (k && k <= 32) k_final_small<<<gf, NT, 0, fin>>>(dT, c, S, nsb, out_ns, k, lists);
+    if (prune) {
+      if (overlap) {
+        if (bkt) k_final_small<2, true><<<gf, NT, 0, fin>>>(dT, c, S, nsb, out_ns, k, lists);
+        else k_final_small<2, false><<<gf, NT, 0, fin>>>(dT, c, S, nsb, out_ns, k, lists);
+      } else {
+        if (bkt) k_final_small<1, true><<<gf, NT, 0, fin>>>(dT, c, S, nsb, out_ns, k, lists);
+        else k_final_small<1, false><<<gf, NT, 0, fin>>>(dT, c, S, nsb, out_ns, k, lists);
+      }
+    } else if (k && k <= 32) k_final_small<0, false><<<gf, NT, 0, fin>>>(dT, c, S, nsb, out_ns, k, lists);
     else k_final<<<gf, NT, 0, fin>>>(dT, c, S, nsb, out_ns, k, lists);
     g_trace.post(tq, fin);
     ++launches;
@@ -1745,8 +1875,11 @@ int launch_eval(hsim_handle* h, const Tables* dT, const hsim_cands* cc, int64_t 
   call_begin(h, st);
   const int nlists = final_grid(h, k) * (k <= 32 ? 1 : NT / 32);  // per block (k <= 32) or per warp
   if (k) {
-    if (ensure_block_scratch(h, (size_t)nlists * 2 * k + 1, &lists)) return HSIM_ENOMEM;
-    cudaMemsetAsync(lists, 0x7F, ((size_t)nlists * 2 * k + 1) * 8, st);  // lists + global bound word
+    // lists + the global bound word + the synced-segment counter
+    if (ensure_block_scratch(h, (size_t)nlists * 2 * k + 2, &lists)) return HSIM_ENOMEM;
+    cudaMemsetAsync(lists, 0x7F, ((size_t)nlists * 2 * k + 1) * 8, st);
+    cudaMemsetAsync(lists + (size_t)nlists * 2 * k + 1, 0, 8, st);
+    set_sync_counter(h, k <= 32 && !out_ns ? lists + (size_t)nlists * 2 * k + 1 : nullptr);
   }
   g_trace.begin(st);
   if (n > 0) {

@@ -144,8 +144,10 @@ def test_launch_count_is_native(torch_cuda, oracle_mod):
     sim.eval_batch(n=1000)
     n_eval = sim.last_launch_count()         # K_split + K_pipe<P> per depth + K_deep + K_sync
     assert n_eval >= 3
-    sim.topk(8, n=1000)
+    sim.topk(8, n=1000, out_ns=torch_cuda.empty(1000, dtype=torch_cuda.int64, device="cuda"))
     assert sim.last_launch_count() == n_eval + 1      # + K_merge
+    sim.topk(8, n=1000)                               # top-k only: the sync runs inside K_final (pruned)
+    assert sim.last_launch_count() == n_eval
 
 
 @pytest.mark.skipif(os.environ.get("HSIM_FULL") != "1", reason="exhaustive run: set HSIM_FULL=1")

@@ -15,7 +15,14 @@ from paper_2508_05370_b200.hsim import hsim_merge_topk  # noqa: E402
 small = len(sys.argv) > 1 and sys.argv[1] == "small"
 n = 4096 if small else 60000
 cfgs = [H.get(2), H.get(3), H.get(4), H.get(5), H.deep_tiny(1), H.four_types_tiny(),
-        H.with_mem_check(H.get(2)), H.with_sync_overlap(H.get(4))]
+        H.with_mem_check(H.get(2)), H.with_sync_overlap(H.get(4)),
+        # f4 / f1 rows: interleaved 1F1B (K_ilv, K_sync_ilv), EP across replicas,
+        # mixed-type TP groups, two gradient buckets (C.8 and S.1)
+        H.with_interleave(H.get(2), 2), H.with_interleave(H.with_changes(H.deep_tiny(0), model__global_batch=7680,
+                                                                         model__layers=192), 2),
+        H.with_ep_dp(H.get(4)), H.with_changes(H.get(2), search__mixtp=1),
+        H.with_changes(H.with_sync_overlap(H.get(2)), search__sync_buckets=2),
+        H.with_changes(H.get(4), search__sync_buckets=2)]
 for cfg in cfgs:
     s = Sim(cfg)
     N = s.space_size()
