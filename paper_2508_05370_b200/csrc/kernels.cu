@@ -1163,8 +1163,11 @@ __device__ __forceinline__ i64 slot_T(const Tables& sT, const Cands& c, const Sl
 // whose T0 already exceeds the global bound (the k-th best T found so far, an
 // upper bound of the final k-th) or its warp list's k-th key is skipped.  Exact:
 // the skipped never belong to the top-k; the others get their exact T.
+#ifndef HSIM_FINALP_MINB
+#define HSIM_FINALP_MINB 8  // pruned K_final: cap registers so the (rarely run) sync code spills, not the loop's occupancy
+#endif
 template <int MODE, bool BK>
-__global__ void __launch_bounds__(NT) k_final_small(const Tables* __restrict__ gT, Cands c, Scratch S, i64 ns,
+__global__ void __launch_bounds__(NT, MODE ? HSIM_FINALP_MINB : 1) k_final_small(const Tables* __restrict__ gT, Cands c, Scratch S, i64 ns,
                                                     i64* __restrict__ out, int k, i64* __restrict__ lists) {
   __shared__ Tables sT;
   __shared__ i64 bt[NT / 32][32], bi[NT / 32][32];
@@ -1480,11 +1483,15 @@ __global__ void __launch_bounds__(1024) k_merge_thresh(const i64* __restrict__ b
   const i64 g = (i64)*gthr;
   if (tid == 0) cnt = 0;
   __syncthreads();
-  for (int b = tid; b < nblk; b += 1024) {
+  // every (list, position) pair is an independent load (no walk down a list:
+  // the loads of a thread's pairs are all in flight at once)
+  const int tot = nblk * k;
+#pragma unroll 4
+  for (int e = tid; e < tot; e += 1024) {
+    const int b = e / k, p = e - b * k;
     const i64* L = blk + (i64)b * 2 * k;
-    for (int p = 0; p < k; ++p) {
-      const i64 t = L[p];
-      if (t == LIST_PAD || t == KEY_INF || t > g) break;
+    const i64 t = L[p];
+    if (t != LIST_PAD && t != KEY_INF && t <= g) {
       const int pos = atomicAdd(&cnt, 1);
       if (pos < CAP) {
         ct[pos] = t;

@@ -59,6 +59,9 @@ VARIANTS = {
     "nb8": ["-DHSIM_NBATCH=8"],
     "p6s5": ["-DHSIM_PIPE_MINB=6", "-DHSIM_SYNC_MINB=5"],
     "p7s4": ["-DHSIM_PIPE_MINB=7", "-DHSIM_SYNC_MINB=4"],
+    "fp6": ["-DHSIM_FINALP_MINB=6"],
+    "fp4": ["-DHSIM_FINALP_MINB=4"],
+    "fp1": ["-DHSIM_FINALP_MINB=1"],
     "f8_nb": ["-DHSIM_FASTP=8"],
     "f8_b3": ["-DHSIM_FASTP=8", "-DHSIM_MINB=3"],
     "f4_b4": ["-DHSIM_FASTP=4", "-DHSIM_MINB=4"],
