@@ -1164,7 +1164,7 @@ __device__ __forceinline__ i64 slot_T(const Tables& sT, const Cands& c, const Sl
 // upper bound of the final k-th) or its warp list's k-th key is skipped.  Exact:
 // the skipped never belong to the top-k; the others get their exact T.
 #ifndef HSIM_FINALP_MINB
-#define HSIM_FINALP_MINB 8  // pruned K_final: cap registers so the (rarely run) sync code spills, not the loop's occupancy
+#define HSIM_FINALP_MINB 4  // pruned K_final: 128 registers (measured: 4 beats 1, 6 and 8 on configs 2-4)
 #endif
 template <int MODE, bool BK>
 __global__ void __launch_bounds__(NT, MODE ? HSIM_FINALP_MINB : 1) k_final_small(const Tables* __restrict__ gT, Cands c, Scratch S, i64 ns,
