@@ -349,6 +349,29 @@ def run_ours(a):
                      "what": "Sim.topk over the whole range (the call `value` times) with the global top-k copied to "
                              "pinned host memory every step, back to back, no L2 flush"}
 
+    # the same sweep without the pruned sync (every candidate's sync computed):
+    # the comparison the pruning is judged against
+    unpruned = None
+    if world == 1:
+        sim.set_prune(False)
+        for _ in range(3):
+            step()
+        torch.cuda.synchronize()
+        ums = []
+        for s in range(min(a.steps, 50)):
+            flush.fill_(s & 0xFF)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            step()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ums.append(e0.elapsed_time(e1))
+        sim.set_prune(True)
+        um = sum(ums) / len(ums)
+        unpruned = {"value": round(N / (um / 1e3), 1), "ms_per_step": round(um, 4), "steps": len(ums),
+                    "what": "hsim_set_prune(0): the same full sweep -> top-k with every candidate's gradient sync "
+                            "computed (K_sync); `value` computes it only where T0 can still enter the top-k"}
+
     # measured issue peaks (tools/alu_peak.cu microbenchmarks, profiles/r02/alu_peak.json)
     measured = None
     try:
@@ -367,7 +390,8 @@ def run_ours(a):
                 "warmup": a.warmup, "ms_per_step": round(tot_ms / a.steps, 4), "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
                 "config": {"workload": cfg["name"], "n_candidates": N, "k": a.k,
-                           "step": "full sweep -> global top-k",
+                           "step": "full sweep -> exact global top-k (gradient sync pruned where T0 already "
+                                   "exceeds the top-k bound; see `unpruned`)",
                            "l2": "flushed between timed steps (512 MiB write, outside the event intervals)",
                            "parallelism": f"block-cyclic shard x{world}" + (" + NCCL all_gather" if world > 1 else "")},
                 "roofline": {"bound": "alu", "achieved": round(achieved, 1), "peak": round(peak_gops, 1),
@@ -385,6 +409,8 @@ def run_ours(a):
             line["e2e"] = e2e
         if e2e_sweep:
             line["e2e_sweep"] = e2e_sweep
+        if unpruned:
+            line["unpruned"] = unpruned
         if world == 1 and not a.no_cpu:
             line["cpu_baseline"] = cpu_baseline(cfg)
         print(json.dumps(line), flush=True)

@@ -267,6 +267,12 @@ int64_t hsim_count_cells(const hsim_handle* h, int64_t first, int64_t n);
  * 32, interleave) or on error.  Blocks until the device is idle. */
 int64_t hsim_last_sync_units(const hsim_handle* h);
 
+/* on = 1 (default): a top-k call with k <= 32 and out_ns == NULL computes the
+ * gradient sync only for candidates whose pipeline time can still enter the
+ * top-k (exact: the same top-k).  on = 0: every candidate's sync is computed
+ * (as with out_ns).  HSIM_ESTATE for a NULL handle. */
+int hsim_set_prune(hsim_handle* h, int on);
+
 /* Message of the last failing call on this thread ("" if none). */
 const char* hsim_last_error(void);
 

@@ -143,6 +143,7 @@ struct hsim_handle {
   cudaStream_t side[NSIDE] = {};     // one stream per phase-kernel type + the final stream
   cudaEvent_t ev_fork = nullptr, ev_join[NSIDE] = {}, ev_pool[NEV] = {};
   int32_t last_launches = 0;
+  int prune = 1;                // hsim_set_prune: the top-k sweep's pruned sync (default on)
   int sm_count = 148;
 
   Link link(int n1, int r1, int n2, int r2) const {
@@ -1219,6 +1220,13 @@ int hsim_flow_resim(hsim_handle* h, const int64_t* idx, int32_t k, int64_t* out,
   return launch_flow(h, h->dT, h->hT, idx, k, out, fct, fct_cap, (cudaStream_t)stream);
 }
 
+int hsim_set_prune(hsim_handle* h, int on) {
+  g_err.clear();
+  if (!h) { g_err = "NULL handle"; return HSIM_ESTATE; }
+  h->prune = on ? 1 : 0;
+  return HSIM_OK;
+}
+
 int64_t hsim_last_sync_units(const hsim_handle* h) {
   g_err.clear();
   if (!h) { g_err = "NULL handle"; return -1; }
@@ -1322,6 +1330,7 @@ int interleave_v(const hsim_handle* h) { return h->ilv; }
 int ilv_jobs_max(const hsim_handle* h) { return h->ilv_jobs_max; }
 int ilv_depth_max(const hsim_handle* h) { return h->ilv_depth_max; }
 int sync_buckets(const hsim_handle* h) { return h->md.sync_buckets == 2 ? 2 : 1; }
+int prune_enabled(const hsim_handle* h) { return h->prune; }
 void set_sync_counter(hsim_handle* h, i64* p) { h->d_sync_units = p; }
 int ensure_block_scratch(hsim_handle* h, size_t entries, int64_t** out) {
   if (entries > h->blk_cap) {

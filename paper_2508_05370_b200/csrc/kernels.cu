@@ -40,6 +40,7 @@ int ensure_block_scratch(hsim_handle* h, size_t entries, int64_t** out);
 int ensure_work_scratch(hsim_handle* h, size_t entries, int64_t** out);
 int sm_count(const hsim_handle* h);
 uint32_t depth_mask(const hsim_handle* h);
+int prune_enabled(const hsim_handle* h);
 int depth_jobs_max(const hsim_handle* h, int P);
 int64_t depth_jobs_space(const hsim_handle* h, int P);
 int stages_max(const hsim_handle* h);
@@ -1619,7 +1620,7 @@ static int run_phases(hsim_handle* h, const Tables* dT, Cands c, int64_t n, int6
     const char* e = getenv("HSIM_PRUNE");
     prune_env = e && e[0] == '0' ? 0 : 1;
   }
-  const bool prune = prune_env && !ilv && !out_ns && k >= 1 && k <= 32 && !count;
+  const bool prune = prune_env && prune_enabled(h) && !ilv && !out_ns && k >= 1 && k <= 32 && !count;
   const size_t ilvcap = ilv ? (size_t)ilv_jobs_max(h) * ns : 0;
   jobw += ilvcap;
   const size_t planw = hplan ? (size_t)(2 * c.nr + 1) : 0;

@@ -20,7 +20,7 @@ STATUS = {1: "HSIM_EINVAL", 2: "HSIM_ENOMEM", 3: "HSIM_ECUDA", 4: "HSIM_ERANGE",
 # symbols include/hsim.h declares (checked by tests/test_abi.py)
 EXPORTS = ("hsim_create", "hsim_destroy", "hsim_space_size", "hsim_n_templates", "hsim_template_first",
            "hsim_decode", "hsim_eval_batch", "hsim_topk", "hsim_last_launch_count", "hsim_count_cells",
-           "hsim_last_error", "hsim_merge_topk", "hsim_flow_resim", "hsim_last_sync_units")
+           "hsim_last_error", "hsim_merge_topk", "hsim_flow_resim", "hsim_last_sync_units", "hsim_set_prune")
 
 
 class HsimError(RuntimeError):
@@ -102,6 +102,8 @@ def lib():
                                 C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
         L.hsim_last_launch_count.restype = C.c_int32
         L.hsim_last_launch_count.argtypes = [C.c_void_p]
+        L.hsim_set_prune.restype = C.c_int
+        L.hsim_set_prune.argtypes = [C.c_void_p, C.c_int]
         L.hsim_last_sync_units.restype = C.c_int64
         L.hsim_last_sync_units.argtypes = [C.c_void_p]
         L.hsim_count_cells.restype = C.c_int64
@@ -318,6 +320,12 @@ class Sim:
 
     def last_launch_count(self):
         return lib().hsim_last_launch_count(self.h)
+
+    def set_prune(self, on):
+        """Pruned sync in top-k sweeps (default on; exact either way)."""
+        rc = lib().hsim_set_prune(self.h, int(bool(on)))
+        if rc:
+            _err(rc)
 
     def last_sync_units(self):
         """Sum over the candidates whose gradient sync the last pruned top-k call

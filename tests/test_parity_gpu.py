@@ -205,3 +205,25 @@ def test_full_sweep_topk_properties(torch_cuda, oracle_mod, n):
     ok = v >= 0
     beat = ok & ((v < t[-1]) | ((v == t[-1]) & (idx < i[-1])))
     assert set(idx[beat].tolist()) <= set(i.tolist())
+
+
+@pytest.mark.parametrize("n,overlap", [(2, False), (4, False), (2, True), (3, False)])
+def test_pruned_and_unpruned_topk_agree(torch_cuda, oracle_mod, n, overlap):
+    """The pruned sync (hsim_set_prune, default on: K_final computes the sync
+    only where T0 can still enter the top-k) returns the same top-k as the
+    unpruned sweep (K_sync for every candidate), for k = 1, 16, 32, and the
+    pruned sweep reports the sync work it did."""
+    from paper_2508_05370_b200 import Sim
+    cfg = H.with_sync_overlap(H.get(n)) if overlap else H.get(n)
+    sim = Sim(cfg)
+    N = min(sim.space_size(), 3_000_000)
+    for k in (1, 16, 32):
+        sim.set_prune(True)
+        t1, i1 = sim.topk(k, n=N)
+        units = sim.last_sync_units()
+        sim.set_prune(False)
+        t0, i0 = sim.topk(k, n=N)
+        assert sim.last_sync_units() == -1
+        assert np.array_equal(t1.cpu().numpy(), t0.cpu().numpy()) and np.array_equal(i1.cpu().numpy(), i0.cpu().numpy())
+        assert units > 0
+    sim.set_prune(True)
