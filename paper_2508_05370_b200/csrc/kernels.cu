@@ -1887,7 +1887,8 @@ int launch_eval(hsim_handle* h, const Tables* dT, const hsim_cands* cc, int64_t 
     if (ensure_block_scratch(h, (size_t)nlists * 2 * k + 2, &lists)) return HSIM_ENOMEM;
     cudaMemsetAsync(lists, 0x7F, ((size_t)nlists * 2 * k + 1) * 8, st);
     cudaMemsetAsync(lists + (size_t)nlists * 2 * k + 1, 0, 8, st);
-    set_sync_counter(h, k <= 32 && !out_ns ? lists + (size_t)nlists * 2 * k + 1 : nullptr);
+    set_sync_counter(h, k <= 32 && !out_ns && prune_enabled(h) && interleave_v(h) <= 1
+                            ? lists + (size_t)nlists * 2 * k + 1 : nullptr);
   }
   g_trace.begin(st);
   if (n > 0) {
