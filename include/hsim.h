@@ -273,6 +273,22 @@ int64_t hsim_last_sync_units(const hsim_handle* h);
  * (as with out_ns).  HSIM_ESTATE for a NULL handle. */
 int hsim_set_prune(hsim_handle* h, int on);
 
+/* on = 1 (default): every call (hsim_eval_batch, hsim_topk, hsim_count_cells)
+ * runs the 1F1B recurrence (PAPER.md:186-190 step 4, DESIGN.md C.7) once per
+ * DISTINCT class pipeline of a batch instead of once per (candidate, class):
+ * a class's T_pipe depends only on (template, class, its layer-boundary
+ * digits, its sub-classes' micro-batch counts), so candidates that agree on
+ * those share one run through a device hash table (DESIGN.md §5 "pipeline
+ * dedupe").  Exact: the same int64 results.  Not used with sync_overlap (S.1
+ * needs per-candidate stage ends) or interleave > 1 (V.2), nor when the key
+ * does not fit 63 bits (hsim_dedup_active says whether it applies).  on = 0:
+ * one run per (candidate, class).  HSIM_ESTATE for a NULL handle. */
+int hsim_set_dedup(hsim_handle* h, int on);
+
+/* 1 if calls on this handle currently use the pipeline dedupe (the knob is on
+ * and the handle's description allows it), 0 if not, -1 for a NULL handle. */
+int hsim_dedup_active(const hsim_handle* h);
+
 /* Message of the last failing call on this thread ("" if none). */
 const char* hsim_last_error(void);
 

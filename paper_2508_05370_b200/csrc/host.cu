@@ -144,6 +144,14 @@ struct hsim_handle {
   cudaEvent_t ev_fork = nullptr, ev_join[NSIDE] = {}, ev_pool[NEV] = {};
   int32_t last_launches = 0;
   int prune = 1;                // hsim_set_prune: the top-k sweep's pruned sync (default on)
+  int dedup = 1;                // hsim_set_dedup: one 1F1B run per distinct class pipeline (default on)
+  int cmax = 1;                 // max classes of a template
+  i64 m_max = 0;                // max micro-batches of a template (dedupe key width)
+  u32 pw_max = 1;               // max digit radix of a class record
+  int u_max = 1;                // max sub-classes of a class record
+  u64* d_hkeys[2] = {};         // dedupe hash tables (per scratch buffer): keys, results
+  i64* d_hres[2] = {};
+  size_t hash_cap[2] = {};
   int sm_count = 148;
 
   Link link(int n1, int r1, int n2, int r2) const {
@@ -608,6 +616,8 @@ int32_t hsim_handle::crec(int bi, int M, int D, const std::vector<std::pair<int,
   hd.pw = 1;
   for (int q = 0; q < hd.nd; ++q) hd.pw *= (u32)(2 * md.r_layer + 1);
   hd.pwdiv = make_fastdiv(hd.pw);
+  pw_max = std::max(pw_max, hd.pw);
+  u_max = std::max(u_max, hd.U);
   pool.resize(off + HDR_WORDS + 16 * P + rep.size() * (P + 1));
   std::memcpy(&pool[off], &hd, sizeof hd);
   std::memcpy(&pool[off + HDR_WORDS], sr.data(), sizeof(StageRec) * P);
@@ -678,6 +688,8 @@ void hsim_handle::enumerate() {
         }
       }
       ilv_jobs_max = std::max(ilv_jobs_max, nilv);
+      cmax = std::max(cmax, (int)classes.size());
+      m_max = std::max(m_max, M);
       for (int q = 0; q <= FASTP; ++q) pcnt_max[q] = std::max(pcnt_max[q], cnt[q]);
       for (int q = 0; q <= FASTP; ++q) depth_jobs_space[q] += R * cnt[q];
       pmask_all |= r.pmask;
@@ -826,6 +838,14 @@ void hsim_handle::prepare() {
   hT.bdiv = make_fastdiv((u32)(2 * md.r_batch + 1));
   hT.n_tpl = (i64)tpl.size();
   hT.N = N;
+  {  // dedupe key widths
+    auto bits = [](u64 v) { int b = 0; while (v) { ++b; v >>= 1; } return b; };
+    hT.dd_wt = bits((u64)(tpl.empty() ? 0 : tpl.size() - 1));
+    hT.dd_wd = bits((u64)pw_max - 1);
+    hT.dd_wm = bits((u64)m_max);
+    hT.dd_wu = bits((u64)(u_max - 1));
+    hT.dd_ok = hT.dd_wt + 2 + hT.dd_wd + hT.dd_wm + 2 * hT.dd_wu <= 63 ? 1 : 0;
+  }
   hT.n_lc = (int32_t)lcs.size();
   hT.n_nodes = cd.n_nodes;
   for (size_t k = 0; k < lcs.size(); ++k) hT.lc[k] = lcs[k];
@@ -1086,6 +1106,10 @@ void hsim_destroy(hsim_handle* h) {
   cudaFree(h->d_blk);
   cudaFree(h->d_cells);
   cudaFree(h->d_flow);
+  for (int q = 0; q < 2; ++q) {
+    cudaFree(h->d_hkeys[q]);
+    cudaFree(h->d_hres[q]);
+  }
   for (int q = 0; q < hsim_handle::NSIDE; ++q) {
     if (h->side[q]) cudaStreamDestroy(h->side[q]);
     if (h->ev_join[q]) cudaEventDestroy(h->ev_join[q]);
@@ -1227,6 +1251,19 @@ int hsim_set_prune(hsim_handle* h, int on) {
   return HSIM_OK;
 }
 
+int hsim_set_dedup(hsim_handle* h, int on) {
+  g_err.clear();
+  if (!h) { g_err = "NULL handle"; return HSIM_ESTATE; }
+  h->dedup = on ? 1 : 0;
+  return HSIM_OK;
+}
+
+int hsim_dedup_active(const hsim_handle* h) {
+  g_err.clear();
+  if (!h) { g_err = "NULL handle"; return -1; }
+  return h->dedup && h->hT.dd_ok && h->ilv <= 1 && !h->md.sync_overlap ? 1 : 0;
+}
+
 int64_t hsim_last_sync_units(const hsim_handle* h) {
   g_err.clear();
   if (!h) { g_err = "NULL handle"; return -1; }
@@ -1331,6 +1368,29 @@ int ilv_jobs_max(const hsim_handle* h) { return h->ilv_jobs_max; }
 int ilv_depth_max(const hsim_handle* h) { return h->ilv_depth_max; }
 int sync_buckets(const hsim_handle* h) { return h->md.sync_buckets == 2 ? 2 : 1; }
 int prune_enabled(const hsim_handle* h) { return h->prune; }
+int dedup_enabled(const hsim_handle* h) { return h->dedup && h->hT.dd_ok; }
+int class_max(const hsim_handle* h) { return h->cmax; }
+// dedupe hash table of scratch buffer q with at least cap entries (a power of
+// two); zeroed when (re)allocated, and K_final clears every key it owns, so
+// the table is all-empty between calls
+int ensure_hash_scratch(hsim_handle* h, int q, size_t cap, u64** keys, int64_t** res) {
+  if (cap > h->hash_cap[q]) {
+    cudaFree(h->d_hkeys[q]);
+    cudaFree(h->d_hres[q]);
+    h->d_hkeys[q] = nullptr;
+    h->d_hres[q] = nullptr;
+    h->hash_cap[q] = 0;
+    if (cudaMalloc(&h->d_hkeys[q], cap * 8) != cudaSuccess || cudaMalloc(&h->d_hres[q], cap * 8) != cudaSuccess ||
+        cudaMemset(h->d_hkeys[q], 0, cap * 8) != cudaSuccess) {
+      g_err = "cudaMalloc dedupe table";
+      return HSIM_ENOMEM;
+    }
+    h->hash_cap[q] = cap;
+  }
+  *keys = h->d_hkeys[q];
+  *res = h->d_hres[q];
+  return 0;
+}
 void set_sync_counter(hsim_handle* h, i64* p) { h->d_sync_units = p; }
 int ensure_block_scratch(hsim_handle* h, size_t entries, int64_t** out) {
   if (entries > h->blk_cap) {

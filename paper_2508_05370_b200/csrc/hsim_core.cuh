@@ -152,6 +152,13 @@ struct Tables {
   double port_cap[MAXT][MAXG][2];  // NVLink egress / ingress port of local rank r, B/ns
   double pcie_cap[MAXT];           // GPU <-> rail NIC path, B/ns
   double nic_cap[MAXT];            // NIC <-> rail switch port, min(NIC, rail), B/ns
+  // pipeline dedupe: a class pipeline is a function of (template,
+  // class, boundary digits, the class's sub-class micro-batch vector) only; the
+  // vector is base + [u < a] + [u < b] (m non-increasing in the replica, at most
+  // two +1 steps).  Key = tau | c << wt | dig << (wt + 2) | base << .. | a | b,
+  // plus 1 (0 = empty), with the field widths below; dd_ok = 0 when they
+  // exceed 63 bits (dedupe then off).
+  int32_t dd_ok, dd_wt, dd_wd, dd_wm, dd_wu, _pad8;
 };
 
 // --- C.0 --------------------------------------------------------------------

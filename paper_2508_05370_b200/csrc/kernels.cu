@@ -41,6 +41,9 @@ int ensure_work_scratch(hsim_handle* h, size_t entries, int64_t** out);
 int sm_count(const hsim_handle* h);
 uint32_t depth_mask(const hsim_handle* h);
 int prune_enabled(const hsim_handle* h);
+int dedup_enabled(const hsim_handle* h);
+int class_max(const hsim_handle* h);
+int ensure_hash_scratch(hsim_handle* h, int q, size_t cap, u64** keys, int64_t** res);
 int depth_jobs_max(const hsim_handle* h, int P);
 int64_t depth_jobs_space(const hsim_handle* h, int P);
 int stages_max(const hsim_handle* h);
@@ -168,10 +171,89 @@ struct Scratch {
   int32_t* deep;      // [ns] slots with a class deeper than FASTP (compacted)
   int32_t* ilv;       // V.2: jobs (slot << 2 | class) of interleaved pipelines (P >= 2), or nullptr
   int32_t* full[FASTP + 1];  // per depth: jobs (slot << 2 | class) of full chunks, 32-aligned groups
-  int32_t* part[FASTP + 1];  // per depth: jobs of partial chunks, packed
+  int32_t* part[FASTP + 1];  // per depth: jobs of partial chunks, packed (dedupe: hash entries of the distinct pipelines)
   unsigned long long* counters;  // [NCNT]
   i64 ns;             // slot capacity (row stride of the [MAXC][ns] arrays)
+  // pipeline dedupe, or hkeys == nullptr: open-addressing table
+  // of 2^hbits entries (key + 1, 0 = empty) and the T_pipe of each entry;
+  // hj[c][slot] = the slot's entry of class c (| HJ_OWN for the slot whose
+  // insert created it), -1 = none
+  u64* hkeys;
+  i64* hres;
+  int32_t* hj;        // [MAXC][ns]
+  int hbits;
 };
+constexpr int32_t HJ_OWN = 1 << 30, HJ_MASK = HJ_OWN - 1;
+
+// --- pipeline dedupe keys ------------------------------------------
+__device__ __forceinline__ u64 dd_pack(const Tables& T, i64 tau, int c, u32 dig, i64 base, int a, int b) {
+  const int sd = T.dd_wt + 2, sm = sd + T.dd_wd, sa = sm + T.dd_wm, sb = sa + T.dd_wu;
+  return ((u64)tau | (u64)c << T.dd_wt | (u64)dig << sd | (u64)base << sm | (u64)a << sa | (u64)b << sb) + 1;
+}
+struct DKey {
+  int tau, c, a, b;
+  u32 dig;
+  i64 base;
+};
+__device__ __forceinline__ u64 dd_field(u64 v, int sh, int w) { return (v >> sh) & (((u64)1 << w) - 1); }
+__device__ __forceinline__ DKey dd_unpack(const Tables& T, u64 key) {
+  key -= 1;
+  const int sd = T.dd_wt + 2, sm = sd + T.dd_wd, sa = sm + T.dd_wm, sb = sa + T.dd_wu;
+  DKey d;
+  d.tau = (int)dd_field(key, 0, T.dd_wt);
+  d.c = (int)dd_field(key, T.dd_wt, 2);
+  d.dig = (u32)dd_field(key, sd, T.dd_wd);
+  d.base = (i64)dd_field(key, sm, T.dd_wm);
+  d.a = (int)dd_field(key, sa, T.dd_wu);
+  d.b = (int)dd_field(key, sb, T.dd_wu);
+  return d;
+}
+// the key of class c's pipeline: base = m of the last sub-class, a / b = the
+// sub-classes with m >= base + 2 / base + 1 (a prefix: sub-classes are in
+// ascending lowest-replica order and m is non-increasing in the replica)
+__device__ __forceinline__ u64 dd_key(const Tables& T, i64 tau, int c, int32_t off, const ClassSplit& cs) {
+  const CrecHdr* h = crec_hdr(T, off);
+  const int P = h->P, U = h->U;
+  const i64 base = mb_of(cs, crec_sub(T, off, P, U - 1)[0]);
+  int a = 0, b = 0;
+  for (int u = 0; u + 1 < U; ++u) {
+    const i64 m = mb_of(cs, crec_sub(T, off, P, u)[0]);
+    a += m >= base + 2;
+    b += m >= base + 1;
+  }
+  return dd_pack(T, tau, c, cs.dig, base, a, b);
+}
+// a ClassSplit reproducing the key's micro-batch vector: sub-class u (lowest
+// replica k_u, ascending) gets base + [k_u < k_a] + [k_u < k_b]
+__device__ __forceinline__ ClassSplit dd_split(const Tables& T, int32_t off, const DKey& d) {
+  const CrecHdr* h = crec_hdr(T, off);
+  ClassSplit cs;
+  cs.dig = d.dig;
+  cs.q = d.base;
+  cs.add = 0;
+  cs.seats = d.a < h->U ? crec_sub(T, off, h->P, d.a)[0] : h->D;
+  cs.rm = d.b < h->U ? crec_sub(T, off, h->P, d.b)[0] : h->D;
+  return cs;
+}
+// insert-or-find; returns the entry, *own = the insert created it
+__device__ __forceinline__ int dd_insert(const Scratch& S, u64 key, bool* own) {
+  u64 x = key;  // splitmix64 finaliser
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+  x ^= x >> 31;
+  const u64 mask = ((u64)1 << S.hbits) - 1;
+  u64 e = x >> (64 - S.hbits);
+  for (;;) {
+    const u64 v = __ldcg(&S.hkeys[e]);
+    if (v == key) { *own = false; return (int)e; }
+    if (v == 0) {
+      const u64 prev = atomicCAS((unsigned long long*)&S.hkeys[e], 0ull, (unsigned long long)key);
+      if (prev == 0) { *own = true; return (int)e; }
+      if (prev == key) { *own = false; return (int)e; }
+    }
+    e = (e + 1) & mask;
+  }
+}
 
 __device__ __forceinline__ ClassSplit load_split(const Scratch& S, int c, int C, i64 t) {
   ClassSplit cs;
@@ -205,7 +287,8 @@ __device__ __forceinline__ i64 warp_sum(i64 v) {
 
 // steps a0 + a1 for a C-class template; stores the compact split of each class
 template <int C, bool ILV>
-__device__ __forceinline__ int split_store(const Tables& T, const TplRec& tp, i64 local, const Scratch& S, i64 slot) {
+__device__ __forceinline__ int split_store(const Tables& T, const TplRec& tp, i64 tau, i64 local, const Scratch& S, i64 slot,
+                                           u64 (&kk)[MAXC]) {
   ClassSplit cs[C];
   const int st = partition_c<C, ILV>(T, tp, local, cs);
   if (st == 0) {
@@ -215,6 +298,7 @@ __device__ __forceinline__ int split_store(const Tables& T, const TplRec& tp, i6
       S.q[k * S.ns + slot] = (int32_t)cs[k].q;
       S.seats[k * S.ns + slot] = (int32_t)cs[k].seats;
       S.add[k * S.ns + slot] = (int32_t)cs[k].add;
+      if (!ILV && S.hkeys) kk[k] = dd_key(T, tau, k, tp.crec[k], cs[k]);
     }
     S.rm[slot] = (int32_t)cs[C - 1].rm;
   }
@@ -268,17 +352,50 @@ __global__ void __launch_bounds__(NT, HSIM_SPLIT_MINB) k_split(const Tables* __r
     S.tau[slot] = (int32_t)tau;
     int st = 1;
     uint32_t mypm = 0;
+    u64 kk[MAXC] = {0, 0, 0, 0};  // dedupe keys of the classes (0: none)
     if (tau >= 0) {
       const TplRec& tp = sT.tpl[tau];
       // class count specialised: the per-class split stays in registers
       switch (tp.C) {
-        case 1: st = split_store<1, ILV>(sT, tp, i - tp.prefix, S, slot); break;
-        case 2: st = split_store<2, ILV>(sT, tp, i - tp.prefix, S, slot); break;
-        case 3: st = split_store<3, ILV>(sT, tp, i - tp.prefix, S, slot); break;
-        default: st = split_store<4, ILV>(sT, tp, i - tp.prefix, S, slot); break;
+        case 1: st = split_store<1, ILV>(sT, tp, tau, i - tp.prefix, S, slot, kk); break;
+        case 2: st = split_store<2, ILV>(sT, tp, tau, i - tp.prefix, S, slot, kk); break;
+        case 3: st = split_store<3, ILV>(sT, tp, tau, i - tp.prefix, S, slot, kk); break;
+        default: st = split_store<4, ILV>(sT, tp, tau, i - tp.prefix, S, slot, kk); break;
       }
       S.status[slot] = st;
       if (st == 0) mypm = tp.pmask;
+    }
+    if (!ILV && S.hkeys) {
+      // pipeline dedupe: lanes with equal keys share one insert (warp match),
+      // then the creator of an entry appends it to its depth's job list; deep
+      // classes (P > FASTP) get an entry too (K_deep runs the owner's)
+#pragma unroll
+      for (int k = 0; k < MAXC; ++k) {
+        const u64 key = kk[k];
+        const unsigned grp = __match_any_sync(FULL, key);
+        const int leader = __ffs(grp) - 1;
+        int e = -1;
+        bool own = false;
+        if (key && lane == leader) e = dd_insert(S, key, &own);
+        e = __shfl_sync(FULL, e, leader);
+        S.hj[k * S.ns + slot] = key ? (e | (own ? HJ_OWN : 0)) : -1;
+        const int P = key ? crec_hdr(sT, sT.tpl[tau].crec[k])->P : 0;
+        bool app = own && P <= FASTP;
+        unsigned pend = __ballot_sync(FULL, app);
+        while (pend) {
+          const int src = __ffs(pend) - 1;
+          const int P0 = __shfl_sync(FULL, P, src);
+          const unsigned bal = __ballot_sync(FULL, app && P == P0);
+          unsigned long long o = 0;
+          if (lane == src) o = atomicAdd(&S.counters[CNT_PART + P0], (unsigned long long)__popc(bal));
+          o = __shfl_sync(FULL, o, src) + __popc(bal & ((1u << lane) - 1));
+          if (app && P == P0) {
+            S.part[P0][o] = e;
+            app = false;
+          }
+          pend &= ~bal;
+        }
+      }
     }
     // deep candidates: compacted, warp-aggregated
     const bool deep = (mypm >> (FASTP + 1)) != 0;
@@ -295,7 +412,7 @@ __global__ void __launch_bounds__(NT, HSIM_SPLIT_MINB) k_split(const Tables* __r
     // templates) are packed densely
     u64 combos = 0;
     uint32_t ilvc = 0;  // V.2: classes of this lane's candidate that run interleaved (K_ilv)
-    if (mypm)
+    if (mypm && (ILV || !S.hkeys))
       for (int k = 0; k < sT.tpl[tau].C; ++k) {
         const int P = crec_hdr(sT, sT.tpl[tau].crec[k])->P;
         if (ILV && P >= 2) ilvc |= 1u << k;
@@ -365,6 +482,21 @@ __global__ void __launch_bounds__(NT, P <= 4 ? HSIM_PIPE_MINB : 1) k_pipe(const 
     const i64 q = item < gfull ? item * 32 + lane : (item - gfull) * 32 + lane;
     if (item >= gfull && q >= npart) continue;
     const int job = item < gfull ? S.full[P][q] : S.part[P][q];
+    constexpr bool rq = P >= HSIM_REQ_MINP && P <= HSIM_REQ_MAXP;
+    if (S.hkeys) {  // dedupe: job = a distinct pipeline's table entry
+      const DKey d = dd_unpack(sT, __ldcg(&S.hkeys[job]));
+      const int32_t off = sT.tpl[d.tau].crec[d.c];
+      const DeferCtx dc{rq ? S.req[rq ? P : 0] : nullptr, &S.counters[CNT_REQ + (rq ? P : 0)], rq ? S.req_cap[rq ? P : 0] : 0,
+                        (i64)job << 16 | d.c};
+      const PipeOut r = class_pipes_inl<P>(sT, off, dd_split(sT, off, d), nullptr, 0, rq ? &dc : nullptr);
+      S.hres[job] = r.T0;
+#ifdef HSIM_WARPCELLS
+      cells += 32 * __reduce_max_sync(__activemask(), (unsigned)r.cells);
+#else
+      cells += r.cells;
+#endif
+      continue;
+    }
     const int c = job & 3;
     const i64 slot = job >> 2;
     const int tau = S.tau[slot];
@@ -373,7 +505,6 @@ __global__ void __launch_bounds__(NT, P <= 4 ? HSIM_PIPE_MINB : 1) k_pipe(const 
     i64* R = S.Rs ? S.Rs + (i64)class_stage_off(sT, tp, c) * S.ns + slot : nullptr;
     // depths gated off on the host have req_cap 0: the re-queue attempt fails
     // and the lane continues in place (rare: only unsettled jobs try)
-    constexpr bool rq = P >= HSIM_REQ_MINP && P <= HSIM_REQ_MAXP;
     const DeferCtx dc{rq ? S.req[rq ? P : 0] : nullptr, &S.counters[CNT_REQ + (rq ? P : 0)], rq ? S.req_cap[rq ? P : 0] : 0,
                       slot << 16 | c};
     const PipeOut r = class_pipes_inl<P>(sT, tp.crec[c], load_split(S, c, tp.C, slot), R, S.ns, rq ? &dc : nullptr);
@@ -412,6 +543,14 @@ __global__ void __launch_bounds__(NT, P <= 4 ? HSIM_PIPE_MINB : 1) k_pipe_cont(c
     const i64 v = S.req[P][q];
     const i64 slot = v >> 16;
     const int u = (int)(v >> 4) & 0xfff, c = (int)v & 15;
+    if (S.hkeys) {  // dedupe: slot = the pipeline's table entry
+      const DKey d = dd_unpack(sT, __ldcg(&S.hkeys[slot]));
+      const int32_t off = sT.tpl[d.tau].crec[d.c];
+      const PipeOut r = class_pipes_inl<P>(sT, off, dd_split(sT, off, d), nullptr, 0, nullptr, u);
+      atomicMax((unsigned long long*)&S.hres[slot], (unsigned long long)r.T0);
+      cells += r.cells;
+      continue;
+    }
     const TplRec& tp = sT.tpl[S.tau[slot]];
     i64* R = S.Rs ? S.Rs + (i64)class_stage_off(sT, tp, c) * S.ns + slot : nullptr;
     const PipeOut r = class_pipes_inl<P>(sT, tp.crec[c], load_split(S, c, tp.C, slot), R, S.ns, nullptr, u);
@@ -687,12 +826,17 @@ __global__ void __launch_bounds__(NT) k_deep(const Tables* __restrict__ gT, Scra
       const int32_t off = tp.crec[c];
       const int P = crec_hdr(sT, off)->P;
       if (P <= FASTP) continue;
+      const int32_t hj = S.hkeys ? S.hj[c * S.ns + sj] : -1;
+      if (S.hkeys && !(hj & HJ_OWN)) continue;  // dedupe: the entry's creator runs it
       const ClassSplit cs = load_split(S, c, tp.C, sj);
       i64 cl = 0;
       i64* R = S.Rs ? S.Rs + (i64)class_stage_off(sT, tp, c) * S.ns + sj : nullptr;
       const i64 T0 = P <= 32 ? warp_pipe_class(sT, off, cs, &cl, R, S.ns) : warp_pipe_class2(sT, off, cs, &cl, R, S.ns);
       cells += cl;
-      if (lane == 0) S.Tc[c * S.ns + sj] = T0;
+      if (lane == 0) {
+        if (S.hkeys) S.hres[hj & HJ_MASK] = T0;
+        else S.Tc[c * S.ns + sj] = T0;
+      }
     }
   }
   if (count) {
@@ -1129,6 +1273,17 @@ __device__ __forceinline__ SlotW slot_load(const Scratch& S, i64 slot) {
   w.tau = __ldcs(&S.tau[slot]);
   w.st = __ldcs(&S.status[slot]);
   w.ex = __ldcs(&S.extra[slot]);
+  if (S.hkeys) {  // dedupe: the class's table entry; its creator clears the key for the next call
+    int32_t hj[MAXC];
+#pragma unroll
+    for (int q = 0; q < MAXC; ++q) hj[q] = __ldcs(&S.hj[q * S.ns + slot]);
+#pragma unroll
+    for (int q = 0; q < MAXC; ++q) {
+      w.tc[q] = hj[q] >= 0 ? __ldcg(&S.hres[hj[q] & HJ_MASK]) : 0;
+      if (hj[q] >= 0 && (hj[q] & HJ_OWN)) S.hkeys[hj[q] & HJ_MASK] = 0;
+    }
+    return w;
+  }
 #pragma unroll
   for (int q = 0; q < MAXC; ++q) w.tc[q] = __ldcs(&S.Tc[q * S.ns + slot]);
   return w;
@@ -1623,8 +1778,18 @@ static int run_phases(hsim_handle* h, const Tables* dT, Cands c, int64_t n, int6
   const bool prune = prune_env && prune_enabled(h) && !ilv && !out_ns && k >= 1 && k <= 32 && !count;
   const size_t ilvcap = ilv ? (size_t)ilv_jobs_max(h) * ns : 0;
   jobw += ilvcap;
+  // pipeline dedupe: not with S.1 (per-candidate stage ends) or V.2
+  const bool dd = dedup_enabled(h) && !sync_overlap(h) && !ilv;
+  size_t hcap = 0;
+  int hbits = 0;
+  if (dd) {  // at most ns * cmax distinct pipelines per batch: load factor <= 1/2
+    const size_t need = 2 * (size_t)ns * (size_t)class_max(h);
+    while (((size_t)1 << hbits) < need || hbits < 10) ++hbits;
+    hcap = (size_t)1 << hbits;
+    if (hbits > 30) return HSIM_ENOMEM;
+  }
   const size_t planw = hplan ? (size_t)(2 * c.nr + 1) : 0;
-  const size_t n32 = (size_t)(4 + 4 * MAXC) * ns + jobw;
+  const size_t n32 = (size_t)(4 + 4 * MAXC + (dd ? MAXC : 0)) * ns + jobw;
   const size_t bufw0 = (size_t)(MAXC + 2) * ns + NCNT + (n32 + 1) / 2 + 8;
   size_t reqw = 0, reqcap[HSIM_REQ_MAXP + 1] = {0};
   for (int P = HSIM_REQ_MINP; P <= HSIM_REQ_MAXP && P <= FASTP; ++P) {
@@ -1670,6 +1835,15 @@ static int run_phases(hsim_handle* h, const Tables* dT, Cands c, int64_t n, int6
       pj += 2 * jobcap[P];
     }
     S.ilv = ilvcap ? pj : nullptr;
+    pj += ilvcap;
+    S.hkeys = nullptr;
+    S.hres = nullptr;
+    S.hj = nullptr;
+    S.hbits = hbits;
+    if (dd) {
+      if (ensure_hash_scratch(h, q, hcap, &S.hkeys, &S.hres)) return HSIM_ENOMEM;
+      S.hj = pj;
+    }
   }
   if (hplan) {
     i64* pw = base + NBUF * bufw;
@@ -1791,6 +1965,7 @@ static int run_phases(hsim_handle* h, const Tables* dT, Cands c, int64_t n, int6
     }
     if (count) {
       unsigned long long v = 0;
+      if (dd) cudaMemsetAsync(S.hkeys, 0, hcap * 8, st);  // no K_final in count mode: clear the table here
       cudaMemcpyAsync(&v, S.counters + CNT_CELLS, 8, cudaMemcpyDeviceToHost, st);
       if (cudaStreamSynchronize(st) != cudaSuccess) break;
       cells += (i64)v;

@@ -20,7 +20,8 @@ STATUS = {1: "HSIM_EINVAL", 2: "HSIM_ENOMEM", 3: "HSIM_ECUDA", 4: "HSIM_ERANGE",
 # symbols include/hsim.h declares (checked by tests/test_abi.py)
 EXPORTS = ("hsim_create", "hsim_destroy", "hsim_space_size", "hsim_n_templates", "hsim_template_first",
            "hsim_decode", "hsim_eval_batch", "hsim_topk", "hsim_last_launch_count", "hsim_count_cells",
-           "hsim_last_error", "hsim_merge_topk", "hsim_flow_resim", "hsim_last_sync_units", "hsim_set_prune")
+           "hsim_last_error", "hsim_merge_topk", "hsim_flow_resim", "hsim_last_sync_units", "hsim_set_prune",
+           "hsim_set_dedup", "hsim_dedup_active")
 
 
 class HsimError(RuntimeError):
@@ -104,6 +105,10 @@ def lib():
         L.hsim_last_launch_count.argtypes = [C.c_void_p]
         L.hsim_set_prune.restype = C.c_int
         L.hsim_set_prune.argtypes = [C.c_void_p, C.c_int]
+        L.hsim_set_dedup.restype = C.c_int
+        L.hsim_set_dedup.argtypes = [C.c_void_p, C.c_int]
+        L.hsim_dedup_active.restype = C.c_int
+        L.hsim_dedup_active.argtypes = [C.c_void_p]
         L.hsim_last_sync_units.restype = C.c_int64
         L.hsim_last_sync_units.argtypes = [C.c_void_p]
         L.hsim_count_cells.restype = C.c_int64
@@ -326,6 +331,16 @@ class Sim:
         rc = lib().hsim_set_prune(self.h, int(bool(on)))
         if rc:
             _err(rc)
+
+    def set_dedup(self, on):
+        """One 1F1B run per distinct class pipeline (default on; exact either way)."""
+        rc = lib().hsim_set_dedup(self.h, int(bool(on)))
+        if rc:
+            _err(rc)
+
+    def dedup_active(self):
+        """Whether calls on this handle use the pipeline dedupe."""
+        return lib().hsim_dedup_active(self.h) == 1
 
     def last_sync_units(self):
         """Sum over the candidates whose gradient sync the last pruned top-k call

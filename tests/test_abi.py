@@ -209,3 +209,20 @@ def test_buckets_validation_and_decode(oracle_mod, L):
         assert e.value.code == hsim.HSIM_EINVAL
     s = hsim.Sim(H.with_changes(H.get(4), search__sync_buckets=2), host_only=True)
     assert s.space_size() == oracle_mod.Oracle(H.get(4)).space_size()
+
+
+def test_dedup_knob_host(L):
+    """hsim_set_dedup / hsim_dedup_active (DESIGN.md §5 pipeline dedupe): on by
+    default for every BASELINE config (the key fits 63 bits), off with S.1 or
+    V.2 whatever the knob says, and switchable per handle."""
+    for n in (1, 2, 3, 4, 5):
+        s = hsim.Sim(H.get(n), host_only=True)
+        assert s.dedup_active(), n
+        s.set_dedup(False)
+        assert not s.dedup_active()
+        s.set_dedup(True)
+        assert s.dedup_active()
+    assert not hsim.Sim(H.with_sync_overlap(H.get(2)), host_only=True).dedup_active()
+    assert not hsim.Sim(H.with_interleave(H.variant_tiny(3)), host_only=True).dedup_active()
+    assert L.hsim_dedup_active(None) == -1
+    assert L.hsim_set_dedup(None, 1) == hsim.HSIM_ESTATE
