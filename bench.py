@@ -372,6 +372,32 @@ def run_ours(a):
                     "what": "hsim_set_prune(0): the same full sweep -> top-k with every candidate's gradient sync "
                             "computed (K_sync); `value` computes it only where T0 can still enter the top-k"}
 
+    # the same sweep with one 1F1B run per (candidate, class) instead of per
+    # distinct class pipeline: the comparison the dedupe is judged against
+    no_dedup = None
+    if world == 1 and sim.dedup_active():
+        sim.set_dedup(False)
+        cells_off = sim.count_cells(0, N)
+        for _ in range(3):
+            step()
+        torch.cuda.synchronize()
+        dms = []
+        for s in range(min(a.steps, 50)):
+            flush.fill_(s & 0xFF)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            step()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            dms.append(e0.elapsed_time(e1))
+        sim.set_dedup(True)
+        dm = sum(dms) / len(dms)
+        no_dedup = {"value": round(N / (dm / 1e3), 1), "ms_per_step": round(dm, 4), "steps": len(dms),
+                    "cells_per_launch": cells_off,
+                    "what": "hsim_set_dedup(0): the same full sweep -> top-k with the 1F1B recurrence run once per "
+                            "(candidate, class) instead of once per distinct class pipeline (DESIGN.md §5); exact "
+                            "either way, `cells_per_launch` counts what executes"}
+
     # measured issue peaks (tools/alu_peak.cu microbenchmarks, profiles/r02/alu_peak.json)
     measured = None
     try:
@@ -390,8 +416,9 @@ def run_ours(a):
                 "warmup": a.warmup, "ms_per_step": round(tot_ms / a.steps, 4), "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
                 "config": {"workload": cfg["name"], "n_candidates": N, "k": a.k,
-                           "step": "full sweep -> exact global top-k (gradient sync pruned where T0 already "
-                                   "exceeds the top-k bound; see `unpruned`)",
+                           "step": "full sweep -> exact global top-k (one 1F1B run per distinct class pipeline, "
+                                   "see `no_dedup`; gradient sync pruned where T0 already exceeds the top-k bound, "
+                                   "see `unpruned`)",
                            "l2": "flushed between timed steps (512 MiB write, outside the event intervals)",
                            "parallelism": f"block-cyclic shard x{world}" + (" + NCCL all_gather" if world > 1 else "")},
                 "roofline": {"bound": "alu", "achieved": round(achieved, 1), "peak": round(peak_gops, 1),
@@ -411,6 +438,8 @@ def run_ours(a):
             line["e2e_sweep"] = e2e_sweep
         if unpruned:
             line["unpruned"] = unpruned
+        if no_dedup:
+            line["no_dedup"] = no_dedup
         if world == 1 and not a.no_cpu:
             line["cpu_baseline"] = cpu_baseline(cfg)
         print(json.dumps(line), flush=True)

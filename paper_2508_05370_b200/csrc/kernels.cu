@@ -214,7 +214,7 @@ __device__ __forceinline__ DKey dd_unpack(const Tables& T, u64 key) {
 __device__ __forceinline__ u64 dd_key(const Tables& T, i64 tau, int c, int32_t off, const ClassSplit& cs) {
   const CrecHdr* h = crec_hdr(T, off);
   const int P = h->P, U = h->U;
-  const i64 base = mb_of(cs, crec_sub(T, off, P, U - 1)[0]);
+  const i64 base = mb_of(cs, U == 1 ? 0 : crec_sub(T, off, P, U - 1)[0]);  // sub-class 0 starts at replica 0
   int a = 0, b = 0;
   for (int u = 0; u + 1 < U; ++u) {
     const i64 m = mb_of(cs, crec_sub(T, off, P, u)[0]);
@@ -235,14 +235,39 @@ __device__ __forceinline__ ClassSplit dd_split(const Tables& T, int32_t off, con
   cs.rm = d.b < h->U ? crec_sub(T, off, h->P, d.b)[0] : h->D;
   return cs;
 }
-// insert-or-find; returns the entry, *own = the insert created it
-__device__ __forceinline__ int dd_insert(const Scratch& S, u64 key, bool* own) {
-  u64 x = key;  // splitmix64 finaliser
+// Table layout: 2^hbits entries = nb buckets of 32.  A key's home keeps the
+// keys of one (template, class, base, a, b) group with consecutive boundary
+// digits in consecutive entries (the lanes of a chunk: class-0 digits run
+// with the lane), so probes, job reads, result gathers and clears of a warp
+// touch one or two lines: offset x = dig + r (r a hash of the group), home
+// bucket = hash(group, x >> 5), entry = bucket * 32 + (x & 31).  Probing
+// steps by one bucket at the same offset (coalescing kept on collisions);
+// after nb steps the offset advances, so the sequence visits every entry.
+__device__ __forceinline__ u64 dd_mix(u64 x) {  // splitmix64 finaliser
   x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
   x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
-  x ^= x >> 31;
-  const u64 mask = ((u64)1 << S.hbits) - 1;
-  u64 e = x >> (64 - S.hbits);
+  return x ^ (x >> 31);
+}
+__device__ __forceinline__ u64 dd_home(const Tables& T, const Scratch& S, u64 key) {
+  const u64 kr = key - 1;
+  const int sd = T.dd_wt + 2;
+  const u64 dmask = (((u64)1 << T.dd_wd) - 1) << sd;
+  const u64 dig = (kr & dmask) >> sd;
+  const u64 h = dd_mix((kr & ~dmask) + 0x9E3779B97F4A7C15ull);
+  const u64 x = dig + (h & 31);
+  const u64 bk = dd_mix(h ^ ((x >> 5) * 0xD1B54A32D192ED03ull)) >> (64 - (S.hbits - 5));
+  return bk << 5 | (x & 31);
+}
+__device__ __forceinline__ u64 dd_step(const Scratch& S, u64 e, u64& j) {
+  const u64 nb = (u64)1 << (S.hbits - 5);
+  ++j;
+  u64 o = e & 31;
+  if ((j & (nb - 1)) == 0) o = (o + 1) & 31;
+  return (((e >> 5) + 1) & (nb - 1)) << 5 | o;
+}
+// insert-or-find along the probe sequence from its j-th entry e; returns the
+// entry, *own = the insert created it
+__device__ __forceinline__ int dd_insert(const Scratch& S, u64 key, u64 e, u64 j, bool* own) {
   for (;;) {
     const u64 v = __ldcg(&S.hkeys[e]);
     if (v == key) { *own = false; return (int)e; }
@@ -251,7 +276,7 @@ __device__ __forceinline__ int dd_insert(const Scratch& S, u64 key, bool* own) {
       if (prev == 0) { *own = true; return (int)e; }
       if (prev == key) { *own = false; return (int)e; }
     }
-    e = (e + 1) & mask;
+    e = dd_step(S, e, j);
   }
 }
 
@@ -288,7 +313,7 @@ __device__ __forceinline__ i64 warp_sum(i64 v) {
 // steps a0 + a1 for a C-class template; stores the compact split of each class
 template <int C, bool ILV>
 __device__ __forceinline__ int split_store(const Tables& T, const TplRec& tp, i64 tau, i64 local, const Scratch& S, i64 slot,
-                                           u64 (&kk)[MAXC]) {
+                                           u64 (&kk)[MAXC], int (&Pk)[MAXC]) {
   ClassSplit cs[C];
   const int st = partition_c<C, ILV>(T, tp, local, cs);
   if (st == 0) {
@@ -298,7 +323,10 @@ __device__ __forceinline__ int split_store(const Tables& T, const TplRec& tp, i6
       S.q[k * S.ns + slot] = (int32_t)cs[k].q;
       S.seats[k * S.ns + slot] = (int32_t)cs[k].seats;
       S.add[k * S.ns + slot] = (int32_t)cs[k].add;
-      if (!ILV && S.hkeys) kk[k] = dd_key(T, tau, k, tp.crec[k], cs[k]);
+      if (!ILV && S.hkeys) {
+        kk[k] = dd_key(T, tau, k, tp.crec[k], cs[k]);
+        Pk[k] = crec_hdr(T, tp.crec[k])->P;
+      }
     }
     S.rm[slot] = (int32_t)cs[C - 1].rm;
   }
@@ -352,48 +380,111 @@ __global__ void __launch_bounds__(NT, HSIM_SPLIT_MINB) k_split(const Tables* __r
     S.tau[slot] = (int32_t)tau;
     int st = 1;
     uint32_t mypm = 0;
-    u64 kk[MAXC] = {0, 0, 0, 0};  // dedupe keys of the classes (0: none)
+    u64 kk[MAXC] = {0, 0, 0, 0};  // dedupe keys of the classes (0: none) and their depths
+    int Pk[MAXC] = {0, 0, 0, 0};
     if (tau >= 0) {
       const TplRec& tp = sT.tpl[tau];
       // class count specialised: the per-class split stays in registers
       switch (tp.C) {
-        case 1: st = split_store<1, ILV>(sT, tp, tau, i - tp.prefix, S, slot, kk); break;
-        case 2: st = split_store<2, ILV>(sT, tp, tau, i - tp.prefix, S, slot, kk); break;
-        case 3: st = split_store<3, ILV>(sT, tp, tau, i - tp.prefix, S, slot, kk); break;
-        default: st = split_store<4, ILV>(sT, tp, tau, i - tp.prefix, S, slot, kk); break;
+        case 1: st = split_store<1, ILV>(sT, tp, tau, i - tp.prefix, S, slot, kk, Pk); break;
+        case 2: st = split_store<2, ILV>(sT, tp, tau, i - tp.prefix, S, slot, kk, Pk); break;
+        case 3: st = split_store<3, ILV>(sT, tp, tau, i - tp.prefix, S, slot, kk, Pk); break;
+        default: st = split_store<4, ILV>(sT, tp, tau, i - tp.prefix, S, slot, kk, Pk); break;
       }
       S.status[slot] = st;
       if (st == 0) mypm = tp.pmask;
     }
     if (!ILV && S.hkeys) {
-      // pipeline dedupe: lanes with equal keys share one insert (warp match),
-      // then the creator of an entry appends it to its depth's job list; deep
-      // classes (P > FASTP) get an entry too (K_deep runs the owner's)
+      // pipeline dedupe: lanes with equal keys share one insert (warp match);
+      // the inserts of all classes are in flight at once (probe load, then the
+      // CAS of the empty home entries, then the rare collision walks); the
+      // creator of an entry appends it to its depth's job list.  Deep classes
+      // (P > FASTP) get an entry too (K_deep runs the owner's).
+      const int Cw = (int)__reduce_max_sync(FULL, (unsigned)((kk[0] != 0) + (kk[1] != 0) + (kk[2] != 0) + (kk[3] != 0)));
+      int ldr[MAXC];
+      bool lead[MAXC], own[MAXC];
+      u64 e[MAXC], v[MAXC];
 #pragma unroll
       for (int k = 0; k < MAXC; ++k) {
-        const u64 key = kk[k];
-        const unsigned grp = __match_any_sync(FULL, key);
-        const int leader = __ffs(grp) - 1;
-        int e = -1;
-        bool own = false;
-        if (key && lane == leader) e = dd_insert(S, key, &own);
-        e = __shfl_sync(FULL, e, leader);
-        S.hj[k * S.ns + slot] = key ? (e | (own ? HJ_OWN : 0)) : -1;
-        const int P = key ? crec_hdr(sT, sT.tpl[tau].crec[k])->P : 0;
-        bool app = own && P <= FASTP;
-        unsigned pend = __ballot_sync(FULL, app);
-        while (pend) {
-          const int src = __ffs(pend) - 1;
-          const int P0 = __shfl_sync(FULL, P, src);
-          const unsigned bal = __ballot_sync(FULL, app && P == P0);
-          unsigned long long o = 0;
-          if (lane == src) o = atomicAdd(&S.counters[CNT_PART + P0], (unsigned long long)__popc(bal));
-          o = __shfl_sync(FULL, o, src) + __popc(bal & ((1u << lane) - 1));
-          if (app && P == P0) {
-            S.part[P0][o] = e;
-            app = false;
+        ldr[k] = 0;
+        lead[k] = own[k] = false;
+        e[k] = v[k] = 0;
+        if (k < Cw) {
+          ldr[k] = __ffs(__match_any_sync(FULL, kk[k])) - 1;
+          lead[k] = kk[k] != 0 && lane == ldr[k];
+          if (lead[k]) e[k] = dd_home(sT, S, kk[k]);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < MAXC; ++k)
+        if (lead[k]) v[k] = __ldcg(&S.hkeys[e[k]]);
+#pragma unroll
+      for (int k = 0; k < MAXC; ++k)
+        if (lead[k] && v[k] == 0) {
+          v[k] = atomicCAS((unsigned long long*)&S.hkeys[e[k]], 0ull, (unsigned long long)kk[k]);
+          own[k] = v[k] == 0;
+        }
+#pragma unroll
+      for (int k = 0; k < MAXC; ++k)
+        if (lead[k] && !own[k] && v[k] != kk[k]) {
+          bool o = false;
+          u64 j = 0;
+          const u64 e1 = dd_step(S, e[k], j);
+          e[k] = (u64)dd_insert(S, kk[k], e1, j, &o);
+          own[k] = o;
+        }
+      bool app[MAXC];
+      unsigned bal[MAXC];
+      int P0[MAXC];
+      bool uni = true;
+#pragma unroll
+      for (int k = 0; k < MAXC; ++k) {
+        app[k] = false;
+        bal[k] = 0;
+        P0[k] = 0;
+        if (k < Cw) {
+          const int ek = __shfl_sync(FULL, (int)e[k], ldr[k]);
+          e[k] = (u64)ek;
+          S.hj[k * S.ns + slot] = kk[k] ? (ek | (own[k] ? HJ_OWN : 0)) : -1;
+          app[k] = own[k] && Pk[k] <= FASTP;
+          bal[k] = __ballot_sync(FULL, app[k]);
+          if (bal[k]) {
+            P0[k] = __shfl_sync(FULL, Pk[k], __ffs(bal[k]) - 1);
+            uni = uni && __ballot_sync(FULL, app[k] && Pk[k] == P0[k]) == bal[k];
           }
-          pend &= ~bal;
+        } else {
+          S.hj[k * S.ns + slot] = -1;
+        }
+      }
+      if (uni) {
+        // one depth per class (range lists: a chunk is one template): lane k
+        // reserves class k's appends, all reservations in flight at once
+        unsigned long long o = 0;
+#pragma unroll
+        for (int k = 0; k < MAXC; ++k)
+          if (lane == k && bal[k]) o = atomicAdd(&S.counters[CNT_PART + P0[k]], (unsigned long long)__popc(bal[k]));
+#pragma unroll
+        for (int k = 0; k < MAXC; ++k) {
+          const unsigned long long ok = __shfl_sync(FULL, o, k) + __popc(bal[k] & ((1u << lane) - 1));
+          if (app[k]) S.part[P0[k]][ok] = (int32_t)e[k];
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < MAXC; ++k) {
+          unsigned pend = bal[k];
+          while (pend) {
+            const int src = __ffs(pend) - 1;
+            const int PP = __shfl_sync(FULL, Pk[k], src);
+            const unsigned bb = __ballot_sync(FULL, app[k] && Pk[k] == PP);
+            unsigned long long o = 0;
+            if (lane == src) o = atomicAdd(&S.counters[CNT_PART + PP], (unsigned long long)__popc(bb));
+            o = __shfl_sync(FULL, o, src) + __popc(bb & ((1u << lane) - 1));
+            if (app[k] && Pk[k] == PP) {
+              S.part[PP][o] = (int32_t)e[k];
+              app[k] = false;
+            }
+            pend &= ~bb;
+          }
         }
       }
     }
@@ -1322,98 +1413,56 @@ __device__ __forceinline__ i64 slot_T(const Tables& sT, const Cands& c, const Sl
 #ifndef HSIM_FINALP_MINB
 #define HSIM_FINALP_MINB 4  // pruned K_final: 128 registers (measured: 4 beats 1, 6 and 8 on configs 2-4)
 #endif
-template <int MODE, bool BK>
-__global__ void __launch_bounds__(NT, MODE ? HSIM_FINALP_MINB : 1) k_final_small(const Tables* __restrict__ gT, Cands c, Scratch S, i64 ns,
-                                                    i64* __restrict__ out, int k, i64* __restrict__ lists) {
-  __shared__ Tables sT;
-  __shared__ i64 bt[NT / 32][32], bi[NT / 32][32];
-  load_tables(sT, gT);
+// offer each lane's (T, i) (valid = a finite key under the global bound) to
+// the warp's register top-k: many candidates (early in the scan) are sorted
+// across the warp (bitonic, 15 compare-exchange steps) and rank-merged with the
+// list, few are inserted one by one; then the global bound is lowered
+__device__ __forceinline__ void warp_offer(RegTopK& r, i64 T, i64 i, bool valid, int k, i64 (*bt)[32], i64 (*bi)[32],
+                                           unsigned long long* gthr) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const i64 wid = (i64)blockIdx.x * (NT / 32) + w;
-  const i64 nw = (i64)gridDim.x * (NT / 32);
-  i64* blist = lists + (i64)blockIdx.x * 2 * k;
-  unsigned long long* gthr = (unsigned long long*)(lists + (i64)gridDim.x * 2 * k);
-  unsigned long long nsync = 0;  // MODE >= 1: sum over the synced candidates of J = sum P - C + 1
-  RegTopK r;
-  r.init();
-  if (w == 0 && lane < k && blist[lane] != LIST_PAD && blist[lane] != KEY_INF) { r.t = blist[lane]; r.i = blist[k + lane]; }
-  SlotW nxt;
-  if (wid * 32 < ns) nxt = slot_load(S, wid * 32 + lane);
-  for (i64 base = wid * 32; base < ns; base += nw * 32) {
-    const SlotW cur = nxt;
-    if (base + nw * 32 < ns) nxt = slot_load(S, base + nw * 32 + lane);  // next chunk's loads in flight
-    i64 t, i;
-    const i64 g = (i64)*(volatile unsigned long long*)gthr;
-    i64 thT = __shfl_sync(FULL, (long long)r.t, k - 1), thI = __shfl_sync(FULL, (long long)r.i, k - 1);
-    i64 T;
-    if constexpr (MODE == 0) {
-      T = slot_T(sT, c, cur, &t, &i);
-      if (out && t >= 0) out[t] = T;
-    } else {
-      SlotW z = cur;
-      z.ex = 0;
-      T = slot_T(sT, c, z, &t, &i);  // T0 (or the status)
-      const i64 slot = base + lane;
-      if (t >= 0 && T >= 0 && T <= g && T <= thT) {
-        const TplRec& tp = sT.tpl[cur.tau];
-        if (tp.D > 1) {
-          if constexpr (MODE == 1) T += sync_any<BK>(sT, tp, S, slot, 0);
-          else T = sync_overlap_any<BK>(sT, tp, S, slot, T);
-          int sp = 0;
-          for (int q = 0; q < tp.C; ++q) sp += crec_hdr(sT, tp.crec[q])->P;
-          nsync += (unsigned long long)(sp - tp.C + 1);
-        }
-      } else if (T >= 0) {
-        T = KEY_INF;  // pruned: cannot enter the top-k
+  i64 thT = __shfl_sync(FULL, (long long)r.t, k - 1), thI = __shfl_sync(FULL, (long long)r.i, k - 1);
+  unsigned cand = __ballot_sync(FULL, valid && key_less(T, i, thT, thI));
+  if (!cand) return;
+  if (__popc(cand) > 6) {
+    const bool mine = cand >> lane & 1;
+    i64 bt_ = mine ? T : KEY_INF, bi_ = mine ? i : KEY_INF;
+#pragma unroll
+    for (int size = 2; size <= 32; size <<= 1)
+#pragma unroll
+      for (int stride = size >> 1; stride > 0; stride >>= 1) {
+        const i64 ot = __shfl_xor_sync(FULL, (long long)bt_, stride), oi = __shfl_xor_sync(FULL, (long long)bi_, stride);
+        const bool up = (lane & size) == 0, lower = (lane & stride) == 0;
+        const bool olt = key_less(ot, oi, bt_, bi_);
+        if (lower == up ? olt : !olt && !(ot == bt_ && oi == bi_)) { bt_ = ot; bi_ = oi; }
       }
+    // rank merge of the sorted lists A = r (lane j = j-th) and B = (bt_, bi_)
+    int lo = 0, hi = 32;  // #B < A[lane]
+#pragma unroll
+    for (int it = 0; it < 6; ++it) {
+      const int mid = (lo + hi) >> 1;
+      const int src = mid < 32 ? mid : 31;
+      const i64 mt = __shfl_sync(FULL, (long long)bt_, src), mi = __shfl_sync(FULL, (long long)bi_, src);
+      if (lo < hi) { if (key_less(mt, mi, r.t, r.i)) lo = mid + 1; else hi = mid; }
     }
-    unsigned cand = __ballot_sync(FULL, t >= 0 && T >= 0 && T != KEY_INF && T <= g && key_less(T, i, thT, thI));
-    if (!cand) continue;
-    if (__popc(cand) > 6) {
-      // many candidates (early in the scan): sort them across the warp
-      // (bitonic, 15 compare-exchange steps) and merge with the list by rank
-      // instead of one insert per candidate
-      const bool mine = cand >> lane & 1;
-      i64 bt_ = mine ? T : KEY_INF, bi_ = mine ? i : KEY_INF;
+    const int pa = lane + lo;
+    int lo2 = 0, hi2 = 32;  // #A < B[lane]
 #pragma unroll
-      for (int size = 2; size <= 32; size <<= 1)
-#pragma unroll
-        for (int stride = size >> 1; stride > 0; stride >>= 1) {
-          const i64 ot = __shfl_xor_sync(FULL, (long long)bt_, stride), oi = __shfl_xor_sync(FULL, (long long)bi_, stride);
-          const bool up = (lane & size) == 0, lower = (lane & stride) == 0;
-          const bool olt = key_less(ot, oi, bt_, bi_);
-          if (lower == up ? olt : !olt && !(ot == bt_ && oi == bi_)) { bt_ = ot; bi_ = oi; }
-        }
-      // rank merge of the sorted lists A = r (lane j = j-th) and B = (bt_, bi_)
-      int lo = 0, hi = 32;  // #B < A[lane]
-#pragma unroll
-      for (int it = 0; it < 6; ++it) {
-        const int mid = (lo + hi) >> 1;
-        const int src = mid < 32 ? mid : 31;
-        const i64 mt = __shfl_sync(FULL, (long long)bt_, src), mi = __shfl_sync(FULL, (long long)bi_, src);
-        if (lo < hi) { if (key_less(mt, mi, r.t, r.i)) lo = mid + 1; else hi = mid; }
-      }
-      const int pa = lane + lo;
-      int lo2 = 0, hi2 = 32;  // #A < B[lane]
-#pragma unroll
-      for (int it = 0; it < 6; ++it) {
-        const int mid = (lo2 + hi2) >> 1;
-        const int src = mid < 32 ? mid : 31;
-        const i64 mt = __shfl_sync(FULL, (long long)r.t, src), mi = __shfl_sync(FULL, (long long)r.i, src);
-        if (lo2 < hi2) { if (key_less(mt, mi, bt_, bi_)) lo2 = mid + 1; else hi2 = mid; }
-      }
-      const int pb = lane + lo2;
-      __syncwarp();
-      if (pa < 32) { bt[w][pa] = r.t; bi[w][pa] = r.i; }
-      if (pb < 32) { bt[w][pb] = bt_; bi[w][pb] = bi_; }
-      __syncwarp();
-      r.t = bt[w][lane];
-      r.i = bi[w][lane];
-      __syncwarp();
-      thT = __shfl_sync(FULL, (long long)r.t, k - 1);
-      if (lane == 0 && thT != KEY_INF) atomicMin(gthr, (unsigned long long)thT);
-      continue;
+    for (int it = 0; it < 6; ++it) {
+      const int mid = (lo2 + hi2) >> 1;
+      const int src = mid < 32 ? mid : 31;
+      const i64 mt = __shfl_sync(FULL, (long long)r.t, src), mi = __shfl_sync(FULL, (long long)r.i, src);
+      if (lo2 < hi2) { if (key_less(mt, mi, bt_, bi_)) lo2 = mid + 1; else hi2 = mid; }
     }
+    const int pb = lane + lo2;
+    __syncwarp();
+    if (pa < 32) { bt[w][pa] = r.t; bi[w][pa] = r.i; }
+    if (pb < 32) { bt[w][pb] = bt_; bi[w][pb] = bi_; }
+    __syncwarp();
+    r.t = bt[w][lane];
+    r.i = bi[w][lane];
+    __syncwarp();
+    thT = __shfl_sync(FULL, (long long)r.t, k - 1);
+  } else {
     while (cand) {
       const int src = __ffs(cand) - 1;
       cand &= cand - 1;
@@ -1424,7 +1473,96 @@ __global__ void __launch_bounds__(NT, MODE ? HSIM_FINALP_MINB : 1) k_final_small
         thI = __shfl_sync(FULL, (long long)r.i, k - 1);
       }
     }
-    if (lane == 0 && thT != KEY_INF) atomicMin(gthr, (unsigned long long)thT);
+  }
+  if (lane == 0 && thT != KEY_INF) atomicMin(gthr, (unsigned long long)thT);
+}
+
+// pruned K_final (MODE >= 1): sync the queue's entries [qn - cnt, qn)
+// (cnt <= 32), one per lane, each re-checked against the (meanwhile lower)
+// bound first, and offer them to the warp's top-k
+template <int MODE, bool BK>
+__device__ __forceinline__ void drain_sync(const Tables& sT, const Scratch& S, RegTopK& r, int& qn, int cnt, const int32_t* qs,
+                                           const i64* q0, const i64* qi, unsigned long long* gthr, int k, i64 (*bt)[32],
+                                           i64 (*bi)[32], unsigned long long& nsync) {
+  const int lane = threadIdx.x & 31;
+  const bool has = lane < cnt;
+  const int e = qn - cnt + lane;
+  const i64 slot = has ? qs[e] : 0, T0 = has ? q0[e] : KEY_INF, i = has ? qi[e] : KEY_INF;
+  __syncwarp();
+  qn -= cnt;
+  const i64 g = (i64)*(volatile unsigned long long*)gthr;
+  const i64 thT = __shfl_sync(FULL, (long long)r.t, k - 1);
+  i64 T = KEY_INF;
+  if (has && T0 <= g && T0 <= thT) {
+    const TplRec& tp = sT.tpl[S.tau[slot]];
+    if constexpr (MODE == 1) T = T0 + sync_any<BK>(sT, tp, S, slot, 0);
+    else T = sync_overlap_any<BK>(sT, tp, S, slot, T0);
+    int sp = 0;
+    for (int q = 0; q < tp.C; ++q) sp += crec_hdr(sT, tp.crec[q])->P;
+    nsync += (unsigned long long)(sp - tp.C + 1);
+  }
+  warp_offer(r, T, i, T != KEY_INF && T <= (i64)*(volatile unsigned long long*)gthr, k, bt, bi, gthr);
+}
+
+template <int MODE, bool BK>
+__global__ void __launch_bounds__(NT, MODE ? HSIM_FINALP_MINB : 1) k_final_small(const Tables* __restrict__ gT, Cands c, Scratch S, i64 ns,
+                                                    i64* __restrict__ out, int k, i64* __restrict__ lists) {
+  __shared__ Tables sT;
+  __shared__ i64 bt[NT / 32][32], bi[NT / 32][32];
+  // MODE >= 1: per-warp queue of the candidates whose sync must be computed
+  // (T0 under the bound), drained 32 at a time so the sync runs with every
+  // lane busy instead of the few lanes of a chunk that pass the bound
+  constexpr int QN = MODE ? 64 : 1;
+  __shared__ int32_t qs[NT / 32][QN];
+  __shared__ i64 q0[NT / 32][QN], qi[NT / 32][QN];
+  load_tables(sT, gT);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const i64 wid = (i64)blockIdx.x * (NT / 32) + w;
+  const i64 nw = (i64)gridDim.x * (NT / 32);
+  i64* blist = lists + (i64)blockIdx.x * 2 * k;
+  unsigned long long* gthr = (unsigned long long*)(lists + (i64)gridDim.x * 2 * k);
+  unsigned long long nsync = 0;  // MODE >= 1: sum over the synced candidates of J = sum P - C + 1
+  RegTopK r;
+  r.init();
+  if (w == 0 && lane < k && blist[lane] != LIST_PAD && blist[lane] != KEY_INF) { r.t = blist[lane]; r.i = blist[k + lane]; }
+  int qn = 0;  // queued entries (warp-uniform)
+  SlotW nxt;
+  if (wid * 32 < ns) nxt = slot_load(S, wid * 32 + lane);
+  for (i64 base = wid * 32; base < ns; base += nw * 32) {
+    const SlotW cur = nxt;
+    if (base + nw * 32 < ns) nxt = slot_load(S, base + nw * 32 + lane);  // next chunk's loads in flight
+    i64 t, i;
+    const i64 g = (i64)*(volatile unsigned long long*)gthr;
+    const i64 thT = __shfl_sync(FULL, (long long)r.t, k - 1), thI = __shfl_sync(FULL, (long long)r.i, k - 1);
+    i64 T;
+    if constexpr (MODE == 0) {
+      T = slot_T(sT, c, cur, &t, &i);
+      if (out && t >= 0) out[t] = T;
+      warp_offer(r, T, i, t >= 0 && T >= 0 && T <= g, k, bt, bi, gthr);
+    } else {
+      SlotW z = cur;
+      z.ex = 0;
+      T = slot_T(sT, c, z, &t, &i);  // T0 (or the status)
+      const bool live = t >= 0 && T >= 0 && T <= g && T <= thT;
+      const bool needs = live && sT.tpl[cur.tau].D > 1;
+      // D = 1: no sync, T = T0 now; D > 1: queued
+      warp_offer(r, T, i, live && !needs, k, bt, bi, gthr);
+      const unsigned nb = __ballot_sync(FULL, needs);
+      if (nb) {
+        const int pos = qn + __popc(nb & ((1u << lane) - 1));
+        if (needs) {
+          qs[w][pos] = (int32_t)(base + lane);
+          q0[w][pos] = T;
+          qi[w][pos] = i;
+        }
+        __syncwarp();
+        qn += __popc(nb);
+        if (qn >= 32) drain_sync<MODE, BK>(sT, S, r, qn, 32, qs[w], q0[w], qi[w], gthr, k, bt, bi, nsync);
+      }
+    }
+  }
+  if constexpr (MODE != 0) {
+    if (qn > 0) drain_sync<MODE, BK>(sT, S, r, qn, qn, qs[w], q0[w], qi[w], gthr, k, bt, bi, nsync);
   }
   bt[w][lane] = r.t;
   bi[w][lane] = r.i;
