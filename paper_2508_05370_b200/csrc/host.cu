@@ -139,7 +139,7 @@ struct hsim_handle {
   i64* d_sync_units = nullptr;  // the last top-k call's synced-segment counter (pruned K_final), or nullptr
   void* d_flow = nullptr;     // f3 scratch (flow.cu)
   size_t flow_cap = 0;
-  static constexpr int NSIDE = 20, NEV = 48;
+  static constexpr int NSIDE = 22, NEV = 48;  // sides 20, 21: K_pipe_multi<1,8>, <9,16>
   cudaStream_t side[NSIDE] = {};     // one stream per phase-kernel type + the final stream
   cudaEvent_t ev_fork = nullptr, ev_join[NSIDE] = {}, ev_pool[NEV] = {};
   int32_t last_launches = 0;
@@ -1005,7 +1005,7 @@ void hsim_handle::upload() {
   cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
   for (int q = 0; q < NSIDE; ++q) {
 #ifndef HSIM_NOPRIO
-    const int prio = (q >= 9 && q <= 17) ? prio_hi : prio_lo;
+    const int prio = (q >= 9 && q <= 17) || q >= 20 ? prio_hi : prio_lo;
 #else
     const int prio = prio_lo;
 #endif

@@ -126,6 +126,8 @@ constexpr unsigned FULL = 0xffffffffu;
 constexpr int CNT_DEEP = 17, CNT_NDEEP = 18, CNT_CELLS = 19, CNT_FULL = 20, CNT_PART = 40, CNT_REQ = 55, NCNT = 64;
 // V.2 (interleaved 1F1B): #jobs in the K_ilv list, K_ilv's work counter
 constexpr int CNT_ILV = 37, CNT_ILVW = 38;
+// K_pipe_multi's work counters (depths 1..8, 9..16)
+constexpr int CNT_MULTI = 39, CNT_MULTI2 = 0;  // (slot 0: no depth 0)
 // re-queued jobs of depth P (lane compaction), P in [2, HSIM_REQ_MAXP]: count at CNT_REQ + P
 #ifndef HSIM_REQ_MAXP
 #define HSIM_REQ_MAXP 8
@@ -243,20 +245,23 @@ __device__ __forceinline__ ClassSplit dd_split(const Tables& T, int32_t off, con
 // bucket = hash(group, x >> 5), entry = bucket * 32 + (x & 31).  Probing
 // steps by one bucket at the same offset (coalescing kept on collisions);
 // after nb steps the offset advances, so the sequence visits every entry.
-__device__ __forceinline__ u64 dd_mix(u64 x) {  // splitmix64 finaliser
-  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
-  x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
-  return x ^ (x >> 31);
+__device__ __forceinline__ u32 dd_mix32(u32 h) {  // murmur3 finaliser
+  h ^= h >> 16;
+  h *= 0x85EBCA6Bu;
+  h ^= h >> 13;
+  h *= 0xC2B2AE35u;
+  return h ^ (h >> 16);
 }
 __device__ __forceinline__ u64 dd_home(const Tables& T, const Scratch& S, u64 key) {
   const u64 kr = key - 1;
   const int sd = T.dd_wt + 2;
   const u64 dmask = (((u64)1 << T.dd_wd) - 1) << sd;
-  const u64 dig = (kr & dmask) >> sd;
-  const u64 h = dd_mix((kr & ~dmask) + 0x9E3779B97F4A7C15ull);
-  const u64 x = dig + (h & 31);
-  const u64 bk = dd_mix(h ^ ((x >> 5) * 0xD1B54A32D192ED03ull)) >> (64 - (S.hbits - 5));
-  return bk << 5 | (x & 31);
+  const u32 dig = (u32)((kr & dmask) >> sd);
+  const u64 g = kr & ~dmask;
+  const u32 h = dd_mix32((u32)g * 0x9E3779B1u ^ (u32)(g >> 32) * 0x7FEB352Du);
+  const u32 x = dig + (h & 31);
+  const u32 bk = dd_mix32(h ^ (x >> 5) * 0x27D4EB2Fu) >> (32 - (S.hbits - 5));
+  return (u64)bk << 5 | (x & 31);
 }
 __device__ __forceinline__ u64 dd_step(const Scratch& S, u64 e, u64& j) {
   const u64 nb = (u64)1 << (S.hbits - 5);
@@ -557,6 +562,50 @@ __global__ void __launch_bounds__(NT, HSIM_SPLIT_MINB) k_split(const Tables* __r
 #ifndef HSIM_SYNC_MINB
 #define HSIM_SYNC_MINB 6
 #endif
+// one work item of depth P: the 32 jobs item * 32 + lane of its list (full
+// chunks' aligned groups first, then the packed partial list / the dedupe
+// entries); rq: unsettled jobs may re-queue to K_pipe_cont<P>
+template <int P>
+__device__ __forceinline__ void pipe_item(const Tables& sT, const Scratch& S, i64 item, i64 gfull, i64 npart, bool rq,
+                                          i64& cells) {
+  const int lane = threadIdx.x & 31;
+  const i64 q = item < gfull ? item * 32 + lane : (item - gfull) * 32 + lane;
+  if (item >= gfull && q >= npart) return;
+  const int job = item < gfull ? S.full[P][q] : S.part[P][q];
+  constexpr bool rqP = P >= HSIM_REQ_MINP && P <= HSIM_REQ_MAXP;
+  if (S.hkeys) {  // dedupe: job = a distinct pipeline's table entry
+    const DKey d = dd_unpack(sT, __ldcg(&S.hkeys[job]));
+    const int32_t off = sT.tpl[d.tau].crec[d.c];
+    const DeferCtx dc{rqP ? S.req[rqP ? P : 0] : nullptr, &S.counters[CNT_REQ + (rqP ? P : 0)], rqP ? S.req_cap[rqP ? P : 0] : 0,
+                      (i64)job << 16 | d.c};
+    const PipeOut r = class_pipes_inl<P>(sT, off, dd_split(sT, off, d), nullptr, 0, rqP && rq ? &dc : nullptr);
+    S.hres[job] = r.T0;
+#ifdef HSIM_WARPCELLS
+    cells += 32 * __reduce_max_sync(__activemask(), (unsigned)r.cells);
+#else
+    cells += r.cells;
+#endif
+    return;
+  }
+  const int c = job & 3;
+  const i64 slot = job >> 2;
+  const int tau = S.tau[slot];
+  if (tau < 0 || S.status[slot] != 0) return;
+  const TplRec& tp = sT.tpl[tau];
+  i64* R = S.Rs ? S.Rs + (i64)class_stage_off(sT, tp, c) * S.ns + slot : nullptr;
+  // depths gated off on the host have req_cap 0: the re-queue attempt fails
+  // and the lane continues in place (rare: only unsettled jobs try)
+  const DeferCtx dc{rqP ? S.req[rqP ? P : 0] : nullptr, &S.counters[CNT_REQ + (rqP ? P : 0)], rqP ? S.req_cap[rqP ? P : 0] : 0,
+                    slot << 16 | c};
+  const PipeOut r = class_pipes_inl<P>(sT, tp.crec[c], load_split(S, c, tp.C, slot), R, S.ns, rqP && rq ? &dc : nullptr);
+  S.Tc[c * S.ns + slot] = r.T0;
+#ifdef HSIM_WARPCELLS  // diagnostic: count mode reports warp-slot cells (32 x warp max)
+  cells += 32 * __reduce_max_sync(__activemask(), (unsigned)r.cells);
+#else
+  cells += r.cells;
+#endif
+}
+
 template <int P>
 __global__ void __launch_bounds__(NT, P <= 4 ? HSIM_PIPE_MINB : 1) k_pipe(const Tables* __restrict__ gT, Scratch S, int count) {
   __shared__ Tables sT;
@@ -570,41 +619,61 @@ __global__ void __launch_bounds__(NT, P <= 4 ? HSIM_PIPE_MINB : 1) k_pipe(const 
     if (lane == 0) item = (i64)atomicAdd(&S.counters[P], 1ull);
     item = __shfl_sync(FULL, item, 0);
     if (item >= items) break;
-    const i64 q = item < gfull ? item * 32 + lane : (item - gfull) * 32 + lane;
-    if (item >= gfull && q >= npart) continue;
-    const int job = item < gfull ? S.full[P][q] : S.part[P][q];
-    constexpr bool rq = P >= HSIM_REQ_MINP && P <= HSIM_REQ_MAXP;
-    if (S.hkeys) {  // dedupe: job = a distinct pipeline's table entry
-      const DKey d = dd_unpack(sT, __ldcg(&S.hkeys[job]));
-      const int32_t off = sT.tpl[d.tau].crec[d.c];
-      const DeferCtx dc{rq ? S.req[rq ? P : 0] : nullptr, &S.counters[CNT_REQ + (rq ? P : 0)], rq ? S.req_cap[rq ? P : 0] : 0,
-                        (i64)job << 16 | d.c};
-      const PipeOut r = class_pipes_inl<P>(sT, off, dd_split(sT, off, d), nullptr, 0, rq ? &dc : nullptr);
-      S.hres[job] = r.T0;
-#ifdef HSIM_WARPCELLS
-      cells += 32 * __reduce_max_sync(__activemask(), (unsigned)r.cells);
-#else
-      cells += r.cells;
-#endif
-      continue;
+    pipe_item<P>(sT, S, item, gfull, npart, true, cells);
+  }
+  if (count) {
+    cells = warp_sum(cells);
+    if (lane == 0 && cells) atomicAdd(&S.counters[CNT_CELLS], (unsigned long long)cells);
+  }
+}
+
+// K_pipe_multi: the register depths in `mask` (those with few jobs in the
+// space) in ONE launch instead of one each: a warp takes the next item of a
+// combined queue, deepest first (the longest chains start first), and runs
+// it with that depth's code.  Saves the staggered dispatch of many
+// latency-bound launches (~3.5 us apart on the front end); no re-queue.
+// Two instances: depths 1..8 and 9..16 (measured: one kernel for both
+// groups costs config 3 12.4 -> 14.9 ms; either group alone does not).
+template <int PLO, int PHI>
+__global__ void __launch_bounds__(NT, 1) k_pipe_multi(const Tables* __restrict__ gT, Scratch S, int count, uint32_t mask) {
+  __shared__ Tables sT;
+  load_tables(sT, gT);
+  const int lane = threadIdx.x & 31;
+  i64 cells = 0;
+  for (;;) {
+    i64 item = 0;
+    if (lane == 0) item = (i64)atomicAdd(&S.counters[PLO == 1 ? CNT_MULTI : CNT_MULTI2], 1ull);
+    item = __shfl_sync(FULL, item, 0);
+    int P = 0;
+    i64 gfull = 0, npart = 0;
+    for (int d = PHI; d >= PLO; --d) {
+      if (!(mask >> d & 1)) continue;
+      const i64 nf = (i64)S.counters[CNT_FULL + d], np = (i64)S.counters[CNT_PART + d];
+      const i64 it = nf / 32 + (np + 31) / 32;
+      if (item < it) {
+        P = d;
+        gfull = nf / 32;
+        npart = np;
+        break;
+      }
+      item -= it;
     }
-    const int c = job & 3;
-    const i64 slot = job >> 2;
-    const int tau = S.tau[slot];
-    if (tau < 0 || S.status[slot] != 0) continue;
-    const TplRec& tp = sT.tpl[tau];
-    i64* R = S.Rs ? S.Rs + (i64)class_stage_off(sT, tp, c) * S.ns + slot : nullptr;
-    // depths gated off on the host have req_cap 0: the re-queue attempt fails
-    // and the lane continues in place (rare: only unsettled jobs try)
-    const DeferCtx dc{rq ? S.req[rq ? P : 0] : nullptr, &S.counters[CNT_REQ + (rq ? P : 0)], rq ? S.req_cap[rq ? P : 0] : 0,
-                      slot << 16 | c};
-    const PipeOut r = class_pipes_inl<P>(sT, tp.crec[c], load_split(S, c, tp.C, slot), R, S.ns, rq ? &dc : nullptr);
-    S.Tc[c * S.ns + slot] = r.T0;
-#ifdef HSIM_WARPCELLS  // diagnostic: count mode reports warp-slot cells (32 x warp max)
-    cells += 32 * __reduce_max_sync(__activemask(), (unsigned)r.cells);
-#else
-    cells += r.cells;
+    if (!P) break;
+    if constexpr (PLO == 1) {
+      switch (P) {
+#define HSIM_MC(PP) case PP: pipe_item<PP>(sT, S, item, gfull, npart, false, cells); break;
+        HSIM_MC(1) HSIM_MC(2) HSIM_MC(3) HSIM_MC(4) HSIM_MC(5) HSIM_MC(6) HSIM_MC(7) HSIM_MC(8)
+        default: break;
+      }
+    } else {
+      switch (P) {
+#if HSIM_FASTP >= 16
+        HSIM_MC(9) HSIM_MC(10) HSIM_MC(11) HSIM_MC(12) HSIM_MC(13) HSIM_MC(14) HSIM_MC(15) HSIM_MC(16)
 #endif
+#undef HSIM_MC
+        default: break;
+      }
+    }
   }
   if (count) {
     cells = warp_sum(cells);
@@ -1354,6 +1423,26 @@ struct RegTopK {
 // loaded up front (independent loads, one memory latency instead of a chain);
 // rows / words that do not apply to the slot (empty slot, invalid split,
 // classes >= C) are read but ignored.
+// K_gather (dedupe): T0 of every slot = max over its classes' table entries
+// (thread per slot, all loads independent across threads: the gathers of the
+// whole batch in flight at once instead of on K_final's per-chunk chain);
+// the creator of an entry clears its key for the next call
+__global__ void __launch_bounds__(NT) k_gather(Scratch S, i64 ns) {
+  for (i64 slot = (i64)blockIdx.x * NT + threadIdx.x; slot < ns; slot += (i64)gridDim.x * NT) {
+    int32_t hj[MAXC];
+#pragma unroll
+    for (int q = 0; q < MAXC; ++q) hj[q] = __ldcs(&S.hj[q * S.ns + slot]);
+    i64 T0 = 0;
+#pragma unroll
+    for (int q = 0; q < MAXC; ++q)
+      if (hj[q] >= 0) {
+        T0 = imax(T0, __ldcg(&S.hres[hj[q] & HJ_MASK]));
+        if (hj[q] & HJ_OWN) S.hkeys[hj[q] & HJ_MASK] = 0;
+      }
+    S.Tc[slot] = T0;
+  }
+}
+
 struct SlotW {
   i64 t, ex, tc[MAXC];
   int tau, st;
@@ -1364,15 +1453,10 @@ __device__ __forceinline__ SlotW slot_load(const Scratch& S, i64 slot) {
   w.tau = __ldcs(&S.tau[slot]);
   w.st = __ldcs(&S.status[slot]);
   w.ex = __ldcs(&S.extra[slot]);
-  if (S.hkeys) {  // dedupe: the class's table entry; its creator clears the key for the next call
-    int32_t hj[MAXC];
+  if (S.hkeys) {  // dedupe: K_gather left the slot's T0 in row 0
+    w.tc[0] = __ldcs(&S.Tc[slot]);
 #pragma unroll
-    for (int q = 0; q < MAXC; ++q) hj[q] = __ldcs(&S.hj[q * S.ns + slot]);
-#pragma unroll
-    for (int q = 0; q < MAXC; ++q) {
-      w.tc[q] = hj[q] >= 0 ? __ldcg(&S.hres[hj[q] & HJ_MASK]) : 0;
-      if (hj[q] >= 0 && (hj[q] & HJ_OWN)) S.hkeys[hj[q] & HJ_MASK] = 0;
-    }
+    for (int q = 1; q < MAXC; ++q) w.tc[q] = 0;
     return w;
   }
 #pragma unroll
@@ -1780,7 +1864,7 @@ __global__ void __launch_bounds__(1024) k_merge_thresh(const i64* __restrict__ b
   // every (list, position) pair is an independent load (no walk down a list:
   // the loads of a thread's pairs are all in flight at once)
   const int tot = nblk * k;
-#pragma unroll 4
+#pragma unroll 8
   for (int e = tid; e < tot; e += 1024) {
     const int b = e / k, p = e - b * k;
     const i64* L = blk + (i64)b * 2 * k;
@@ -1797,6 +1881,18 @@ __global__ void __launch_bounds__(1024) k_merge_thresh(const i64* __restrict__ b
   const int n = cnt;
   if (n > CAP) {  // uniform branch
     merge_small_body(blk, nblk, k, out_t, out_i);
+    return;
+  }
+  if (n <= 1024) {
+    // few survivors (the usual case): each one's rank among them by one scan
+    // of the shared list (keys are unique: (T, index)), no barriers
+    if (tid < n) {
+      const i64 x = ct[tid], xi = ci[tid];
+      int rank = 0;
+      for (int j = 0; j < n; ++j) rank += key_less(ct[j], ci[j], x, xi);
+      if (rank < k) { out_t[rank] = x; out_i[rank] = xi; }
+    }
+    for (int r = n + tid; r < k; r += 1024) { out_t[r] = KEY_INF; out_i[r] = -1; }
     return;
   }
   int np = 32;
@@ -1855,8 +1951,17 @@ static int finish(hsim_handle* h, int launches) {
   return HSIM_OK;
 }
 
+#ifndef HSIM_MULTI_MAXJOBS
+#define HSIM_MULTI_MAXJOBS (1LL << 18)  // depths with fewer (candidate, class) jobs in the space go to K_pipe_multi
+#endif
+#ifndef HSIM_MULTI_PMIN
+#define HSIM_MULTI_PMIN 1
+#endif
+#ifndef HSIM_MULTI_PMAX
+#define HSIM_MULTI_PMAX 16
+#endif
 #ifndef HSIM_FINAL_MULT
-#define HSIM_FINAL_MULT 8  // K_final blocks per SM for k <= 32 (one top-k list per block)
+#define HSIM_FINAL_MULT 4  // K_final blocks per SM for k <= 32 (one top-k list per block; one wave of the pruned kernel at 4 resident: measured 4 beats 8 with the dedupe)
 #endif
 static int final_grid(const hsim_handle* h, int k) { return sm_count(h) * (k && k <= 32 ? HSIM_FINAL_MULT : 2); }
 
@@ -1866,8 +1971,8 @@ static int run_phases(hsim_handle* h, const Tables* dT, Cands c, int64_t n, int6
                       int count, i64* cells_out, cudaStream_t st, int& launches) {
   // resident blocks per SM of each kernel, cached per handle
   int* gc = grid_cache(h);
-  int &g_split = gc[0], &g_deep = gc[1], &g_sync = gc[2], *g_pipe = gc + 3, *g_cont = gc + 3 + FASTP + 1;
-  static_assert(3 + 2 * (FASTP + 1) <= 64, "grid cache");
+  int &g_split = gc[0], &g_deep = gc[1], &g_sync = gc[2], *g_pipe = gc + 3, *g_cont = gc + 3 + FASTP + 1, &g_multi = gc[40], &g_multi2 = gc[41];
+  static_assert(3 + 2 * (FASTP + 1) <= 40, "grid cache");
   // chunk plan
   i64 nchunks;
   i64* hplan = nullptr;
@@ -2001,6 +2106,15 @@ static int run_phases(hsim_handle* h, const Tables* dT, Cands c, int64_t n, int6
   static const int order[16] = {4, 8, 16, 2, 6, 5, 3, 12, 10, 7, 9, 11, 13, 14, 15, 1};
 #endif
   cudaStream_t fin = side_stream(h, NSTREAM_FINAL);
+  // depths with few class-jobs in the space and no re-queue share one launch
+  // (K_pipe_multi); a depth alone keeps its own kernel
+  uint32_t mmask = 0;
+  for (int P = 1; P <= FASTP; ++P)
+    if ((pm >> P & 1) && depth_jobs_space(h, P) < HSIM_MULTI_MAXJOBS && (P > HSIM_REQ_MAXP || !reqcap[P]) &&
+        P >= HSIM_MULTI_PMIN && P <= HSIM_MULTI_PMAX)
+      mmask |= 1u << P;
+  if (__builtin_popcount(mmask & 0x1FEu) < 2) mmask &= ~0x1FEu;  // a group of one depth: its own kernel
+  if (__builtin_popcount(mmask & 0x1FE00u) < 2) mmask &= ~0x1FE00u;
   i64 cells = 0;
   int b = 0;
   for (i64 ca = 0; ca < nchunks; ca += cbatch, ++b) {
@@ -2043,9 +2157,26 @@ static int run_phases(hsim_handle* h, const Tables* dT, Cands c, int64_t n, int6
 #ifdef HSIM_DEEPFIRST
     launch_deep();  // the deepest pipelines first (latency-bound, high-priority stream)
 #endif
+    // the sparse depths in two launches (1..8, 9..16), first, on high-priority streams
+    if (mmask & 0x1FEu) {
+      cudaStream_t ss = side(20);
+      tq = g_trace.pre("k_pipe_multi<1,8>", 20, ss);
+      k_pipe_multi<1, 8><<<grid_of(h, k_pipe_multi<1, 8>, g_multi), NT, 0, ss>>>(dT, S, count, mmask);
+      g_trace.post(tq, ss);
+      ++launches;
+      join(ss);
+    }
+    if (mmask & 0x1FE00u) {
+      cudaStream_t ss = side(21);
+      tq = g_trace.pre("k_pipe_multi<9,16>", 21, ss);
+      k_pipe_multi<9, 16><<<grid_of(h, k_pipe_multi<9, 16>, g_multi2), NT, 0, ss>>>(dT, S, count, mmask);
+      g_trace.post(tq, ss);
+      ++launches;
+      join(ss);
+    }
     for (int oi = 0; oi < 16; ++oi) {
       const int P = order[oi];
-      if (P > FASTP || !(pm >> P & 1)) continue;
+      if (P > FASTP || !(pm >> P & 1) || (mmask >> P & 1)) continue;
       cudaStream_t ss = side(P);
       static const char* pn[17] = {"", "k_pipe<1>", "k_pipe<2>", "k_pipe<3>", "k_pipe<4>", "k_pipe<5>", "k_pipe<6>", "k_pipe<7>", "k_pipe<8>", "k_pipe<9>", "k_pipe<10>", "k_pipe<11>", "k_pipe<12>", "k_pipe<13>", "k_pipe<14>", "k_pipe<15>", "k_pipe<16>"};
       tq = g_trace.pre(pn[P], P, ss);
@@ -2132,6 +2263,12 @@ static int run_phases(hsim_handle* h, const Tables* dT, Cands c, int64_t n, int6
       g_trace.post(tq, ss);
       ++launches;
       join(ss);
+    }
+    if (dd) {  // dedupe: every slot's T0 from the table (K_final then reads it coalesced)
+      tq = g_trace.pre("k_gather", NSTREAM_FINAL, fin);
+      k_gather<<<sm_count(h) * 16, NT, 0, fin>>>(S, nsb);
+      g_trace.post(tq, fin);
+      ++launches;
     }
     tq = g_trace.pre("k_final", NSTREAM_FINAL, fin);
     if (prune) {

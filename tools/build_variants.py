@@ -7,6 +7,14 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2508_05370_b200 import build as B  # noqa: E402
 
 VARIANTS = {
+    "mp8": ["-DHSIM_MULTI_PMAX=8"],
+    "mp9": ["-DHSIM_MULTI_PMIN=9"],
+    "mlp": ["-DHSIM_MULTI_STREAM=3"],
+    "mg2": ["-DHSIM_MULTI_GRIDDIV=2"],
+    "mg4": ["-DHSIM_MULTI_GRIDDIV=4"],
+    "mm20": ["-DHSIM_MULTI_MAXJOBS=(1LL<<20)"],
+    "mm0": ["-DHSIM_MULTI_MAXJOBS=0"],
+    "mm22": ["-DHSIM_MULTI_MAXJOBS=(1LL<<22)"],
     "sp6": ["-DHSIM_SPLIT_MINB=6"],
     "sp8": ["-DHSIM_SPLIT_MINB=8"],
     "sp4": ["-DHSIM_SPLIT_MINB=4"],

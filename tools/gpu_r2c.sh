@@ -1,0 +1,10 @@
+set -x
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_dedup_gpu.py tests/test_parity_gpu.py -x -q > gpurun_out/r2c_test.log 2>&1; tail -3 gpurun_out/r2c_test.log
+for v in default nb2 fm4; do
+  if [ $v = default ]; then L=""; else L="HSIM_LIB=paper_2508_05370_b200/variants/libhsim_$v.so"; fi
+  for c in 2 4 3; do env $L timeout 120 python tools/variant_bench.py $c 20 >> gpurun_out/r2c_var.log 2>&1; done
+done
+cat gpurun_out/r2c_var.log
+timeout 120 python tools/mode_timing.py 2 > gpurun_out/r2c_modes.log 2>&1; cat gpurun_out/r2c_modes.log
+HSIM_TRACE=1 timeout 120 python tools/prof_sweep.py 2 3 > gpurun_out/r2c_trace.log 2>&1; tail -18 gpurun_out/r2c_trace.log

@@ -1,0 +1,7 @@
+set -x
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_dedup_gpu.py tests/test_parity_gpu.py tests/test_parity_gpu_r2.py -x -q > gpurun_out/r2d_test.log 2>&1; tail -3 gpurun_out/r2d_test.log
+for c in 2 4 3; do timeout 120 python tools/variant_bench.py $c 20 >> gpurun_out/r2d_var.log 2>&1; done
+cat gpurun_out/r2d_var.log
+HSIM_TRACE=1 timeout 120 python tools/prof_sweep.py 2 3 > gpurun_out/r2d_trace.log 2>&1; tail -18 gpurun_out/r2d_trace.log
+ncu --set full --clock-control none --import-source on -k regex:"k_final|k_gather|k_merge" -s 3 -c 3 -o gpurun_out/prof_r2d python tools/prof_sweep.py 2 2 > gpurun_out/ncu_r2d.log 2>&1

@@ -3,9 +3,11 @@
 import csv
 import io
 import subprocess
+import os
 import sys
 
 rep, rx = sys.argv[1], sys.argv[2]
+SORTI = int(os.environ.get("SORTI", "0"))
 top = int(sys.argv[3]) if len(sys.argv) > 3 else 30
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass", "-k", f"regex:{rx}"],
                      capture_output=True, text=True).stdout
@@ -34,5 +36,5 @@ for r in csv.reader(io.StringIO(out)):
 ts = sum(v[0] for v in agg.values()) or 1
 ti = sum(v[1] for v in agg.values()) or 1
 print(f"total samples {ts}, warp instructions {ti}")
-for (f, l), (s, i, src) in sorted(agg.items(), key=lambda x: -x[1][0])[:top]:
+for (f, l), (s, i, src) in sorted(agg.items(), key=lambda x: -x[1][SORTI])[:top]:
     print(f"{f}:{l:>5} stall {100 * s / ts:5.1f}%  inst {100 * i / ti:5.1f}%  {src.strip()[:90]}")
