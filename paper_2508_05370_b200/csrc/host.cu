@@ -1005,7 +1005,11 @@ void hsim_handle::upload() {
   cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
   for (int q = 0; q < NSIDE; ++q) {
 #ifndef HSIM_NOPRIO
+#ifdef HSIM_PRIO4
+    const int prio = (q >= 9 && q <= 17) || q >= 20 || q == 4 ? prio_hi : prio_lo;
+#else
     const int prio = (q >= 9 && q <= 17) || q >= 20 ? prio_hi : prio_lo;
+#endif
 #else
     const int prio = prio_lo;
 #endif

@@ -340,7 +340,7 @@ __device__ __forceinline__ int split_store(const Tables& T, const TplRec& tp, i6
 
 // ---- K_split -------------------------------------------------------------------
 #ifndef HSIM_SPLIT_MINB
-#define HSIM_SPLIT_MINB 6  // measured: 8 is ~1 % faster on range sweeps but ~8 % slower on explicit lists (e2e)
+#define HSIM_SPLIT_MINB 8  // measured with the dedupe: 8 beats 6 on configs 2-4 (0.301 -> 0.296 ms on config 2)
 #endif
 // ILV: V.2 (interleaved schedule) compiled in -- its partition rules and the
 // K_ilv job list; the default path carries none of it

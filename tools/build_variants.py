@@ -7,6 +7,9 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2508_05370_b200 import build as B  # noqa: E402
 
 VARIANTS = {
+    "prio4": ["-DHSIM_PRIO4"],
+    "norq2": ["-DHSIM_REQ_MINJOBS=(1LL<<40)"],
+    "fp3": ["-DHSIM_FINALP_MINB=3"],
     "mp8": ["-DHSIM_MULTI_PMAX=8"],
     "mp9": ["-DHSIM_MULTI_PMIN=9"],
     "mlp": ["-DHSIM_MULTI_STREAM=3"],

@@ -35,6 +35,10 @@ for cfg in cfgs:
     s.topk(16, n=m, first=first)
     s.topk(100, n=m, first=first)
     s.topk(8, n=min(m, 5000), first=0, block=1000, stride=3000) if N > 15000 else None
+    s.count_cells(first, min(m, 2000))  # count mode (the dedupe table is cleared by a memset there)
+    s.set_dedup(False)                  # the per-(candidate, class) path too
+    s.topk(16, n=min(m, 8000), first=first)
+    s.set_dedup(True)
     torch.cuda.synchronize()
     print("ok", cfg["name"], m, flush=True)
 lists = torch.full((4, 64), 2**63 - 1, dtype=torch.int64, device="cuda")
