@@ -128,6 +128,8 @@ struct hsim_handle {
   size_t work_cap = 0;
   TplRec* d_tpl = nullptr;
   i64* d_pool = nullptr;
+  std::vector<i64> wtab;      // partition weight table (host build, device copy)
+  i64* d_wtab = nullptr;
   int8_t* d_node_type = nullptr;
   std::vector<int8_t> node_type8;
   std::vector<int32_t> type_nodes;   // f3: node ids grouped by type
@@ -616,6 +618,7 @@ int32_t hsim_handle::crec(int bi, int M, int D, const std::vector<std::pair<int,
   hd.pw = 1;
   for (int q = 0; q < hd.nd; ++q) hd.pw *= (u32)(2 * md.r_layer + 1);
   hd.pwdiv = make_fastdiv(hd.pw);
+  hd.woff = -1;
   pw_max = std::max(pw_max, hd.pw);
   u_max = std::max(u_max, hd.U);
   pool.resize(off + HDR_WORDS + 16 * P + rep.size() * (P + 1));
@@ -948,6 +951,35 @@ void hsim_handle::prepare() {
       hT.nic_cap[t] = std::min(types[t].nic_gbps / 8.0, cd.rail_gbps / 8.0);
     }
   }
+  // partition weight table: every class record's rows for all
+  // of its boundary digits, while the total stays under 2^26 entries
+  wtab.clear();
+  for (auto& kv : crec_of) {
+    CrecHdr* hd = (CrecHdr*)&pool[kv.second];
+    const StageRec* st = (const StageRec*)&pool[kv.second + HDR_WORDS];
+    if (wtab.size() + hd->pw > ((size_t)1 << 26)) continue;
+    hd->woff = (int32_t)wtab.size();
+    const int r = md.r_layer, base = 2 * md.r_layer + 1;
+    for (u32 dig = 0; dig < hd->pw; ++dig) {
+      u32 dd = dig;
+      int dprev = 0, lmin = 1 << 30;
+      i64 worst = 0;
+      for (int s = 0; s < hd->P; ++s) {
+        int d = 0;
+        if (s < hd->nd) {
+          d = (int)(dd % (u32)base) - r;
+          dd /= (u32)base;
+        }
+        const int l = st[s].l0 + d - dprev;
+        dprev = d;
+        lmin = std::min(lmin, l);
+        worst = std::max(worst, (i64)l * st[s].tcomp + st[s].wext);
+      }
+      const i64 w = lmin >= 1 && worst > 0 ? ((i64)1 << 40) / worst : 0;
+      wtab.push_back(w | (i64)std::max(0, std::min(lmin, 65535)) << 48);
+    }
+  }
+  hT.wtab = nullptr;  // host paths walk the stages
   hT.tpl_prefix = prefix.data();
   hT.tpl = tpl.data();
   hT.pool = pool.data();
@@ -990,6 +1022,9 @@ void hsim_handle::upload() {
   ck(cudaMalloc(&d_type_nodes, std::max<size_t>(1, type_nodes.size()) * 4), "cudaMalloc type nodes");
   ck(cudaMemcpy(d_type_nodes, type_nodes.data(), type_nodes.size() * 4, cudaMemcpyHostToDevice), "H2D type nodes");
   dt.type_nodes = d_type_nodes;
+  ck(cudaMalloc(&d_wtab, std::max<size_t>(1, wtab.size()) * 8), "cudaMalloc wtab");
+  if (!wtab.empty()) ck(cudaMemcpy(d_wtab, wtab.data(), wtab.size() * 8, cudaMemcpyHostToDevice), "H2D wtab");
+  dt.wtab = d_wtab;
   ck(cudaMemcpy(dT, &dt, sizeof(Tables), cudaMemcpyHostToDevice), "H2D tables");
   int dev = 0;
   cudaGetDevice(&dev);
@@ -1104,6 +1139,7 @@ void hsim_destroy(hsim_handle* h) {
   cudaFree(h->d_work);
   cudaFree(h->d_tpl);
   cudaFree(h->d_pool);
+  cudaFree(h->d_wtab);
   cudaFree(h->d_node_type);
   cudaFree(h->d_type_nodes);
   cudaFree(h->dT);

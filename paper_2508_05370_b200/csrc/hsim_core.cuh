@@ -82,7 +82,7 @@ struct CrecHdr {
   int32_t P, D, U, nd;    // stages, replicas, sub-classes, #layer digits
   u32 pw;                 // (2 r_layer + 1)^nd: radix of the class's digit block
   FastDiv pwdiv;          // division by pw
-  int32_t _pad;
+  int32_t woff;           // offset of the class's rows in Tables.wtab, -1 = none
 };
 static_assert(sizeof(CrecHdr) == 32, "CrecHdr layout");
 // crec layout in the int64 pool: CrecHdr (4 x i64) | StageRec[P] (16 x i64 each) |
@@ -159,6 +159,11 @@ struct Tables {
   // plus 1 (0 = empty), with the field widths below; dd_ok = 0 when they
   // exceed 63 bits (dedupe then off).
   int32_t dd_ok, dd_wt, dd_wd, dd_wm, dd_wu, _pad8;
+  // partition weight table (device only; host: nullptr): for class record h
+  // and boundary digits dig, wtab[h.woff + dig] = floor(2^40 / max_s(l_s
+  // tcomp_s + wext_s)) | min_s(l_s) << 48 (w = 0 and min 0 when some l_s < 1)
+  // -- the per-candidate stage walk of step a1 precomputed per (class, digits)
+  const i64* wtab;
 };
 
 // --- C.0 --------------------------------------------------------------------
@@ -278,7 +283,18 @@ HD i64 find_template(const Tables& T, i64 i) {
 // subroutine; on the host the plain operators.  Exact either way.
 HD void divmod_est(i64 n, i64 d, i64& q, i64& r) {
 #ifdef __CUDA_ARCH__
-  q = (i64)floor((double)n / (double)d);
+  // 1/d from the hardware approximation (~2^-20) and two explicit Newton
+  // steps (error ~1 ulp; explicit fma, no contraction), so n * (1/d) is
+  // within 2^-11 of n / d for quotients < 2^40: the floor is off by at most
+  // one and the exact int64 remainder below fixes it
+  const double dd = (double)d;
+  double rc;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(rc) : "d"(dd));
+  double e = fma(-dd, rc, 1.0);
+  rc = fma(rc, e, rc);
+  e = fma(-dd, rc, 1.0);
+  rc = fma(rc, e, rc);
+  q = (i64)floor((double)n * rc);
   r = n - q * d;
   if (r < 0) { q -= 1; r += d; }
   if (r >= d) { q += 1; r -= d; }
@@ -345,9 +361,17 @@ HD int partition_c(const Tables& T, const TplRec& tp, i64 local, ClassSplit (&cs
     const u32 lq = h->pwdiv.div(loc);
     cs[c].dig = loc - lq * h->pw;
     loc = lq;
+    const int lmin = ILV && h->P >= 2 ? T.interleave : 1;  // V.2: every chunk holds a layer
+#ifdef __CUDA_ARCH__
+    if (T.wtab && h->woff >= 0) {  // precomputed per (class, digits)
+      const i64 e = __ldg(&T.wtab[h->woff + cs[c].dig]);
+      if ((int)(e >> 48) < lmin) status = -1;
+      w[c] = e & (((i64)1 << 48) - 1);
+      continue;
+    }
+#endif
     LayerWalk lw = walk(T, h, cs[c].dig);
     i64 worst = 0;
-    const int lmin = ILV && h->P >= 2 ? T.interleave : 1;  // V.2: every chunk holds a layer
     for (int s = 0; s < h->P; ++s) {
       const int l = lw.next(st);
       if (l < lmin) status = -1;
@@ -386,7 +410,16 @@ HD int partition_c(const Tables& T, const TplRec& tp, i64 local, ClassSplit (&cs
   const i64 Dl = D[C - 1];
   // |R| <= sum_c D_c r_batch and D_l are small: 32-bit floor division
   const int32_t R32 = (int32_t)R, D32 = (int32_t)Dl;
+#ifdef __CUDA_ARCH__
+  // floor(R / D): fp32 estimate (|R| < 2^24, off by at most one) + exact fix-up
+  int32_t f32 = (int32_t)floorf(__fdividef((float)R32, (float)D32));
+  const int32_t rr = R32 - f32 * D32;
+  if (rr < 0) f32 -= 1;
+  else if (rr >= D32) f32 += 1;
+  const i64 fl = f32;
+#else
   const i64 fl = R32 >= 0 ? R32 / D32 : -((-R32 + D32 - 1) / D32);
+#endif
   cs[C - 1].add = fl;
   cs[C - 1].rm = R - fl * Dl;
 #pragma unroll

@@ -557,7 +557,7 @@ __global__ void __launch_bounds__(NT, HSIM_SPLIT_MINB) k_split(const Tables* __r
 #define HSIM_NBATCH 1  // target number of batches per call (more only when the scratch cap forces it; measured: 1 beats 2 and 3 on config 2 once the deep tails were fixed)
 #endif
 #ifndef HSIM_PIPE_MINB
-#define HSIM_PIPE_MINB 8
+#define HSIM_PIPE_MINB 6  // measured with the dedupe: 6 beats 8 (and 4) on configs 2-4
 #endif
 #ifndef HSIM_SYNC_MINB
 #define HSIM_SYNC_MINB 6
