@@ -1884,15 +1884,42 @@ __global__ void __launch_bounds__(1024) k_merge_thresh(const i64* __restrict__ b
     return;
   }
   if (n <= 1024) {
-    // few survivors (the usual case): each one's rank among them by one scan
-    // of the shared list (keys are unique: (T, index)), no barriers
-    if (tid < n) {
-      const i64 x = ct[tid], xi = ci[tid];
-      int rank = 0;
-      for (int j = 0; j < n; ++j) rank += key_less(ct[j], ci[j], x, xi);
-      if (rank < k) { out_t[rank] = x; out_i[rank] = xi; }
+    // few survivors (the usual case; keys are unique: (T, index)): each warp
+    // sorts its 32 (bitonic, shuffles), the smallest warp k-th key bounds the
+    // top-k, and only the survivors under it are ranked against each other
+    const int lane = tid & 31, w = tid >> 5;
+    __shared__ i64 wk[32];
+    __shared__ int cnt2;
+    i64 x = tid < n ? ct[tid] : KEY_INF, xi = tid < n ? ci[tid] : KEY_INF;
+#pragma unroll
+    for (int size = 2; size <= 32; size <<= 1)
+#pragma unroll
+      for (int stride = size >> 1; stride > 0; stride >>= 1) {
+        const i64 ot = __shfl_xor_sync(FULL, (long long)x, stride), oi = __shfl_xor_sync(FULL, (long long)xi, stride);
+        const bool up = (lane & size) == 0, lower = (lane & stride) == 0;
+        const bool olt = key_less(ot, oi, x, xi);
+        if (lower == up ? olt : !olt && !(ot == x && oi == xi)) { x = ot; xi = oi; }
+      }
+    if (lane == k - 1) wk[w] = x;
+    if (tid == 0) cnt2 = 0;
+    __syncthreads();
+    i64 thr = KEY_INF;
+    for (int q = 0; q < 32; ++q) thr = imin(thr, wk[q]);
+    __syncthreads();  // every thread has read ct / ci (the compaction below overwrites them)
+    if (x != KEY_INF && x <= thr) {
+      const int pos = atomicAdd(&cnt2, 1);
+      ct[pos] = x;
+      ci[pos] = xi;
     }
-    for (int r = n + tid; r < k; r += 1024) { out_t[r] = KEY_INF; out_i[r] = -1; }
+    __syncthreads();
+    const int n2 = cnt2;
+    if (tid < n2) {
+      const i64 y = ct[tid], yi = ci[tid];
+      int rank = 0;
+      for (int j = 0; j < n2; ++j) rank += key_less(ct[j], ci[j], y, yi);
+      if (rank < k) { out_t[rank] = y; out_i[rank] = yi; }
+    }
+    for (int r = n2 + tid; r < k; r += 1024) { out_t[r] = KEY_INF; out_i[r] = -1; }
     return;
   }
   int np = 32;
