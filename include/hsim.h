@@ -255,7 +255,9 @@ int32_t hsim_last_launch_count(const hsim_handle* h);
  * micro-batches has 2 P m cells; the exact steady-regime jumps of DESIGN.md §5
  * skip some of them, and only the cells actually executed are counted (this is
  * the numerator of the ALU-roofline fraction in bench.py).  A re-queued job
- * (lane compaction) is counted once, by its complete run.  Returns -1 on error. */
+ * (lane compaction) is counted once, by its complete run; with the pipeline
+ * dedupe on (hsim_set_dedup) a class pipeline shared by several candidates of
+ * a batch is run, and counted, once.  Returns -1 on error. */
 int64_t hsim_count_cells(const hsim_handle* h, int64_t first, int64_t n);
 
 /* Gradient-sync work of the last hsim_topk call on this handle: with k <= 32
