@@ -1439,7 +1439,7 @@ __global__ void __launch_bounds__(NT) k_gather(Scratch S, i64 ns) {
         T0 = imax(T0, __ldcg(&S.hres[hj[q] & HJ_MASK]));
         if (hj[q] & HJ_OWN) S.hkeys[hj[q] & HJ_MASK] = 0;
       }
-    S.Tc[slot] = T0;
+    S.Tc[slot] = hj[0] >= 0 ? T0 : KEY_INF;  // no valid split: never a warp's best chunk (K_final)
   }
 }
 
@@ -1588,7 +1588,7 @@ __device__ __forceinline__ void drain_sync(const Tables& sT, const Scratch& S, R
   warp_offer(r, T, i, T != KEY_INF && T <= (i64)*(volatile unsigned long long*)gthr, k, bt, bi, gthr);
 }
 
-template <int MODE, bool BK>
+template <int MODE, bool BK, bool BF = false>
 __global__ void __launch_bounds__(NT, MODE ? HSIM_FINALP_MINB : 1) k_final_small(const Tables* __restrict__ gT, Cands c, Scratch S, i64 ns,
                                                     i64* __restrict__ out, int k, i64* __restrict__ lists) {
   __shared__ Tables sT;
@@ -1610,11 +1610,39 @@ __global__ void __launch_bounds__(NT, MODE ? HSIM_FINALP_MINB : 1) k_final_small
   r.init();
   if (w == 0 && lane < k && blist[lane] != LIST_PAD && blist[lane] != KEY_INF) { r.t = blist[lane]; r.i = blist[k + lane]; }
   int qn = 0;  // queued entries (warp-uniform)
+  // the warp's chunks first + j * step, j < nch, visited from its best chunk
+  // (smallest T0, dedupe mode: K_gather's row) and its sync drained at once:
+  // the warp's first synced candidates then set a tight list bound and a tight
+  // global bound, instead of whatever its first chunk in index order holds.
+  // First batch of a call only (BF): later batches start with the bound the
+  // earlier ones left and run the BF = false instance (measured: the scan,
+  // and the registers it takes, cost config 3 2-4 % when every batch runs it)
+  const i64 first = wid * 32, step = nw * 32;
+  const i64 nch = first < ns ? (ns - first + step - 1) / step : 0;
+  i64 jbest = 0;
+  if (BF && MODE != 0 && S.hkeys && nch > 1) {
+    i64 bT = KEY_INF, bj = 0;
+#pragma unroll 4
+    for (i64 j = 0; j < nch; ++j) {
+      const i64 v = __ldcg(&S.Tc[first + j * step + lane]);
+      if (v < bT) { bT = v; bj = j; }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const i64 ot = __shfl_xor_sync(FULL, (long long)bT, o), oj = __shfl_xor_sync(FULL, (long long)bj, o);
+      if (ot < bT || (ot == bT && oj < bj)) { bT = ot; bj = oj; }
+    }
+    jbest = bj;
+  }
   SlotW nxt;
-  if (wid * 32 < ns) nxt = slot_load(S, wid * 32 + lane);
-  for (i64 base = wid * 32; base < ns; base += nw * 32) {
+  i64 nbase = first + jbest * step;  // the chunk after the current one (wrapping to the warp's first)
+  if (nch > 0) nxt = slot_load(S, nbase + lane);
+  for (i64 j = 0; j < nch; ++j) {
+    const i64 base = nbase;
+    nbase += step;
+    if (nbase >= ns) nbase = first;
     const SlotW cur = nxt;
-    if (base + nw * 32 < ns) nxt = slot_load(S, base + nw * 32 + lane);  // next chunk's loads in flight
+    if (j + 1 < nch) nxt = slot_load(S, nbase + lane);  // next chunk's loads in flight
     i64 t, i;
     const i64 g = (i64)*(volatile unsigned long long*)gthr;
     const i64 thT = __shfl_sync(FULL, (long long)r.t, k - 1), thI = __shfl_sync(FULL, (long long)r.i, k - 1);
@@ -1643,6 +1671,7 @@ __global__ void __launch_bounds__(NT, MODE ? HSIM_FINALP_MINB : 1) k_final_small
         qn += __popc(nb);
         if (qn >= 32) drain_sync<MODE, BK>(sT, S, r, qn, 32, qs[w], q0[w], qi[w], gthr, k, bt, bi, nsync);
       }
+      if (BF && j == 0 && qn > 0) drain_sync<MODE, BK>(sT, S, r, qn, qn, qs[w], q0[w], qi[w], gthr, k, bt, bi, nsync);
     }
   }
   if constexpr (MODE != 0) {
@@ -2303,7 +2332,9 @@ static int run_phases(hsim_handle* h, const Tables* dT, Cands c, int64_t n, int6
         if (bkt) k_final_small<2, true><<<gf, NT, 0, fin>>>(dT, c, S, nsb, out_ns, k, lists);
         else k_final_small<2, false><<<gf, NT, 0, fin>>>(dT, c, S, nsb, out_ns, k, lists);
       } else {
-        if (bkt) k_final_small<1, true><<<gf, NT, 0, fin>>>(dT, c, S, nsb, out_ns, k, lists);
+        if (bkt && b == 0) k_final_small<1, true, true><<<gf, NT, 0, fin>>>(dT, c, S, nsb, out_ns, k, lists);
+        else if (bkt) k_final_small<1, true><<<gf, NT, 0, fin>>>(dT, c, S, nsb, out_ns, k, lists);
+        else if (b == 0) k_final_small<1, false, true><<<gf, NT, 0, fin>>>(dT, c, S, nsb, out_ns, k, lists);
         else k_final_small<1, false><<<gf, NT, 0, fin>>>(dT, c, S, nsb, out_ns, k, lists);
       }
     } else if (k && k <= 32) k_final_small<0, false><<<gf, NT, 0, fin>>>(dT, c, S, nsb, out_ns, k, lists);
