@@ -2405,14 +2405,21 @@ int launch_eval(hsim_handle* h, const Tables* dT, const hsim_cands* cc, int64_t 
   }
   if (k) {
     // n == 0 merges no list and only writes the (INT64_MAX, -1) padding
-    const int tq = g_trace.pre("k_merge", 0, st);
+    // after the sweep: on the final stream right behind K_final (no cross-stream
+    // event on the chain), then the caller's stream waits for it
+    cudaStream_t ms = n > 0 ? side_stream(h, NSTREAM_FINAL) : st;
+    const int tq = g_trace.pre("k_merge", n > 0 ? NSTREAM_FINAL : 0, ms);
     if (n > 0 && k <= 32)
-      k_merge_thresh<<<1, 1024, 0, st>>>(lists, nlists, k, (const unsigned long long*)(lists + (size_t)nlists * 2 * k),
+      k_merge_thresh<<<1, 1024, 0, ms>>>(lists, nlists, k, (const unsigned long long*)(lists + (size_t)nlists * 2 * k),
                                          out_t, out_i);
     else
-      launch_merge_any(lists, n > 0 ? nlists : 0, k, out_t, out_i, st);
-    g_trace.post(tq, st);
+      launch_merge_any(lists, n > 0 ? nlists : 0, k, out_t, out_i, ms);
+    g_trace.post(tq, ms);
     ++launches;
+    if (n > 0) {
+      cudaEventRecord(pool_event(h, 46), ms);
+      cudaStreamWaitEvent(st, pool_event(h, 46), 0);
+    }
   }
   call_end(h, st);
   g_trace.dump();
