@@ -7,6 +7,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2508_05370_b200 import build as B  # noqa: E402
 
 VARIANTS = {
+    "fm3": ["-DHSIM_FINAL_MULT=3"],
     "prio4": ["-DHSIM_PRIO4"],
     "norq2": ["-DHSIM_REQ_MINJOBS=(1LL<<40)"],
     "fp3": ["-DHSIM_FINALP_MINB=3"],
