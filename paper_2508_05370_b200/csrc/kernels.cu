@@ -1609,6 +1609,10 @@ __global__ void __launch_bounds__(NT, MODE ? HSIM_FINALP_MINB : 1) k_final_small
   RegTopK r;
   r.init();
   if (w == 0 && lane < k && blist[lane] != LIST_PAD && blist[lane] != KEY_INF) { r.t = blist[lane]; r.i = blist[k + lane]; }
+  // launched as a programmatic dependent of K_gather (dedupe mode): the
+  // prologue above overlaps its tail; the batch's scratch is read only after
+  // K_gather has completed (a no-op for an ordinary launch)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   int qn = 0;  // queued entries (warp-uniform)
   // the warp's chunks first + j * step, j < nch, visited from its best chunk
   // (smallest T0, dedupe mode: K_gather's row) and its sync drained at once:
@@ -2332,10 +2336,20 @@ static int run_phases(hsim_handle* h, const Tables* dT, Cands c, int64_t n, int6
         if (bkt) k_final_small<2, true><<<gf, NT, 0, fin>>>(dT, c, S, nsb, out_ns, k, lists);
         else k_final_small<2, false><<<gf, NT, 0, fin>>>(dT, c, S, nsb, out_ns, k, lists);
       } else {
-        if (bkt && b == 0) k_final_small<1, true, true><<<gf, NT, 0, fin>>>(dT, c, S, nsb, out_ns, k, lists);
-        else if (bkt) k_final_small<1, true><<<gf, NT, 0, fin>>>(dT, c, S, nsb, out_ns, k, lists);
-        else if (b == 0) k_final_small<1, false, true><<<gf, NT, 0, fin>>>(dT, c, S, nsb, out_ns, k, lists);
-        else k_final_small<1, false><<<gf, NT, 0, fin>>>(dT, c, S, nsb, out_ns, k, lists);
+        // dedupe: a programmatic dependent launch behind K_gather (same stream)
+        cudaLaunchConfig_t lc = {};
+        lc.gridDim = dim3(gf);
+        lc.blockDim = dim3(NT);
+        lc.stream = fin;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = dd ? 1 : 0;
+        lc.attrs = at;
+        lc.numAttrs = 1;
+        if (bkt && b == 0) cudaLaunchKernelEx(&lc, k_final_small<1, true, true>, dT, c, S, nsb, out_ns, k, lists);
+        else if (bkt) cudaLaunchKernelEx(&lc, k_final_small<1, true, false>, dT, c, S, nsb, out_ns, k, lists);
+        else if (b == 0) cudaLaunchKernelEx(&lc, k_final_small<1, false, true>, dT, c, S, nsb, out_ns, k, lists);
+        else cudaLaunchKernelEx(&lc, k_final_small<1, false, false>, dT, c, S, nsb, out_ns, k, lists);
       }
     } else if (k && k <= 32) k_final_small<0, false><<<gf, NT, 0, fin>>>(dT, c, S, nsb, out_ns, k, lists);
     else k_final<<<gf, NT, 0, fin>>>(dT, c, S, nsb, out_ns, k, lists);
