@@ -1891,6 +1891,9 @@ __global__ void __launch_bounds__(1024) k_merge_thresh(const i64* __restrict__ b
   __shared__ i64 ct[CAP], ci[CAP];
   __shared__ int cnt;
   const int tid = threadIdx.x;
+  // a programmatic dependent of K_final when the sweep ran (same stream): wait
+  // for its lists before reading them (a no-op for an ordinary launch)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const i64 g = (i64)*gthr;
   if (tid == 0) cnt = 0;
   __syncthreads();
@@ -2423,9 +2426,19 @@ int launch_eval(hsim_handle* h, const Tables* dT, const hsim_cands* cc, int64_t 
     // event on the chain), then the caller's stream waits for it
     cudaStream_t ms = n > 0 ? side_stream(h, NSTREAM_FINAL) : st;
     const int tq = g_trace.pre("k_merge", n > 0 ? NSTREAM_FINAL : 0, ms);
-    if (n > 0 && k <= 32)
-      k_merge_thresh<<<1, 1024, 0, ms>>>(lists, nlists, k, (const unsigned long long*)(lists + (size_t)nlists * 2 * k),
-                                         out_t, out_i);
+    if (n > 0 && k <= 32) {
+      cudaLaunchConfig_t lc = {};
+      lc.gridDim = dim3(1);
+      lc.blockDim = dim3(1024);
+      lc.stream = ms;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      at[0].val.programmaticStreamSerializationAllowed = 1;
+      lc.attrs = at;
+      lc.numAttrs = 1;
+      cudaLaunchKernelEx(&lc, k_merge_thresh, (const i64*)lists, (int)nlists, (int)k,
+                         (const unsigned long long*)(lists + (size_t)nlists * 2 * k), (i64*)out_t, (i64*)out_i);
+    }
     else
       launch_merge_any(lists, n > 0 ? nlists : 0, k, out_t, out_i, ms);
     g_trace.post(tq, ms);
